@@ -1,0 +1,242 @@
+/* homs_b200.h -- C ABI of the B200-native HyperOMS hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++ or torch types.  The reference
+ * (`homs_core`, C++20, CPU only) has no FFI layer of its own; its boundary is the public C++ API
+ * of proj/core.  Each entry point below names the reference interface it
+ * replaces (paths relative to /root/reference/proj/core/).  The C++ facade that keeps the
+ * reference's signatures on top of this ABI is include/homs_b200/homs.hpp; INTEGRATION.md shows
+ * the binding a reference maintainer would add.
+ *
+ * Conventions
+ *   - every function returns HOMS_B200_OK (0) or an error code; homs_b200_last_error(ctx) gives
+ *     the message.  HOMS_B200_ERR_CONFIG / _INVARIANT correspond to the reference's
+ *     homs::ConfigError / homs::InvariantError (include/homs/errors.hpp:16-56); the C++ facade
+ *     re-throws them as such.  No exception ever crosses this boundary.
+ *   - hypervectors are little-endian u64 words, bit d at word d/64 bit d%64, tail bits zero,
+ *     W = ceil(dim/64) words per row, rows dense (include/homs/hypervector.hpp:12-15).
+ *   - spectra travel as CSR: offsets u64[n+1], mz f64[], intensity f64[]; peaks of one spectrum
+ *     strictly ascending in m/z (RawSpectrum invariant, include/homs/spectrum.hpp:34-35).
+ *   - the caller owns every host buffer for the duration of the call; the context owns all device
+ *     memory.  Calls on one context are serialised internally; results never depend on the
+ *     reference's `threads` / `batch_size` knobs (search.hpp:102-103), which therefore do not
+ *     appear here.
+ *   - functions with the suffix _dev take DEVICE pointers and enqueue work on the context's
+ *     stream without synchronising; all others take HOST pointers and are blocking.
+ *   - there is no CPU fallback: without a CUDA device homs_b200_ctx_create fails.
+ */
+#ifndef HOMS_B200_H
+#define HOMS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HOMS_B200_ABI_VERSION 1
+
+enum {
+  HOMS_B200_OK = 0,
+  HOMS_B200_ERR_CONFIG = 1,    /* homs::ConfigError    */
+  HOMS_B200_ERR_INVARIANT = 2, /* homs::InvariantError */
+  HOMS_B200_ERR_CUDA = 3,      /* CUDA runtime failure (message carries cudaGetErrorString) */
+  HOMS_B200_ERR_ARGUMENT = 4,  /* null pointer / size out of the supported range */
+  HOMS_B200_ERR_STATE = 5      /* call order (e.g. search before library upload) */
+};
+
+enum { HOMS_B200_TOL_PPM = 0, HOMS_B200_TOL_DALTON = 1 };
+#define HOMS_B200_NO_HIT 0xFFFFFFFFu
+#define HOMS_B200_MAX_TOPK 64u
+
+typedef struct homs_b200_ctx homs_b200_ctx;
+
+/* PreprocessConfig, include/homs/preprocess.hpp:13-25 */
+typedef struct {
+  double min_mz, max_mz, bin_size;
+  uint32_t max_peaks, min_peaks;
+  double intensity_floor;
+  uint32_t scaling; /* IntensityScaling: 0 none, 1 sqrt (preprocess.hpp:11) */
+  uint32_t reserved;
+} homs_b200_preprocess_config;
+
+/* EncoderConfig, include/homs/codebook.hpp:12-23 */
+typedef struct {
+  uint32_t dim, step_flips, levels, reserved;
+  uint64_t seed;
+} homs_b200_encoder_config;
+
+/* Tolerance, include/homs/search.hpp:16-33 */
+typedef struct {
+  uint32_t kind; /* HOMS_B200_TOL_PPM | HOMS_B200_TOL_DALTON */
+  uint32_t reserved;
+  double value;
+} homs_b200_tolerance;
+
+/* One candidate of the windowed top-k: 16 bytes, ordered lexicographically by
+ * (distance, abs_diff_bits, id_rank) == the reference's key (score desc, |q - r| asc, id asc,
+ * ordinal asc) of search.cpp:133-146.  distance = dim - raw_score; abs_diff_bits is the IEEE-754
+ * pattern of the non-negative double |q_mz - ref_mz| (monotone as an integer); id_rank is the
+ * entry's position in the library-wide sort by (id, ordinal).  distance == 0xFFFFFFFF: empty. */
+typedef struct {
+  uint32_t distance;
+  uint32_t id_rank;
+  uint64_t abs_diff_bits;
+} homs_b200_candidate;
+
+/* ---- context ------------------------------------------------------------------------------- */
+
+int homs_b200_abi_version(void);
+/* Creates a context on CUDA device `device`.  *out is NULL on failure; the message is then
+ * available through homs_b200_last_error(NULL). */
+int homs_b200_ctx_create(int device, homs_b200_ctx** out);
+void homs_b200_ctx_destroy(homs_b200_ctx* ctx);
+const char* homs_b200_last_error(const homs_b200_ctx* ctx);
+/* Adopt an external cudaStream_t for all subsequent work (NULL: back to the context's own). */
+int homs_b200_ctx_set_stream(homs_b200_ctx* ctx, void* cuda_stream);
+int homs_b200_ctx_synchronize(homs_b200_ctx* ctx);
+/* Kernels launched by this context so far (bench.py's gpu_launches). */
+uint64_t homs_b200_ctx_launch_count(const homs_b200_ctx* ctx);
+
+/* ---- host-side configuration (no device work) ----------------------------------------------- */
+
+/* PreprocessConfig::validate, src/preprocess.cpp:21-34 */
+int homs_b200_preprocess_validate(const homs_b200_preprocess_config* cfg);
+/* dimension(), src/preprocess.cpp:36-39 */
+uint32_t homs_b200_dimension(const homs_b200_preprocess_config* cfg);
+/* EncoderConfig::validate, src/codebook.cpp:26-36 */
+int homs_b200_encoder_validate(const homs_b200_encoder_config* cfg);
+/* quantize_intensity, src/encoder.cpp:11-17 (HOMS_B200_ERR_INVARIANT outside [0,1]) */
+int homs_b200_quantize_intensity(double v, uint32_t levels, uint32_t* out_level);
+/* make_codebook, src/codebook.cpp:87-94 (gen_position_hvs :38-53, gen_level_hvs :55-85).  The
+ * RNG chain is inherently serial, so this runs on the host once per configuration.
+ * pos: n_bins x W words, lvl: (levels+1) x W words. */
+int homs_b200_make_codebook(const homs_b200_encoder_config* cfg, uint32_t n_bins, uint64_t* pos,
+                            uint64_t* lvl);
+/* compute_fdr_curve, src/fdr.cpp:8-50.  out_input_index[p] = input position of sorted position
+ * p, out_fdr / out_q_value per sorted position. */
+int homs_b200_compute_fdr_curve(uint64_t n, const double* score, const uint8_t* is_decoy,
+                                uint64_t* out_input_index, double* out_fdr, double* out_q_value);
+
+/* ---- encoding (preprocess.cpp:41-110, encoder.cpp:19-55, pipeline.cpp:60-85) --------------- */
+
+/* Makes a codebook resident on the device (replaces the `const Codebook&` argument of
+ * encode()/encode_spectra(), include/homs/codebook.hpp:29-34). */
+int homs_b200_codebook_upload(homs_b200_ctx* ctx, uint32_t dim, uint32_t n_bins, uint32_t levels,
+                              const uint64_t* pos, const uint64_t* lvl);
+
+/* encode_spectra, src/pipeline.cpp:60-85: refine_peaks -> vectorize -> encode per spectrum.
+ * out_ok[i] = 1 and row i of out_words holds the hypervector when spectrum i is processable,
+ * else out_ok[i] = 0 and the row is zero (the reference drops such spectra; the C++ facade
+ * compacts).  HOMS_B200_ERR_INVARIANT when homs_b200_dimension(cfg) != uploaded n_bins. */
+int homs_b200_encode_batch(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint64_t n,
+                           const uint64_t* offsets, const double* mz, const double* intensity,
+                           uint64_t* out_words, uint8_t* out_ok);
+int homs_b200_encode_batch_dev(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg,
+                               uint64_t n, uint64_t n_peaks_total, const uint64_t* d_offsets,
+                               const double* d_mz, const double* d_intensity,
+                               uint64_t* d_out_words, uint8_t* d_out_ok);
+
+/* refine_peaks + vectorize + quantize_intensity only (preprocess.cpp:41-110, encoder.cpp:11-17):
+ * per spectrum the ascending bin list and its levels.  out_bins / out_levels are
+ * n x cfg->max_peaks (row i holds out_count[i] entries; out_count[i] = 0: unprocessable). */
+int homs_b200_preprocess_batch(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg,
+                               uint32_t levels, uint64_t n, const uint64_t* offsets,
+                               const double* mz, const double* intensity, uint32_t* out_bins,
+                               uint32_t* out_levels, uint32_t* out_count);
+
+/* encode(), src/encoder.cpp:19-55, on already vectorized spectra (SpectrumVector,
+ * preprocess.hpp:29-34) given as CSR (sv_offsets u64[n+1], bins u32[], intensities f64[] in
+ * [0,1]).  HOMS_B200_ERR_INVARIANT on an empty vector, a bin >= n_bins or an intensity outside
+ * [0,1] (encoder.cpp:20-25, :12-14). */
+int homs_b200_encode_vectors(homs_b200_ctx* ctx, uint64_t n, const uint64_t* sv_offsets,
+                             const uint32_t* bins, const double* intensities,
+                             uint64_t* out_words);
+
+/* hamming_similarity, include/homs/hypervector.hpp:70-81, for n row pairs. */
+int homs_b200_hamming_similarity(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* a,
+                                 const uint64_t* b, uint32_t* out_similarity);
+
+/* ---- library index (build_index, src/search.cpp:17-60) ------------------------------------- */
+
+/* Builds the charge-partitioned, precursor-m/z-sorted device index from entries in INPUT order
+ * (ordinal = position in these arrays).  Sort key inside a charge bucket: (mz asc, id asc,
+ * ordinal asc) == (mz asc, id_rank asc) where id_rank[i] is the position of entry i in the
+ * library-wide sort by (id, ordinal); id_rank == NULL means "all ids equal" (rank = ordinal).
+ * shard_index / shard_count: this context keeps hypervectors only for slice shard_index of
+ * every bucket (contiguous equal-row m/z slices); metadata is replicated.  Use 0 / 1 for a
+ * single GPU.  HOMS_B200_ERR_INVARIANT on n == 0 (search.cpp:18). */
+int homs_b200_library_upload(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* words,
+                             const double* precursor_mz, const uint8_t* charge,
+                             const uint32_t* id_rank, uint32_t shard_index, uint32_t shard_count);
+/* Same, hypervector rows already on the device (e.g. straight from homs_b200_encode_batch_dev);
+ * the metadata arrays stay host pointers. */
+int homs_b200_library_upload_dev(homs_b200_ctx* ctx, uint32_t dim, uint64_t n,
+                                 const uint64_t* d_words, const double* precursor_mz,
+                                 const uint8_t* charge, const uint32_t* id_rank,
+                                 uint32_t shard_index, uint32_t shard_count);
+int homs_b200_library_bucket_count(const homs_b200_ctx* ctx, uint32_t* out_count);
+/* Bucket `which` in ascending charge order: its charge, full size, and the slice
+ * [shard_begin, shard_end) of it resident on this context. */
+int homs_b200_library_bucket_info(const homs_b200_ctx* ctx, uint32_t which, uint8_t* out_charge,
+                                  uint64_t* out_size, uint64_t* out_shard_begin,
+                                  uint64_t* out_shard_end);
+/* LibraryIndex::Bucket arrays (search.hpp:41-47): precursor_mz / ordinal for the FULL bucket,
+ * words for the resident slice only.  Any pointer may be NULL. */
+int homs_b200_library_bucket_export(homs_b200_ctx* ctx, uint32_t which, double* out_mz,
+                                    uint32_t* out_ordinal, uint64_t* out_words);
+
+/* ---- search (src/search.cpp:62-183) -------------------------------------------------------- */
+
+/* select_candidates, src/search.cpp:62-89: [first,last) inside the query's charge bucket (full
+ * bucket coordinates); out_has_bucket[i] = 0 when the charge is unknown (0) or has no bucket. */
+int homs_b200_window_bounds(homs_b200_ctx* ctx, uint64_t nq, const double* q_mz,
+                            const uint8_t* q_charge, const homs_b200_tolerance* tol,
+                            uint64_t* out_first, uint64_t* out_last, uint8_t* out_has_bucket);
+
+/* search_batch, src/search.cpp:171-183, generalised to the k best per query (k = 1 is the
+ * reference's search_one).  Entry j of query i: out_raw_score[i*k+j] (Hamming similarity) and
+ * out_ordinal[i*k+j] (input position of the library entry; HOMS_B200_NO_HIT and score 0 when
+ * fewer than j+1 candidates exist).  out_first / out_last (nullable) as in window_bounds.
+ * Requires a single-shard library; sharded contexts use the _resident/_merge calls below.
+ * HOMS_B200_ERR_INVARIANT when query_dim differs from the library's (search.cpp:107-109). */
+int homs_b200_search_batch(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq,
+                           const uint64_t* q_words, const double* q_mz, const uint8_t* q_charge,
+                           const homs_b200_tolerance* tol, uint32_t k, uint32_t* out_raw_score,
+                           uint32_t* out_ordinal, uint64_t* out_first, uint64_t* out_last);
+
+/* Device-resident query set: upload once, search many times (cascade stages, benchmarks). */
+int homs_b200_queries_upload(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq,
+                             const uint64_t* q_words, const double* q_mz, const uint8_t* q_charge);
+int homs_b200_queries_upload_dev(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq,
+                                 const uint64_t* d_q_words, const double* d_q_mz,
+                                 const uint8_t* d_q_charge);
+/* Searches the resident queries (all of them, or the n_subset positions listed in the DEVICE
+ * array d_subset) against this context's library shard; writes n*k candidate records (16 B
+ * each, see homs_b200_candidate) to the DEVICE buffer d_out.  Asynchronous. */
+int homs_b200_search_resident_dev(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n_subset,
+                                  const homs_b200_tolerance* tol, uint32_t k,
+                                  homs_b200_candidate* d_out);
+/* Lexicographic k-way merge of per-shard candidate lists: d_parts is [n_parts][n][k] (the
+ * layout an all-gather produces), d_out is [n][k].  Asynchronous. */
+int homs_b200_merge_candidates_dev(homs_b200_ctx* ctx, uint64_t n, uint32_t k, uint32_t n_parts,
+                                   const homs_b200_candidate* d_parts, homs_b200_candidate* d_out);
+/* Candidate records -> (raw_score, ordinal) on the host.  Blocking. */
+int homs_b200_candidates_decode(homs_b200_ctx* ctx, uint64_t n, uint32_t k,
+                                const homs_b200_candidate* d_records, uint32_t* out_raw_score,
+                                uint32_t* out_ordinal);
+
+/* cascade_search, src/search.cpp:219-248 (run_stage :188-215): narrow stage on all queries,
+ * target-decoy FDR, wide stage on the not-accepted rest, FDR again.  lib_is_decoy is indexed by
+ * library ordinal.  Outputs need room for nq entries; accepted matches come narrow block first,
+ * then wide, each in query order.  Query hypervectors stay on the device between stages. */
+int homs_b200_cascade_search(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq,
+                             const uint64_t* q_words, const double* q_mz, const uint8_t* q_charge,
+                             const homs_b200_tolerance* narrow, const homs_b200_tolerance* wide,
+                             double fdr_q, const uint8_t* lib_is_decoy, uint64_t* out_query,
+                             uint32_t* out_ordinal, uint8_t* out_stage, uint32_t* out_raw_score,
+                             double* out_q_value, uint64_t* out_count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOMS_B200_H */

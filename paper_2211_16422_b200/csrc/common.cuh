@@ -1,0 +1,145 @@
+// Internal definitions shared by the translation units of libhoms_b200.so.
+// Nothing here is part of the ABI (that is include/homs_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "homs_b200.h"
+
+namespace hb {
+
+// Device row layout: every hypervector row is padded with zero words to a multiple of 128 bytes
+// (16 u64) so that a row is a whole number of 128-byte cp.async / LDS.128 chunks groups.  Padding
+// is zero in library AND query rows, so XOR+popcount over the padded row equals the reference's
+// sum over W words (hypervector.hpp:70-81).
+constexpr uint32_t kRowAlignWords = 16;
+
+inline uint32_t words_for(uint32_t dim) { return (dim + 63u) / 64u; }
+inline uint32_t stride_for(uint32_t dim) {
+  return (words_for(dim) + kRowAlignWords - 1) / kRowAlignWords * kRowAlignWords;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct BucketDev {           // one charge bucket, device + host view
+  uint64_t begin;            // offset of the bucket in the library-wide sorted order
+  uint64_t size;             // rows in the full bucket
+  uint64_t shard_begin;      // [shard_begin, shard_end) of the bucket is resident here ...
+  uint64_t shard_end;
+  uint64_t local_offset;     // ... at local rows [local_offset, local_offset + shard_end - shard_begin)
+};
+
+struct Library {
+  bool ready = false;
+  uint32_t dim = 0, W = 0, S = 0;  // bits, dense words, padded stride (u64 words)
+  uint64_t n = 0, n_local = 0;
+  uint32_t shard_index = 0, shard_count = 1;
+  std::vector<uint8_t> bucket_charge;
+  std::vector<BucketDev> buckets;
+  std::vector<double> h_mz;         // full library, sorted order
+  std::vector<uint32_t> h_ordinal;  // full library, sorted order
+  // device (owned through ctx buffers)
+  DevBuf d_mz, d_id_rank, d_ord_of_rank, d_mz_local, d_id_rank_local, d_words, d_buckets,
+      d_bucket_of_charge;
+};
+
+struct Queries {
+  bool ready = false;
+  uint32_t dim = 0;
+  uint64_t nq = 0;
+  DevBuf d_words, d_mz, d_charge;  // words: padded stride of the query dim
+};
+
+struct Codebook {
+  bool ready = false;
+  uint32_t dim = 0, n_bins = 0, levels = 0, W = 0, S = 0;
+  DevBuf d_pos, d_lvl;  // padded rows
+};
+
+}  // namespace hb
+
+struct homs_b200_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  mutable std::string error;
+  uint64_t launches = 0;
+  hb::Codebook cb;
+  hb::Library lib;
+  hb::Queries q;
+  // grow-only scratch, keyed by purpose
+  enum { kScratchSlots = 24 };
+  hb::DevBuf scratch[kScratchSlots];
+  void* pinned = nullptr;  // small pinned staging block
+  size_t pinned_cap = 0;
+};
+
+namespace hb {
+
+int set_error(const homs_b200_ctx* ctx, int code, const std::string& msg);
+
+#define HB_CUDA(ctx, expr)                                                                   \
+  do {                                                                                       \
+    cudaError_t e__ = (expr);                                                                \
+    if (e__ != cudaSuccess)                                                                  \
+      return ::hb::set_error((ctx), HOMS_B200_ERR_CUDA,                                      \
+                             std::string(#expr) + ": " + cudaGetErrorString(e__));           \
+  } while (0)
+
+#define HB_TRY(expr)                      \
+  do {                                    \
+    int rc__ = (expr);                    \
+    if (rc__ != HOMS_B200_OK) return rc__; \
+  } while (0)
+
+#define HB_REQUIRE(ctx, cond, code, msg)                     \
+  do {                                                       \
+    if (!(cond)) return ::hb::set_error((ctx), (code), (msg)); \
+  } while (0)
+
+// Kernel launch bookkeeping: counts the launch and checks for launch errors.
+#define HB_LAUNCHED(ctx)               \
+  do {                                 \
+    ++(ctx)->launches;                 \
+    HB_CUDA((ctx), cudaGetLastError()); \
+  } while (0)
+
+int ensure(homs_b200_ctx* ctx, DevBuf& b, size_t bytes);
+int ensure_pinned(homs_b200_ctx* ctx, size_t bytes);
+void release(DevBuf& b);
+
+// scratch slot names
+enum Scratch {
+  kScrOffsets = 0, kScrMz, kScrInt, kScrSvBins, kScrSvLev, kScrSvCount, kScrEncOut, kScrEncOk,
+  kScrQFirst, kScrQLast, kScrKeys, kScrKeysAlt, kScrVals, kScrValsAlt, kScrCub, kScrPlan,
+  kScrPartial, kScrRecords, kScrSubset, kScrDecode, kScrMisc, kScrMisc2, kScrRecords2, kScrHas
+};
+
+// dense host rows (W words) -> padded device rows (S words), zero padded.  Async on ctx->stream.
+int upload_rows(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* h_src, uint64_t n, uint32_t W,
+                uint32_t S);
+int download_rows(homs_b200_ctx* ctx, uint64_t* h_dst, const uint64_t* d_src, uint64_t n,
+                  uint32_t W, uint32_t S);
+// dense device rows -> padded device rows
+int repack_rows_dev(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src, uint64_t n,
+                    uint32_t W, uint32_t S);
+
+struct Lock {
+  explicit Lock(homs_b200_ctx* c) : g(c->mu) { cudaSetDevice(c->device); }
+  std::lock_guard<std::mutex> g;
+};
+
+}  // namespace hb

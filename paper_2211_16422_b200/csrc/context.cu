@@ -1,0 +1,311 @@
+// Context lifetime, device buffers, and the host-only pieces of the ABI (configuration checks,
+// codebook generation, FDR curve).  Reference lines cited are under /root/reference/proj/core/.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <random>
+
+#include "common.cuh"
+
+namespace {
+thread_local std::string g_global_error;
+}
+
+namespace hb {
+
+int set_error(const homs_b200_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->error = msg;
+  else g_global_error = msg;
+  return code;
+}
+
+int ensure(homs_b200_ctx* ctx, DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return HOMS_B200_OK;
+  if (b.p) {
+    // pending work may still read the old block
+    HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    HB_CUDA(ctx, cudaFree(b.p));
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  const size_t want = (bytes + 255) / 256 * 256;
+  HB_CUDA(ctx, cudaMalloc(&b.p, want));
+  b.cap = want;
+  return HOMS_B200_OK;
+}
+
+void release(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+int ensure_pinned(homs_b200_ctx* ctx, size_t bytes) {
+  if (ctx->pinned_cap >= bytes) return HOMS_B200_OK;
+  if (ctx->pinned) {
+    HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    ctx->pinned_cap = 0;
+  }
+  HB_CUDA(ctx, cudaMallocHost(&ctx->pinned, bytes));
+  ctx->pinned_cap = bytes;
+  return HOMS_B200_OK;
+}
+
+int upload_rows(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* h_src, uint64_t n, uint32_t W,
+                uint32_t S) {
+  if (n == 0) return HOMS_B200_OK;
+  if (W == S) {
+    HB_CUDA(ctx, cudaMemcpyAsync(d_dst, h_src, n * W * 8, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    HB_CUDA(ctx, cudaMemsetAsync(d_dst, 0, n * S * 8, ctx->stream));
+    HB_CUDA(ctx, cudaMemcpy2DAsync(d_dst, size_t(S) * 8, h_src, size_t(W) * 8, size_t(W) * 8, n,
+                                   cudaMemcpyHostToDevice, ctx->stream));
+  }
+  return HOMS_B200_OK;
+}
+
+int download_rows(homs_b200_ctx* ctx, uint64_t* h_dst, const uint64_t* d_src, uint64_t n,
+                  uint32_t W, uint32_t S) {
+  if (n == 0) return HOMS_B200_OK;
+  if (W == S) {
+    HB_CUDA(ctx, cudaMemcpyAsync(h_dst, d_src, n * W * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  } else {
+    HB_CUDA(ctx, cudaMemcpy2DAsync(h_dst, size_t(W) * 8, d_src, size_t(S) * 8, size_t(W) * 8, n,
+                                   cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  return HOMS_B200_OK;
+}
+
+int repack_rows_dev(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src, uint64_t n,
+                    uint32_t W, uint32_t S) {
+  if (n == 0) return HOMS_B200_OK;
+  if (W == S) {
+    HB_CUDA(ctx, cudaMemcpyAsync(d_dst, d_src, n * W * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    HB_CUDA(ctx, cudaMemsetAsync(d_dst, 0, n * S * 8, ctx->stream));
+    HB_CUDA(ctx, cudaMemcpy2DAsync(d_dst, size_t(S) * 8, d_src, size_t(W) * 8, size_t(W) * 8, n,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  return HOMS_B200_OK;
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" {
+
+int homs_b200_abi_version(void) { return HOMS_B200_ABI_VERSION; }
+
+int homs_b200_ctx_create(int device, homs_b200_ctx** out) {
+  if (!out) return set_error(nullptr, HOMS_B200_ERR_ARGUMENT, "ctx_create: out is null");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return set_error(nullptr, HOMS_B200_ERR_CUDA,
+                     std::string("no CUDA device available (this library has no CPU fallback): ") +
+                         cudaGetErrorString(e));
+  if (device < 0 || device >= count)
+    return set_error(nullptr, HOMS_B200_ERR_ARGUMENT, "ctx_create: device index out of range");
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess)
+    return set_error(nullptr, HOMS_B200_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  auto* ctx = new homs_b200_ctx;
+  ctx->device = device;
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return set_error(nullptr, HOMS_B200_ERR_CUDA, std::string("cudaGetDeviceProperties: ") + cudaGetErrorString(e));
+  }
+  ctx->sm_count = prop.multiProcessorCount;
+  e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return set_error(nullptr, HOMS_B200_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+  }
+  ctx->stream = ctx->own_stream;
+  *out = ctx;
+  return HOMS_B200_OK;
+}
+
+void homs_b200_ctx_destroy(homs_b200_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& b : ctx->scratch) release(b);
+  for (DevBuf* b : {&ctx->cb.d_pos, &ctx->cb.d_lvl, &ctx->lib.d_mz, &ctx->lib.d_id_rank,
+                    &ctx->lib.d_ord_of_rank, &ctx->lib.d_mz_local, &ctx->lib.d_id_rank_local,
+                    &ctx->lib.d_words, &ctx->lib.d_buckets, &ctx->lib.d_bucket_of_charge,
+                    &ctx->q.d_words, &ctx->q.d_mz, &ctx->q.d_charge})
+    release(*b);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+const char* homs_b200_last_error(const homs_b200_ctx* ctx) {
+  return ctx ? ctx->error.c_str() : g_global_error.c_str();
+}
+
+int homs_b200_ctx_set_stream(homs_b200_ctx* ctx, void* cuda_stream) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+  return HOMS_B200_OK;
+}
+
+int homs_b200_ctx_synchronize(homs_b200_ctx* ctx) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return HOMS_B200_OK;
+}
+
+uint64_t homs_b200_ctx_launch_count(const homs_b200_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---- host-only configuration --------------------------------------------------------------
+
+static constexpr double kBinEpsilon = 1e-9;  // preprocess.cpp:17
+
+int homs_b200_preprocess_validate(const homs_b200_preprocess_config* c) {  // preprocess.cpp:21-34
+  if (!c) return set_error(nullptr, HOMS_B200_ERR_ARGUMENT, "preprocess config is null");
+  if (!(c->min_mz < c->max_mz))
+    return set_error(nullptr, HOMS_B200_ERR_CONFIG, "preprocess: min_mz must be smaller than max_mz");
+  if (!(c->bin_size > 0.0))
+    return set_error(nullptr, HOMS_B200_ERR_CONFIG, "preprocess: bin_size must be positive");
+  if (c->min_peaks < 1 || c->max_peaks < c->min_peaks)
+    return set_error(nullptr, HOMS_B200_ERR_CONFIG, "preprocess: need max_peaks >= min_peaks >= 1");
+  if (!(c->intensity_floor >= 0.0 && c->intensity_floor < 1.0))
+    return set_error(nullptr, HOMS_B200_ERR_CONFIG, "preprocess: intensity_floor must lie in [0, 1)");
+  return HOMS_B200_OK;
+}
+
+uint32_t homs_b200_dimension(const homs_b200_preprocess_config* c) {  // preprocess.cpp:36-39
+  const double q = (c->max_mz - c->min_mz) / c->bin_size;
+  return static_cast<uint32_t>(std::ceil(q - kBinEpsilon));
+}
+
+int homs_b200_encoder_validate(const homs_b200_encoder_config* c) {  // codebook.cpp:26-36
+  if (!c) return set_error(nullptr, HOMS_B200_ERR_ARGUMENT, "encoder config is null");
+  if (c->dim < 64 || c->dim % 64 != 0)
+    return set_error(nullptr, HOMS_B200_ERR_CONFIG, "encoder dim must be a multiple of 64 and at least 64");
+  if (c->step_flips < 1)
+    return set_error(nullptr, HOMS_B200_ERR_CONFIG, "encoder step_flips must be at least 1");
+  if (c->levels < 2)
+    return set_error(nullptr, HOMS_B200_ERR_CONFIG, "encoder levels must be at least 2");
+  return HOMS_B200_OK;
+}
+
+int homs_b200_quantize_intensity(double v, uint32_t levels, uint32_t* out) {  // encoder.cpp:11-17
+  if (!(v >= 0.0 && v <= 1.0))
+    return set_error(nullptr, HOMS_B200_ERR_INVARIANT, "quantize_intensity: intensity outside [0, 1]");
+  const double level = std::round(v * static_cast<double>(levels));
+  *out = std::min(static_cast<uint32_t>(level), levels);
+  return HOMS_B200_OK;
+}
+
+namespace {
+
+// rng.hpp:10-44.  std::mt19937_64 is fully specified by ISO C++, so the streams are identical to
+// the reference's on every toolchain.
+uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+uint64_t named_stream(uint64_t seed, uint64_t tag) { return mix64(seed ^ mix64(tag)); }
+
+uint64_t draw_below(std::mt19937_64& rng, uint64_t n) {  // mask rejection, rng.hpp:26-39
+  uint64_t mask = n - 1;
+  for (int s = 1; s < 64; s <<= 1) mask |= mask >> s;
+  for (;;) {
+    const uint64_t v = rng() & mask;
+    if (v < n) return v;
+  }
+}
+
+void fill_random(uint64_t* w, uint32_t dim, std::mt19937_64& rng) {  // codebook.cpp:17-22
+  const uint32_t W = hb::words_for(dim);
+  for (uint32_t i = 0; i < W; ++i) w[i] = rng();
+  if (dim % 64) w[W - 1] &= (uint64_t{1} << (dim % 64)) - 1;
+}
+
+inline void toggle(uint64_t* w, uint32_t bit) { w[bit >> 6] ^= uint64_t{1} << (bit & 63); }
+
+}  // namespace
+
+int homs_b200_make_codebook(const homs_b200_encoder_config* c, uint32_t n_bins, uint64_t* pos,
+                            uint64_t* lvl) {
+  if (!c || !pos || !lvl) return set_error(nullptr, HOMS_B200_ERR_ARGUMENT, "make_codebook: null argument");
+  if (c->dim == 0 || c->levels == 0)
+    return set_error(nullptr, HOMS_B200_ERR_ARGUMENT, "make_codebook: dim and levels must be positive");
+  const uint32_t dim = c->dim, W = hb::words_for(dim);
+
+  // position rows: a chain, each row = predecessor with step_flips with-replacement flips
+  // (codebook.cpp:38-53); stream tag "position" (:14)
+  {
+    std::mt19937_64 rng(named_stream(c->seed, 0x706f736974696f6eULL));
+    std::vector<uint64_t> cur(W);
+    fill_random(cur.data(), dim, rng);
+    for (uint32_t i = 0; i < n_bins; ++i) {
+      if (i > 0)
+        for (uint32_t k = 0; k < c->step_flips; ++k)
+          toggle(cur.data(), static_cast<uint32_t>(draw_below(rng, dim)));
+      std::memcpy(pos + size_t(i) * W, cur.data(), size_t(W) * 8);
+    }
+  }
+  // level rows: level q = level 0 with the first floor((dim/2) q / Q) entries of one partial
+  // Fisher-Yates order flipped (codebook.cpp:55-85); stream tag "levelhvs" (:15)
+  {
+    std::mt19937_64 rng(named_stream(c->seed, 0x6c6576656c687673ULL));
+    const uint32_t half = dim / 2;
+    std::vector<uint64_t> cur(W);
+    fill_random(cur.data(), dim, rng);
+    std::vector<uint32_t> order(dim);
+    std::iota(order.begin(), order.end(), 0u);
+    for (uint32_t i = 0; i < half; ++i)
+      std::swap(order[i], order[i + static_cast<uint32_t>(draw_below(rng, dim - i))]);
+    uint64_t done = 0;
+    for (uint32_t q = 0; q <= c->levels; ++q) {
+      const uint64_t cut = uint64_t(half) * q / c->levels;
+      for (; done < cut; ++done) toggle(cur.data(), order[done]);
+      std::memcpy(lvl + size_t(q) * W, cur.data(), size_t(W) * 8);
+    }
+  }
+  return HOMS_B200_OK;
+}
+
+int homs_b200_compute_fdr_curve(uint64_t n, const double* score, const uint8_t* is_decoy,
+                                uint64_t* out_input_index, double* out_fdr, double* out_q) {
+  // fdr.cpp:8-50: stable order by (score desc, decoy before target), running counts,
+  // fdr = decoys / max(1, targets), q = suffix minimum.
+  if (n == 0) return HOMS_B200_OK;
+  if (!score || !is_decoy || !out_input_index || !out_fdr || !out_q)
+    return set_error(nullptr, HOMS_B200_ERR_ARGUMENT, "compute_fdr_curve: null argument");
+  std::iota(out_input_index, out_input_index + n, uint64_t{0});
+  std::stable_sort(out_input_index, out_input_index + n, [&](uint64_t a, uint64_t b) {
+    if (score[a] != score[b]) return score[a] > score[b];
+    return (is_decoy[a] != 0) > (is_decoy[b] != 0);
+  });
+  uint64_t targets = 0, decoys = 0;
+  for (uint64_t p = 0; p < n; ++p) {
+    (is_decoy[out_input_index[p]] ? decoys : targets) += 1;
+    out_fdr[p] = static_cast<double>(decoys) / static_cast<double>(std::max<uint64_t>(1, targets));
+  }
+  double low = out_fdr[n - 1];
+  for (uint64_t p = n; p-- > 0;) {
+    low = std::min(low, out_fdr[p]);
+    out_q[p] = low;
+  }
+  return HOMS_B200_OK;
+}
+
+}  // extern "C"

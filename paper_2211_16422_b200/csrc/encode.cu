@@ -1,0 +1,654 @@
+// Spectrum preprocessing (K1) and ID-level hypervector encoding (K2) for sm_100a.
+//
+// Reference semantics (paths under /root/reference/proj/core/):
+//   refine_peaks   src/preprocess.cpp:41-75      vectorize  src/preprocess.cpp:77-110
+//   quantize       src/encoder.cpp:11-17         encode     src/encoder.cpp:19-55
+//   encode_spectra src/pipeline.cpp:60-85
+//
+// K1  one warp per spectrum, fp64 throughout (compiled with -fmad=false; every operation is a
+//     single IEEE add/sub/mul/div/sqrt/floor/round exactly as in the reference), peaks staged in
+//     shared memory, order-preserving ballot compaction.
+// K2  one warp per spectrum, bit-sliced: lane owns one 128-bit column slab per pass; per peak the
+//     lane XNORs its slab of the position row (L2 gather, LDG.128) with the level row (shared
+//     memory) and feeds the 32x4 one-bit votes into a carry-save adder tree (7:3 compressors,
+//     LOP3) that accumulates vertical counters; the strict majority 2*votes > n is a bit-serial
+//     comparison of the counter planes against floor(n/2)+1.  Output rows are written with
+//     coalesced 128-bit stores.
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace hb {
+
+// ------------------------------------------------------------------------------------------
+// K1: refine_peaks + vectorize + quantize_intensity
+// ------------------------------------------------------------------------------------------
+
+struct PreParams {
+  double min_mz, max_mz, bin_size, intensity_floor;
+  uint32_t max_peaks, min_peaks, scaling, dims, levels;
+};
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t quantize_level(double v, uint32_t levels) {
+  // encoder.cpp:15-16: min(u32(round(v * Q)), Q); round() is half-away-from-zero
+  const double level = round(v * static_cast<double>(levels));
+  const uint32_t l = static_cast<uint32_t>(level);
+  return l < levels ? l : levels;
+}
+
+// One warp per spectrum.  Shared memory per warp: max_peaks * (8 + 8 + 4) bytes.
+__global__ void __launch_bounds__(256)
+preprocess_kernel(PreParams p, uint64_t n, const uint64_t* __restrict__ offsets,
+                  const double* __restrict__ mz, const double* __restrict__ inten,
+                  uint32_t* __restrict__ out_bins, uint32_t* __restrict__ out_levels,
+                  uint32_t* __restrict__ out_count, int warps_per_cta) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t MP = p.max_peaks;
+  double* s_mz = reinterpret_cast<double*>(smem_raw) + size_t(warp) * 2 * MP;
+  double* s_int = s_mz + MP;
+  uint32_t* s_bin = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(smem_raw) +
+                                                size_t(warps_per_cta) * 2 * MP) +
+                    size_t(warp) * MP;
+  double* o_val = s_mz;  // reused once the bins have been computed
+
+  for (uint64_t spec = uint64_t(blockIdx.x) * warps_per_cta + warp; spec < n;
+       spec += uint64_t(gridDim.x) * warps_per_cta) {
+    const uint64_t a = offsets[spec], b = offsets[spec + 1];
+
+    // preprocess.cpp:45-49 range / positivity filter, :52-53 base peak over the filtered set
+    double base = 0.0;
+    for (uint64_t j = a + lane; j < b; j += 32) {
+      const double m = mz[j], v = inten[j];
+      if (m >= p.min_mz && m < p.max_mz && v > 0.0) base = fmax(base, v);
+    }
+    base = warp_max(base);
+    const double floor_intensity = p.intensity_floor * base;  // :54
+
+    // survivors of :55 (strict <), counted
+    uint32_t m_surv = 0;
+    for (uint64_t j = a + lane; j < b; j += 32) {
+      const double m = mz[j], v = inten[j];
+      m_surv += (m >= p.min_mz && m < p.max_mz && v > 0.0 && !(v < floor_intensity));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m_surv += __shfl_xor_sync(0xffffffffu, m_surv, o);
+    const bool truncate = m_surv > MP;  // :58
+
+    // ordered compaction of the kept peaks into shared memory
+    uint32_t kept = 0;
+    for (uint64_t c = a; c < b; c += 32) {
+      const uint64_t j = c + lane;
+      bool keep = false;
+      double m = 0.0, v = 0.0;
+      if (j < b) {
+        m = mz[j];
+        v = inten[j];
+        keep = m >= p.min_mz && m < p.max_mz && v > 0.0 && !(v < floor_intensity);
+      }
+      if (truncate && __any_sync(0xffffffffu, keep)) {
+        // :60-64 keep the max_peaks first in (intensity desc, m/z asc) order.  rank = number of
+        // survivors that precede this peak in that order (position breaks exact duplicates).
+        uint32_t rank = 0;
+        for (uint64_t jj = a; jj < b; ++jj) {
+          const double m2 = mz[jj], v2 = inten[jj];  // warp-uniform address: broadcast load
+          const bool surv2 = m2 >= p.min_mz && m2 < p.max_mz && v2 > 0.0 && !(v2 < floor_intensity);
+          const bool before = v2 > v || (v2 == v && (m2 < m || (m2 == m && jj < j)));
+          rank += (surv2 && before);
+        }
+        keep = keep && rank < MP;
+      }
+      const uint32_t mask = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const uint32_t slot = kept + __popc(mask & ((1u << lane) - 1u));
+        s_mz[slot] = m;
+        s_int[slot] = v;
+      }
+      kept += __popc(mask);
+    }
+    __syncwarp();
+
+    if (kept < p.min_peaks || kept == 0) {  // :69 (kept == 0 cannot encode; validate() forbids min_peaks 0)
+      if (lane == 0) out_count[spec] = 0;
+      continue;
+    }
+
+    // vectorize :91-94 bin index
+    for (uint32_t s = lane; s < kept; s += 32) {
+      const double q = (s_mz[s] - p.min_mz) / p.bin_size + 1e-9;
+      double f = floor(q);
+      const double hi = static_cast<double>(p.dims - 1);
+      f = f < 0.0 ? 0.0 : (hi < f ? hi : f);  // std::clamp
+      s_bin[s] = static_cast<uint32_t>(f);
+    }
+    __syncwarp();
+
+    // :95-100 adjacent equal bins are summed left to right (sequential fp64 adds per run)
+    uint32_t nb = 0;
+    for (uint32_t c = 0; c < kept; c += 32) {
+      const uint32_t s = c + lane;
+      bool head = false;
+      uint32_t bin = 0;
+      if (s < kept) {
+        bin = s_bin[s];
+        head = s == 0 || s_bin[s - 1] != bin;
+      }
+      const uint32_t mask = __ballot_sync(0xffffffffu, head);
+      double sum = 0.0;
+      uint32_t slot = 0;
+      if (head) {
+        slot = nb + __popc(mask & ((1u << lane) - 1u));
+        sum = s_int[s];
+        for (uint32_t t = s + 1; t < kept && s_bin[t] == bin; ++t) sum += s_int[t];
+        if (p.scaling == 1) sum = sqrt(sum);  // :103-105
+      }
+      // o_val aliases s_mz: all lanes of this chunk have consumed s_mz already (bins done),
+      // and s_int (the source of the sums) is a different array.
+      __syncwarp();
+      if (head) {
+        o_val[slot] = sum;
+        out_bins[spec * MP + slot] = bin;
+      }
+      nb += __popc(mask);
+    }
+    __syncwarp();
+
+    // :107-108 divide by the maximum, then encoder.cpp:11-17
+    double top = 0.0;
+    for (uint32_t k = lane; k < nb; k += 32) top = fmax(top, o_val[k]);
+    top = warp_max(top);
+    for (uint32_t k = lane; k < nb; k += 32)
+      out_levels[spec * MP + k] = quantize_level(o_val[k] / top, p.levels);
+    if (lane == 0) out_count[spec] = nb;
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K2: encode
+// ------------------------------------------------------------------------------------------
+
+struct U4 {
+  uint32_t v[4];
+};
+
+__device__ __forceinline__ U4 ld_global_u4(const uint4* p) {
+  const uint4 t = __ldg(p);
+  return U4{{t.x, t.y, t.z, t.w}};
+}
+
+// carry-save adder on 4 independent 32-bit lanes: (a + b + c) = s + 2*k
+#define HB_CSA(s, k, a, b, c)                                                 \
+  _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_) {                          \
+    const uint32_t a_ = (a).v[i_], b_ = (b).v[i_], c_ = (c).v[i_];            \
+    (s).v[i_] = a_ ^ b_ ^ c_;                                                 \
+    (k).v[i_] = (a_ & b_) | (a_ & c_) | (b_ & c_);                            \
+  }
+
+// Encodes spectra [0, n).  The (bin, level) list of spectrum i is
+//   strided mode (sv_offsets == nullptr): sv_bins[i*stride .. +sv_count[i])
+//   CSR mode:                              sv_bins[sv_offsets[i] .. sv_offsets[i+1])
+// NP = number of vertical counter planes (counts < 2^NP).
+template <int NP>
+__global__ void __launch_bounds__(256)
+encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stride,
+              const uint32_t* __restrict__ sv_bins, const uint32_t* __restrict__ sv_levels,
+              const uint32_t* __restrict__ sv_count, const uint4* __restrict__ pos,
+              const uint4* __restrict__ lvl_global, uint32_t n_level_rows, uint32_t row_u4,
+              uint32_t dim, uint32_t W, int lvl_in_smem, int vec_store,
+              uint64_t* __restrict__ out_words,
+              uint8_t* __restrict__ out_ok) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint4* lvl = lvl_global;
+  if (lvl_in_smem) {
+    uint4* s_lvl = reinterpret_cast<uint4*>(smem_raw);
+    for (uint32_t i = threadIdx.x; i < n_level_rows * row_u4; i += blockDim.x) s_lvl[i] = lvl_global[i];
+    __syncthreads();
+    lvl = s_lvl;
+  }
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5;
+
+  for (uint64_t spec = uint64_t(blockIdx.x) * warps + warp; spec < n;
+       spec += uint64_t(gridDim.x) * warps) {
+    uint64_t start;
+    uint32_t nb;
+    if (sv_offsets) {
+      start = sv_offsets[spec];
+      nb = static_cast<uint32_t>(sv_offsets[spec + 1] - start);
+    } else {
+      start = spec * stride;
+      nb = sv_count[spec];
+    }
+    uint64_t* out_row = out_words + spec * W;
+    if (nb == 0) {  // unprocessable: zero row (pipeline.cpp:68 `continue`)
+      for (uint32_t w = lane; w < W; w += 32) out_row[w] = 0;
+      if (lane == 0 && out_ok) out_ok[spec] = 0;
+      continue;
+    }
+    const uint32_t thresh = nb / 2 + 1;  // 2*votes > n  <=>  votes >= floor(n/2)+1  (encoder.cpp:52)
+
+    for (uint32_t sb = 0; sb < row_u4; sb += 32) {
+      const uint32_t u = sb + lane;
+      const bool active = u < row_u4;
+      U4 c[NP];
+#pragma unroll
+      for (int b = 0; b < NP; ++b) c[b] = U4{{0, 0, 0, 0}};
+
+      for (uint32_t k0 = 0; k0 < nb; k0 += 7) {
+        U4 x[7];
+#pragma unroll
+        for (int j = 0; j < 7; ++j) {
+          x[j] = U4{{0, 0, 0, 0}};
+          if (k0 + j < nb && active) {
+            const uint32_t bin = sv_bins[start + k0 + j];    // warp-uniform: broadcast
+            const uint32_t lev = sv_levels[start + k0 + j];
+            const U4 pw = ld_global_u4(pos + size_t(bin) * row_u4 + u);
+            const uint4 lw4 = lvl[size_t(lev) * row_u4 + u];
+            x[j].v[0] = ~(pw.v[0] ^ lw4.x);  // encoder.cpp:41 agree = ~(pos ^ lvl)
+            x[j].v[1] = ~(pw.v[1] ^ lw4.y);
+            x[j].v[2] = ~(pw.v[2] ^ lw4.z);
+            x[j].v[3] = ~(pw.v[3] ^ lw4.w);
+          }
+        }
+        // 7:3 compressor
+        U4 s1, k1, s2, k2, ones, k3, twos, fours;
+        HB_CSA(s1, k1, x[0], x[1], x[2]);
+        HB_CSA(s2, k2, x[3], x[4], x[5]);
+        HB_CSA(ones, k3, s1, s2, x[6]);
+        HB_CSA(twos, fours, k1, k2, k3);
+        // add the 3-bit number (fours twos ones) into the vertical counters
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t carry;
+          {
+            const uint32_t a = c[0].v[i], o = ones.v[i];
+            c[0].v[i] = a ^ o;
+            carry = a & o;
+          }
+          if (NP > 1) {
+            const uint32_t a = c[1].v[i], t = twos.v[i];
+            c[1].v[i] = a ^ t ^ carry;
+            carry = (a & t) | (a & carry) | (t & carry);
+          }
+          if (NP > 2) {
+            const uint32_t a = c[2].v[i], f = fours.v[i];
+            c[2].v[i] = a ^ f ^ carry;
+            carry = (a & f) | (a & carry) | (f & carry);
+          }
+#pragma unroll
+          for (int b = 3; b < NP; ++b) {
+            const uint32_t a = c[b].v[i];
+            c[b].v[i] = a ^ carry;
+            carry = a & carry;
+          }
+        }
+      }
+
+      // votes >= thresh, plane by plane from the top
+      U4 res;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t gt = 0, eq = 0xffffffffu;
+#pragma unroll
+        for (int b = NP - 1; b >= 0; --b) {
+          const uint32_t cb = c[b].v[i];
+          if ((thresh >> b) & 1u) {
+            eq &= cb;
+          } else {
+            gt |= eq & cb;
+            eq &= ~cb;
+          }
+        }
+        uint32_t r = gt | eq;
+        // clear tail bits >= dim (Hypervector keeps them zero, hypervector.hpp:12-15); the zero
+        // padding of both codebook rows XNORs to ones and must not leak out.
+        const uint32_t bit0 = (u * 4 + i) * 32;
+        if (bit0 >= dim) r = 0;
+        else if (bit0 + 32 > dim) r &= (1u << (dim - bit0)) - 1u;
+        res.v[i] = r;
+      }
+      if (active) {
+        const uint32_t w0 = u * 2;  // first u64 word of this slab
+        const uint64_t lo = uint64_t(res.v[0]) | (uint64_t(res.v[1]) << 32);
+        const uint64_t hi = uint64_t(res.v[2]) | (uint64_t(res.v[3]) << 32);
+        if (vec_store) {
+          if (w0 < W) *reinterpret_cast<ulonglong2*>(out_row + w0) = make_ulonglong2(lo, hi);
+        } else {
+          if (w0 < W) out_row[w0] = lo;
+          if (w0 + 1 < W) out_row[w0 + 1] = hi;
+        }
+      }
+    }
+    if (lane == 0 && out_ok) out_ok[spec] = 1;
+  }
+}
+
+// quantize host-provided SpectrumVector intensities and validate (encoder.cpp:12-14, :20-25)
+__global__ void quantize_kernel(uint64_t total, const double* __restrict__ intens,
+                                const uint32_t* __restrict__ bins, uint32_t levels, uint32_t n_bins,
+                                uint32_t* __restrict__ out_levels, uint32_t* __restrict__ bad) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const double v = intens[i];
+  if (!(v >= 0.0 && v <= 1.0)) {
+    atomicOr(bad, 1u);
+    out_levels[i] = 0;
+  } else {
+    out_levels[i] = quantize_level(v, levels);
+  }
+  if (bins[i] >= n_bins) atomicOr(bad, 2u);
+}
+
+// hypervector.hpp:70-81: one warp per row pair
+__global__ void hamming_kernel(uint64_t n, uint32_t W, uint32_t dim, const uint64_t* __restrict__ a,
+                               const uint64_t* __restrict__ b, uint32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t row = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n) return;
+  uint32_t diff = 0;
+  for (uint32_t w = lane; w < W; w += 32) diff += __popcll(a[row * W + w] ^ b[row * W + w]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) diff += __shfl_xor_sync(0xffffffffu, diff, o);
+  if (lane == 0) out[row] = dim - diff;
+}
+
+// ------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------
+
+static int fill_pre_params(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg,
+                           uint32_t levels, PreParams* p) {
+  HB_REQUIRE(ctx, cfg != nullptr, HOMS_B200_ERR_ARGUMENT, "preprocess config is null");
+  HB_REQUIRE(ctx, cfg->max_peaks >= 1, HOMS_B200_ERR_CONFIG, "preprocess: max_peaks must be at least 1");
+  HB_REQUIRE(ctx, cfg->bin_size > 0.0 && cfg->min_mz < cfg->max_mz, HOMS_B200_ERR_CONFIG,
+             "preprocess: need bin_size > 0 and min_mz < max_mz");
+  p->min_mz = cfg->min_mz;
+  p->max_mz = cfg->max_mz;
+  p->bin_size = cfg->bin_size;
+  p->intensity_floor = cfg->intensity_floor;
+  p->max_peaks = cfg->max_peaks;
+  p->min_peaks = cfg->min_peaks;
+  p->scaling = cfg->scaling;
+  p->dims = homs_b200_dimension(cfg);
+  p->levels = levels;
+  return HOMS_B200_OK;
+}
+
+static int launch_preprocess(homs_b200_ctx* ctx, const PreParams& p, uint64_t n,
+                             const uint64_t* d_off, const double* d_mz, const double* d_int,
+                             uint32_t* d_bins, uint32_t* d_lev, uint32_t* d_count) {
+  if (n == 0) return HOMS_B200_OK;
+  const size_t per_warp = size_t(p.max_peaks) * 20;
+  const size_t budget = 200 * 1024;
+  int warps = static_cast<int>(std::min<size_t>(8, budget / per_warp));
+  HB_REQUIRE(ctx, warps >= 1, HOMS_B200_ERR_ARGUMENT,
+             "preprocess: max_peaks above 10240 is not supported by the device path");
+  const size_t smem = per_warp * warps;
+  HB_CUDA(ctx, cudaFuncSetAttribute(preprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+  const uint64_t want = (n + warps - 1) / warps;
+  const int grid = static_cast<int>(std::min<uint64_t>(want, uint64_t(ctx->sm_count) * 16));
+  preprocess_kernel<<<grid, warps * 32, smem, ctx->stream>>>(p, n, d_off, d_mz, d_int, d_bins,
+                                                             d_lev, d_count, warps);
+  HB_LAUNCHED(ctx);
+  return HOMS_B200_OK;
+}
+
+static int launch_encode(homs_b200_ctx* ctx, uint64_t n, const uint64_t* d_sv_off, uint32_t stride,
+                         const uint32_t* d_bins, const uint32_t* d_lev, const uint32_t* d_count,
+                         uint32_t max_count, uint64_t* d_out, uint8_t* d_ok) {
+  if (n == 0) return HOMS_B200_OK;
+  const Codebook& cb = ctx->cb;
+  const uint32_t row_u4 = cb.S / 2;
+  const size_t lvl_bytes = size_t(cb.levels + 1) * cb.S * 8;
+  const int lvl_in_smem = lvl_bytes <= 96 * 1024;
+  const size_t smem = lvl_in_smem ? lvl_bytes : 0;
+  const int warps = 8;
+  const uint64_t want = (n + warps - 1) / warps;
+  const int grid = static_cast<int>(std::min<uint64_t>(want, uint64_t(ctx->sm_count) * 8));
+  // 128-bit stores need an even word count and a 16-byte aligned destination
+  const int vec_store = (cb.W % 2 == 0) && (reinterpret_cast<uintptr_t>(d_out) % 16 == 0);
+  HB_REQUIRE(ctx, max_count <= 65535, HOMS_B200_ERR_ARGUMENT,
+             "encode: more than 65535 bins per spectrum is not supported by the device path");
+#define HB_ENC_LAUNCH(NP)                                                                        \
+  do {                                                                                           \
+    HB_CUDA(ctx, cudaFuncSetAttribute(encode_kernel<NP>,                                         \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,               \
+                                      static_cast<int>(smem)));                                  \
+    encode_kernel<NP><<<grid, warps * 32, smem, ctx->stream>>>(                                  \
+        n, d_sv_off, stride, d_bins, d_lev, d_count, cb.d_pos.as<uint4>(), cb.d_lvl.as<uint4>(), \
+        cb.levels + 1, row_u4, cb.dim, cb.W, lvl_in_smem, vec_store, d_out, d_ok);                          \
+  } while (0)
+  if (max_count <= 255) HB_ENC_LAUNCH(8);
+  else HB_ENC_LAUNCH(16);
+#undef HB_ENC_LAUNCH
+  HB_LAUNCHED(ctx);
+  return HOMS_B200_OK;
+}
+
+static int encode_dev_locked(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint64_t n,
+                             const uint64_t* d_off, const double* d_mz, const double* d_int,
+                             uint64_t* d_out, uint8_t* d_ok) {
+  HB_REQUIRE(ctx, ctx->cb.ready, HOMS_B200_ERR_STATE, "encode: no codebook uploaded");
+  PreParams p;
+  HB_TRY(fill_pre_params(ctx, cfg, ctx->cb.levels, &p));
+  // encoder.cpp:20-22: the spectrum vector's dims must equal the codebook's spectrum_dims
+  HB_REQUIRE(ctx, p.dims == ctx->cb.n_bins, HOMS_B200_ERR_INVARIANT,
+             "encode: spectrum vector dims do not match codebook");
+  if (n == 0) return HOMS_B200_OK;
+  const size_t sv = size_t(n) * p.max_peaks * 4;
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvBins], sv));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvLev], sv));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvCount], size_t(n) * 4));
+  uint32_t* d_bins = ctx->scratch[kScrSvBins].as<uint32_t>();
+  uint32_t* d_lev = ctx->scratch[kScrSvLev].as<uint32_t>();
+  uint32_t* d_cnt = ctx->scratch[kScrSvCount].as<uint32_t>();
+  HB_TRY(launch_preprocess(ctx, p, n, d_off, d_mz, d_int, d_bins, d_lev, d_cnt));
+  HB_TRY(launch_encode(ctx, n, nullptr, p.max_peaks, d_bins, d_lev, d_cnt, p.max_peaks, d_out, d_ok));
+  return HOMS_B200_OK;
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" {
+
+int homs_b200_codebook_upload(homs_b200_ctx* ctx, uint32_t dim, uint32_t n_bins, uint32_t levels,
+                              const uint64_t* pos, const uint64_t* lvl) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_REQUIRE(ctx, pos && lvl, HOMS_B200_ERR_ARGUMENT, "codebook_upload: null codebook");
+  HB_REQUIRE(ctx, dim >= 1 && n_bins >= 1 && levels >= 1, HOMS_B200_ERR_ARGUMENT,
+             "codebook_upload: dim, n_bins and levels must be positive");
+  Codebook& cb = ctx->cb;
+  cb.ready = false;
+  cb.dim = dim;
+  cb.n_bins = n_bins;
+  cb.levels = levels;
+  cb.W = words_for(dim);
+  cb.S = stride_for(dim);
+  HB_TRY(ensure(ctx, cb.d_pos, size_t(n_bins) * cb.S * 8));
+  HB_TRY(ensure(ctx, cb.d_lvl, size_t(levels + 1) * cb.S * 8));
+  HB_TRY(upload_rows(ctx, cb.d_pos.as<uint64_t>(), pos, n_bins, cb.W, cb.S));
+  HB_TRY(upload_rows(ctx, cb.d_lvl.as<uint64_t>(), lvl, levels + 1, cb.W, cb.S));
+  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  cb.ready = true;
+  return HOMS_B200_OK;
+}
+
+int homs_b200_encode_batch_dev(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg,
+                               uint64_t n, uint64_t n_peaks_total, const uint64_t* d_offsets,
+                               const double* d_mz, const double* d_intensity,
+                               uint64_t* d_out_words, uint8_t* d_out_ok) {
+  (void)n_peaks_total;
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_REQUIRE(ctx, n == 0 || (d_offsets && d_out_words), HOMS_B200_ERR_ARGUMENT,
+             "encode_batch_dev: null argument");
+  return encode_dev_locked(ctx, cfg, n, d_offsets, d_mz, d_intensity, d_out_words, d_out_ok);
+}
+
+int homs_b200_encode_batch(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint64_t n,
+                           const uint64_t* offsets, const double* mz, const double* intensity,
+                           uint64_t* out_words, uint8_t* out_ok) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_REQUIRE(ctx, ctx->cb.ready, HOMS_B200_ERR_STATE, "encode: no codebook uploaded");
+  if (n == 0) {
+    PreParams p;
+    HB_TRY(fill_pre_params(ctx, cfg, ctx->cb.levels, &p));
+    HB_REQUIRE(ctx, p.dims == ctx->cb.n_bins, HOMS_B200_ERR_INVARIANT,
+               "encode: spectrum vector dims do not match codebook");
+    return HOMS_B200_OK;
+  }
+  HB_REQUIRE(ctx, offsets && out_words && out_ok, HOMS_B200_ERR_ARGUMENT, "encode_batch: null argument");
+  const uint64_t total = offsets[n] - offsets[0];
+  HB_REQUIRE(ctx, total == 0 || (mz && intensity), HOMS_B200_ERR_ARGUMENT, "encode_batch: null peaks");
+  HB_REQUIRE(ctx, offsets[0] == 0, HOMS_B200_ERR_ARGUMENT, "encode_batch: offsets[0] must be 0");
+  const uint32_t W = ctx->cb.W;
+  HB_TRY(ensure(ctx, ctx->scratch[kScrOffsets], (n + 1) * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrMz], total * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrInt], total * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrEncOut], n * W * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrEncOk], n));
+  auto* d_off = ctx->scratch[kScrOffsets].as<uint64_t>();
+  auto* d_mz = ctx->scratch[kScrMz].as<double>();
+  auto* d_int = ctx->scratch[kScrInt].as<double>();
+  auto* d_out = ctx->scratch[kScrEncOut].as<uint64_t>();
+  auto* d_ok = ctx->scratch[kScrEncOk].as<uint8_t>();
+  HB_CUDA(ctx, cudaMemcpyAsync(d_off, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (total) {
+    HB_CUDA(ctx, cudaMemcpyAsync(d_mz, mz, total * 8, cudaMemcpyHostToDevice, ctx->stream));
+    HB_CUDA(ctx, cudaMemcpyAsync(d_int, intensity, total * 8, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  HB_TRY(encode_dev_locked(ctx, cfg, n, d_off, d_mz, d_int, d_out, d_ok));
+  HB_CUDA(ctx, cudaMemcpyAsync(out_words, d_out, n * W * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(ctx, cudaMemcpyAsync(out_ok, d_ok, n, cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return HOMS_B200_OK;
+}
+
+int homs_b200_preprocess_batch(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg,
+                               uint32_t levels, uint64_t n, const uint64_t* offsets,
+                               const double* mz, const double* intensity, uint32_t* out_bins,
+                               uint32_t* out_levels, uint32_t* out_count) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  PreParams p;
+  HB_TRY(fill_pre_params(ctx, cfg, levels, &p));
+  if (n == 0) return HOMS_B200_OK;
+  HB_REQUIRE(ctx, offsets && out_bins && out_levels && out_count, HOMS_B200_ERR_ARGUMENT,
+             "preprocess_batch: null argument");
+  const uint64_t total = offsets[n];
+  const size_t sv = size_t(n) * p.max_peaks * 4;
+  HB_TRY(ensure(ctx, ctx->scratch[kScrOffsets], (n + 1) * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrMz], total * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrInt], total * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvBins], sv));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvLev], sv));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvCount], size_t(n) * 4));
+  auto* d_off = ctx->scratch[kScrOffsets].as<uint64_t>();
+  auto* d_mz = ctx->scratch[kScrMz].as<double>();
+  auto* d_int = ctx->scratch[kScrInt].as<double>();
+  auto* d_bins = ctx->scratch[kScrSvBins].as<uint32_t>();
+  auto* d_lev = ctx->scratch[kScrSvLev].as<uint32_t>();
+  auto* d_cnt = ctx->scratch[kScrSvCount].as<uint32_t>();
+  HB_CUDA(ctx, cudaMemcpyAsync(d_off, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (total) {
+    HB_CUDA(ctx, cudaMemcpyAsync(d_mz, mz, total * 8, cudaMemcpyHostToDevice, ctx->stream));
+    HB_CUDA(ctx, cudaMemcpyAsync(d_int, intensity, total * 8, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  HB_CUDA(ctx, cudaMemsetAsync(d_bins, 0, sv, ctx->stream));
+  HB_CUDA(ctx, cudaMemsetAsync(d_lev, 0, sv, ctx->stream));
+  HB_TRY(launch_preprocess(ctx, p, n, d_off, d_mz, d_int, d_bins, d_lev, d_cnt));
+  HB_CUDA(ctx, cudaMemcpyAsync(out_bins, d_bins, sv, cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(ctx, cudaMemcpyAsync(out_levels, d_lev, sv, cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(ctx, cudaMemcpyAsync(out_count, d_cnt, size_t(n) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return HOMS_B200_OK;
+}
+
+int homs_b200_encode_vectors(homs_b200_ctx* ctx, uint64_t n, const uint64_t* sv_offsets,
+                             const uint32_t* bins, const double* intensities,
+                             uint64_t* out_words) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_REQUIRE(ctx, ctx->cb.ready, HOMS_B200_ERR_STATE, "encode: no codebook uploaded");
+  if (n == 0) return HOMS_B200_OK;
+  HB_REQUIRE(ctx, sv_offsets && bins && intensities && out_words, HOMS_B200_ERR_ARGUMENT,
+             "encode_vectors: null argument");
+  uint32_t max_count = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t c = sv_offsets[i + 1] - sv_offsets[i];
+    HB_REQUIRE(ctx, c >= 1, HOMS_B200_ERR_INVARIANT, "encode: empty spectrum vector");  // encoder.cpp:23-25
+    HB_REQUIRE(ctx, c <= 65535, HOMS_B200_ERR_ARGUMENT, "encode: more than 65535 bins per spectrum");
+    max_count = std::max<uint32_t>(max_count, static_cast<uint32_t>(c));
+  }
+  const uint64_t total = sv_offsets[n];
+  const uint32_t W = ctx->cb.W;
+  HB_TRY(ensure(ctx, ctx->scratch[kScrOffsets], (n + 1) * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrInt], total * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvBins], total * 4));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvLev], total * 4));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrEncOut], n * W * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrMisc], 16));
+  auto* d_off = ctx->scratch[kScrOffsets].as<uint64_t>();
+  auto* d_int = ctx->scratch[kScrInt].as<double>();
+  auto* d_bins = ctx->scratch[kScrSvBins].as<uint32_t>();
+  auto* d_lev = ctx->scratch[kScrSvLev].as<uint32_t>();
+  auto* d_out = ctx->scratch[kScrEncOut].as<uint64_t>();
+  auto* d_bad = ctx->scratch[kScrMisc].as<uint32_t>();
+  HB_CUDA(ctx, cudaMemcpyAsync(d_off, sv_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  HB_CUDA(ctx, cudaMemcpyAsync(d_int, intensities, total * 8, cudaMemcpyHostToDevice, ctx->stream));
+  HB_CUDA(ctx, cudaMemcpyAsync(d_bins, bins, total * 4, cudaMemcpyHostToDevice, ctx->stream));
+  HB_CUDA(ctx, cudaMemsetAsync(d_bad, 0, 4, ctx->stream));
+  quantize_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, ctx->stream>>>(
+      total, d_int, d_bins, ctx->cb.levels, ctx->cb.n_bins, d_lev, d_bad);
+  HB_LAUNCHED(ctx);
+  uint32_t bad = 0;
+  HB_CUDA(ctx, cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  HB_REQUIRE(ctx, !(bad & 1u), HOMS_B200_ERR_INVARIANT, "quantize_intensity: intensity outside [0, 1]");
+  HB_REQUIRE(ctx, !(bad & 2u), HOMS_B200_ERR_INVARIANT, "encode: spectrum vector dims do not match codebook");
+  HB_TRY(launch_encode(ctx, n, d_off, 0, d_bins, d_lev, nullptr, max_count, d_out, nullptr));
+  HB_CUDA(ctx, cudaMemcpyAsync(out_words, d_out, n * W * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return HOMS_B200_OK;
+}
+
+int homs_b200_hamming_similarity(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* a,
+                                 const uint64_t* b, uint32_t* out) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  if (n == 0) return HOMS_B200_OK;
+  HB_REQUIRE(ctx, a && b && out, HOMS_B200_ERR_ARGUMENT, "hamming_similarity: null argument");
+  const uint32_t W = words_for(dim);
+  HB_TRY(ensure(ctx, ctx->scratch[kScrEncOut], n * W * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrMz], n * W * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvCount], n * 4));
+  auto* d_a = ctx->scratch[kScrEncOut].as<uint64_t>();
+  auto* d_b = ctx->scratch[kScrMz].as<uint64_t>();
+  auto* d_o = ctx->scratch[kScrSvCount].as<uint32_t>();
+  HB_CUDA(ctx, cudaMemcpyAsync(d_a, a, n * W * 8, cudaMemcpyHostToDevice, ctx->stream));
+  HB_CUDA(ctx, cudaMemcpyAsync(d_b, b, n * W * 8, cudaMemcpyHostToDevice, ctx->stream));
+  const uint64_t threads = n * 32;
+  hamming_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, ctx->stream>>>(n, W, dim, d_a,
+                                                                                       d_b, d_o);
+  HB_LAUNCHED(ctx);
+  HB_CUDA(ctx, cudaMemcpyAsync(out, d_o, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return HOMS_B200_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+"""Helpers shared by the test modules (golden loading, config conversion, random inputs)."""
+import json
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def fingerprints():
+    with open(os.path.join(GOLDEN, "fingerprints.json")) as f:
+        return json.load(f)
+
+
+def _nested(npz):
+    out = {}
+    for key in npz.files:
+        parts = key.split("/")
+        d = out
+        for p in parts[:-1]:
+            d = d.setdefault(p, {})
+        d[parts[-1]] = npz[key]
+    return out
+
+
+def encode_cases():
+    return _nested(np.load(os.path.join(GOLDEN, "encode_cases.npz")))
+
+
+def search_cases():
+    return _nested(np.load(os.path.join(GOLDEN, "search_cases.npz")))
+
+
+def oracle_precfg(v):
+    from oracle.binding import PreCfg
+    return PreCfg(float(v[0]), float(v[1]), float(v[2]), int(v[3]), int(v[4]), float(v[5]), int(v[6]))
+
+
+def product_precfg(v):
+    import paper_2211_16422_b200 as hb
+    return hb.PreprocessConfig(float(v[0]), float(v[1]), float(v[2]), int(v[3]), int(v[4]),
+                               float(v[5]), int(v[6]))
+
+
+def csr(spectra):
+    offsets = np.zeros(len(spectra) + 1, np.uint64)
+    if spectra:
+        offsets[1:] = np.cumsum([len(s[0]) for s in spectra])
+    mz = np.concatenate([np.asarray(s[0], np.float64) for s in spectra] + [np.zeros(0)])
+    it = np.concatenate([np.asarray(s[1], np.float64) for s in spectra] + [np.zeros(0)])
+    return offsets, mz, it
+
+
+def random_hvs(rng, n, dim):
+    W = (dim + 63) // 64
+    w = rng.integers(0, 2**64, (n, W), dtype=np.uint64)
+    if dim % 64:
+        w[:, -1] &= np.uint64((1 << (dim % 64)) - 1)
+    return w
+
+
+TOLS = {"ppm150": ("ppm", 150.0), "da30": ("da", 30.0), "da500": ("da", 500.0), "da1": ("da", 1.0),
+        "ppm20": ("ppm", 20.0)}
+
+
+def product_tol(t):
+    import paper_2211_16422_b200 as hb
+    return hb.Tolerance("ppm" if t[0] == "ppm" else "dalton", t[1])

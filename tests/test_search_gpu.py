@@ -1,0 +1,218 @@
+"""GPU: index build, candidate windows, windowed Hamming top-k, sharded merge and the cascade,
+bit for bit against the oracle and the golden fixtures, through the C ABI."""
+import numpy as np
+import pytest
+
+from oracle.binding import PreCfg, SynthCfg, fnv1a64_words
+from tests import _util as U
+
+pytestmark = pytest.mark.gpu
+
+
+def _index(ctx, c):
+    dim = int(c["dim"][0])
+    ids = [x.decode() for x in c["ids"]]
+    ctx.build_index(dim, c["words"], c["mz"], c["charge"], ids=ids, is_decoy=c["decoy"])
+    return dim, ids
+
+
+def test_golden_search_cases(hb, ctx):
+    for name, c in U.search_cases().items():
+        dim, ids = _index(ctx, c)
+        for bi, b in enumerate(ctx.buckets()):  # build_index order, search.cpp:37-46
+            assert b["charge"] == int(c[f"bucket{bi}"]["charge"][0])
+            assert np.array_equal(b["ordinal"], c[f"bucket{bi}"]["ordinal"]), name
+            assert np.array_equal(b["words"], c["words"][b["ordinal"]]), name
+            assert np.array_equal(b["precursor_mz"], c["mz"][b["ordinal"]]), name
+        for tname, tol in U.TOLS.items():
+            g = c[tname]
+            first, last, has_b = ctx.select_candidates(c["q_mz"], c["q_charge"], U.product_tol(tol))
+            nonempty = g["last"] > g["first"]
+            assert np.array_equal(last - first, g["last"] - g["first"]), (name, tname)
+            assert np.array_equal(first[nonempty], g["first"][nonempty]), (name, tname)
+            assert np.array_equal(has_b, g["has_bucket"])
+            m = ctx.search_batch(c["q_words"], c["q_mz"], c["q_charge"], U.product_tol(tol))
+            assert np.array_equal(m.has_hit[:, 0], g["has"].astype(bool)), (name, tname)
+            assert np.array_equal(m.raw_score[:, 0], g["score"]), (name, tname)
+            assert np.array_equal(m.ordinal[:, 0], g["ordinal"]), (name, tname)
+        for cname, narrow, wide, fq in (("c1", ("ppm", 150.0), ("da", 30.0), 0.05),
+                                        ("c2", ("da", 0.3), ("da", 500.0), 0.5)):
+            got = ctx.cascade_search(c["q_words"], c["q_mz"], c["q_charge"], U.product_tol(narrow),
+                                     U.product_tol(wide), fq)
+            for k in got:
+                assert np.array_equal(got[k], c[cname][k]), (name, cname, k)
+
+
+def test_reference_known_answers(hb, ctx):
+    """test_search.cpp:116-171 windows, :205-243 tie-breaks, :173-203 self / empty / mismatch."""
+    rng = np.random.default_rng(5)
+    ctx.build_index(256, U.random_hvs(rng, 5, 256), [999.9799, 999.98, 1000.0, 1000.02, 1000.0201], [2] * 5)
+    f, l, has = ctx.select_candidates([1000.0], [2], hb.Tolerance("ppm", 20.0))
+    assert (f[0], l[0]) == (1, 4)
+    f, l, has = ctx.select_candidates([1000.0], [2], hb.Tolerance("dalton", 500.0))
+    assert l[0] - f[0] == 5
+    f, l, has = ctx.select_candidates([1000.0, 1000.0], [5, 0], hb.Tolerance("ppm", 20.0))
+    assert not has.any() and (l == f).all()
+    ctx.build_index(256, U.random_hvs(rng, 4, 256), [499.99, 500.0, 1500.0, 1500.01], [2] * 4)
+    f, l, _ = ctx.select_candidates([1000.0], [2], hb.Tolerance("dalton", 500.0))
+    assert (f[0], l[0]) == (1, 3)
+
+    shared = U.random_hvs(rng, 1, 256)
+    two = np.repeat(shared, 2, 0)
+    da1 = hb.Tolerance("dalton", 1.0)
+    ctx.build_index(256, two, [1000.30, 1000.10], [2, 2], ids=["far", "near"])
+    assert ctx.search_batch(shared, [1000.0], [2], da1).ordinal[0, 0] == 1
+    ctx.build_index(256, two, [999.75, 1000.25], [2, 2], ids=["zz", "aa"])
+    assert ctx.search_batch(shared, [1000.0], [2], da1).ordinal[0, 0] == 1
+    ctx.build_index(256, two, [1000.0, 1000.0], [2, 2], ids=["dup", "dup"])
+    assert ctx.search_batch(shared, [1000.0], [2], da1).ordinal[0, 0] == 0
+
+    refs = U.random_hvs(rng, 50, 256)
+    mz = rng.uniform(400, 1200, 50)
+    ch = rng.integers(2, 4, 50).astype(np.uint8)
+    ctx.build_index(256, refs, mz, ch)
+    m = ctx.search_batch(refs[17:18], mz[17:18], ch[17:18], hb.Tolerance("ppm", 20.0))
+    assert m.ordinal[0, 0] == 17 and m.raw_score[0, 0] == 256
+    m = ctx.search_batch(refs[:1], [2000.0], [2], hb.Tolerance("ppm", 20.0))
+    assert not m.has_hit[0, 0] and m.raw_score[0, 0] == 0
+    with pytest.raises(hb.InvariantError):  # search.cpp:107-109
+        ctx.search_batch(U.random_hvs(rng, 1, 128), [800.0], [2], hb.Tolerance("ppm", 20.0), query_dim=128)
+    with pytest.raises(hb.InvariantError):  # search.cpp:18
+        ctx.build_index(256, np.zeros((0, 4), np.uint64), [], [])
+    with pytest.raises(hb.ConfigError):  # search.cpp:13-15 through cascade :223-224
+        ctx.cascade_search(refs[:1], [800.0], [2], hb.Tolerance("ppm", 0.0), hb.Tolerance("dalton", 5.0), 0.01)
+    assert ctx.search_batch(np.zeros((0, 4), np.uint64), [], [], da1).ordinal.shape == (0, 1)
+
+
+def test_config1_search_and_cascade(hb, ctx, best_oracle):
+    """BASELINE config 1 end to end on the device: synth -> encode -> index -> open / narrow
+    search -> cascade; compared with the golden fingerprints and with the live oracle."""
+    fp = U.fingerprints()["config1"]
+    s = best_oracle.synth(SynthCfg(n_library=5000, n_query=1000, fraction_modified=0.6, seed=1))
+    L, Q = s["library"], s["queries"]
+    pre = hb.PreprocessConfig()
+    ctx.upload_codebook(hb.make_codebook(hb.dimension(pre), hb.EncoderConfig(2048, 1024, 16, 1)))
+    lw, _ = ctx.encode_batch(L["offsets"], L["mz"], L["intensity"], pre)
+    qw, _ = ctx.encode_batch(Q["offsets"], Q["mz"], Q["intensity"], pre)
+    ctx.build_index(2048, lw, L["precursor_mz"], L["charge"], ids=L["ids"], is_decoy=L["is_decoy"])
+    m = ctx.search_batch(qw, Q["precursor_mz"], Q["charge"], hb.Tolerance("dalton", 500.0))
+    assert int((m.last - m.first).sum()) == fp["open_candidates_total"]
+    assert int(m.has_hit.sum()) == fp["open_hits"]
+    assert f"{fnv1a64_words(m.raw_score[:, 0].astype(np.uint64)):016x}" == fp["open_score_fnv"]
+    assert f"{fnv1a64_words(m.ordinal[:, 0].astype(np.uint64)):016x}" == fp["open_ordinal_fnv"]
+    n = ctx.search_batch(qw, Q["precursor_mz"], Q["charge"], hb.Tolerance("ppm", 20.0))
+    assert int(n.has_hit.sum()) == fp["narrow_hits"]
+    assert f"{fnv1a64_words(n.ordinal[:, 0].astype(np.uint64)):016x}" == fp["narrow_ordinal_fnv"]
+    c = ctx.cascade_search(qw, Q["precursor_mz"], Q["charge"], hb.Tolerance("ppm", 20.0),
+                           hb.Tolerance("dalton", 500.0), 0.01)
+    assert (len(c["query"]), int((c["stage"] == 0).sum()), int((c["stage"] == 1).sum())) == (1000, 385, 615)
+    assert f"{fnv1a64_words(c['ordinal'].astype(np.uint64)):016x}" == fp["cascade_ordinal_fnv"]
+    assert f"{fnv1a64_words(c['q_value'].view(np.uint64)):016x}" == fp["cascade_qvalue_fnv"]
+
+
+@pytest.mark.parametrize("dim", [64, 1024, 2048, 4096, 8192, 16384, 32768])
+def test_random_library_vs_oracle(hb, ctx, best_oracle, dim):
+    """Dimension sweep (BASELINE config 5 shapes, small n): random hypervectors, both tolerance
+    kinds, clones for ties; top-1 vs the oracle's search_batch."""
+    rng = np.random.default_rng(dim)
+    n, nq = 3000, 300
+    words = U.random_hvs(rng, n, dim)
+    words[n - 200:] = words[:200]  # clones -> exact score ties resolved by |diff| / id
+    mz = np.round(rng.uniform(400.0, 1200.0, n), 3)
+    charge = rng.integers(1, 4, n).astype(np.uint8)
+    ids = [f"e{rng.integers(0, 500)}" for _ in range(n)]  # many duplicate ids
+    qw = U.random_hvs(rng, nq, dim)
+    qw[:100] = words[rng.integers(0, n, 100)]
+    qmz = np.round(rng.uniform(380.0, 1220.0, nq), 3)
+    qch = rng.integers(0, 5, nq).astype(np.uint8)
+    ctx.build_index(dim, words, mz, charge, ids=ids)
+    oix = best_oracle.build_index(dim, words, mz, charge, None, ids)
+    for tol in (("da", 500.0), ("ppm", 2000.0), ("da", 0.0005)):
+        m = ctx.search_batch(qw, qmz, qch, U.product_tol(tol))
+        has, score, ordinal, _ = oix.search_batch(qw, qmz, qch, tol, threads=8)
+        assert np.array_equal(m.has_hit[:, 0], has.astype(bool)), tol
+        assert np.array_equal(m.raw_score[:, 0], score), tol
+        assert np.array_equal(m.ordinal[:, 0], ordinal), tol
+    oix.close()
+
+
+def test_topk_vs_port(hb, ctx, port):
+    """k > 1 (north-star top-k): equals a full sort of the window on the reference key."""
+    rng = np.random.default_rng(17)
+    dim, n, nq = 512, 1500, 120
+    words = U.random_hvs(rng, n, dim)
+    words[1000:] = words[:500]
+    mz = np.round(rng.uniform(500.0, 600.0, n), 2)
+    charge = rng.integers(2, 4, n).astype(np.uint8)
+    ids = [f"id{rng.integers(0, 300)}" for _ in range(n)]
+    qw = words[rng.integers(0, n, nq)]
+    qmz = np.round(rng.uniform(495.0, 605.0, nq), 2)
+    qch = rng.integers(2, 4, nq).astype(np.uint8)
+    ctx.build_index(dim, words, mz, charge, ids=ids)
+    oix = port.build_index(dim, words, mz, charge, None, ids)
+    for tol, k in ((("da", 500.0), 5), (("da", 0.05), 8), (("ppm", 50.0), 3), (("da", 2.0), 1)):
+        m = ctx.search_batch(qw, qmz, qch, U.product_tol(tol), k=k)
+        score, ordinal = oix.search_topk(qw, qmz, qch, tol, k)
+        assert np.array_equal(m.ordinal, ordinal), (tol, k)
+        assert np.array_equal(m.raw_score, score), (tol, k)
+
+
+def test_sharded_search_merges_to_single(hb):
+    """Multi-GPU path on one device: G contexts each hold slice g of every bucket; per-shard
+    candidates -> concatenate (what the all-gather yields) -> merge == unsharded result."""
+    import torch
+    rng = np.random.default_rng(23)
+    dim, n, nq, k = 1024, 4000, 200, 3
+    words = U.random_hvs(rng, n, dim)
+    words[3500:] = words[:500]
+    mz = np.round(rng.uniform(400.0, 1200.0, n), 2)
+    charge = rng.integers(2, 5, n).astype(np.uint8)
+    ids = [f"x{rng.integers(0, 900)}" for _ in range(n)]
+    qw = words[rng.integers(0, n, nq)]
+    qmz = mz[rng.integers(0, n, nq)] + rng.choice([0.0, 0.01, 40.0], nq)
+    qch = rng.integers(2, 5, nq).astype(np.uint8)
+    with hb.Context(0) as single:
+        single.build_index(dim, words, mz, charge, ids=ids)
+        for tol in (hb.Tolerance("dalton", 500.0), hb.Tolerance("ppm", 30.0)):
+            want = single.search_batch(qw, qmz, qch, tol, k=k)
+            for G in (2, 3, 8):
+                gathered = torch.zeros(G, nq * k * 16, dtype=torch.uint8, device="cuda")
+                shards = [hb.Context(0) for _ in range(G)]
+                covered = 0
+                for g, c in enumerate(shards):
+                    c.build_index(dim, words, mz, charge, ids=ids, shard_index=g, shard_count=G)
+                    covered += sum(b["shard_end"] - b["shard_begin"] for b in c.buckets())
+                    c.queries_upload(dim, qw, qmz, qch)
+                    c.search_resident_dev(tol, k, gathered[g].data_ptr())
+                    c.synchronize()
+                assert covered == n  # the slices partition the library
+                out = torch.zeros(nq * k * 16, dtype=torch.uint8, device="cuda")
+                shards[0].merge_candidates_dev(nq, k, G, gathered.data_ptr(), out.data_ptr())
+                score, ordinal = shards[0].candidates_decode(nq, k, out.data_ptr())
+                for c in shards:
+                    c.close()
+                assert np.array_equal(ordinal, want.ordinal), (tol, G)
+                assert np.array_equal(score, want.raw_score), (tol, G)
+
+
+def test_large_open_search_properties(hb, ctx):
+    """Size-independent properties at a larger scale (D = 8192, 60k rows, many work items):
+    self-search returns the entry itself with score D, and widening the tolerance never lowers
+    the best score (test_search.cpp:280-296)."""
+    rng = np.random.default_rng(31)
+    dim, n, nq = 8192, 60000, 512
+    words = U.random_hvs(rng, n, dim)
+    mz = rng.uniform(400.0, 1200.0, n)
+    charge = rng.integers(2, 4, n).astype(np.uint8)
+    ctx.build_index(dim, words, mz, charge)
+    pick = rng.integers(0, n, nq)
+    m = ctx.search_batch(words[pick], mz[pick], charge[pick], hb.Tolerance("dalton", 500.0))
+    assert (m.raw_score[:, 0] == dim).all()
+    # the entry itself or an exact duplicate position cannot exist in a random library
+    assert np.array_equal(m.ordinal[:, 0], pick.astype(np.uint32))
+    qw = U.random_hvs(rng, nq, dim)
+    prev = np.zeros(nq, np.uint32)
+    for da in (1.0, 5.0, 25.0, 125.0, 700.0):
+        s = ctx.search_batch(qw, mz[pick], charge[pick], hb.Tolerance("dalton", da)).raw_score[:, 0]
+        assert (s >= prev).all()
+        prev = s
