@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Headline benchmark: open-modification (±500 Da) spectral-library search throughput.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+One "step" = one pass of the hot path (window bounds -> windowed Hamming top-1) over the whole
+query batch of the workload (default: BASELINE.json configs[1], iPRG2012-shaped: 16k queries x
+1.2M library, D = 8192, on one B200; with --gpus N the library is sharded by contiguous m/z
+slices across N ranks and per-shard candidates are all-gathered and merged).  Prints ONE JSON
+line (see the task contract): `value` is device-timed with inputs resident in HBM, `e2e` goes
+through the public host-buffer call, `roofline` is the search kernel against the measured HBM
+peak, `cpu_baseline` is the compiled reference timed on this box's cores on a bounded sample.
+
+--impl reference times the unmodified reference (oracle/_ref) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "query spectra/sec (open search, device-timed)"
+UNIT = "queries/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        busy = [x for x in sm if x > 0.5 * max(mx, default=1)] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_workload(name: str):
+    from paper_2211_16422_b200 import workload as wl
+    n_targets, n_query, dim, peaks, seed = wl.WORKLOADS[name]
+    t = time.time()
+    lib = wl.synth_library(n_targets, peaks, 1.0, seed)
+    qry = wl.synth_queries(lib, n_query, seed=seed)
+    log(f"[bench] workload {name}: {len(lib['precursor_mz'])} library / {n_query} query spectra "
+        f"generated in {time.time() - t:.1f}s")
+    return lib, qry, dim
+
+
+# --------------------------------------------------------------------------------------------
+# reference arm
+# --------------------------------------------------------------------------------------------
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import binding as ob
+    kind = "ref" if ob.available("ref") else "port"
+    oracle = ob.Oracle(kind)
+    cores = os.cpu_count() or 1
+    lib, qry, dim = make_workload(args.workload)
+    pre = ob.PreCfg()
+    t = time.time()
+    cb = oracle.make_codebook(dim, dim // 2, 16, 1, oracle.dimension(pre))
+    lw, lok = oracle.encode_spectra(cb, pre, lib["offsets"], lib["mz"], lib["intensity"], threads=cores, batch=64)
+    qw, qok = oracle.encode_spectra(cb, pre, qry["offsets"], qry["mz"], qry["intensity"], threads=cores, batch=64)
+    log(f"[bench/reference] encoded library+queries on {cores} threads in {time.time() - t:.1f}s")
+    ix = oracle.build_index(dim, lw, lib["precursor_mz"], lib["charge"], lib["is_decoy"], lib["ids"])
+    tol = ("da", 500.0)
+    nq = len(qry["precursor_mz"])
+
+    def run(n):
+        t0 = time.perf_counter()
+        ix.search_batch(qw[:n], qry["precursor_mz"][:n], qry["charge"][:n], tol, threads=cores, batch=8)
+        return time.perf_counter() - t0
+
+    probe = min(nq, 2 * cores)
+    t_probe = run(probe)
+    budget = 150.0 / max(1, args.steps + args.warmup)  # whole run within a few minutes
+    sample = int(max(cores, min(nq, probe * min(budget, 10.0) / max(t_probe, 1e-6))))
+    for _ in range(args.warmup):
+        run(sample)
+    times = [run(sample) for _ in range(args.steps)]
+    sec = sum(times) / len(times)
+    value = sample / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": workload_name(args.workload, dim, len(lok), nq), "tolerance": "dalton 500",
+                   "k": 1, "sample_queries_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
+                         "kind": "reference" if kind == "ref" else "port",
+                         "sample": f"search_batch over the first {sample} queries against the full library, "
+                                   f"{cores} threads, as-shipped flags (-O3, no -march)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(name, dim, n_lib, nq):
+    return f"{name}: {nq} queries x {n_lib} library (targets+decoys), D={dim}, open +-500 Da, top-1"
+
+
+# --------------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------------
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_16422_b200 as hb
+    from paper_2211_16422_b200 import capi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+
+    lib, qry, dim = make_workload(args.workload)
+    n_lib, nq, k = len(lib["precursor_mz"]), len(qry["precursor_mz"]), args.k
+    W = hb.words_for(dim)
+    pre = hb.PreprocessConfig()
+    tol = hb.Tolerance("dalton", 500.0)
+
+    ctx = hb.Context(local_rank)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    t = time.time()
+    ctx.upload_codebook(hb.make_codebook(hb.dimension(pre), hb.EncoderConfig(dim, dim // 2, 16, 1)))
+    log(f"[bench] codebook generated + uploaded in {time.time() - t:.1f}s")
+
+    def encode_on_device(spec, chunk=200_000):
+        n = len(spec["offsets"]) - 1
+        out = torch.empty((n, W), dtype=torch.int64, device=dev)
+        ok = torch.empty(n, dtype=torch.uint8, device=dev)
+        for a in range(0, n, chunk):
+            b = min(n, a + chunk)
+            p0, p1 = int(spec["offsets"][a]), int(spec["offsets"][b])
+            off = torch.from_numpy((spec["offsets"][a:b + 1] - spec["offsets"][a]).astype(np.int64)).to(dev)
+            mz = torch.from_numpy(spec["mz"][p0:p1]).to(dev)
+            it = torch.from_numpy(spec["intensity"][p0:p1]).to(dev)
+            ctx.encode_batch_dev(pre, b - a, p1 - p0, off.data_ptr(), mz.data_ptr(), it.data_ptr(),
+                                 out[a:b].data_ptr(), ok[a:b].data_ptr())
+            ctx.synchronize()
+        return out, ok
+
+    t = time.time()
+    ctx.profile(True)
+    lib_words, lib_ok = encode_on_device(lib)
+    enc_ms, _ = ctx.kernel_time(capi.KERNEL_ENCODE)
+    pre_ms, _ = ctx.kernel_time(capi.KERNEL_PREPROCESS)
+    ctx.profile(False)
+    assert int(lib_ok.sum().item()) == n_lib, "synthetic library spectra must all be processable"
+    log(f"[bench] library encoded on GPU in {time.time() - t:.1f}s "
+        f"(kernels: preprocess {pre_ms:.1f} ms + encode {enc_ms:.1f} ms = "
+        f"{n_lib / ((pre_ms + enc_ms) * 1e-3):.3g} spectra/s)")
+    t = time.time()
+    id_rank = hb.id_ranks(lib["ids"])
+    ctx.build_index_dev(dim, lib_words.data_ptr(), n_lib, lib["precursor_mz"], lib["charge"],
+                        is_decoy=lib["is_decoy"], id_rank=id_rank, shard_index=rank, shard_count=world)
+    log(f"[bench] index built in {time.time() - t:.1f}s (shard {rank}/{world})")
+    q_words, q_ok = encode_on_device(qry)
+    assert int(q_ok.sum().item()) == nq
+    d_qmz = torch.from_numpy(qry["precursor_mz"]).to(dev)
+    d_qch = torch.from_numpy(qry["charge"]).to(dev)
+    ctx.queries_upload_dev(dim, nq, q_words.data_ptr(), d_qmz.data_ptr(), d_qch.data_ptr())
+    ctx.synchronize()
+
+    first, last, _ = ctx.select_candidates(qry["precursor_mz"], qry["charge"], tol)
+    n_pairs = int((last - first).sum())
+    # bytes the reference's own access pattern touches
+    bytes_alg = n_pairs * (dim // 8 + 8) + nq * (dim // 8 + 9) + nq * k * 24
+
+    rec = torch.empty(nq * k * 16, dtype=torch.uint8, device=dev)
+    gathered = torch.empty(world * nq * k * 16, dtype=torch.uint8, device=dev) if world > 1 else None
+    merged = torch.empty(nq * k * 16, dtype=torch.uint8, device=dev) if world > 1 else None
+
+    def step():
+        ctx.search_resident_dev(tol, k, rec.data_ptr())
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, rec)
+            ctx.merge_candidates_dev(nq, k, world, gathered.data_ptr(), merged.data_ptr())
+
+    def sync_all():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    sync_all()
+    launches0 = ctx.launch_count()
+    ctx.profile(True)
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    sync_all()
+    clocks = sampler.stop() if sampler else None
+    ms_total = e0.elapsed_time(e1)
+    search_ms, search_launches = ctx.kernel_time(capi.KERNEL_SEARCH)
+    ctx.profile(False)
+    launches = ctx.launch_count() - launches0
+    if world > 1:
+        tmax = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        ms_total = float(tmax.item())
+    ms_step = ms_total / args.steps
+    value = nq / (ms_step * 1e-3)
+
+    # results of the device-resident path (for the parity check below)
+    final = merged if world > 1 else rec
+    dev_score, dev_ord = ctx.candidates_decode(nq, k, final.data_ptr())
+
+    # ---- end to end through the public host-buffer call ----------------------------------
+    h_words = torch.empty((nq, W), dtype=torch.int64).pin_memory()
+    h_words.copy_(q_words.cpu())
+    hq = h_words.numpy().view(np.uint64)
+    h2d = nq * W * 8 + nq * 9
+    d2h = nq * k * 8 + 2 * nq * 8
+    e2e_times = []
+    e2e_result = None
+    for i in range(args.warmup + args.steps):
+        sync_all()
+        t0 = time.perf_counter()
+        if world == 1:
+            e2e_result = ctx.search_batch(hq, qry["precursor_mz"], qry["charge"], tol, k=k)
+        else:
+            ctx.queries_upload(dim, hq, qry["precursor_mz"], qry["charge"])
+            step()
+            e2e_result = ctx.candidates_decode(nq, k, merged.data_ptr())
+        dt = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        if i >= args.warmup:
+            e2e_times.append(dt)
+    e2e_value = nq / (sum(e2e_times) / len(e2e_times))
+    if world == 1:
+        assert np.array_equal(e2e_result.ordinal, dev_ord) and np.array_equal(e2e_result.raw_score, dev_score)
+
+    # ---- roofline of the dominant kernel ---------------------------------------------------
+    peak, peak_src = measured_peak_hbm()
+    # per launch: this rank's share of the algorithmic bytes (1/world of the rows of every window)
+    bytes_per_launch = bytes_alg / world
+    achieved = bytes_per_launch / (search_ms / max(1, search_launches) * 1e-3) / 1e9 if search_ms > 0 else 0.0
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "kernel": "search_kernel", "kernel_ms_per_launch": search_ms / max(1, search_launches),
+                "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
+                "algorithmic_bytes_per_launch": bytes_per_launch, "pairs_per_launch": n_pairs / world,
+                "note": "achieved > peak is legitimate: QB queries share each reference tile, so DRAM "
+                        "traffic is ~1/QB of the algorithmic bytes (see profiles/ for ncu dram bytes)"}
+
+    # ---- CPU baseline: the compiled reference on this box's cores, bounded sample ----------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(lib, qry, dim, lib_words, hq, dev_score[:, 0], dev_ord[:, 0])
+        except Exception as exc:  # the baseline is a report, never a reason to lose the bench line
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
+                   "sample": f"failed: {exc!r}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": workload_name(args.workload, dim, n_lib, nq), "tolerance": "dalton 500",
+                       "k": k, "candidate_pairs_per_step": n_pairs,
+                       "l2_policy": "inputs larger than L2 (library hypervectors "
+                                    f"{n_lib * W * 8 / 1e9:.2f} GB >> 126 MB)",
+                       "parallelism": f"library sharded by m/z slices x{world}, queries replicated, "
+                                      "all-gather + merge of 16-byte candidates" if world > 1 else "single GPU"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "encode": {"spectra_per_s": n_lib / ((pre_ms + enc_ms) * 1e-3), "preprocess_ms": pre_ms,
+                       "encode_ms": enc_ms, "spectra": n_lib, "peaks": lib["peaks"]},
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(lib, qry, dim, lib_words, hq, dev_score, dev_ord):
+    from oracle import binding as ob
+    kind = "ref" if ob.available("ref") else "port"
+    oracle = ob.Oracle(kind)
+    cores = os.cpu_count() or 1
+    t = time.time()
+    lw = lib_words.cpu().numpy().view(np.uint64)
+    ix = oracle.build_index(dim, lw, lib["precursor_mz"], lib["charge"], lib["is_decoy"], lib["ids"])
+    log(f"[bench] reference index built on the host in {time.time() - t:.1f}s")
+    tol = ("da", 500.0)
+
+    def run(n):
+        t0 = time.perf_counter()
+        r = ix.search_batch(hq[:n], qry["precursor_mz"][:n], qry["charge"][:n], tol, threads=cores, batch=8)
+        return time.perf_counter() - t0, r
+
+    probe = min(len(hq), 2 * cores)
+    t_probe, _ = run(probe)
+    sample = int(max(cores, min(len(hq), probe * 15.0 / max(t_probe, 1e-6))))
+    sec, (has, score, ordinal, _) = run(sample)
+    parity = bool(np.array_equal(score, dev_score[:sample]) and np.array_equal(ordinal, dev_ord[:sample]))
+    out = {"value": sample / sec, "unit": UNIT, "cores": cores,
+           "kind": "reference" if kind == "ref" else "port",
+           "sample": f"search_batch over the first {sample} queries against the full library, {cores} threads, "
+                     "as-shipped flags (-O3, no -march)",
+           "parity_with_gpu_on_sample": "bit-exact" if parity else "MISMATCH"}
+    if ob.available("ref_v3"):
+        o3 = ob.Oracle("ref_v3")
+        ix3 = o3.build_index(dim, lw, lib["precursor_mz"], lib["charge"], lib["is_decoy"], lib["ids"])
+        n3 = min(len(hq), sample * 4)
+        t0 = time.perf_counter()
+        ix3.search_batch(hq[:n3], qry["precursor_mz"][:n3], qry["charge"][:n3], tol, threads=cores, batch=8)
+        out["tuned_value"] = n3 / (time.perf_counter() - t0)
+        out["tuned_note"] = f"same sources with -march=x86-64-v3 (hardware popcnt), {n3} queries"
+        ix3.close()
+    ix.close()
+    if not parity:
+        raise AssertionError("GPU results differ from the reference on the CPU-baseline sample")
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="iprg2012")
+    ap.add_argument("--k", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -96,6 +96,13 @@ int homs_b200_ctx_set_stream(homs_b200_ctx* ctx, void* cuda_stream);
 int homs_b200_ctx_synchronize(homs_b200_ctx* ctx);
 /* Kernels launched by this context so far (bench.py's gpu_launches). */
 uint64_t homs_b200_ctx_launch_count(const homs_b200_ctx* ctx);
+/* Per-kernel device timing for roofline reports: while enabled, every launch of the three hot
+ * kernels is bracketed by CUDA events on the context's stream.  kernel_time() synchronises, returns
+ * the summed duration and launch count since the last call, and resets the counters. */
+enum { HOMS_B200_KERNEL_SEARCH = 0, HOMS_B200_KERNEL_ENCODE = 1, HOMS_B200_KERNEL_PREPROCESS = 2 };
+int homs_b200_ctx_profile(homs_b200_ctx* ctx, int enable);
+int homs_b200_ctx_kernel_time(homs_b200_ctx* ctx, int which, double* out_total_ms,
+                              uint64_t* out_launches);
 
 /* ---- host-side configuration (no device work) ----------------------------------------------- */
 

@@ -70,6 +70,9 @@ last_error = _decl("homs_b200_last_error", C.c_char_p, [_VP])
 ctx_set_stream = _decl("homs_b200_ctx_set_stream", _I, [_VP, _VP])
 ctx_synchronize = _decl("homs_b200_ctx_synchronize", _I, [_VP])
 ctx_launch_count = _decl("homs_b200_ctx_launch_count", _U64, [_VP])
+ctx_profile = _decl("homs_b200_ctx_profile", _I, [_VP, _I])
+ctx_kernel_time = _decl("homs_b200_ctx_kernel_time", _I, [_VP, _I, _P(_F64), _P(_U64)])
+KERNEL_SEARCH, KERNEL_ENCODE, KERNEL_PREPROCESS = 0, 1, 2
 
 preprocess_validate = _decl("homs_b200_preprocess_validate", _I, [_P(PreprocessConfigPod)])
 dimension = _decl("homs_b200_dimension", _U32, [_P(PreprocessConfigPod)])

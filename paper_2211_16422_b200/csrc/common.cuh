@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "homs_b200.h"
@@ -85,6 +86,9 @@ struct homs_b200_ctx {
   hb::DevBuf scratch[kScratchSlots];
   void* pinned = nullptr;  // small pinned staging block
   size_t pinned_cap = 0;
+  // optional per-kernel timing (homs_b200_ctx_profile)
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[3];
 };
 
 namespace hb {
@@ -116,6 +120,24 @@ int set_error(const homs_b200_ctx* ctx, int code, const std::string& msg);
     ++(ctx)->launches;                 \
     HB_CUDA((ctx), cudaGetLastError()); \
   } while (0)
+
+// Brackets one kernel launch with events when profiling is on.
+struct KernelTimer {
+  KernelTimer(homs_b200_ctx* c, int which) : ctx(c), slot(which) {
+    if (!ctx->profiling) return;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, ctx->stream);
+  }
+  ~KernelTimer() {
+    if (!e0) return;
+    cudaEventRecord(e1, ctx->stream);
+    ctx->prof[slot].emplace_back(e0, e1);
+  }
+  homs_b200_ctx* ctx;
+  int slot;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
 
 int ensure(homs_b200_ctx* ctx, DevBuf& b, size_t bytes);
 int ensure_pinned(homs_b200_ctx* ctx, size_t bytes);

@@ -170,6 +170,32 @@ int homs_b200_ctx_synchronize(homs_b200_ctx* ctx) {
 
 uint64_t homs_b200_ctx_launch_count(const homs_b200_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int homs_b200_ctx_profile(homs_b200_ctx* ctx, int enable) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  ctx->profiling = enable != 0;
+  return HOMS_B200_OK;
+}
+
+int homs_b200_ctx_kernel_time(homs_b200_ctx* ctx, int which, double* out_total_ms,
+                              uint64_t* out_launches) {
+  if (!ctx || which < 0 || which > 2) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  double total = 0.0;
+  for (auto& pr : ctx->prof[which]) {
+    float ms = 0.f;
+    HB_CUDA(ctx, cudaEventElapsedTime(&ms, pr.first, pr.second));
+    total += ms;
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  if (out_total_ms) *out_total_ms = total;
+  if (out_launches) *out_launches = ctx->prof[which].size();
+  ctx->prof[which].clear();
+  return HOMS_B200_OK;
+}
+
 // ---- host-only configuration --------------------------------------------------------------
 
 static constexpr double kBinEpsilon = 1e-9;  // preprocess.cpp:17

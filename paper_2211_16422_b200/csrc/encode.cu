@@ -398,8 +398,11 @@ static int launch_preprocess(homs_b200_ctx* ctx, const PreParams& p, uint64_t n,
                                     static_cast<int>(smem)));
   const uint64_t want = (n + warps - 1) / warps;
   const int grid = static_cast<int>(std::min<uint64_t>(want, uint64_t(ctx->sm_count) * 16));
-  preprocess_kernel<<<grid, warps * 32, smem, ctx->stream>>>(p, n, d_off, d_mz, d_int, d_bins,
-                                                             d_lev, d_count, warps);
+  {
+    KernelTimer timer(ctx, HOMS_B200_KERNEL_PREPROCESS);
+    preprocess_kernel<<<grid, warps * 32, smem, ctx->stream>>>(p, n, d_off, d_mz, d_int, d_bins,
+                                                               d_lev, d_count, warps);
+  }
   HB_LAUNCHED(ctx);
   return HOMS_B200_OK;
 }
@@ -429,8 +432,11 @@ static int launch_encode(homs_b200_ctx* ctx, uint64_t n, const uint64_t* d_sv_of
         n, d_sv_off, stride, d_bins, d_lev, d_count, cb.d_pos.as<uint4>(), cb.d_lvl.as<uint4>(), \
         cb.levels + 1, row_u4, cb.dim, cb.W, lvl_in_smem, vec_store, d_out, d_ok);                          \
   } while (0)
-  if (max_count <= 255) HB_ENC_LAUNCH(8);
-  else HB_ENC_LAUNCH(16);
+  {
+    KernelTimer timer(ctx, HOMS_B200_KERNEL_ENCODE);
+    if (max_count <= 255) HB_ENC_LAUNCH(8);
+    else HB_ENC_LAUNCH(16);
+  }
 #undef HB_ENC_LAUNCH
   HB_LAUNCHED(ctx);
   return HOMS_B200_OK;

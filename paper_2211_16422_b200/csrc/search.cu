@@ -521,7 +521,10 @@ static int launch_search(homs_b200_ctx* ctx, const SearchParams& sp, int grid) {
   const size_t smem = search_smem(QB, sp.row_bytes);
   HB_CUDA(ctx, cudaFuncSetAttribute(search_kernel<QB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
-  search_kernel<QB><<<grid, kTileRows, smem, ctx->stream>>>(sp);
+  {
+    KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
+    search_kernel<QB><<<grid, kTileRows, smem, ctx->stream>>>(sp);
+  }
   HB_LAUNCHED(ctx);
   return HOMS_B200_OK;
 }

@@ -226,6 +226,15 @@ class Context:
     def launch_count(self) -> int:
         return int(capi.ctx_launch_count(self._h))
 
+    def profile(self, enable: bool) -> None:
+        _check(capi.ctx_profile(self._h, int(enable)), self._h)
+
+    def kernel_time(self, which: int):
+        """(total milliseconds, launches) of one hot kernel since the last call."""
+        ms, cnt = C.c_double(), C.c_uint64()
+        _check(capi.ctx_kernel_time(self._h, which, C.byref(ms), C.byref(cnt)), self._h)
+        return ms.value, cnt.value
+
     # -- encoding ---------------------------------------------------------------------------
     def upload_codebook(self, cb: Codebook) -> None:
         pos = _arr(cb.position, np.uint64)

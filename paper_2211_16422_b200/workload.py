@@ -1,0 +1,108 @@
+"""Synthetic workloads of the BASELINE.json shapes (numpy, deterministic, no dataset needed).
+
+Shapes follow the reference's benchmark generator (src/synth.cpp:114-197: fragment m/z on a
+0.01 Th grid in [150, 1300), intensities U[0.05, 1], precursors U[380, 1070], charge in {2, 3},
+one decoy per target with the target's precursor/charge/intensities on fresh positions, queries
+derived from targets with a planted +79.97 Da shift and 5 % intensity noise), but this is an
+independent vectorised generator: the streams are NOT the reference's, only the distribution is.
+Bit-exact parity tests use the oracle's generator instead; this module feeds bench.py.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+GRID = 0.01
+MZ_LO, MZ_HI = 150.0, 1300.0
+
+
+def _distinct_grid_rows(rng: np.random.Generator, n: int, peaks: int) -> np.ndarray:
+    """n rows of `peaks` distinct sorted grid indices in [lo, hi]."""
+    lo, hi = int(round(MZ_LO / GRID)), int(round(MZ_HI / GRID)) - 1
+    out = np.empty((n, peaks), np.int32)
+    step = 200_000
+    for a in range(0, n, step):
+        b = min(n, a + step)
+        rows = np.sort(rng.integers(lo, hi + 1, (b - a, peaks), dtype=np.int32), axis=1)
+        while True:
+            dup = (np.diff(rows, axis=1) == 0).any(axis=1)
+            if not dup.any():
+                break
+            rows[dup] = np.sort(rng.integers(lo, hi + 1, (int(dup.sum()), peaks), dtype=np.int32), axis=1)
+        out[a:b] = rows
+    return out
+
+
+def synth_library(n_targets: int, peaks: int = 50, decoy_ratio: float = 1.0, seed: int = 2) -> dict:
+    rng = np.random.default_rng(seed)
+    n_decoys = int(round(decoy_ratio * n_targets))
+    n = n_targets + n_decoys
+    idx = _distinct_grid_rows(rng, n, peaks)
+    mz = idx.astype(np.float64) * GRID
+    inten = np.empty((n, peaks), np.float64)
+    inten[:n_targets] = 0.05 + 0.95 * rng.random((n_targets, peaks))
+    src = np.arange(n_decoys) % n_targets
+    inten[n_targets:] = inten[src]
+    span = MZ_HI - MZ_LO
+    prec = np.empty(n, np.float64)
+    prec[:n_targets] = (MZ_LO + 0.2 * span) + (0.6 * span) * rng.random(n_targets)
+    prec[n_targets:] = prec[src]
+    charge = np.empty(n, np.uint8)
+    charge[:n_targets] = rng.integers(2, 4, n_targets)
+    charge[n_targets:] = charge[src]
+    decoy = np.zeros(n, np.uint8)
+    decoy[n_targets:] = 1
+    ids = [f"LIB_{i + 1:06d}" for i in range(n_targets)] + [f"DECOY_{j + 1:06d}" for j in range(n_decoys)]
+    offsets = np.arange(n + 1, dtype=np.uint64) * np.uint64(peaks)
+    return dict(offsets=offsets, mz=mz.ravel(), intensity=inten.ravel(), precursor_mz=prec,
+                charge=charge, is_decoy=decoy, ids=ids, n_targets=n_targets, peaks=peaks)
+
+
+def synth_queries(lib: dict, n_query: int, fraction_modified: float = 0.6, shift: float = 79.97,
+                  fraction_peaks_shifted: float = 0.3, noise: float = 0.05, seed: int = 2) -> dict:
+    rng = np.random.default_rng(seed + 0x9E3779B9)
+    peaks = lib["peaks"]
+    src = rng.integers(0, lib["n_targets"], n_query)
+    mz = lib["mz"].reshape(-1, peaks)[src].copy()
+    inten = lib["intensity"].reshape(-1, peaks)[src].copy()
+    charge = lib["charge"][src].copy()
+    prec = lib["precursor_mz"][src].copy()
+    modified = rng.random(n_query) < fraction_modified
+    prec[modified] += shift / charge[modified]
+    shifted = (rng.random((n_query, peaks)) < fraction_peaks_shifted) & modified[:, None]
+    mz[shifted] += shift
+    inten *= 1.0 + noise * (2.0 * rng.random((n_query, peaks)) - 1.0)
+    order = np.argsort(mz, axis=1, kind="stable")
+    mz = np.take_along_axis(mz, order, 1)
+    inten = np.take_along_axis(inten, order, 1)
+    # RawSpectrum invariant: strictly ascending m/z; merge the (rare) exact collisions
+    counts = np.full(n_query, peaks, np.int64)
+    dup_rows = np.flatnonzero((np.diff(mz, axis=1) == 0).any(axis=1))
+    flat_mz, flat_in = [mz[i] for i in range(0)], []
+    if len(dup_rows):
+        keep = np.ones((n_query, peaks), bool)
+        for r in dup_rows:
+            m, v = mz[r], inten[r]
+            j = 0
+            for t in range(1, peaks):
+                if m[t] == m[j]:
+                    v[j] += v[t]
+                    keep[r, t] = False
+                else:
+                    j = t
+        counts = keep.sum(axis=1)
+        flat_mz, flat_in = mz[keep], inten[keep]
+    else:
+        flat_mz, flat_in = mz.ravel(), inten.ravel()
+    offsets = np.zeros(n_query + 1, np.uint64)
+    offsets[1:] = np.cumsum(counts)
+    return dict(offsets=offsets, mz=np.ascontiguousarray(flat_mz), intensity=np.ascontiguousarray(flat_in),
+                precursor_mz=prec, charge=charge, source=src, modified=modified)
+
+
+WORKLOADS = {
+    # name: (n_targets, n_query, dim, peaks, seed)  -- BASELINE.json configs
+    "config1": (5_000, 1_000, 2048, 50, 1),       # reference CPU test workload
+    "iprg2012": (600_000, 16_000, 8192, 50, 2),   # 16k queries x 1.2M library, D = 8192
+    "hek293": (2_150_000, 65_536, 8192, 50, 3),   # 4.3M library; query prefix of the 1M set
+    "tiny": (2_000, 256, 2048, 50, 9),            # CI-sized
+}
