@@ -187,7 +187,12 @@ def run_ours(args) -> None:
     tol = hb.Tolerance("dalton", 500.0)
 
     ctx = hb.Context(local_rank)
-    stream = torch.cuda.current_stream(dev)
+    # a real (non-NULL) stream shared by torch, NCCL and the context: the NULL handle of torch's
+    # default stream would mean "context's own stream" to ctx_set_stream and the step events
+    # below would then time nothing
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     ctx.set_stream(stream.cuda_stream)
     t = time.time()
     ctx.upload_codebook(hb.make_codebook(hb.dimension(pre), hb.EncoderConfig(dim, dim // 2, 16, 1)))

@@ -5,7 +5,7 @@ Shapes follow the reference's benchmark generator (src/synth.cpp:114-197: fragme
 one decoy per target with the target's precursor/charge/intensities on fresh positions, queries
 derived from targets with a planted +79.97 Da shift and 5 % intensity noise), but this is an
 independent vectorised generator: the streams are NOT the reference's, only the distribution is.
-Bit-exact parity tests use the oracle's generator instead; this module feeds bench.py.
+Bit-exact parity tests use the reference's own generator instead; this module feeds bench.py.
 """
 from __future__ import annotations
 
