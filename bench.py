@@ -44,6 +44,19 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def measured_peak_tensor_i8():
+    """Dense int8 tensor peak: MEASURED_PEAKS.json holds the measured dense bf16 rate; the B200
+    tensor core runs 8-bit operands at twice the 16-bit rate (4.5 vs 2.25 PFLOP/s nominal), so the
+    denominator is 2 x the measured sustained bf16 figure (the kernel is timed inside a long step)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return 2.0 * float(j.get("bf16_tflops_sustained") or j["bf16_tflops"]), \
+            "2 x measured sustained dense bf16 (MEASURED_PEAKS.json)"
+    except Exception:
+        return 2.0 * 1500.0, "fallback: 2 x 1500 TFLOP/s bf16 (B200_PROFILING.md)"
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons during the timed region."""
 
@@ -187,6 +200,7 @@ def run_ours(args) -> None:
     tol = hb.Tolerance("dalton", 500.0)
 
     ctx = hb.Context(local_rank)
+    ctx.set_engine(args.engine)
     # a real (non-NULL) stream shared by torch, NCCL and the context: the NULL handle of torch's
     # default stream would mean "context's own stream" to ctx_set_stream and the step events
     # below would then time nothing
@@ -317,13 +331,33 @@ def run_ours(args) -> None:
     # per launch: this rank's share of the algorithmic bytes (1/world of the rows of every window)
     bytes_per_launch = bytes_alg / world
     achieved = bytes_per_launch / (search_ms / max(1, search_launches) * 1e-3) / 1e9 if search_ms > 0 else 0.0
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                "kernel": "search_kernel", "kernel_ms_per_launch": search_ms / max(1, search_launches),
-                "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
-                "algorithmic_bytes_per_launch": bytes_per_launch, "pairs_per_launch": n_pairs / world,
-                "note": "achieved > peak is legitimate: QB queries share each reference tile, so DRAM "
-                        "traffic is ~1/QB of the algorithmic bytes (see profiles/ for ncu dram bytes)"}
+    kernel_ms = search_ms / max(1, search_launches)
+    tensor = args.engine != "popc" and k == 1
+    hbm_view = {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_per_launch,
+                "note": "SURVEY 8(d) algorithmic bytes (every candidate row read once per query) over the "
+                        "kernel time; > peak is legitimate because queries share library tiles on chip"}
+    if tensor:
+        # int8 contraction: 2 ops per (pair, dimension); K is padded to a multiple of 128
+        kpad = (dim + 127) // 128 * 128
+        ops = 2.0 * (n_pairs / world) * kpad
+        tpeak, tsrc = measured_peak_tensor_i8()
+        ach = ops / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else 0.0
+        roofline = {"bound": "tensor", "achieved": ach, "peak": tpeak, "unit": "TFLOP/s", "frac": ach / tpeak,
+                    "traffic": None, "peak_source": tsrc, "kernel": "tc_search_kernel",
+                    "kernel_ms_per_launch": kernel_ms,
+                    "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
+                    "algorithmic_ops_per_launch": ops, "pairs_per_launch": n_pairs / world,
+                    "note": "int8 tensor ops (tcgen05 kind::i8) counted over the candidate pairs of the "
+                            "windows only; masked columns of edge tiles are not counted",
+                    "hbm_view": hbm_view}
+    else:
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                    "kernel": "search_kernel", "kernel_ms_per_launch": kernel_ms,
+                    "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
+                    "algorithmic_bytes_per_launch": bytes_per_launch, "pairs_per_launch": n_pairs / world,
+                    "note": hbm_view["note"]}
 
     # ---- CPU baseline: the compiled reference on this box's cores, bounded sample ----------
     cpu = None
@@ -338,9 +372,10 @@ def run_ours(args) -> None:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "s8 (+-1 expansion of the packed u64 bits), s32 accumulate" if tensor else "u64", "data": "synthetic",
             "config": {"workload": workload_name(args.workload, dim, n_lib, nq), "tolerance": "dalton 500",
                        "k": k, "candidate_pairs_per_step": n_pairs,
+                       "engine": "tensor (tcgen05 int8)" if tensor else "popc",
                        "l2_policy": "inputs larger than L2 (library hypervectors "
                                     f"{n_lib * W * 8 / 1e9:.2f} GB >> 126 MB)",
                        "parallelism": f"library sharded by m/z slices x{world}, queries replicated, "
@@ -406,6 +441,8 @@ def main():
     ap.add_argument("--workload", default="iprg2012")
     ap.add_argument("--k", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--engine", default="auto", choices=["auto", "popc", "tensor"],
+                    help="top-1 search engine (auto = tensor cores)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -100,6 +100,13 @@ uint64_t homs_b200_ctx_launch_count(const homs_b200_ctx* ctx);
  * kernels is bracketed by CUDA events on the context's stream.  kernel_time() synchronises, returns
  * the summed duration and launch count since the last call, and resets the counters. */
 enum { HOMS_B200_KERNEL_SEARCH = 0, HOMS_B200_KERNEL_ENCODE = 1, HOMS_B200_KERNEL_PREPROCESS = 2 };
+/* Search engine for top-1 searches: AUTO (= TENSOR whenever the library has a tensor image),
+ * POPC (XOR + POPC on the integer pipes) or TENSOR (tcgen05 int8 contraction of the +-1 expanded
+ * hypervectors; similarity = (dim + dot) / 2, exact in int32).  Both are bit-exact; k > 1 always
+ * runs on the POPC engine.  Set it BEFORE library_upload: POPC skips building the 8x larger
+ * tensor image of the library. */
+enum { HOMS_B200_ENGINE_AUTO = 0, HOMS_B200_ENGINE_POPC = 1, HOMS_B200_ENGINE_TENSOR = 2 };
+int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine);
 int homs_b200_ctx_profile(homs_b200_ctx* ctx, int enable);
 int homs_b200_ctx_kernel_time(homs_b200_ctx* ctx, int which, double* out_total_ms,
                               uint64_t* out_launches);

@@ -41,6 +41,16 @@ struct BucketDev {           // one charge bucket, device + host view
   uint64_t local_offset;     // ... at local rows [local_offset, local_offset + shard_end - shard_begin)
 };
 
+// One candidate of the windowed top-k, == homs_b200_candidate (16 bytes).  Lexicographic order on
+// (d, ad, rk) is the reference's key (score desc, |q - r| asc, id asc, ordinal asc),
+// search.cpp:133-146.
+struct Cand {
+  uint32_t d, rk;
+  uint64_t ad;
+};
+static_assert(sizeof(Cand) == 16 && sizeof(homs_b200_candidate) == 16, "candidate record is 16 bytes");
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
 struct Library {
   bool ready = false;
   uint32_t dim = 0, W = 0, S = 0;  // bits, dense words, padded stride (u64 words)
@@ -53,6 +63,11 @@ struct Library {
   // device (owned through ctx buffers)
   DevBuf d_mz, d_id_rank, d_ord_of_rank, d_mz_local, d_id_rank_local, d_words, d_buckets,
       d_bucket_of_charge;
+  // +-1 int8 image of the resident rows for the tensor-core engine (search_tc.cu):
+  // [n_kc][x_rows][128 B], every 128-byte row pre-swizzled for a SWIZZLE_128B K-major UMMA operand
+  DevBuf d_x;
+  uint64_t x_rows = 0;  // n_local rounded up to 256, plus one all-zero 256-row tile of slack
+  uint32_t n_kc = 0;    // ceil(dim / 128)
 };
 
 struct Queries {
@@ -82,10 +97,13 @@ struct homs_b200_ctx {
   hb::Library lib;
   hb::Queries q;
   // grow-only scratch, keyed by purpose
-  enum { kScratchSlots = 24 };
+  enum { kScratchSlots = 32 };
   hb::DevBuf scratch[kScratchSlots];
+  int engine = HOMS_B200_ENGINE_AUTO;  // homs_b200_ctx_set_engine
   void* pinned = nullptr;  // small pinned staging block
   size_t pinned_cap = 0;
+  void* pinned_plan = nullptr;  // pinned block of the tensor engine's host planner
+  size_t pinned_plan_cap = 0;
   // optional per-kernel timing (homs_b200_ctx_profile)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[3];
@@ -141,14 +159,23 @@ struct KernelTimer {
 
 int ensure(homs_b200_ctx* ctx, DevBuf& b, size_t bytes);
 int ensure_pinned(homs_b200_ctx* ctx, size_t bytes);
+int ensure_pinned_plan(homs_b200_ctx* ctx, size_t bytes);
 void release(DevBuf& b);
 
 // scratch slot names
 enum Scratch {
   kScrOffsets = 0, kScrMz, kScrInt, kScrSvBins, kScrSvLev, kScrSvCount, kScrEncOut, kScrEncOk,
   kScrQFirst, kScrQLast, kScrKeys, kScrKeysAlt, kScrVals, kScrValsAlt, kScrCub, kScrPlan,
-  kScrPartial, kScrRecords, kScrSubset, kScrDecode, kScrMisc, kScrMisc2, kScrRecords2, kScrHas
+  kScrPartial, kScrRecords, kScrSubset, kScrDecode, kScrMisc, kScrMisc2, kScrRecords2, kScrHas,
+  kScrTcQx, kScrTcPlan, kScrTcPartial, kScrTcTiles
 };
+
+// Tensor-core engine (search_tc.cu).  expand: packed rows -> +-1 int8 swizzled image.
+int tc_expand_library(homs_b200_ctx* ctx);
+// top-1 of n sorted slots (keys/vals as produced by bounds + radix sort) -> out[slot * k_stride]
+int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
+                     const uint32_t* d_vals, Cand* d_out, uint32_t k_stride);
+bool tc_available(const homs_b200_ctx* ctx);
 
 // dense host rows (W words) -> padded device rows (S words), zero padded.  Async on ctx->stream.
 int upload_rows(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* h_src, uint64_t n, uint32_t W,

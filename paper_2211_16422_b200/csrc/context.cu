@@ -55,6 +55,20 @@ int ensure_pinned(homs_b200_ctx* ctx, size_t bytes) {
   return HOMS_B200_OK;
 }
 
+int ensure_pinned_plan(homs_b200_ctx* ctx, size_t bytes) {
+  if (ctx->pinned_plan_cap >= bytes) return HOMS_B200_OK;
+  if (ctx->pinned_plan) {
+    HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFreeHost(ctx->pinned_plan);
+    ctx->pinned_plan = nullptr;
+    ctx->pinned_plan_cap = 0;
+  }
+  const size_t want = std::max<size_t>(bytes * 2, 1 << 20);
+  HB_CUDA(ctx, cudaMallocHost(&ctx->pinned_plan, want));
+  ctx->pinned_plan_cap = want;
+  return HOMS_B200_OK;
+}
+
 int upload_rows(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* h_src, uint64_t n, uint32_t W,
                 uint32_t S) {
   if (n == 0) return HOMS_B200_OK;
@@ -141,10 +155,11 @@ void homs_b200_ctx_destroy(homs_b200_ctx* ctx) {
   for (auto& b : ctx->scratch) release(b);
   for (DevBuf* b : {&ctx->cb.d_pos, &ctx->cb.d_lvl, &ctx->lib.d_mz, &ctx->lib.d_id_rank,
                     &ctx->lib.d_ord_of_rank, &ctx->lib.d_mz_local, &ctx->lib.d_id_rank_local,
-                    &ctx->lib.d_words, &ctx->lib.d_buckets, &ctx->lib.d_bucket_of_charge,
+                    &ctx->lib.d_words, &ctx->lib.d_buckets, &ctx->lib.d_bucket_of_charge, &ctx->lib.d_x,
                     &ctx->q.d_words, &ctx->q.d_mz, &ctx->q.d_charge})
     release(*b);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->pinned_plan) cudaFreeHost(ctx->pinned_plan);
   cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -158,6 +173,18 @@ int homs_b200_ctx_set_stream(homs_b200_ctx* ctx, void* cuda_stream) {
   Lock lock(ctx);
   HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+  return HOMS_B200_OK;
+}
+
+int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_REQUIRE(ctx, engine == HOMS_B200_ENGINE_AUTO || engine == HOMS_B200_ENGINE_POPC ||
+                      engine == HOMS_B200_ENGINE_TENSOR,
+             HOMS_B200_ERR_ARGUMENT, "set_engine: unknown engine");
+  HB_REQUIRE(ctx, engine != HOMS_B200_ENGINE_TENSOR || !ctx->lib.ready || tc_available(ctx),
+             HOMS_B200_ERR_STATE, "set_engine: the resident library was uploaded without a tensor image");
+  ctx->engine = engine;
   return HOMS_B200_OK;
 }
 

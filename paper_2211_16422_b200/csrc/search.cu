@@ -34,17 +34,10 @@
 
 namespace hb {
 
-constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kTileRows = 256;    // threads per CTA == reference rows per tile
 constexpr int kChunkBytes = 64;   // bytes of every row per pipeline stage
 constexpr int kStages = 4;
 constexpr int kStageBytes = kTileRows * kChunkBytes;
-
-struct Cand {  // == homs_b200_candidate
-  uint32_t d, rk;
-  uint64_t ad;
-};
-static_assert(sizeof(Cand) == 16 && sizeof(homs_b200_candidate) == 16, "candidate record is 16 bytes");
 
 __device__ __forceinline__ bool cand_less(uint32_t d1, uint64_t ad1, uint32_t rk1, uint32_t d2,
                                           uint64_t ad2, uint32_t rk2) {
@@ -587,6 +580,9 @@ static int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint6
                    ctx->scratch[kScrValsAlt].as<uint32_t>(), static_cast<int>(n), 32, 64, ctx->stream));
   const uint64_t* keys = ctx->scratch[kScrKeysAlt].as<uint64_t>();
   const uint32_t* vals = ctx->scratch[kScrValsAlt].as<uint32_t>();
+
+  if (k == 1 && ctx->engine != HOMS_B200_ENGINE_POPC && tc_available(ctx))
+    return tc_search_sorted(ctx, d_subset, n, keys, vals, d_out, 1);
 
   const uint32_t n_blocks = static_cast<uint32_t>((n + qb - 1) / qb);
   const int grid = ctx->sm_count * 2;

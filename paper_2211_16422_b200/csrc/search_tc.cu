@@ -1,0 +1,626 @@
+// Tensor-core engine of the windowed Hamming top-1 search (sm_100a: tcgen05 + TMEM + bulk copies).
+//
+// Reference semantics are those of search.cu (search.cpp:93-169): per query the candidate row with
+// the largest Hamming similarity inside its precursor window, ties broken by (|q - r|, id, ordinal).
+//
+// The similarity of two D-bit hypervectors is an inner product once every bit b is expanded to the
+// int8 value 2b - 1:   dot(x, y) = #agree - #differ = D - 2 * popcount(x ^ y)
+//                      raw_score = D - popcount(x ^ y) = (D + dot) / 2        (hypervector.hpp:70-81)
+// exactly, in int32.  tools/microbench.cu measured the alternatives on a B200: the XOR+POPC pipe
+// tops out at 15.3 32-bit words/clk/SM (23 with a carry-save tree), mma.sync.s8 at 61 word
+// equivalents, and the 5th-generation tensor core (tcgen05.mma kind::i8) at 8192 MAC/clk/SM =
+// 256 word equivalents.  So the search becomes a windowed GEMM:
+//
+//   C[query, row] = Qx[query, :] . Lx[row, :]      Qx, Lx in {-1, +1}^D (0 in padding)
+//
+// * Lx is built once per library upload, Qx once per search, both in HBM as
+//   [k-chunk][row][128 bytes] with the 16-byte units of every row XOR-swizzled by (row & 7): a
+//   tile of R consecutive rows of one k-chunk is then ONE contiguous R*128-byte block that is
+//   already in the SWIZZLE_128B K-major layout tcgen05.mma wants, so a stage of the pipeline is
+//   two cp.async.bulk copies (no tensor map needed) completing on an mbarrier.
+// * queries are sorted by window start (search.cu) and cut into tiles of 128 = the 128 TMEM lanes;
+//   the library rows a tile needs (union of its windows) are cut into 256-row MMA tiles aligned
+//   to absolute multiples of 256, so that different query tiles fetch identical blocks (L2 hits).
+// * one CTA = 6 warps: warp 0 issues the bulk copies (4-stage ring, 48 KB per stage), one thread
+//   of warp 1 issues the MMAs (4 x K=32 per stage) into one of two 128x256 int32 accumulators
+//   in TMEM, warps 2-5 drain the other accumulator: lane = query, column = library row; every
+//   thread keeps the running best of its query with the exact 3-level key and masks columns
+//   outside the query's own window.  The drain (256 columns) costs ~2 % of the 64-stage K loop
+//   at D = 8192 and overlaps with the next tile's MMAs.
+// * work items (query tile x strip of row tiles) are planned on the host from 8 bytes per query
+//   tile and ordered so that CTAs running at the same time share both query and row tiles in L2.
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace hb {
+
+constexpr int kTcM = 128;      // queries per tile == TMEM lanes
+constexpr int kTcN = 256;      // library rows per MMA tile == TMEM columns per accumulator
+constexpr int kTcKB = 128;     // K bytes per pipeline stage == one swizzle atom == 128 dimensions
+constexpr int kTcStages = 4;
+constexpr uint32_t kTcABytes = kTcM * kTcKB;  // 16 KB
+constexpr uint32_t kTcBBytes = kTcN * kTcKB;  // 32 KB
+constexpr uint32_t kTcStageBytes = kTcABytes + kTcBBytes;
+constexpr int kTcThreads = 192;
+constexpr uint32_t kTcBarBytes = 256;
+constexpr uint32_t kTcSmemBytes = kTcStages * kTcStageBytes + 1024 + kTcBarBytes;
+constexpr uint32_t kTcTmemCols = 512;  // two 256-column accumulators
+constexpr uint32_t kTcGroupTiles = 12;  // query tiles per L2 group
+constexpr uint64_t kTcBatch = 64 * 1024;  // sorted slots per planning batch
+
+struct TcItem {
+  uint32_t tile;       // query tile (128 sorted positions) inside the batch
+  uint32_t row_begin;  // local library rows [row_begin, row_end), row_begin % 256 == 0
+  uint32_t row_end;
+  uint32_t pad;
+};
+
+struct TcParams {
+  const uint8_t* lib_x;
+  const uint8_t* q_x;
+  uint64_t lib_rows;  // rows per k-chunk plane of lib_x
+  uint64_t q_rows;    // rows per k-chunk plane of q_x
+  uint32_t n_kc;
+  uint32_t dim;
+  const TcItem* items;
+  uint32_t n_items;
+  uint32_t pad;
+  const uint64_t* keys;  // sorted (local first row << 32 | local last row), batch base applied
+  const uint32_t* vals;  // sorted slot ids
+  const uint32_t* subset;
+  const double* q_mz;
+  const double* lib_mz;
+  const uint32_t* lib_rank;
+  uint64_t n;  // sorted positions in this batch
+  Cand* partial;  // [n_items][128]
+};
+
+// ---- PTX wrappers ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// A wait that can never hang the GPU: a pipeline bug traps after ~4 s instead of spinning forever.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  uint32_t spins = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if ((++spins & 0xFFFu) == 0 && clock64() - t0 > 8000000000ll) __trap();
+  }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, int8 x int8 -> int32, M = 128, N = 256, K = 32
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 consecutive int32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor of a K-major SWIZZLE_128B operand whose rows are 128 bytes:
+// start address >> 4 in bits [0,14), leading byte offset (unused for one swizzle atom along K) in
+// [16,30), stride byte offset = 1024 B between 8-row groups in [32,46), descriptor version 1 in
+// [46,48), layout type 2 = SWIZZLE_128B in [61,64).
+__device__ __forceinline__ uint64_t tc_smem_desc(uint32_t smem_addr) {
+  const uint64_t lo = (uint64_t(smem_addr & 0x3FFFFu) >> 4) | (uint64_t(1) << 16);
+  const uint64_t hi = uint64_t(1024 >> 4) | (uint64_t(1) << 14) | (uint64_t(2) << 29);
+  return lo | (hi << 32);
+}
+// Instruction descriptor, kind::i8: D = S32 (bits [4,6) = 2), A = B = signed 8 bit (bits [7,10) and
+// [10,13) = 1), both K-major (bits 15, 16 = 0), N >> 3 in [17,23), M >> 4 in [24,29).
+constexpr uint32_t kTcIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kTcN >> 3) << 17) |
+                              (uint32_t(kTcM >> 4) << 24);
+
+// ---- expansion: packed bits -> swizzled +-1 int8 image --------------------------------------
+
+// One warp per (row, group of 4 k-chunks): lane = (k-chunk in group) * 8 + 16-byte unit.  Bit b of
+// the row becomes byte 2b - 1; bits at or above dim and rows at or above n_rows become 0 so that
+// they contribute nothing to any dot product.
+__global__ void tc_expand_kernel(uint64_t out_rows, uint64_t n_rows, const uint32_t* __restrict__ src_pos,
+                                 const uint32_t* __restrict__ src_subset, uint64_t pos_base,
+                                 const uint64_t* __restrict__ words, uint32_t stride_words, uint32_t dim,
+                                 uint32_t n_kc, uint8_t* __restrict__ out) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t groups = (n_kc + 3) / 4;
+  const uint64_t row = warp / groups;
+  const uint32_t kc = static_cast<uint32_t>(warp % groups) * 4 + (lane >> 3);
+  if (row >= out_rows || kc >= n_kc) return;
+  const uint32_t unit = lane & 7;
+  uint4 o = make_uint4(0, 0, 0, 0);
+  if (row < n_rows) {
+    uint64_t src = row;
+    if (src_pos) {  // queries: sorted position -> slot -> resident query
+      src = src_pos[pos_base + row];
+      if (src_subset) src = src_subset[src];
+    }
+    const uint32_t bit0 = kc * 128 + unit * 16;
+    const uint32_t widx = bit0 >> 6;
+    uint32_t bits = 0;
+    if (bit0 < dim) bits = static_cast<uint32_t>(words[src * stride_words + widx] >> (bit0 & 63)) & 0xFFFFu;
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t nib = (bits >> (4 * i)) & 0xFu;
+      const uint32_t one = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+      uint32_t v = ((one ^ 0x01010101u) * 0xFFu) | one;  // bit 1 -> 0x01, bit 0 -> 0xFF
+      const uint32_t b = bit0 + 4 * i;                    // zero the bytes of dimensions >= dim
+      if (b + 4 > dim) {
+        uint32_t keep = 0;
+        for (int j = 0; j < 4; ++j)
+          if (b + j < dim) keep |= 0xFFu << (8 * j);
+        v &= keep;
+      }
+      w[i] = v;
+    }
+    o = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  uint8_t* dst = out + ((uint64_t(kc) * out_rows + row) * 128) + ((unit ^ (row & 7)) << 4);
+  *reinterpret_cast<uint4*>(dst) = o;
+}
+
+// per query tile of the batch: union [lo, hi) of the windows of its 128 sorted positions
+__global__ void tc_tile_ranges_kernel(uint64_t n, const uint64_t* __restrict__ keys, uint32_t n_tiles,
+                                      uint2* __restrict__ ranges) {
+  const uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (tile >= n_tiles) return;
+  uint32_t lo = kNone, hi = 0;
+  for (uint32_t j = lane; j < kTcM; j += 32) {
+    const uint64_t p = uint64_t(tile) * kTcM + j;
+    if (p >= n) break;
+    const uint64_t key = keys[p];
+    if (key == ~0ull) continue;
+    lo = min(lo, static_cast<uint32_t>(key >> 32));
+    hi = max(hi, static_cast<uint32_t>(key));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (lane == 0) ranges[tile] = (lo == kNone || hi <= lo) ? make_uint2(0, 0) : make_uint2(lo, hi);
+}
+
+// ---- the search kernel ----------------------------------------------------------------------
+
+__device__ __forceinline__ bool key_less(uint64_t ad1, uint32_t rk1, uint64_t ad2, uint32_t rk2) {
+  return ad1 != ad2 ? ad1 < ad2 : rk1 < rk2;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams p) {
+  extern __shared__ unsigned char tc_smem_raw[];
+  const uint32_t raw = smem_u32(tc_smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-byte alignment
+  unsigned char* gen_base = tc_smem_raw + (base - raw);
+  const uint32_t bar0 = base + kTcStages * kTcStageBytes;
+  // barriers: full[4], empty[4], tfull[2], tempty[2]; then the TMEM base address
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (kTcStages + s); };
+  auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kTcStages + a); };
+  auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kTcStages + 2 + a); };
+  volatile uint32_t* tmem_slot =
+      reinterpret_cast<volatile uint32_t*>(gen_base + kTcStages * kTcStageBytes + 8 * (2 * kTcStages + 4));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 4);  // one arrival per drain warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(const_cast<uint32_t*>(tmem_slot))),
+                 "r"(kTcTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const uint32_t n_kc = p.n_kc;
+
+  if (warp == 0) {
+    // ===== producer: two bulk copies per stage =====
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+        const TcItem it = p.items[item];
+        const uint32_t n_nt = (it.row_end - it.row_begin + kTcN - 1) / kTcN;
+        const uint8_t* a_src = p.q_x + uint64_t(it.tile) * kTcM * kTcKB;
+        for (uint32_t nt = 0; nt < n_nt; ++nt) {
+          const uint8_t* b_src = p.lib_x + (uint64_t(it.row_begin) + uint64_t(nt) * kTcN) * kTcKB;
+          for (uint32_t kc = 0; kc < n_kc; ++kc) {
+            mbar_wait(empty_bar(stage), phase ^ 1u);
+            const uint32_t sa = base + stage * kTcStageBytes;
+            mbar_expect_tx(full_bar(stage), kTcStageBytes);
+            bulk_g2s(sa, a_src + uint64_t(kc) * p.q_rows * kTcKB, kTcABytes, full_bar(stage));
+            bulk_g2s(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, kTcBBytes, full_bar(stage));
+            if (++stage == kTcStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer: one thread =====
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;  // aphase: one parity bit per accumulator
+      for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+        const TcItem it = p.items[item];
+        const uint32_t n_nt = (it.row_end - it.row_begin + kTcN - 1) / kTcN;
+        for (uint32_t nt = 0; nt < n_nt; ++nt) {
+          mbar_wait(tempty_bar(acc), ((aphase >> acc) & 1u) ^ 1u);  // drain warps released this accumulator
+          aphase ^= 1u << acc;
+          tc_fence_after();
+          const uint32_t tmem_d = tmem_base + acc * kTcN;
+          for (uint32_t kc = 0; kc < n_kc; ++kc) {
+            mbar_wait(full_bar(stage), phase);
+            tc_fence_after();
+            const uint32_t sa = base + stage * kTcStageBytes;
+            const uint64_t adesc = tc_smem_desc(sa);
+            const uint64_t bdesc = tc_smem_desc(sa + kTcABytes);
+#pragma unroll
+            for (uint32_t k = 0; k < kTcKB / 32; ++k)  // +32 bytes along K inside the swizzle atom
+              tc_mma_i8(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdesc, (kc | k) != 0u);
+            tc_commit(empty_bar(stage));  // stage reusable once these MMAs have read it
+            if (++stage == kTcStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          tc_commit(tfull_bar(acc));  // accumulator complete
+          acc ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ===== drain warps 2..5: TMEM -> running best per query =====
+    const int quarter = warp & 3;  // a warp may only touch TMEM lanes [32 * (warp % 4), +32)
+    const int qrow = quarter * 32 + lane;
+    uint32_t acc = 0, tphase = 0;
+    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      const TcItem it = p.items[item];
+      const uint32_t n_nt = (it.row_end - it.row_begin + kTcN - 1) / kTcN;
+      const uint64_t pos = uint64_t(it.tile) * kTcM + qrow;
+      uint32_t lf = 0, ll = 0;
+      double qmz = 0.0;
+      if (pos < p.n) {
+        const uint64_t key = p.keys[pos];
+        if (key != ~0ull) {
+          lf = static_cast<uint32_t>(key >> 32);
+          ll = static_cast<uint32_t>(key);
+        }
+        const uint32_t slot = p.vals[pos];
+        qmz = p.q_mz[p.subset ? p.subset[slot] : slot];
+      }
+      int best_dot = INT_MIN;
+      uint32_t best_row = kNone, best_rk = 0;
+      uint64_t best_ad = 0;
+      bool have_key = false;
+
+      for (uint32_t nt = 0; nt < n_nt; ++nt) {
+        const uint32_t row0 = it.row_begin + nt * kTcN;
+        // this query's valid columns [c0, c1) of the tile
+        int c0 = lf > row0 ? static_cast<int>(min(lf - row0, uint32_t(kTcN))) : 0;
+        int c1 = ll > row0 ? static_cast<int>(min(ll - row0, uint32_t(kTcN))) : 0;
+        if (c1 <= c0) c0 = c1 = 0;
+
+        mbar_wait(tfull_bar(acc), (tphase >> acc) & 1u);
+        tphase ^= 1u << acc;
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + acc * kTcN;
+
+        // pass 1: maximum over the valid columns
+        int m = INT_MIN;
+#pragma unroll 1
+        for (int ch = 0; ch < kTcN / 32; ++ch) {
+          int v[32];
+          tc_ld32(taddr + ch * 32, v);
+          const int cb = ch * 32;
+          if (c0 <= cb && cb + 32 <= c1) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) m = max(m, v[j]);
+          } else if (cb < c1 && cb + 32 > c0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (cb + j >= c0 && cb + j < c1) m = max(m, v[j]);
+          }
+        }
+        // pass 2 (rare after the first tiles): locate the columns that reach the maximum
+        const bool need = c1 > c0 && m >= best_dot;
+        if (__any_sync(0xffffffffu, need)) {
+#pragma unroll 1
+          for (int ch = 0; ch < kTcN / 32; ++ch) {
+            int v[32];
+            tc_ld32(taddr + ch * 32, v);
+            const int cb = ch * 32;
+            uint32_t hits = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) hits |= (v[j] == m ? 1u : 0u) << j;
+            if (!need) hits = 0;
+            while (hits) {
+              const int j = __ffs(hits) - 1;
+              hits &= hits - 1;
+              const int c = cb + j;
+              if (c < c0 || c >= c1) continue;
+              const uint32_t r = row0 + c;
+              if (m > best_dot) {
+                best_dot = m;
+                best_row = r;
+                have_key = false;
+              } else {  // tie on score: |mass diff|, then id, then ordinal (search.cpp:137-145)
+                if (!have_key) {
+                  best_ad = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - p.lib_mz[best_row])));
+                  best_rk = p.lib_rank[best_row];
+                  have_key = true;
+                }
+                const uint64_t ad = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - p.lib_mz[r])));
+                const uint32_t rk = p.lib_rank[r];
+                if (key_less(ad, rk, best_ad, best_rk)) {
+                  best_row = r;
+                  best_ad = ad;
+                  best_rk = rk;
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty_bar(acc));
+        acc ^= 1u;
+      }
+
+      Cand out{kNone, kNone, ~0ull};
+      if (best_row != kNone) {
+        if (!have_key) {
+          best_ad = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - p.lib_mz[best_row])));
+          best_rk = p.lib_rank[best_row];
+        }
+        // dot = dim - 2 * distance
+        out.d = static_cast<uint32_t>(static_cast<int>(p.dim) - best_dot) >> 1;
+        out.rk = best_rk;
+        out.ad = best_ad;
+      }
+      p.partial[uint64_t(item) * kTcM + qrow] = out;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcTmemCols)
+                 : "memory");
+  }
+}
+
+// per sorted position: minimum over the items of its query tile
+__global__ void tc_reduce_kernel(uint64_t n, const uint32_t* __restrict__ vals,
+                                 const uint32_t* __restrict__ tile_item_start,
+                                 const uint32_t* __restrict__ tile_items, const Cand* __restrict__ partial,
+                                 Cand* __restrict__ out, uint32_t k_stride) {
+  const uint64_t pos = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (pos >= n) return;
+  const uint32_t t = static_cast<uint32_t>(pos / kTcM), r = static_cast<uint32_t>(pos % kTcM);
+  Cand best{kNone, kNone, ~0ull};
+  for (uint32_t i = tile_item_start[t]; i < tile_item_start[t + 1]; ++i) {
+    const Cand c = partial[uint64_t(tile_items[i]) * kTcM + r];
+    if (c.d != best.d ? c.d < best.d : key_less(c.ad, c.rk, best.ad, best.rk)) best = c;
+  }
+  out[uint64_t(vals[pos]) * k_stride] = best;
+}
+
+// ---- host side --------------------------------------------------------------------------------
+
+bool tc_available(const homs_b200_ctx* ctx) { return ctx->lib.d_x.p != nullptr && ctx->lib.x_rows > 0; }
+
+int tc_expand_library(homs_b200_ctx* ctx) {
+  Library& lib = ctx->lib;
+  lib.n_kc = (lib.dim + kTcKB - 1) / kTcKB;
+  lib.x_rows = (lib.n_local + kTcN - 1) / kTcN * kTcN + kTcN;
+  HB_TRY(ensure(ctx, lib.d_x, size_t(lib.n_kc) * lib.x_rows * kTcKB));
+  const uint32_t groups = (lib.n_kc + 3) / 4;
+  const uint64_t warps = lib.x_rows * groups;
+  tc_expand_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+      lib.x_rows, lib.n_local, nullptr, nullptr, 0, lib.d_words.as<uint64_t>(), lib.S, lib.dim, lib.n_kc,
+      lib.d_x.as<uint8_t>());
+  HB_LAUNCHED(ctx);
+  return HOMS_B200_OK;
+}
+
+int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
+                     const uint32_t* d_vals, Cand* d_out, uint32_t k_stride) {
+  const Library& lib = ctx->lib;
+  const Queries& q = ctx->q;
+  HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kTcSmemBytes)));
+  const uint32_t q_stride = stride_for(q.dim);
+  for (uint64_t b0 = 0; b0 < n; b0 += kTcBatch) {
+    const uint64_t nb = std::min<uint64_t>(kTcBatch, n - b0);
+    const uint32_t n_tiles = static_cast<uint32_t>((nb + kTcM - 1) / kTcM);
+    const uint64_t q_rows = uint64_t(n_tiles) * kTcM;
+
+    // 1. union window of every query tile -> host
+    HB_TRY(ensure(ctx, ctx->scratch[kScrTcTiles], size_t(n_tiles) * sizeof(uint2)));
+    auto* d_ranges = ctx->scratch[kScrTcTiles].as<uint2>();
+    tc_tile_ranges_kernel<<<(n_tiles * 32 + 255) / 256, 256, 0, ctx->stream>>>(nb, d_keys + b0, n_tiles, d_ranges);
+    HB_LAUNCHED(ctx);
+    // 2. expand the batch's queries in sorted order (overlaps with the host planning below)
+    HB_TRY(ensure(ctx, ctx->scratch[kScrTcQx], size_t(lib.n_kc) * q_rows * kTcKB));
+    {
+      const uint32_t groups = (lib.n_kc + 3) / 4;
+      const uint64_t warps = q_rows * groups;
+      tc_expand_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+          q_rows, nb, d_vals, d_subset, b0, q.d_words.as<uint64_t>(), q_stride, q.dim, lib.n_kc,
+          ctx->scratch[kScrTcQx].as<uint8_t>());
+      HB_LAUNCHED(ctx);
+    }
+    // tuning knobs (development): query tiles per L2 group, work items per SM
+    uint32_t group_tiles = kTcGroupTiles, items_per_sm = 400;
+    if (const char* e = getenv("HOMS_B200_TC_GROUP")) group_tiles = std::max(1, atoi(e));
+    if (const char* e = getenv("HOMS_B200_TC_ITEMS_PER_SM")) items_per_sm = std::max(1, atoi(e));
+    const size_t plan_cap_items = size_t(ctx->sm_count) * (items_per_sm + 8) + 2 * size_t(n_tiles) + 64;
+    const size_t pinned_bytes = size_t(n_tiles) * sizeof(uint2) + plan_cap_items * (sizeof(TcItem) + 4) +
+                                (size_t(n_tiles) + 1) * 4 + 256;
+    HB_TRY(ensure_pinned_plan(ctx, pinned_bytes));
+    auto* h_ranges = static_cast<uint2*>(ctx->pinned_plan);
+    HB_CUDA(ctx, cudaMemcpyAsync(h_ranges, d_ranges, size_t(n_tiles) * sizeof(uint2), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+
+    // 3. plan: strips of row tiles at absolute multiples of `strip` tiles; items ordered
+    //    (query-tile group, strip, tile) so that concurrently running CTAs share operands in L2
+    std::vector<uint32_t> t_lo(n_tiles), t_hi(n_tiles);  // in 256-row tiles
+    uint64_t work = 0;
+    for (uint32_t t = 0; t < n_tiles; ++t) {
+      t_lo[t] = h_ranges[t].x / kTcN;
+      t_hi[t] = h_ranges[t].y > h_ranges[t].x ? (h_ranges[t].y + kTcN - 1) / kTcN : t_lo[t];
+      work += t_hi[t] - t_lo[t];
+    }
+    const uint64_t target = uint64_t(ctx->sm_count) * items_per_sm;
+    const uint32_t strip = static_cast<uint32_t>(std::max<uint64_t>(1, (work + target - 1) / target));
+    std::vector<TcItem> items;
+    std::vector<std::vector<uint32_t>> per_tile(n_tiles);
+    for (uint32_t g0 = 0; g0 < n_tiles; g0 += group_tiles) {
+      const uint32_t g1 = std::min(n_tiles, g0 + group_tiles);
+      uint32_t lo = ~0u, hi = 0;
+      for (uint32_t t = g0; t < g1; ++t)
+        if (t_hi[t] > t_lo[t]) {
+          lo = std::min(lo, t_lo[t]);
+          hi = std::max(hi, t_hi[t]);
+        }
+      if (lo == ~0u) continue;
+      for (uint32_t s = lo / strip; s * uint64_t(strip) < hi; ++s)
+        for (uint32_t t = g0; t < g1; ++t) {
+          const uint32_t a = std::max<uint32_t>(t_lo[t], s * strip);
+          const uint32_t b = std::min<uint64_t>(t_hi[t], (uint64_t(s) + 1) * strip);
+          if (b <= a) continue;
+          per_tile[t].push_back(static_cast<uint32_t>(items.size()));
+          items.push_back(TcItem{t, a * kTcN, b * kTcN, 0});
+        }
+    }
+    const uint32_t n_items = static_cast<uint32_t>(items.size());
+    HB_REQUIRE(ctx, n_items <= plan_cap_items, HOMS_B200_ERR_STATE, "tensor search: plan overflow");
+    auto* h_items = reinterpret_cast<TcItem*>(static_cast<unsigned char*>(ctx->pinned_plan) +
+                                              (size_t(n_tiles) * sizeof(uint2) + 15) / 16 * 16);
+    auto* h_start = reinterpret_cast<uint32_t*>(h_items + plan_cap_items);
+    auto* h_list = h_start + n_tiles + 1;
+    std::memcpy(h_items, items.data(), size_t(n_items) * sizeof(TcItem));
+    uint32_t cursor = 0;
+    for (uint32_t t = 0; t < n_tiles; ++t) {
+      h_start[t] = cursor;
+      for (uint32_t i : per_tile[t]) h_list[cursor++] = i;
+    }
+    h_start[n_tiles] = cursor;
+
+    const size_t plan_bytes = plan_cap_items * (sizeof(TcItem) + 4) + (size_t(n_tiles) + 1) * 4;
+    HB_TRY(ensure(ctx, ctx->scratch[kScrTcPlan], plan_bytes));
+    auto* d_items = ctx->scratch[kScrTcPlan].as<TcItem>();
+    auto* d_start = reinterpret_cast<uint32_t*>(d_items + plan_cap_items);
+    auto* d_list = d_start + n_tiles + 1;
+    HB_CUDA(ctx, cudaMemcpyAsync(d_items, h_items, plan_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], std::max<size_t>(1, n_items) * kTcM * sizeof(Cand)));
+
+    // 4. search + reduce
+    if (n_items > 0) {
+      TcParams tp;
+      tp.lib_x = lib.d_x.as<uint8_t>();
+      tp.q_x = ctx->scratch[kScrTcQx].as<uint8_t>();
+      tp.lib_rows = lib.x_rows;
+      tp.q_rows = q_rows;
+      tp.n_kc = lib.n_kc;
+      tp.dim = lib.dim;
+      tp.items = d_items;
+      tp.n_items = n_items;
+      tp.pad = 0;
+      tp.keys = d_keys + b0;
+      tp.vals = d_vals + b0;
+      tp.subset = d_subset;
+      tp.q_mz = q.d_mz.as<double>();
+      tp.lib_mz = lib.d_mz_local.as<double>();
+      tp.lib_rank = lib.d_id_rank_local.as<uint32_t>();
+      tp.n = nb;
+      tp.partial = ctx->scratch[kScrTcPartial].as<Cand>();
+      const int grid = static_cast<int>(std::min<uint32_t>(n_items, static_cast<uint32_t>(ctx->sm_count)));
+      {
+        KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
+        tc_search_kernel<<<grid, kTcThreads, kTcSmemBytes, ctx->stream>>>(tp);
+      }
+      HB_LAUNCHED(ctx);
+    }
+    tc_reduce_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, ctx->stream>>>(
+        nb, d_vals + b0, d_start, d_list, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k_stride);
+    HB_LAUNCHED(ctx);
+    // the pinned plan block is reused by the next batch
+    if (b0 + kTcBatch < n) HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  return HOMS_B200_OK;
+}
+
+}  // namespace hb

@@ -220,6 +220,12 @@ class Context:
     def set_stream(self, cuda_stream: int | None) -> None:
         _check(capi.ctx_set_stream(self._h, cuda_stream or 0), self._h)
 
+    def set_engine(self, engine: str | int) -> None:
+        """Top-1 search engine: "auto" (tensor when available), "popc" or "tensor".  Choose it
+        before build_index: "popc" skips the tensor image of the library."""
+        code = {"auto": capi.ENGINE_AUTO, "popc": capi.ENGINE_POPC, "tensor": capi.ENGINE_TENSOR}.get(engine, engine)
+        _check(capi.ctx_set_engine(self._h, int(code)), self._h)
+
     def synchronize(self) -> None:
         _check(capi.ctx_synchronize(self._h), self._h)
 

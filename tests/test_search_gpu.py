@@ -9,6 +9,16 @@ from tests import _util as U
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["tensor", "popc"])
+def ctx(hb, request):
+    """Every search test runs on both top-1 engines: the tcgen05 int8 contraction and XOR+POPC."""
+    c = hb.Context(0)
+    c.set_engine(request.param)
+    c.engine_name = request.param
+    yield c
+    c.close()
+
+
 def _index(ctx, c):
     dim = int(c["dim"][0])
     ids = [x.decode() for x in c["ids"]]
@@ -162,7 +172,7 @@ def test_sharded_search_merges_to_single(hb):
     candidates -> concatenate (what the all-gather yields) -> merge == unsharded result."""
     import torch
     rng = np.random.default_rng(23)
-    dim, n, nq, k = 1024, 4000, 200, 3
+    dim, n, nq = 1024, 4000, 200
     words = U.random_hvs(rng, n, dim)
     words[3500:] = words[:500]
     mz = np.round(rng.uniform(400.0, 1200.0, n), 2)
@@ -173,7 +183,9 @@ def test_sharded_search_merges_to_single(hb):
     qch = rng.integers(2, 5, nq).astype(np.uint8)
     with hb.Context(0) as single:
         single.build_index(dim, words, mz, charge, ids=ids)
-        for tol in (hb.Tolerance("dalton", 500.0), hb.Tolerance("ppm", 30.0)):
+        # k = 3 runs on the POPC engine, k = 1 on the tensor engine
+        for tol, k in ((hb.Tolerance("dalton", 500.0), 3), (hb.Tolerance("ppm", 30.0), 3),
+                       (hb.Tolerance("dalton", 500.0), 1), (hb.Tolerance("ppm", 30.0), 1)):
             want = single.search_batch(qw, qmz, qch, tol, k=k)
             for G in (2, 3, 8):
                 gathered = torch.zeros(G, nq * k * 16, dtype=torch.uint8, device="cuda")
@@ -191,8 +203,8 @@ def test_sharded_search_merges_to_single(hb):
                 score, ordinal = shards[0].candidates_decode(nq, k, out.data_ptr())
                 for c in shards:
                     c.close()
-                assert np.array_equal(ordinal, want.ordinal), (tol, G)
-                assert np.array_equal(score, want.raw_score), (tol, G)
+                assert np.array_equal(ordinal, want.ordinal), (tol, k, G)
+                assert np.array_equal(score, want.raw_score), (tol, k, G)
 
 
 def test_large_open_search_properties(hb, ctx):
@@ -216,3 +228,46 @@ def test_large_open_search_properties(hb, ctx):
         s = ctx.search_batch(qw, mz[pick], charge[pick], hb.Tolerance("dalton", da)).raw_score[:, 0]
         assert (s >= prev).all()
         prev = s
+
+
+def test_many_queries_span_planning_batches(hb, best_oracle):
+    """More than 65536 queries: the tensor engine plans in batches of 64k sorted slots; results
+    must equal the POPC engine's and (on a sample) the oracle's.  Also: a query set that reaches
+    no bucket at all (no work items)."""
+    rng = np.random.default_rng(41)
+    dim, n, nq = 128, 3000, 70000
+    words = U.random_hvs(rng, n, dim)
+    words[2500:] = words[:500]
+    mz = np.round(rng.uniform(400.0, 1200.0, n), 2)
+    charge = rng.integers(2, 4, n).astype(np.uint8)
+    ids = [f"m{rng.integers(0, 700)}" for _ in range(n)]
+    qw = words[rng.integers(0, n, nq)] ^ U.random_hvs(rng, nq, dim) & U.random_hvs(rng, nq, dim)
+    qmz = np.round(rng.uniform(380.0, 1220.0, nq), 2)
+    qch = rng.integers(1, 4, nq).astype(np.uint8)
+    got = {}
+    for eng in ("tensor", "popc"):
+        with hb.Context(0) as c:
+            c.set_engine(eng)
+            c.build_index(dim, words, mz, charge, ids=ids)
+            got[eng] = c.search_batch(qw, qmz, qch, hb.Tolerance("dalton", 3.0))
+            none = c.search_batch(qw[:300], qmz[:300], np.zeros(300, np.uint8), hb.Tolerance("dalton", 3.0))
+            assert not none.has_hit.any()
+    assert np.array_equal(got["tensor"].ordinal, got["popc"].ordinal)
+    assert np.array_equal(got["tensor"].raw_score, got["popc"].raw_score)
+    oix = best_oracle.build_index(dim, words, mz, charge, None, ids)
+    sample = rng.integers(0, nq, 2000)
+    has, score, ordinal, _ = oix.search_batch(qw[sample], qmz[sample], qch[sample], ("da", 3.0), threads=8)
+    assert np.array_equal(got["tensor"].ordinal[sample, 0], ordinal)
+    assert np.array_equal(got["tensor"].raw_score[sample, 0], score)
+    oix.close()
+
+
+def test_engine_selection_errors(hb):
+    with hb.Context(0) as c:
+        with pytest.raises(hb.HomsError):
+            c.set_engine(7)
+        c.set_engine("popc")
+        rng = np.random.default_rng(3)
+        c.build_index(256, U.random_hvs(rng, 10, 256), np.linspace(500, 600, 10), [2] * 10)
+        with pytest.raises(hb.HomsError):  # no tensor image was built for this library
+            c.set_engine("tensor")
