@@ -1,0 +1,458 @@
+// homs_b200/homs.hpp -- C++20 host facade over the C ABI (include/homs_b200.h).
+//
+// It keeps the call shapes of the reference's encoder/search API so that a caller of `homs_core`
+// can switch to the GPU by changing a namespace (paths under /root/reference/proj/core/):
+//
+//   encode_spectra   include/homs/pipeline.hpp:45-48     src/pipeline.cpp:60-85
+//   encode           include/homs/encoder.hpp:20         src/encoder.cpp:19-55
+//   build_index      include/homs/search.hpp:82          src/search.cpp:17-60
+//   search_one       include/homs/search.hpp:99-100      src/search.cpp:105-169
+//   search_batch     include/homs/search.hpp:104-107     src/search.cpp:171-183
+//   cascade_search   include/homs/search.hpp:114-117     src/search.cpp:219-248
+//
+// The facade is header-only and generic over the data types: instantiate it with a traits struct
+// that names the caller's own types.  With the reference's headers that is
+//
+//   struct HomsApi {
+//     using RawSpectrum = homs::RawSpectrum;   using EncodedSpectrum = homs::EncodedSpectrum; ...
+//   };
+//   auto out = homs_b200::encode_spectra<HomsApi>(spectra, codebook, preprocess, threads, batch);
+//
+// and homs_b200::types / homs_b200::DefaultApi provide structurally identical stand-alone types.
+// Errors surface as the Api's ConfigError / InvariantError (include/homs/errors.hpp:16-56) with the
+// library's message; everything else as Api::Error.  `threads` and `batch_size` are accepted for
+// signature parity and never change results (search.hpp:102-103).  There is no CPU fallback: every
+// call needs a CUDA device.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../homs_b200.h"
+
+namespace homs_b200 {
+
+// ---- stand-alone mirror of the reference's boundary types -----------------------------------
+namespace types {
+
+struct Error : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ConfigError : Error { using Error::Error; };
+struct InvariantError : Error { using Error::Error; };
+
+struct Peak { double mz = 0.0, intensity = 0.0; };
+struct SpectrumMeta {
+  std::string id;
+  double precursor_mz = 0.0;
+  std::uint8_t charge = 0;
+  bool is_decoy = false;
+  std::string peptide;
+};
+struct RawSpectrum { SpectrumMeta meta; std::vector<Peak> peaks; };
+
+class Hypervector {
+ public:
+  Hypervector() = default;
+  explicit Hypervector(std::uint32_t bits) : bits_(bits), words_((std::size_t(bits) + 63) / 64, 0) {}
+  std::uint32_t size_bits() const noexcept { return bits_; }
+  std::span<const std::uint64_t> words() const noexcept { return words_; }
+  std::span<std::uint64_t> words() noexcept { return words_; }
+  friend bool operator==(const Hypervector&, const Hypervector&) = default;
+ private:
+  std::uint32_t bits_ = 0;
+  std::vector<std::uint64_t> words_;
+};
+
+struct EncodedSpectrum { SpectrumMeta meta; Hypervector hv; };
+enum class IntensityScaling : std::uint8_t { none = 0, sqrt = 1 };
+struct PreprocessConfig {
+  double min_mz = 101.0, max_mz = 1500.0, bin_size = 0.05;
+  std::uint32_t max_peaks = 50, min_peaks = 10;
+  double intensity_floor = 0.01;
+  IntensityScaling scaling = IntensityScaling::none;
+};
+struct EncoderConfig { std::uint32_t dim = 8192, step_flips = 4096, levels = 16; std::uint64_t seed = 1; };
+struct Codebook {
+  EncoderConfig config;
+  std::uint32_t spectrum_dims = 0;
+  std::vector<Hypervector> position, level;
+};
+struct SpectrumVector {
+  std::uint32_t dims = 0;
+  std::vector<std::uint32_t> bins;
+  std::vector<double> intensities;
+  SpectrumMeta meta;
+};
+struct Tolerance {
+  enum class Kind : std::uint8_t { ppm, dalton };
+  Kind kind = Kind::ppm;
+  double value = 20.0;
+};
+enum class SearchStage : std::uint8_t { narrow = 0, wide = 1 };
+struct Ssm {
+  std::string query_id, library_id, peptide;
+  std::uint8_t charge = 0;
+  double query_precursor_mz = 0.0, library_precursor_mz = 0.0, mass_diff = 0.0;
+  std::uint32_t raw_score = 0;
+  double score = 0.0;
+  bool is_decoy = false;
+  SearchStage stage = SearchStage::narrow;
+  std::optional<double> q_value;
+};
+struct EncodeOutcome { std::vector<EncodedSpectrum> encoded; std::size_t unprocessable = 0; };
+struct SearchOptions { unsigned threads = 1; std::size_t batch_size = 512; };
+
+}  // namespace types
+
+struct DefaultApi {
+  using Error = types::Error;
+  using ConfigError = types::ConfigError;
+  using InvariantError = types::InvariantError;
+  using SpectrumMeta = types::SpectrumMeta;
+  using RawSpectrum = types::RawSpectrum;
+  using Hypervector = types::Hypervector;
+  using EncodedSpectrum = types::EncodedSpectrum;
+  using PreprocessConfig = types::PreprocessConfig;
+  using Codebook = types::Codebook;
+  using SpectrumVector = types::SpectrumVector;
+  using Tolerance = types::Tolerance;
+  using SearchStage = types::SearchStage;
+  using Ssm = types::Ssm;
+  using EncodeOutcome = types::EncodeOutcome;
+  using SearchOptions = types::SearchOptions;
+};
+
+namespace detail {
+
+template <class Api>
+[[noreturn]] inline void raise(int rc, const homs_b200_ctx* ctx) {
+  const char* m = homs_b200_last_error(ctx);
+  const std::string msg = (m && *m) ? m : ("homs_b200 error " + std::to_string(rc));
+  if (rc == HOMS_B200_ERR_CONFIG) throw typename Api::ConfigError(msg);
+  if (rc == HOMS_B200_ERR_INVARIANT) throw typename Api::InvariantError(msg);
+  throw typename Api::Error(msg);
+}
+template <class Api>
+inline void check(int rc, const homs_b200_ctx* ctx) {
+  if (rc != HOMS_B200_OK) raise<Api>(rc, ctx);
+}
+
+struct CtxDeleter { void operator()(homs_b200_ctx* c) const { homs_b200_ctx_destroy(c); } };
+using CtxPtr = std::unique_ptr<homs_b200_ctx, CtxDeleter>;
+
+template <class Api>
+inline CtxPtr make_ctx(int device) {
+  homs_b200_ctx* raw = nullptr;
+  const int rc = homs_b200_ctx_create(device, &raw);
+  if (rc != HOMS_B200_OK) raise<Api>(rc, nullptr);
+  return CtxPtr(raw);
+}
+
+template <class Cfg>
+inline homs_b200_preprocess_config pod(const Cfg& c) {
+  homs_b200_preprocess_config p{};
+  p.min_mz = c.min_mz;
+  p.max_mz = c.max_mz;
+  p.bin_size = c.bin_size;
+  p.max_peaks = c.max_peaks;
+  p.min_peaks = c.min_peaks;
+  p.intensity_floor = c.intensity_floor;
+  p.scaling = static_cast<std::uint32_t>(c.scaling);
+  return p;
+}
+
+template <class Tol>
+inline homs_b200_tolerance pod_tol(const Tol& t) {
+  homs_b200_tolerance p{};
+  p.kind = t.kind == Tol::Kind::ppm ? HOMS_B200_TOL_PPM : HOMS_B200_TOL_DALTON;
+  p.value = t.value;
+  return p;
+}
+
+// dense row-major words of a list of hypervectors
+template <class Range, class GetHv>
+inline std::vector<std::uint64_t> flatten(const Range& items, std::size_t W, GetHv get) {
+  std::vector<std::uint64_t> flat(items.size() * W);
+  std::size_t i = 0;
+  for (const auto& it : items) {
+    const auto w = get(it).words();
+    std::memcpy(flat.data() + i * W, w.data(), W * sizeof(std::uint64_t));
+    ++i;
+  }
+  return flat;
+}
+
+// One context per device for encoding; remembers which codebook is resident.
+template <class Api>
+struct Encoder {
+  CtxPtr ctx;
+  std::mutex mu;
+  const void* cb_data = nullptr;
+  std::uint64_t cb_tag = 0;
+
+  static Encoder& on(int device) {
+    static std::mutex table_mu;
+    static std::vector<std::unique_ptr<Encoder>> table;
+    std::lock_guard<std::mutex> g(table_mu);
+    if (table.size() <= static_cast<std::size_t>(device)) table.resize(device + 1);
+    if (!table[device]) {
+      table[device] = std::make_unique<Encoder>();
+      table[device]->ctx = make_ctx<Api>(device);
+    }
+    return *table[device];
+  }
+
+  void ensure_codebook(const typename Api::Codebook& cb) {
+    const std::uint32_t dim = cb.config.dim;
+    const std::size_t W = (std::size_t(dim) + 63) / 64;
+    if (cb.position.size() != cb.spectrum_dims || cb.level.size() != std::size_t(cb.config.levels) + 1)
+      throw typename Api::InvariantError("encode: codebook shape does not match its configuration");
+    // identity of the resident codebook: storage address + a few sampled words
+    std::uint64_t tag = (std::uint64_t(dim) << 32) ^ cb.spectrum_dims ^ (cb.config.seed * 0x9E3779B97F4A7C15ull);
+    for (std::size_t i = 0; i < cb.position.size(); i += cb.position.size() / 7 + 1)
+      tag = tag * 1099511628211ull ^ cb.position[i].words()[0];
+    for (const auto& l : cb.level) tag = tag * 1099511628211ull ^ l.words()[W - 1];
+    if (cb_data == static_cast<const void*>(cb.position.data()) && cb_tag == tag) return;
+    const auto pos = flatten(cb.position, W, [](const auto& h) -> const auto& { return h; });
+    const auto lvl = flatten(cb.level, W, [](const auto& h) -> const auto& { return h; });
+    check<Api>(homs_b200_codebook_upload(ctx.get(), dim, cb.spectrum_dims, cb.config.levels, pos.data(),
+                                         lvl.data()),
+               ctx.get());
+    cb_data = cb.position.data();
+    cb_tag = tag;
+  }
+};
+
+}  // namespace detail
+
+// ---- LibraryIndex (search.hpp:39-66): the device-resident index --------------------------------
+// Owns a context whose library is the charge-partitioned, m/z-sorted matrix built by
+// homs_b200_library_upload; keeps the metadata in input order like the reference (search.cpp:27).
+template <class Api = DefaultApi>
+class LibraryIndex {
+ public:
+  std::uint32_t dim() const noexcept { return dim_; }
+  std::size_t size() const noexcept { return metas_.size(); }
+  const typename Api::SpectrumMeta& meta(std::size_t ordinal) const { return metas_[ordinal]; }
+  homs_b200_ctx* context() const noexcept { return ctx_.get(); }
+  const std::vector<std::uint8_t>& decoy_flags() const noexcept { return decoy_; }
+
+ private:
+  template <class A>
+  friend LibraryIndex<A> build_index(std::span<const typename A::EncodedSpectrum>, int);
+  std::uint32_t dim_ = 0;
+  std::vector<typename Api::SpectrumMeta> metas_;
+  std::vector<std::uint8_t> decoy_;
+  detail::CtxPtr ctx_;
+};
+
+// ---- encode_spectra (pipeline.cpp:60-85) --------------------------------------------------------
+template <class Api = DefaultApi>
+typename Api::EncodeOutcome encode_spectra(std::span<const typename Api::RawSpectrum> spectra,
+                                           const typename Api::Codebook& codebook,
+                                           const typename Api::PreprocessConfig& preprocess,
+                                           unsigned /*threads*/ = 1, std::size_t /*batch_size*/ = 0,
+                                           int device = 0) {
+  auto& enc = detail::Encoder<Api>::on(device);
+  std::lock_guard<std::mutex> g(enc.mu);
+  typename Api::EncodeOutcome outcome;
+  if (spectra.empty()) return outcome;
+  enc.ensure_codebook(codebook);
+  const std::size_t n = spectra.size();
+  const std::uint32_t dim = codebook.config.dim;
+  const std::size_t W = (std::size_t(dim) + 63) / 64;
+  std::vector<std::uint64_t> offsets(n + 1, 0);
+  for (std::size_t i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + spectra[i].peaks.size();
+  std::vector<double> mz(offsets[n]), intensity(offsets[n]);
+  for (std::size_t i = 0; i < n; ++i) {
+    std::size_t o = offsets[i];
+    for (const auto& p : spectra[i].peaks) {
+      mz[o] = p.mz;
+      intensity[o] = p.intensity;
+      ++o;
+    }
+  }
+  std::vector<std::uint64_t> words(n * W);
+  std::vector<std::uint8_t> ok(n);
+  const auto cfg = detail::pod(preprocess);
+  detail::check<Api>(homs_b200_encode_batch(enc.ctx.get(), &cfg, n, offsets.data(), mz.data(), intensity.data(),
+                                            words.data(), ok.data()),
+                     enc.ctx.get());
+  outcome.encoded.reserve(n);
+  for (std::size_t i = 0; i < n; ++i) {  // order-preserving compaction, pipeline.cpp:75-83
+    if (!ok[i]) {
+      ++outcome.unprocessable;
+      continue;
+    }
+    typename Api::EncodedSpectrum e{spectra[i].meta, typename Api::Hypervector(dim)};
+    std::memcpy(e.hv.words().data(), words.data() + i * W, W * sizeof(std::uint64_t));
+    outcome.encoded.push_back(std::move(e));
+  }
+  return outcome;
+}
+
+// ---- encode (encoder.cpp:19-55) on one vectorized spectrum --------------------------------------
+template <class Api = DefaultApi>
+typename Api::Hypervector encode(const typename Api::SpectrumVector& sv, const typename Api::Codebook& codebook,
+                                 int device = 0) {
+  auto& enc = detail::Encoder<Api>::on(device);
+  std::lock_guard<std::mutex> g(enc.mu);
+  if (sv.dims != codebook.spectrum_dims)  // encoder.cpp:20-22
+    throw typename Api::InvariantError("encode: spectrum vector dimensionality does not match codebook");
+  enc.ensure_codebook(codebook);
+  const std::uint64_t off[2] = {0, sv.bins.size()};
+  typename Api::Hypervector hv(codebook.config.dim);
+  detail::check<Api>(homs_b200_encode_vectors(enc.ctx.get(), 1, off, sv.bins.data(), sv.intensities.data(),
+                                              hv.words().data()),
+                     enc.ctx.get());
+  return hv;
+}
+
+// ---- build_index (search.cpp:17-60) -------------------------------------------------------------
+template <class Api = DefaultApi>
+LibraryIndex<Api> build_index(std::span<const typename Api::EncodedSpectrum> refs, int device = 0) {
+  if (refs.empty()) throw typename Api::InvariantError("build_index: library is empty");  // search.cpp:18
+  LibraryIndex<Api> index;
+  index.dim_ = refs.front().hv.size_bits();
+  const std::size_t n = refs.size(), W = (std::size_t(index.dim_) + 63) / 64;
+  for (const auto& r : refs)
+    if (r.hv.size_bits() != index.dim_)  // search.cpp:24-26
+      throw typename Api::InvariantError("build_index: mixed hypervector dimensionalities");
+  index.metas_.reserve(n);
+  std::vector<double> mz(n);
+  std::vector<std::uint8_t> charge(n);
+  index.decoy_.resize(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    index.metas_.push_back(refs[i].meta);
+    mz[i] = refs[i].meta.precursor_mz;
+    charge[i] = refs[i].meta.charge;
+    index.decoy_[i] = refs[i].meta.is_decoy ? 1 : 0;
+  }
+  // id_rank: position in the sort by (id, ordinal) -- the integer form of search.cpp:43
+  std::vector<std::uint32_t> order(n), rank(n);
+  for (std::size_t i = 0; i < n; ++i) order[i] = static_cast<std::uint32_t>(i);
+  std::stable_sort(order.begin(), order.end(), [&](std::uint32_t a, std::uint32_t b) {
+    return index.metas_[a].id < index.metas_[b].id;
+  });
+  for (std::size_t p = 0; p < n; ++p) rank[order[p]] = static_cast<std::uint32_t>(p);
+  const auto words = detail::flatten(refs, W, [](const auto& r) -> const auto& { return r.hv; });
+  index.ctx_ = detail::make_ctx<Api>(device);
+  detail::check<Api>(homs_b200_library_upload(index.ctx_.get(), index.dim_, n, words.data(), mz.data(),
+                                              charge.data(), rank.data(), 0, 1),
+                     index.ctx_.get());
+  return index;
+}
+
+namespace detail {
+
+template <class Api>
+typename Api::Ssm make_ssm(const typename Api::EncodedSpectrum& query, const LibraryIndex<Api>& index,
+                           std::uint32_t ordinal, std::uint32_t raw_score) {  // search.cpp:155-168
+  const auto& lib = index.meta(ordinal);
+  typename Api::Ssm s;
+  s.query_id = query.meta.id;
+  s.library_id = lib.id;
+  s.peptide = lib.peptide;
+  s.charge = query.meta.charge;
+  s.query_precursor_mz = query.meta.precursor_mz;
+  s.library_precursor_mz = lib.precursor_mz;
+  s.mass_diff = query.meta.precursor_mz - lib.precursor_mz;
+  s.raw_score = raw_score;
+  s.score = static_cast<double>(raw_score) / static_cast<double>(index.dim());
+  s.is_decoy = lib.is_decoy;
+  s.stage = Api::SearchStage::narrow;
+  return s;
+}
+
+template <class Api>
+struct FlatQueries {
+  std::vector<std::uint64_t> words;
+  std::vector<double> mz;
+  std::vector<std::uint8_t> charge;
+  std::uint32_t dim = 0;
+  explicit FlatQueries(std::span<const typename Api::EncodedSpectrum> q, std::uint32_t index_dim) {
+    dim = index_dim;
+    for (const auto& e : q)
+      if (e.hv.size_bits() != index_dim)  // search.cpp:107-109
+        throw typename Api::InvariantError("search_one: query dimensionality does not match index");
+    const std::size_t W = (std::size_t(dim) + 63) / 64;
+    words = flatten(q, W, [](const auto& e) -> const auto& { return e.hv; });
+    mz.reserve(q.size());
+    charge.reserve(q.size());
+    for (const auto& e : q) {
+      mz.push_back(e.meta.precursor_mz);
+      charge.push_back(e.meta.charge);
+    }
+  }
+};
+
+}  // namespace detail
+
+// ---- search_batch / search_one (search.cpp:105-183) ---------------------------------------------
+template <class Api = DefaultApi>
+std::vector<std::optional<typename Api::Ssm>> search_batch(std::span<const typename Api::EncodedSpectrum> queries,
+                                                           const LibraryIndex<Api>& index,
+                                                           const typename Api::Tolerance& tol,
+                                                           const typename Api::SearchOptions& = {}) {
+  std::vector<std::optional<typename Api::Ssm>> results(queries.size());
+  if (queries.empty()) return results;
+  const detail::FlatQueries<Api> q(queries, index.dim());
+  std::vector<std::uint32_t> score(queries.size()), ordinal(queries.size());
+  const auto t = detail::pod_tol(tol);
+  detail::check<Api>(homs_b200_search_batch(index.context(), q.dim, queries.size(), q.words.data(), q.mz.data(),
+                                            q.charge.data(), &t, 1, score.data(), ordinal.data(), nullptr, nullptr),
+                     index.context());
+  for (std::size_t i = 0; i < queries.size(); ++i)
+    if (ordinal[i] != HOMS_B200_NO_HIT) results[i] = detail::make_ssm<Api>(queries[i], index, ordinal[i], score[i]);
+  return results;
+}
+
+template <class Api = DefaultApi>
+std::optional<typename Api::Ssm> search_one(const typename Api::EncodedSpectrum& query,
+                                            const LibraryIndex<Api>& index, const typename Api::Tolerance& tol) {
+  return search_batch<Api>(std::span<const typename Api::EncodedSpectrum>(&query, 1), index, tol)[0];
+}
+
+// ---- cascade_search (search.cpp:219-248) ---------------------------------------------------------
+template <class Api = DefaultApi>
+std::vector<typename Api::Ssm> cascade_search(std::span<const typename Api::EncodedSpectrum> queries,
+                                              const LibraryIndex<Api>& index,
+                                              const typename Api::Tolerance& narrow,
+                                              const typename Api::Tolerance& wide, double fdr_q,
+                                              const typename Api::SearchOptions& = {}) {
+  if (!(narrow.value > 0.0) || !(wide.value > 0.0))  // Tolerance::validate, search.cpp:13-15
+    throw typename Api::ConfigError("tolerance value must be positive");
+  std::vector<typename Api::Ssm> out;
+  if (queries.empty()) return out;
+  const detail::FlatQueries<Api> q(queries, index.dim());
+  const std::size_t n = queries.size();
+  std::vector<std::uint64_t> which(n);
+  std::vector<std::uint32_t> ordinal(n), score(n);
+  std::vector<std::uint8_t> stage(n);
+  std::vector<double> qv(n);
+  std::uint64_t count = 0;
+  const auto tn = detail::pod_tol(narrow), tw = detail::pod_tol(wide);
+  detail::check<Api>(homs_b200_cascade_search(index.context(), q.dim, n, q.words.data(), q.mz.data(),
+                                              q.charge.data(), &tn, &tw, fdr_q, index.decoy_flags().data(),
+                                              which.data(), ordinal.data(), stage.data(), score.data(), qv.data(),
+                                              &count),
+                     index.context());
+  out.reserve(count);
+  for (std::uint64_t m = 0; m < count; ++m) {  // narrow block, then wide, each in query order
+    auto s = detail::make_ssm<Api>(queries[which[m]], index, ordinal[m], score[m]);
+    s.stage = stage[m] == 0 ? Api::SearchStage::narrow : Api::SearchStage::wide;
+    s.q_value = qv[m];
+    out.push_back(std::move(s));
+  }
+  return out;
+}
+
+}  // namespace homs_b200

@@ -1,0 +1,147 @@
+// Parity of the C++ facade (include/homs_b200/homs.hpp) against the UNMODIFIED reference, in the
+// style of the reference's own acceptance binary (proj/tests/acceptance/acceptance_main.cpp):
+// plain main(), one "[PASS]/[FAIL] <check>" line per check, exit code 0 iff all pass.
+//
+// TEST INFRASTRUCTURE: this program links the reference objects compiled by oracle/Makefile and the
+// reference headers from $(REF); it is built only where /root/reference exists (tests/cpp/Makefile)
+// and the binary travels to the GPU box.  Needs a CUDA device to run.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "homs/codebook.hpp"
+#include "homs/encoder.hpp"
+#include "homs/errors.hpp"
+#include "homs/pipeline.hpp"
+#include "homs/preprocess.hpp"
+#include "homs/search.hpp"
+#include "homs/synth.hpp"
+
+#include "homs_b200/homs.hpp"
+
+// the traits a reference maintainer would write
+struct HomsApi {
+  using Error = homs::Error;
+  using ConfigError = homs::ConfigError;
+  using InvariantError = homs::InvariantError;
+  using SpectrumMeta = homs::SpectrumMeta;
+  using RawSpectrum = homs::RawSpectrum;
+  using Hypervector = homs::Hypervector;
+  using EncodedSpectrum = homs::EncodedSpectrum;
+  using PreprocessConfig = homs::PreprocessConfig;
+  using Codebook = homs::Codebook;
+  using SpectrumVector = homs::SpectrumVector;
+  using Tolerance = homs::Tolerance;
+  using SearchStage = homs::SearchStage;
+  using Ssm = homs::Ssm;
+  using EncodeOutcome = homs::EncodeOutcome;
+  using SearchOptions = homs::SearchOptions;
+};
+namespace gpu = homs_b200;
+
+static int g_failed = 0;
+static void report(bool ok, const std::string& what) {
+  std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", what.c_str());
+  if (!ok) ++g_failed;
+}
+
+static bool same_ssm(const homs::Ssm& a, const homs::Ssm& b) {
+  return a.query_id == b.query_id && a.library_id == b.library_id && a.peptide == b.peptide &&
+         a.charge == b.charge && a.query_precursor_mz == b.query_precursor_mz &&
+         a.library_precursor_mz == b.library_precursor_mz && a.mass_diff == b.mass_diff &&
+         a.raw_score == b.raw_score && a.score == b.score && a.is_decoy == b.is_decoy && a.stage == b.stage &&
+         a.q_value.has_value() == b.q_value.has_value() &&
+         (!a.q_value || std::memcmp(&*a.q_value, &*b.q_value, sizeof(double)) == 0);
+}
+
+int main() {
+  using homs::Tolerance;
+  // BASELINE config 1: 5000 targets + 5000 decoys, 1000 queries, D = 2048
+  homs::SynthConfig sc;
+  sc.n_library = 5000;
+  sc.n_query = 1000;
+  sc.fraction_modified = 0.6;
+  sc.seed = 1;
+  homs::SynthOutput synth = homs::generate_benchmark(sc);
+  // a few unprocessable spectra and an unknown-charge query exercise the compaction / bucket rules
+  synth.library[7].peaks.resize(3);
+  synth.queries[11].peaks.clear();
+  synth.queries[5].meta.charge = 0;
+
+  const homs::PreprocessConfig pre;
+  const homs::EncoderConfig ec{2048, 1024, 16, 1};
+  const homs::Codebook cb = homs::make_codebook(homs::dimension(pre), ec);
+
+  const auto ref_lib = homs::encode_spectra(synth.library, cb, pre, 8, 64);
+  const auto gpu_lib = gpu::encode_spectra<HomsApi>(synth.library, cb, pre, 8, 64);
+  report(gpu_lib.unprocessable == ref_lib.unprocessable && gpu_lib.encoded == ref_lib.encoded,
+         "encode_spectra(library): identical EncodedSpectrum list, unprocessable = " +
+             std::to_string(gpu_lib.unprocessable));
+  const auto ref_q = homs::encode_spectra(synth.queries, cb, pre, 8, 64);
+  const auto gpu_q = gpu::encode_spectra<HomsApi>(synth.queries, cb, pre, 1, 0);
+  report(gpu_q.unprocessable == ref_q.unprocessable && gpu_q.encoded == ref_q.encoded,
+         "encode_spectra(queries): identical, unprocessable = " + std::to_string(gpu_q.unprocessable));
+
+  {  // encode() on one vectorized spectrum
+    const auto refined = homs::refine_peaks(synth.library[0], pre);
+    const homs::SpectrumVector sv = homs::vectorize(*refined, pre);
+    report(gpu::encode<HomsApi>(sv, cb) == homs::encode(sv, cb), "encode(SpectrumVector): identical hypervector");
+  }
+
+  const homs::LibraryIndex ref_ix = homs::build_index(ref_lib.encoded);
+  const auto gpu_ix = gpu::build_index<HomsApi>(gpu_lib.encoded);
+  report(gpu_ix.dim() == ref_ix.dim() && gpu_ix.size() == ref_ix.size(), "build_index: dim and size");
+
+  for (const Tolerance tol : {Tolerance{Tolerance::Kind::dalton, 500.0}, Tolerance{Tolerance::Kind::ppm, 20.0}}) {
+    const auto want = homs::search_batch(ref_q.encoded, ref_ix, tol, homs::SearchOptions{8, 64});
+    const auto got = gpu::search_batch<HomsApi>(gpu_q.encoded, gpu_ix, tol);
+    bool ok = want.size() == got.size();
+    std::size_t hits = 0;
+    for (std::size_t i = 0; ok && i < want.size(); ++i) {
+      ok = want[i].has_value() == got[i].has_value() && (!want[i] || same_ssm(*want[i], *got[i]));
+      hits += want[i].has_value();
+    }
+    report(ok, std::string("search_batch ") + (tol.kind == Tolerance::Kind::ppm ? "20 ppm" : "500 Da") +
+                   ": identical optional<Ssm> list, hits = " + std::to_string(hits));
+  }
+  {
+    const auto one_ref = homs::search_one(ref_q.encoded[3], ref_ix, Tolerance{Tolerance::Kind::dalton, 500.0});
+    const auto one_gpu = gpu::search_one<HomsApi>(gpu_q.encoded[3], gpu_ix, Tolerance{Tolerance::Kind::dalton, 500.0});
+    report(one_ref.has_value() == one_gpu.has_value() && (!one_ref || same_ssm(*one_ref, *one_gpu)), "search_one");
+  }
+  {
+    const Tolerance narrow{Tolerance::Kind::ppm, 20.0}, wide{Tolerance::Kind::dalton, 500.0};
+    const auto want = homs::cascade_search(ref_q.encoded, ref_ix, narrow, wide, 0.01, homs::SearchOptions{8, 64});
+    const auto got = gpu::cascade_search<HomsApi>(gpu_q.encoded, gpu_ix, narrow, wide, 0.01);
+    bool ok = want.size() == got.size();
+    std::size_t n_narrow = 0;
+    for (std::size_t i = 0; ok && i < want.size(); ++i) {
+      ok = same_ssm(want[i], got[i]);
+      n_narrow += want[i].stage == homs::SearchStage::narrow;
+    }
+    report(ok, "cascade_search (20 ppm, 500 Da, 1% FDR): identical accepted list = " + std::to_string(want.size()) +
+                   " (" + std::to_string(n_narrow) + " narrow)");
+  }
+  // error behaviour
+  {
+    bool threw = false;
+    try {
+      gpu::build_index<HomsApi>(std::span<const homs::EncodedSpectrum>{});
+    } catch (const homs::InvariantError&) { threw = true; }
+    report(threw, "build_index(empty) throws InvariantError (search.cpp:18)");
+    threw = false;
+    try {
+      homs::EncodedSpectrum bad{ref_q.encoded[0].meta, homs::Hypervector(1024)};
+      gpu::search_one<HomsApi>(bad, gpu_ix, Tolerance{});
+    } catch (const homs::InvariantError&) { threw = true; }
+    report(threw, "search_one(dim mismatch) throws InvariantError (search.cpp:107-109)");
+    threw = false;
+    try {
+      gpu::cascade_search<HomsApi>(gpu_q.encoded, gpu_ix, Tolerance{Tolerance::Kind::ppm, 0.0},
+                                   Tolerance{Tolerance::Kind::dalton, 500.0}, 0.01);
+    } catch (const homs::ConfigError&) { threw = true; }
+    report(threw, "cascade_search(zero tolerance) throws ConfigError (search.cpp:13-15)");
+  }
+  std::printf("%s: %d check(s) failed\n", g_failed ? "FAILED" : "OK", g_failed);
+  return g_failed ? 1 : 0;
+}
