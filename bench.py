@@ -339,17 +339,21 @@ def run_ours(args) -> None:
                         "kernel time; > peak is legitimate because queries share library tiles on chip"}
     if tensor:
         # int8 contraction: 2 ops per (pair, dimension); K is padded to a multiple of 128
-        kpad = (dim + 127) // 128 * 128
+        fp4 = args.engine in ("auto", "tensor_fp4")
+        kpad = (dim + 255) // 256 * 256 if fp4 else (dim + 127) // 128 * 128
         ops = 2.0 * (n_pairs / world) * kpad
         tpeak, tsrc = measured_peak_tensor_i8()
+        if fp4:  # 4-bit operands: twice the 8-bit rate (9 vs 4.5 PFLOP/s nominal)
+            tpeak, tsrc = 2.0 * tpeak, tsrc.replace("2 x", "4 x")
         ach = ops / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else 0.0
         roofline = {"bound": "tensor", "achieved": ach, "peak": tpeak, "unit": "TFLOP/s", "frac": ach / tpeak,
                     "traffic": None, "peak_source": tsrc, "kernel": "tc_search_kernel",
                     "kernel_ms_per_launch": kernel_ms,
                     "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
                     "algorithmic_ops_per_launch": ops, "pairs_per_launch": n_pairs / world,
-                    "note": "int8 tensor ops (tcgen05 kind::i8) counted over the candidate pairs of the "
-                            "windows only; masked columns of edge tiles are not counted",
+                    "note": ("e2m1 tensor ops (tcgen05 kind::mxf4, unit block scales)" if fp4 else
+                             "int8 tensor ops (tcgen05 kind::i8)") + " counted over the candidate pairs of "
+                            "the windows only; masked columns of edge tiles are not counted",
                     "hbm_view": hbm_view}
     else:
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -372,10 +376,10 @@ def run_ours(args) -> None:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "s8 (+-1 expansion of the packed u64 bits), s32 accumulate" if tensor else "u64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": (("e2m1 (+-1 expansion of the packed u64 bits, unit block scales), f32 accumulate (exact)" if args.engine in ("auto", "tensor_fp4") else "s8 (+-1 expansion of the packed u64 bits), s32 accumulate") if tensor else "u64"), "data": "synthetic",
             "config": {"workload": workload_name(args.workload, dim, n_lib, nq), "tolerance": "dalton 500",
                        "k": k, "candidate_pairs_per_step": n_pairs,
-                       "engine": "tensor (tcgen05 int8)" if tensor else "popc",
+                       "engine": ("tensor (tcgen05 mxf4 e2m1)" if args.engine in ("auto", "tensor_fp4") else "tensor (tcgen05 int8)") if tensor else "popc",
                        "l2_policy": "inputs larger than L2 (library hypervectors "
                                     f"{n_lib * W * 8 / 1e9:.2f} GB >> 126 MB)",
                        "parallelism": f"library sharded by m/z slices x{world}, queries replicated, "
@@ -441,8 +445,8 @@ def main():
     ap.add_argument("--workload", default="iprg2012")
     ap.add_argument("--k", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--engine", default="auto", choices=["auto", "popc", "tensor"],
-                    help="top-1 search engine (auto = tensor cores)")
+    ap.add_argument("--engine", default="auto", choices=["auto", "popc", "tensor", "tensor_fp4"],
+                    help="top-1 search engine (auto = tensor cores, e2m1 operands)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -100,12 +100,18 @@ uint64_t homs_b200_ctx_launch_count(const homs_b200_ctx* ctx);
  * kernels is bracketed by CUDA events on the context's stream.  kernel_time() synchronises, returns
  * the summed duration and launch count since the last call, and resets the counters. */
 enum { HOMS_B200_KERNEL_SEARCH = 0, HOMS_B200_KERNEL_ENCODE = 1, HOMS_B200_KERNEL_PREPROCESS = 2 };
-/* Search engine for top-1 searches: AUTO (= TENSOR whenever the library has a tensor image),
- * POPC (XOR + POPC on the integer pipes) or TENSOR (tcgen05 int8 contraction of the +-1 expanded
- * hypervectors; similarity = (dim + dot) / 2, exact in int32).  Both are bit-exact; k > 1 always
- * runs on the POPC engine.  Set it BEFORE library_upload: POPC skips building the 8x larger
- * tensor image of the library. */
-enum { HOMS_B200_ENGINE_AUTO = 0, HOMS_B200_ENGINE_POPC = 1, HOMS_B200_ENGINE_TENSOR = 2 };
+/* Search engine for top-1 searches: POPC (XOR + POPC on the integer pipes) or a tcgen05 tensor-core
+ * contraction of the +-1 expanded hypervectors (similarity = (dim + dot) / 2, exact): TENSOR with
+ * int8 operands, TENSOR_FP4 with e2m1 operands and unit block scales (twice the rate, half the
+ * bytes).  AUTO = TENSOR_FP4.  All engines are bit-exact; k > 1 always runs on the POPC engine.
+ * Set it BEFORE library_upload: the tensor image of the library (8x / 4x the packed size) is built
+ * there for the selected engine, and POPC skips it. */
+enum {
+  HOMS_B200_ENGINE_AUTO = 0,
+  HOMS_B200_ENGINE_POPC = 1,
+  HOMS_B200_ENGINE_TENSOR = 2,     /* int8 operands, int32 accumulate (kind::i8) */
+  HOMS_B200_ENGINE_TENSOR_FP4 = 3  /* e2m1 operands with unit block scales, fp32 accumulate (kind::mxf4) */
+};
 int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine);
 int homs_b200_ctx_profile(homs_b200_ctx* ctx, int enable);
 int homs_b200_ctx_kernel_time(homs_b200_ctx* ctx, int which, double* out_total_ms,

@@ -64,10 +64,12 @@ struct Library {
   DevBuf d_mz, d_id_rank, d_ord_of_rank, d_mz_local, d_id_rank_local, d_words, d_buckets,
       d_bucket_of_charge;
   // +-1 int8 image of the resident rows for the tensor-core engine (search_tc.cu):
-  // [n_kc][x_rows][128 B], every 128-byte row pre-swizzled for a SWIZZLE_128B K-major UMMA operand
+  // (int8 or e2m1 nibbles): [n_kc][x_rows][128 B], every 128-byte row pre-swizzled for a
+  // SWIZZLE_128B K-major UMMA operand
   DevBuf d_x;
-  uint64_t x_rows = 0;  // n_local rounded up to 256, plus one all-zero 256-row tile of slack
-  uint32_t n_kc = 0;    // ceil(dim / 128)
+  uint64_t x_rows = 0;  // n_local rounded up to the row tile (256 / 240), plus one all-zero tile of slack
+  uint32_t n_kc = 0;    // k-chunks: ceil(dim / 128) for int8, ceil(dim / 256) for fp4
+  bool x_fp4 = false;   // operand encoding of d_x
 };
 
 struct Queries {

@@ -179,11 +179,13 @@ int homs_b200_ctx_set_stream(homs_b200_ctx* ctx, void* cuda_stream) {
 int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
-  HB_REQUIRE(ctx, engine == HOMS_B200_ENGINE_AUTO || engine == HOMS_B200_ENGINE_POPC ||
-                      engine == HOMS_B200_ENGINE_TENSOR,
+  HB_REQUIRE(ctx, engine >= HOMS_B200_ENGINE_AUTO && engine <= HOMS_B200_ENGINE_TENSOR_FP4,
              HOMS_B200_ERR_ARGUMENT, "set_engine: unknown engine");
-  HB_REQUIRE(ctx, engine != HOMS_B200_ENGINE_TENSOR || !ctx->lib.ready || tc_available(ctx),
-             HOMS_B200_ERR_STATE, "set_engine: the resident library was uploaded without a tensor image");
+  const bool tensor = engine == HOMS_B200_ENGINE_TENSOR || engine == HOMS_B200_ENGINE_TENSOR_FP4;
+  HB_REQUIRE(ctx, !tensor || !ctx->lib.ready ||
+                      (tc_available(ctx) && ctx->lib.x_fp4 == (engine == HOMS_B200_ENGINE_TENSOR_FP4)),
+             HOMS_B200_ERR_STATE,
+             "set_engine: the resident library was uploaded without the tensor image of this engine");
   ctx->engine = engine;
   return HOMS_B200_OK;
 }

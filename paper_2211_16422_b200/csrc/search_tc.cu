@@ -40,16 +40,29 @@
 namespace hb {
 
 constexpr int kTcM = 128;      // queries per tile == TMEM lanes
-constexpr int kTcN = 256;      // library rows per MMA tile == TMEM columns per accumulator
-constexpr int kTcKB = 128;     // K bytes per pipeline stage == one swizzle atom == 128 dimensions
+constexpr int kTcKB = 128;     // K bytes per pipeline stage == one swizzle atom
 constexpr int kTcStages = 4;
 constexpr uint32_t kTcABytes = kTcM * kTcKB;  // 16 KB
-constexpr uint32_t kTcBBytes = kTcN * kTcKB;  // 32 KB
-constexpr uint32_t kTcStageBytes = kTcABytes + kTcBBytes;
 constexpr int kTcThreads = 192;
 constexpr uint32_t kTcBarBytes = 256;
-constexpr uint32_t kTcSmemBytes = kTcStages * kTcStageBytes + 1024 + kTcBarBytes;
-constexpr uint32_t kTcTmemCols = 512;  // two 256-column accumulators
+constexpr uint32_t kTcTmemCols = 512;  // two accumulators (+ the scale-factor columns in fp4 mode)
+
+// Two operand encodings of the same +-1 contraction:
+//   int8 (kind::i8):   1 byte per dimension, 128 dimensions per stage row, N = 256, int32 accumulate
+//   fp4  (kind::mxf4): e2m1 nibbles (+1.0 = 0x2, -1.0 = 0xA), 256 dimensions per stage row, block
+//                      scale factors all 1.0 (UE8M0 0x7F), fp32 accumulate (exact: |dot| <= D < 2^24);
+//                      twice the MACs per byte and per tensor-pipe cycle.  N = 240 leaves 32 TMEM
+//                      columns for the (constant) scale factors next to two accumulators.
+template <bool kFp4>
+struct TcMode {
+  static constexpr int N = kFp4 ? 240 : 256;              // library rows per MMA tile
+  static constexpr int kDims = kFp4 ? 256 : 128;          // dimensions per 128-byte stage row
+  static constexpr uint32_t BBytes = N * kTcKB;
+  static constexpr uint32_t StageBytes = kTcABytes + BBytes;  // multiple of 1024
+  static constexpr uint32_t SmemBytes = kTcStages * StageBytes + 1024 + kTcBarBytes;
+  static constexpr int CW = kFp4 ? 16 : 32;               // columns per TMEM load in the drain
+  static constexpr uint32_t SfCol = 480;                  // fp4: scale-factor columns [480, 512)
+};
 constexpr uint32_t kTcGroupTiles = 12;  // query tiles per L2 group
 constexpr uint64_t kTcBatch = 64 * 1024;  // sorted slots per planning batch
 
@@ -135,6 +148,38 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint6
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem] (+)= A * B^T, e2m1 x e2m1 with per-32 UE8M0 block scales from TMEM -> fp32, K = 64
+__device__ __forceinline__ void tc_mma_fp4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(
+          tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate)
+      : "memory");
+}
+// fill 32 consecutive columns of this thread's TMEM lane with one word
+__device__ __forceinline__ void tc_st32_fill(uint32_t taddr, uint32_t w) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+      "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
+      "r"(w)
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, int (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tc_ld(uint32_t taddr, int (&v)[16]) { tc_ld16(taddr, v); }
 // 32 consecutive int32 columns of this thread's TMEM lane
 __device__ __forceinline__ void tc_ld32(uint32_t taddr, int (&v)[32]) {
   asm volatile(
@@ -151,6 +196,8 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, int (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tc_ld(uint32_t taddr, int (&v)[32]) { tc_ld32(taddr, v); }
+
 // Shared-memory matrix descriptor of a K-major SWIZZLE_128B operand whose rows are 128 bytes:
 // start address >> 4 in bits [0,14), leading byte offset (unused for one swizzle atom along K) in
 // [16,30), stride byte offset = 1024 B between 8-row groups in [32,46), descriptor version 1 in
@@ -162,18 +209,26 @@ __device__ __forceinline__ uint64_t tc_smem_desc(uint32_t smem_addr) {
 }
 // Instruction descriptor, kind::i8: D = S32 (bits [4,6) = 2), A = B = signed 8 bit (bits [7,10) and
 // [10,13) = 1), both K-major (bits 15, 16 = 0), N >> 3 in [17,23), M >> 4 in [24,29).
-constexpr uint32_t kTcIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kTcN >> 3) << 17) |
-                              (uint32_t(kTcM >> 4) << 24);
+constexpr uint32_t kTcIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(TcMode<false>::N >> 3) << 17) |
+                                (uint32_t(kTcM >> 4) << 24);
+// Block-scaled descriptor, kind::mxf4: A = B = E2M1 (format 1 in [7,10) and [10,13)), K-major,
+// N >> 3 in [17,23), scale format UE8M0 (bit 23), M >> 4 in [24,29), scale-factor ids 0, K = 64.
+constexpr uint32_t kTcIdescFp4 = (1u << 7) | (1u << 10) | (uint32_t(TcMode<true>::N >> 3) << 17) | (1u << 23) |
+                                 (uint32_t(kTcM >> 4) << 24);
 
-// ---- expansion: packed bits -> swizzled +-1 int8 image --------------------------------------
+// ---- expansion: packed bits -> swizzled +-1 operand image -----------------------------------
 
-// One warp per (row, group of 4 k-chunks): lane = (k-chunk in group) * 8 + 16-byte unit.  Bit b of
-// the row becomes byte 2b - 1; bits at or above dim and rows at or above n_rows become 0 so that
-// they contribute nothing to any dot product.
+// One warp per (row, group of 4 k-chunks): lane = (k-chunk in group) * 8 + 16-byte unit.  A bit b
+// becomes the int8 2b - 1 (16 dimensions per unit) or the e2m1 nibble +-1.0 (32 dimensions per
+// unit); dimensions at or above dim and rows at or above n_rows become 0 so that they contribute
+// nothing to any dot product.  The order of the dimensions inside a unit is irrelevant as long as
+// library and queries use the same one (a dot product is invariant under a common permutation).
+template <bool kFp4>
 __global__ void tc_expand_kernel(uint64_t out_rows, uint64_t n_rows, const uint32_t* __restrict__ src_pos,
                                  const uint32_t* __restrict__ src_subset, uint64_t pos_base,
                                  const uint64_t* __restrict__ words, uint32_t stride_words, uint32_t dim,
                                  uint32_t n_kc, uint8_t* __restrict__ out) {
+  constexpr uint32_t kUnitDims = kFp4 ? 32 : 16;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint32_t groups = (n_kc + 3) / 4;
@@ -188,24 +243,36 @@ __global__ void tc_expand_kernel(uint64_t out_rows, uint64_t n_rows, const uint3
       src = src_pos[pos_base + row];
       if (src_subset) src = src_subset[src];
     }
-    const uint32_t bit0 = kc * 128 + unit * 16;
-    const uint32_t widx = bit0 >> 6;
+    const uint32_t bit0 = kc * TcMode<kFp4>::kDims + unit * kUnitDims;
     uint32_t bits = 0;
-    if (bit0 < dim) bits = static_cast<uint32_t>(words[src * stride_words + widx] >> (bit0 & 63)) & 0xFFFFu;
+    if (bit0 < dim)
+      bits = static_cast<uint32_t>(words[src * stride_words + (bit0 >> 6)] >> (bit0 & 63)) &
+             (kFp4 ? 0xFFFFFFFFu : 0xFFFFu);
+    const uint32_t valid = dim - min(dim, bit0);  // dimensions of this unit below dim
     uint32_t w[4];
+    if constexpr (kFp4) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t nib = (bits >> (4 * i)) & 0xFu;
-      const uint32_t one = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
-      uint32_t v = ((one ^ 0x01010101u) * 0xFFu) | one;  // bit 1 -> 0x01, bit 0 -> 0xFF
-      const uint32_t b = bit0 + 4 * i;                    // zero the bytes of dimensions >= dim
-      if (b + 4 > dim) {
-        uint32_t keep = 0;
-        for (int j = 0; j < 4; ++j)
-          if (b + j < dim) keep |= 0xFFu << (8 * j);
-        v &= keep;
+      for (int i = 0; i < 4; ++i) {  // 8 dimensions -> 8 nibbles: bit 1 -> 0x2 (+1.0), bit 0 -> 0xA (-1.0)
+        const uint32_t b8 = (bits >> (8 * i)) & 0xFFu;
+        uint32_t spread = 0, keep = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          spread |= ((b8 >> j) & 1u) << (4 * j + 3);
+          if (uint32_t(8 * i + j) < valid) keep |= 0xFu << (4 * j);
+        }
+        w[i] = (0xAAAAAAAAu ^ spread) & keep;
       }
-      w[i] = v;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // 4 dimensions -> 4 bytes: bit 1 -> 0x01, bit 0 -> 0xFF
+        const uint32_t nib = (bits >> (4 * i)) & 0xFu;
+        const uint32_t one = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+        uint32_t keep = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (uint32_t(4 * i + j) < valid) keep |= 0xFFu << (8 * j);
+        w[i] = (((one ^ 0x01010101u) * 0xFFu) | one) & keep;
+      }
     }
     o = make_uint4(w[0], w[1], w[2], w[3]);
   }
@@ -241,19 +308,43 @@ __device__ __forceinline__ bool key_less(uint64_t ad1, uint32_t rk1, uint64_t ad
   return ad1 != ad2 ? ad1 < ad2 : rk1 < rk2;
 }
 
+// accumulator word -> score domain of the drain: int32 as is, fp32 (exact integers) as float
+template <bool kFp4>
+struct TcAcc;
+template <>
+struct TcAcc<false> {
+  using T = int;
+  static __device__ __forceinline__ T lowest() { return INT_MIN; }
+  static __device__ __forceinline__ T get(int raw) { return raw; }
+  static __device__ __forceinline__ int to_int(T v) { return v; }
+};
+template <>
+struct TcAcc<true> {
+  using T = float;
+  static __device__ __forceinline__ T lowest() { return -3.0e38f; }
+  static __device__ __forceinline__ T get(int raw) { return __int_as_float(raw); }
+  static __device__ __forceinline__ int to_int(T v) { return __float2int_rn(v); }
+};
+
+template <bool kFp4>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams p) {
+  using Mode = TcMode<kFp4>;
+  using Acc = TcAcc<kFp4>;
+  using AccT = typename Acc::T;
+  constexpr int kN = Mode::N;
+  constexpr int kCW = Mode::CW;
   extern __shared__ unsigned char tc_smem_raw[];
   const uint32_t raw = smem_u32(tc_smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-byte alignment
   unsigned char* gen_base = tc_smem_raw + (base - raw);
-  const uint32_t bar0 = base + kTcStages * kTcStageBytes;
+  const uint32_t bar0 = base + kTcStages * Mode::StageBytes;
   // barriers: full[4], empty[4], tfull[2], tempty[2]; then the TMEM base address
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (kTcStages + s); };
   auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kTcStages + a); };
   auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kTcStages + 2 + a); };
   volatile uint32_t* tmem_slot =
-      reinterpret_cast<volatile uint32_t*>(gen_base + kTcStages * kTcStageBytes + 8 * (2 * kTcStages + 4));
+      reinterpret_cast<volatile uint32_t*>(gen_base + kTcStages * Mode::StageBytes + 8 * (2 * kTcStages + 4));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -279,6 +370,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if constexpr (kFp4) {
+    // every block scale is 1.0 = UE8M0 0x7F: fill all 32 scale-factor columns of all 128 lanes once,
+    // so whatever bytes the MMA reads for A or B rows it reads 1.0
+    if (warp >= 2) tc_st32_fill(tmem_base + (uint32_t((warp & 3) * 32) << 16) + Mode::SfCol, 0x7F7F7F7Fu);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   const uint32_t n_kc = p.n_kc;
 
@@ -288,16 +387,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
       uint32_t stage = 0, phase = 0;
       for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
         const TcItem it = p.items[item];
-        const uint32_t n_nt = (it.row_end - it.row_begin + kTcN - 1) / kTcN;
+        const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
         const uint8_t* a_src = p.q_x + uint64_t(it.tile) * kTcM * kTcKB;
         for (uint32_t nt = 0; nt < n_nt; ++nt) {
-          const uint8_t* b_src = p.lib_x + (uint64_t(it.row_begin) + uint64_t(nt) * kTcN) * kTcKB;
+          const uint8_t* b_src = p.lib_x + (uint64_t(it.row_begin) + uint64_t(nt) * kN) * kTcKB;
           for (uint32_t kc = 0; kc < n_kc; ++kc) {
             mbar_wait(empty_bar(stage), phase ^ 1u);
-            const uint32_t sa = base + stage * kTcStageBytes;
-            mbar_expect_tx(full_bar(stage), kTcStageBytes);
+            const uint32_t sa = base + stage * Mode::StageBytes;
+            mbar_expect_tx(full_bar(stage), Mode::StageBytes);
             bulk_g2s(sa, a_src + uint64_t(kc) * p.q_rows * kTcKB, kTcABytes, full_bar(stage));
-            bulk_g2s(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, kTcBBytes, full_bar(stage));
+            bulk_g2s(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, Mode::BBytes, full_bar(stage));
             if (++stage == kTcStages) {
               stage = 0;
               phase ^= 1u;
@@ -312,21 +411,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;  // aphase: one parity bit per accumulator
       for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
         const TcItem it = p.items[item];
-        const uint32_t n_nt = (it.row_end - it.row_begin + kTcN - 1) / kTcN;
+        const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
         for (uint32_t nt = 0; nt < n_nt; ++nt) {
           mbar_wait(tempty_bar(acc), ((aphase >> acc) & 1u) ^ 1u);  // drain warps released this accumulator
           aphase ^= 1u << acc;
           tc_fence_after();
-          const uint32_t tmem_d = tmem_base + acc * kTcN;
+          const uint32_t tmem_d = tmem_base + acc * kN;
           for (uint32_t kc = 0; kc < n_kc; ++kc) {
             mbar_wait(full_bar(stage), phase);
             tc_fence_after();
-            const uint32_t sa = base + stage * kTcStageBytes;
+            const uint32_t sa = base + stage * Mode::StageBytes;
             const uint64_t adesc = tc_smem_desc(sa);
             const uint64_t bdesc = tc_smem_desc(sa + kTcABytes);
 #pragma unroll
-            for (uint32_t k = 0; k < kTcKB / 32; ++k)  // +32 bytes along K inside the swizzle atom
-              tc_mma_i8(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdesc, (kc | k) != 0u);
+            for (uint32_t k = 0; k < kTcKB / 32; ++k) {  // +32 bytes along K inside the swizzle atom
+              if constexpr (kFp4)
+                tc_mma_fp4(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescFp4, tmem_base + Mode::SfCol,
+                           tmem_base + Mode::SfCol + 16, (kc | k) != 0u);
+              else
+                tc_mma_i8(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescI8, (kc | k) != 0u);
+            }
             tc_commit(empty_bar(stage));  // stage reusable once these MMAs have read it
             if (++stage == kTcStages) {
               stage = 0;
@@ -345,7 +449,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     uint32_t acc = 0, tphase = 0;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const TcItem it = p.items[item];
-      const uint32_t n_nt = (it.row_end - it.row_begin + kTcN - 1) / kTcN;
+      const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
       const uint64_t pos = uint64_t(it.tile) * kTcM + qrow;
       uint32_t lf = 0, ll = 0;
       double qmz = 0.0;
@@ -358,50 +462,50 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         const uint32_t slot = p.vals[pos];
         qmz = p.q_mz[p.subset ? p.subset[slot] : slot];
       }
-      int best_dot = INT_MIN;
+      AccT best_dot = Acc::lowest();
       uint32_t best_row = kNone, best_rk = 0;
       uint64_t best_ad = 0;
       bool have_key = false;
 
       for (uint32_t nt = 0; nt < n_nt; ++nt) {
-        const uint32_t row0 = it.row_begin + nt * kTcN;
+        const uint32_t row0 = it.row_begin + nt * kN;
         // this query's valid columns [c0, c1) of the tile
-        int c0 = lf > row0 ? static_cast<int>(min(lf - row0, uint32_t(kTcN))) : 0;
-        int c1 = ll > row0 ? static_cast<int>(min(ll - row0, uint32_t(kTcN))) : 0;
+        int c0 = lf > row0 ? static_cast<int>(min(lf - row0, uint32_t(kN))) : 0;
+        int c1 = ll > row0 ? static_cast<int>(min(ll - row0, uint32_t(kN))) : 0;
         if (c1 <= c0) c0 = c1 = 0;
 
         mbar_wait(tfull_bar(acc), (tphase >> acc) & 1u);
         tphase ^= 1u << acc;
         tc_fence_after();
-        const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + acc * kTcN;
+        const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + acc * kN;
 
         // pass 1: maximum over the valid columns
-        int m = INT_MIN;
+        AccT m = Acc::lowest();
 #pragma unroll 1
-        for (int ch = 0; ch < kTcN / 32; ++ch) {
-          int v[32];
-          tc_ld32(taddr + ch * 32, v);
-          const int cb = ch * 32;
-          if (c0 <= cb && cb + 32 <= c1) {
+        for (int ch = 0; ch < kN / kCW; ++ch) {
+          int v[kCW];
+          tc_ld(taddr + ch * kCW, v);
+          const int cb = ch * kCW;
+          if (c0 <= cb && cb + kCW <= c1) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) m = max(m, v[j]);
-          } else if (cb < c1 && cb + 32 > c0) {
+            for (int j = 0; j < kCW; ++j) m = max(m, Acc::get(v[j]));
+          } else if (cb < c1 && cb + kCW > c0) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (cb + j >= c0 && cb + j < c1) m = max(m, v[j]);
+            for (int j = 0; j < kCW; ++j)
+              if (cb + j >= c0 && cb + j < c1) m = max(m, Acc::get(v[j]));
           }
         }
         // pass 2 (rare after the first tiles): locate the columns that reach the maximum
         const bool need = c1 > c0 && m >= best_dot;
         if (__any_sync(0xffffffffu, need)) {
 #pragma unroll 1
-          for (int ch = 0; ch < kTcN / 32; ++ch) {
-            int v[32];
-            tc_ld32(taddr + ch * 32, v);
-            const int cb = ch * 32;
+          for (int ch = 0; ch < kN / kCW; ++ch) {
+            int v[kCW];
+            tc_ld(taddr + ch * kCW, v);
+            const int cb = ch * kCW;
             uint32_t hits = 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) hits |= (v[j] == m ? 1u : 0u) << j;
+            for (int j = 0; j < kCW; ++j) hits |= (Acc::get(v[j]) == m ? 1u : 0u) << j;
             if (!need) hits = 0;
             while (hits) {
               const int j = __ffs(hits) - 1;
@@ -443,7 +547,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           best_rk = p.lib_rank[best_row];
         }
         // dot = dim - 2 * distance
-        out.d = static_cast<uint32_t>(static_cast<int>(p.dim) - best_dot) >> 1;
+        out.d = static_cast<uint32_t>(static_cast<int>(p.dim) - Acc::to_int(best_dot)) >> 1;
         out.rk = best_rk;
         out.ad = best_ad;
       }
@@ -480,26 +584,42 @@ __global__ void tc_reduce_kernel(uint64_t n, const uint32_t* __restrict__ vals,
 
 bool tc_available(const homs_b200_ctx* ctx) { return ctx->lib.d_x.p != nullptr && ctx->lib.x_rows > 0; }
 
-int tc_expand_library(homs_b200_ctx* ctx) {
-  Library& lib = ctx->lib;
-  lib.n_kc = (lib.dim + kTcKB - 1) / kTcKB;
-  lib.x_rows = (lib.n_local + kTcN - 1) / kTcN * kTcN + kTcN;
-  HB_TRY(ensure(ctx, lib.d_x, size_t(lib.n_kc) * lib.x_rows * kTcKB));
-  const uint32_t groups = (lib.n_kc + 3) / 4;
-  const uint64_t warps = lib.x_rows * groups;
-  tc_expand_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, ctx->stream>>>(
-      lib.x_rows, lib.n_local, nullptr, nullptr, 0, lib.d_words.as<uint64_t>(), lib.S, lib.dim, lib.n_kc,
-      lib.d_x.as<uint8_t>());
+template <bool kFp4>
+static int expand_launch(homs_b200_ctx* ctx, uint64_t out_rows, uint64_t n_rows, const uint32_t* src_pos,
+                         const uint32_t* src_subset, uint64_t pos_base, const uint64_t* words,
+                         uint32_t stride_words, uint32_t dim, uint32_t n_kc, uint8_t* out) {
+  const uint32_t groups = (n_kc + 3) / 4;
+  const uint64_t warps = out_rows * groups;
+  tc_expand_kernel<kFp4><<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+      out_rows, n_rows, src_pos, src_subset, pos_base, words, stride_words, dim, n_kc, out);
   HB_LAUNCHED(ctx);
   return HOMS_B200_OK;
 }
 
-int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
-                     const uint32_t* d_vals, Cand* d_out, uint32_t k_stride) {
+int tc_expand_library(homs_b200_ctx* ctx) {
+  Library& lib = ctx->lib;
+  lib.x_fp4 = ctx->engine != HOMS_B200_ENGINE_TENSOR;  // AUTO = fp4, the faster encoding
+  const uint32_t tile_n = lib.x_fp4 ? TcMode<true>::N : TcMode<false>::N;
+  const uint32_t dims = lib.x_fp4 ? TcMode<true>::kDims : TcMode<false>::kDims;
+  lib.n_kc = (lib.dim + dims - 1) / dims;
+  lib.x_rows = (lib.n_local + tile_n - 1) / tile_n * tile_n + tile_n;
+  HB_TRY(ensure(ctx, lib.d_x, size_t(lib.n_kc) * lib.x_rows * kTcKB));
+  if (lib.x_fp4)
+    return expand_launch<true>(ctx, lib.x_rows, lib.n_local, nullptr, nullptr, 0, lib.d_words.as<uint64_t>(), lib.S,
+                               lib.dim, lib.n_kc, lib.d_x.as<uint8_t>());
+  return expand_launch<false>(ctx, lib.x_rows, lib.n_local, nullptr, nullptr, 0, lib.d_words.as<uint64_t>(), lib.S,
+                              lib.dim, lib.n_kc, lib.d_x.as<uint8_t>());
+}
+
+template <bool kFp4>
+static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
+                                 const uint32_t* d_vals, Cand* d_out, uint32_t k_stride) {
+  using Mode = TcMode<kFp4>;
+  constexpr uint32_t kN = Mode::N;
   const Library& lib = ctx->lib;
   const Queries& q = ctx->q;
-  HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kTcSmemBytes)));
+  HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<kFp4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(Mode::SmemBytes)));
   const uint32_t q_stride = stride_for(q.dim);
   for (uint64_t b0 = 0; b0 < n; b0 += kTcBatch) {
     const uint64_t nb = std::min<uint64_t>(kTcBatch, n - b0);
@@ -513,14 +633,8 @@ int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, c
     HB_LAUNCHED(ctx);
     // 2. expand the batch's queries in sorted order (overlaps with the host planning below)
     HB_TRY(ensure(ctx, ctx->scratch[kScrTcQx], size_t(lib.n_kc) * q_rows * kTcKB));
-    {
-      const uint32_t groups = (lib.n_kc + 3) / 4;
-      const uint64_t warps = q_rows * groups;
-      tc_expand_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, ctx->stream>>>(
-          q_rows, nb, d_vals, d_subset, b0, q.d_words.as<uint64_t>(), q_stride, q.dim, lib.n_kc,
-          ctx->scratch[kScrTcQx].as<uint8_t>());
-      HB_LAUNCHED(ctx);
-    }
+    HB_TRY(expand_launch<kFp4>(ctx, q_rows, nb, d_vals, d_subset, b0, q.d_words.as<uint64_t>(), q_stride, q.dim,
+                               lib.n_kc, ctx->scratch[kScrTcQx].as<uint8_t>()));
     // tuning knobs (development): query tiles per L2 group, work items per SM
     uint32_t group_tiles = kTcGroupTiles, items_per_sm = 400;
     if (const char* e = getenv("HOMS_B200_TC_GROUP")) group_tiles = std::max(1, atoi(e));
@@ -536,11 +650,11 @@ int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, c
 
     // 3. plan: strips of row tiles at absolute multiples of `strip` tiles; items ordered
     //    (query-tile group, strip, tile) so that concurrently running CTAs share operands in L2
-    std::vector<uint32_t> t_lo(n_tiles), t_hi(n_tiles);  // in 256-row tiles
+    std::vector<uint32_t> t_lo(n_tiles), t_hi(n_tiles);  // in row tiles of kN rows
     uint64_t work = 0;
     for (uint32_t t = 0; t < n_tiles; ++t) {
-      t_lo[t] = h_ranges[t].x / kTcN;
-      t_hi[t] = h_ranges[t].y > h_ranges[t].x ? (h_ranges[t].y + kTcN - 1) / kTcN : t_lo[t];
+      t_lo[t] = h_ranges[t].x / kN;
+      t_hi[t] = h_ranges[t].y > h_ranges[t].x ? (h_ranges[t].y + kN - 1) / kN : t_lo[t];
       work += t_hi[t] - t_lo[t];
     }
     const uint64_t target = uint64_t(ctx->sm_count) * items_per_sm;
@@ -562,7 +676,7 @@ int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, c
           const uint32_t b = std::min<uint64_t>(t_hi[t], (uint64_t(s) + 1) * strip);
           if (b <= a) continue;
           per_tile[t].push_back(static_cast<uint32_t>(items.size()));
-          items.push_back(TcItem{t, a * kTcN, b * kTcN, 0});
+          items.push_back(TcItem{t, a * kN, b * kN, 0});
         }
     }
     const uint32_t n_items = static_cast<uint32_t>(items.size());
@@ -610,7 +724,7 @@ int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, c
       const int grid = static_cast<int>(std::min<uint32_t>(n_items, static_cast<uint32_t>(ctx->sm_count)));
       {
         KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
-        tc_search_kernel<<<grid, kTcThreads, kTcSmemBytes, ctx->stream>>>(tp);
+        tc_search_kernel<kFp4><<<grid, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
       }
       HB_LAUNCHED(ctx);
     }
@@ -621,6 +735,12 @@ int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, c
     if (b0 + kTcBatch < n) HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   }
   return HOMS_B200_OK;
+}
+
+int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
+                     const uint32_t* d_vals, Cand* d_out, uint32_t k_stride) {
+  return ctx->lib.x_fp4 ? tc_search_sorted_mode<true>(ctx, d_subset, n, d_keys, d_vals, d_out, k_stride)
+                        : tc_search_sorted_mode<false>(ctx, d_subset, n, d_keys, d_vals, d_out, k_stride);
 }
 
 }  // namespace hb

@@ -223,7 +223,8 @@ class Context:
     def set_engine(self, engine: str | int) -> None:
         """Top-1 search engine: "auto" (tensor when available), "popc" or "tensor".  Choose it
         before build_index: "popc" skips the tensor image of the library."""
-        code = {"auto": capi.ENGINE_AUTO, "popc": capi.ENGINE_POPC, "tensor": capi.ENGINE_TENSOR}.get(engine, engine)
+        code = {"auto": capi.ENGINE_AUTO, "popc": capi.ENGINE_POPC, "tensor": capi.ENGINE_TENSOR,
+                "tensor_fp4": capi.ENGINE_TENSOR_FP4}.get(engine, engine)
         _check(capi.ctx_set_engine(self._h, int(code)), self._h)
 
     def synchronize(self) -> None:

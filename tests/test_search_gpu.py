@@ -9,9 +9,9 @@ from tests import _util as U
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["tensor", "popc"])
+@pytest.fixture(params=["tensor_fp4", "tensor", "popc"])
 def ctx(hb, request):
-    """Every search test runs on both top-1 engines: the tcgen05 int8 contraction and XOR+POPC."""
+    """Every search test runs on all top-1 engines: tcgen05 mxf4 (e2m1), tcgen05 int8, XOR+POPC."""
     c = hb.Context(0)
     c.set_engine(request.param)
     c.engine_name = request.param
@@ -245,15 +245,16 @@ def test_many_queries_span_planning_batches(hb, best_oracle):
     qmz = np.round(rng.uniform(380.0, 1220.0, nq), 2)
     qch = rng.integers(1, 4, nq).astype(np.uint8)
     got = {}
-    for eng in ("tensor", "popc"):
+    for eng in ("tensor", "tensor_fp4", "popc"):
         with hb.Context(0) as c:
             c.set_engine(eng)
             c.build_index(dim, words, mz, charge, ids=ids)
             got[eng] = c.search_batch(qw, qmz, qch, hb.Tolerance("dalton", 3.0))
             none = c.search_batch(qw[:300], qmz[:300], np.zeros(300, np.uint8), hb.Tolerance("dalton", 3.0))
             assert not none.has_hit.any()
-    assert np.array_equal(got["tensor"].ordinal, got["popc"].ordinal)
-    assert np.array_equal(got["tensor"].raw_score, got["popc"].raw_score)
+    for eng in ("tensor", "tensor_fp4"):
+        assert np.array_equal(got[eng].ordinal, got["popc"].ordinal), eng
+        assert np.array_equal(got[eng].raw_score, got["popc"].raw_score), eng
     oix = best_oracle.build_index(dim, words, mz, charge, None, ids)
     sample = rng.integers(0, nq, 2000)
     has, score, ordinal, _ = oix.search_batch(qw[sample], qmz[sample], qch[sample], ("da", 3.0), threads=8)
@@ -270,4 +271,9 @@ def test_engine_selection_errors(hb):
         rng = np.random.default_rng(3)
         c.build_index(256, U.random_hvs(rng, 10, 256), np.linspace(500, 600, 10), [2] * 10)
         with pytest.raises(hb.HomsError):  # no tensor image was built for this library
+            c.set_engine("tensor")
+        c.set_engine("auto")
+        c.build_index(256, U.random_hvs(rng, 10, 256), np.linspace(500, 600, 10), [2] * 10)
+        c.set_engine("tensor_fp4")  # auto builds the e2m1 image
+        with pytest.raises(hb.HomsError):
             c.set_engine("tensor")

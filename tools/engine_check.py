@@ -13,6 +13,9 @@ sys.path.insert(0, ROOT)
 import paper_2211_16422_b200 as hb  # noqa: E402
 
 
+ENGINES = ("popc", "tensor", "tensor_fp4")
+
+
 def random_hvs(rng, n, dim):
     W = (dim + 63) // 64
     w = rng.integers(0, 2**64, (n, W), dtype=np.uint64)
@@ -46,7 +49,7 @@ def case(name, dim, n_lib, nq, tol, seed, clones=0):
         mz[b] = mz[a] if i % 2 else 2 * qmz[i % nq] - mz[a]
     ids = [f"lib{(i * 7919) % n_lib:07d}" for i in range(n_lib)]
     out = {}
-    for eng in ("popc", "tensor"):
+    for eng in ENGINES:
         with hb.Context(0) as ctx:
             ctx.set_engine(eng)
             ctx.build_index(dim, lw, mz, ch, ids=ids)
@@ -54,17 +57,20 @@ def case(name, dim, n_lib, nq, tol, seed, clones=0):
             m = ctx.search_batch(qw, qmz, qch, tol)
             dt = time.time() - t
             out[eng] = (m.raw_score.copy(), m.ordinal.copy(), dt)
-    ok = np.array_equal(out["popc"][0], out["tensor"][0]) and np.array_equal(out["popc"][1], out["tensor"][1])
-    nbad = int((out["popc"][1] != out["tensor"][1]).sum() + (out["popc"][0] != out["tensor"][0]).sum())
-    print(f"{name:28s} dim={dim:5d} lib={n_lib:7d} nq={nq:6d} tol={tol.kind}:{tol.value:g} "
-          f"hits={int((out['popc'][1] != 0xFFFFFFFF).sum()):6d} popc={out['popc'][2]*1e3:8.1f}ms "
-          f"tensor={out['tensor'][2]*1e3:8.1f}ms {'OK' if ok else 'MISMATCH ' + str(nbad)}", flush=True)
-    if not ok:
-        bad = np.flatnonzero((out["popc"][1] != out["tensor"][1]).ravel() | (out["popc"][0] != out["tensor"][0]).ravel())[:8]
-        for i in bad:
-            print("   q", i, "popc", out["popc"][0].ravel()[i], out["popc"][1].ravel()[i], "tensor",
-                  out["tensor"][0].ravel()[i], out["tensor"][1].ravel()[i])
-    return ok
+    all_ok = True
+    for eng in ENGINES[1:]:
+        ok = np.array_equal(out["popc"][0], out[eng][0]) and np.array_equal(out["popc"][1], out[eng][1])
+        nbad = int(((out["popc"][1] != out[eng][1]) | (out["popc"][0] != out[eng][0])).sum())
+        print(f"{name:22s} dim={dim:5d} lib={n_lib:7d} nq={nq:6d} tol={tol.kind}:{tol.value:g} "
+              f"hits={int((out['popc'][1] != 0xFFFFFFFF).sum()):6d} popc={out['popc'][2]*1e3:8.1f}ms "
+              f"{eng}={out[eng][2]*1e3:8.1f}ms {'OK' if ok else 'MISMATCH ' + str(nbad)}", flush=True)
+        if not ok:
+            bad = np.flatnonzero((out["popc"][1] != out[eng][1]).ravel() | (out["popc"][0] != out[eng][0]).ravel())[:8]
+            for i in bad:
+                print("   q", i, "popc", out["popc"][0].ravel()[i], out["popc"][1].ravel()[i], eng,
+                      out[eng][0].ravel()[i], out[eng][1].ravel()[i])
+        all_ok &= ok
+    return all_ok
 
 
 def main():
