@@ -332,6 +332,16 @@ def run_ours(args) -> None:
     bytes_per_launch = bytes_alg / world
     achieved = bytes_per_launch / (search_ms / max(1, search_launches) * 1e-3) / 1e9 if search_ms > 0 else 0.0
     kernel_ms = search_ms / max(1, search_launches)
+    # DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` captures of
+    # this exact command (dram__bytes_read.sum + dram__bytes_write.sum); only valid for the default
+    # single-GPU workload, null otherwise
+    ncu_traffic = {"tensor_fp4": (29.553690e9 + 0.107591e9, "profiles/r01_search_kernel_tensor_fp4_ncu.csv"),
+                   "tensor": (260.988723e9 + 0.019967e9, "profiles/r01_search_kernel_tensor_ncu.csv (before the "
+                                                         "short-strip planner)"),
+                   "popc": (301.799285e9 + 0.036848e9, "profiles/r01_search_kernel_popc_ncu.csv")}
+    eng_key = "tensor_fp4" if args.engine == "auto" else args.engine
+    traffic, traffic_src = (ncu_traffic[eng_key] if (args.workload == "iprg2012" and world == 1 and k == 1)
+                            else (None, None))
     tensor = args.engine != "popc" and k == 1
     hbm_view = {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_per_launch,
@@ -347,7 +357,7 @@ def run_ours(args) -> None:
             tpeak, tsrc = 2.0 * tpeak, tsrc.replace("2 x", "4 x")
         ach = ops / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else 0.0
         roofline = {"bound": "tensor", "achieved": ach, "peak": tpeak, "unit": "TFLOP/s", "frac": ach / tpeak,
-                    "traffic": None, "peak_source": tsrc, "kernel": "tc_search_kernel",
+                    "traffic": traffic, "traffic_source": traffic_src, "peak_source": tsrc, "kernel": "tc_search_kernel",
                     "kernel_ms_per_launch": kernel_ms,
                     "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
                     "algorithmic_ops_per_launch": ops, "pairs_per_launch": n_pairs / world,
@@ -357,8 +367,8 @@ def run_ours(args) -> None:
                     "hbm_view": hbm_view}
     else:
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                    "kernel": "search_kernel", "kernel_ms_per_launch": kernel_ms,
+                    "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                    "peak_source": peak_src, "kernel": "search_kernel", "kernel_ms_per_launch": kernel_ms,
                     "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
                     "algorithmic_bytes_per_launch": bytes_per_launch, "pairs_per_launch": n_pairs / world,
                     "note": hbm_view["note"]}
