@@ -60,7 +60,6 @@ struct TcMode {
   static constexpr uint32_t BBytes = N * kTcKB;
   static constexpr uint32_t StageBytes = kTcABytes + BBytes;  // multiple of 1024
   static constexpr uint32_t SmemBytes = kTcStages * StageBytes + 1024 + kTcBarBytes;
-  static constexpr int CW = kFp4 ? 16 : 32;               // columns per TMEM load in the drain
   static constexpr uint32_t SfCol = 480;                  // fp4: scale-factor columns [480, 512)
 };
 constexpr uint32_t kTcGroupTiles = 12;  // query tiles per L2 group
@@ -91,6 +90,7 @@ struct TcParams {
   const uint32_t* lib_rank;
   uint64_t n;  // sorted positions in this batch
   Cand* partial;  // [n_items][128]
+  int* gbest;     // [q_rows] best dot found so far per sorted position (a lower bound; see the drain)
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
@@ -158,6 +158,32 @@ __device__ __forceinline__ void tc_mma_fp4(uint32_t tmem_d, uint64_t adesc, uint
           tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate)
       : "memory");
+}
+// issue a load of 32 consecutive columns of this thread's TMEM lane; v is valid after tc_ld_wait()
+__device__ __forceinline__ void tc_ld32_issue(uint32_t taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+// wait for the outstanding TMEM loads; the registers are listed as in/out operands so that the
+// compiler cannot move any use of them above the wait
+__device__ __forceinline__ void tc_ld_wait(int (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                 "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
+                 "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
+                 "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
 }
 // fill 32 consecutive columns of this thread's TMEM lane with one word
 __device__ __forceinline__ void tc_st32_fill(uint32_t taddr, uint32_t w) {
@@ -317,6 +343,7 @@ struct TcAcc<false> {
   static __device__ __forceinline__ T lowest() { return INT_MIN; }
   static __device__ __forceinline__ T get(int raw) { return raw; }
   static __device__ __forceinline__ int to_int(T v) { return v; }
+  static __device__ __forceinline__ T from_int(int v) { return v; }
 };
 template <>
 struct TcAcc<true> {
@@ -324,6 +351,7 @@ struct TcAcc<true> {
   static __device__ __forceinline__ T lowest() { return -3.0e38f; }
   static __device__ __forceinline__ T get(int raw) { return __int_as_float(raw); }
   static __device__ __forceinline__ int to_int(T v) { return __float2int_rn(v); }
+  static __device__ __forceinline__ T from_int(int v) { return static_cast<float>(v); }
 };
 
 template <bool kFp4>
@@ -332,7 +360,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   using Acc = TcAcc<kFp4>;
   using AccT = typename Acc::T;
   constexpr int kN = Mode::N;
-  constexpr int kCW = Mode::CW;
   extern __shared__ unsigned char tc_smem_raw[];
   const uint32_t raw = smem_u32(tc_smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-byte alignment
@@ -444,8 +471,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     }
   } else {
     // ===== drain warps 2..5: TMEM -> running best per query =====
+    // One pass over the accumulator, 32 columns per TMEM load, the next load in flight while the
+    // current chunk is reduced.  Per chunk a thread takes the maximum of its query's valid columns
+    // (1 MNMX per element); only when that maximum reaches `bar` -- the larger of the item's own
+    // running best and `floor`, a lower bound of the query's final score published by work items
+    // that finished earlier (gbest) -- does it look for the columns that hold it and apply the
+    // exact tie-break.  Candidates below `floor` can never win, ties with it must be kept.
     const int quarter = warp & 3;  // a warp may only touch TMEM lanes [32 * (warp % 4), +32)
     const int qrow = quarter * 32 + lane;
+    constexpr int kChunks = (kN + 31) / 32;
     uint32_t acc = 0, tphase = 0;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const TcItem it = p.items[item];
@@ -453,6 +487,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
       const uint64_t pos = uint64_t(it.tile) * kTcM + qrow;
       uint32_t lf = 0, ll = 0;
       double qmz = 0.0;
+      int floor_i = INT_MIN;
       if (pos < p.n) {
         const uint64_t key = p.keys[pos];
         if (key != ~0ull) {
@@ -461,7 +496,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         }
         const uint32_t slot = p.vals[pos];
         qmz = p.q_mz[p.subset ? p.subset[slot] : slot];
+        floor_i = __ldcg(p.gbest + pos);
       }
+      AccT bar = Acc::from_int(floor_i);
       AccT best_dot = Acc::lowest();
       uint32_t best_row = kNone, best_rk = 0;
       uint64_t best_ad = 0;
@@ -479,60 +516,63 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         tc_fence_after();
         const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + acc * kN;
 
-        // pass 1: maximum over the valid columns
-        AccT m = Acc::lowest();
-#pragma unroll 1
-        for (int ch = 0; ch < kN / kCW; ++ch) {
-          int v[kCW];
-          tc_ld(taddr + ch * kCW, v);
-          const int cb = ch * kCW;
-          if (c0 <= cb && cb + kCW <= c1) {
+        auto reduce_chunk = [&](const int (&v)[32], int cb) {
+          AccT cm = Acc::lowest();
+          if (c0 <= cb && cb + 32 <= c1) {
 #pragma unroll
-            for (int j = 0; j < kCW; ++j) m = max(m, Acc::get(v[j]));
-          } else if (cb < c1 && cb + kCW > c0) {
+            for (int j = 0; j < 32; ++j) cm = max(cm, Acc::get(v[j]));
+          } else if (cb < c1 && cb + 32 > c0) {
 #pragma unroll
-            for (int j = 0; j < kCW; ++j)
-              if (cb + j >= c0 && cb + j < c1) m = max(m, Acc::get(v[j]));
+            for (int j = 0; j < 32; ++j)
+              if (cb + j >= c0 && cb + j < c1) cm = max(cm, Acc::get(v[j]));
+          } else {
+            return;
           }
-        }
-        // pass 2 (rare after the first tiles): locate the columns that reach the maximum
-        const bool need = c1 > c0 && m >= best_dot;
-        if (__any_sync(0xffffffffu, need)) {
-#pragma unroll 1
-          for (int ch = 0; ch < kN / kCW; ++ch) {
-            int v[kCW];
-            tc_ld(taddr + ch * kCW, v);
-            const int cb = ch * kCW;
-            uint32_t hits = 0;
+          if (cm < bar) return;
+          uint32_t hits = 0;  // the columns that hold the chunk maximum
 #pragma unroll
-            for (int j = 0; j < kCW; ++j) hits |= (Acc::get(v[j]) == m ? 1u : 0u) << j;
-            if (!need) hits = 0;
-            while (hits) {
-              const int j = __ffs(hits) - 1;
-              hits &= hits - 1;
-              const int c = cb + j;
-              if (c < c0 || c >= c1) continue;
-              const uint32_t r = row0 + c;
-              if (m > best_dot) {
-                best_dot = m;
+          for (int j = 0; j < 32; ++j) hits |= (Acc::get(v[j]) == cm ? 1u : 0u) << j;
+          while (hits) {
+            const int c = cb + __ffs(hits) - 1;
+            hits &= hits - 1;
+            if (c < c0 || c >= c1) continue;
+            const uint32_t r = row0 + c;
+            if (best_row == kNone || cm > best_dot) {
+              best_dot = cm;
+              best_row = r;
+              have_key = false;
+            } else {  // tie on score: |mass diff|, then id, then ordinal (search.cpp:137-145)
+              if (!have_key) {
+                best_ad = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - p.lib_mz[best_row])));
+                best_rk = p.lib_rank[best_row];
+                have_key = true;
+              }
+              const uint64_t ad = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - p.lib_mz[r])));
+              const uint32_t rk = p.lib_rank[r];
+              if (key_less(ad, rk, best_ad, best_rk)) {
                 best_row = r;
-                have_key = false;
-              } else {  // tie on score: |mass diff|, then id, then ordinal (search.cpp:137-145)
-                if (!have_key) {
-                  best_ad = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - p.lib_mz[best_row])));
-                  best_rk = p.lib_rank[best_row];
-                  have_key = true;
-                }
-                const uint64_t ad = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - p.lib_mz[r])));
-                const uint32_t rk = p.lib_rank[r];
-                if (key_less(ad, rk, best_ad, best_rk)) {
-                  best_row = r;
-                  best_ad = ad;
-                  best_rk = rk;
-                }
+                best_ad = ad;
+                best_rk = rk;
               }
             }
           }
+          if (best_row != kNone) bar = best_dot;
+        };
+
+        // the last chunk of a 240-column accumulator also reads 16 columns of its neighbour
+        // (other accumulator or scale factors): harmless, c1 <= kN masks them
+        int va[32], vb[32];
+        static_assert(kChunks % 2 == 0, "the drain loop handles chunk pairs");
+        tc_ld32_issue(taddr, va);
+        tc_ld_wait(va);
+#pragma unroll 1
+        for (int ch = 0; ch < kChunks; ch += 2) {
+          tc_ld32_issue(taddr + (ch + 1) * 32, vb);
+          reduce_chunk(va, ch * 32);
+          tc_ld_wait(vb);
+          if (ch + 2 < kChunks) tc_ld32_issue(taddr + (ch + 2) * 32, va);
+          reduce_chunk(vb, (ch + 1) * 32);
+          if (ch + 2 < kChunks) tc_ld_wait(va);
         }
         tc_fence_before();
         __syncwarp();
@@ -546,8 +586,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           best_ad = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - p.lib_mz[best_row])));
           best_rk = p.lib_rank[best_row];
         }
+        const int dot = Acc::to_int(best_dot);
+        if (dot > floor_i) atomicMax(p.gbest + pos, dot);  // raise the floor for later items
         // dot = dim - 2 * distance
-        out.d = static_cast<uint32_t>(static_cast<int>(p.dim) - Acc::to_int(best_dot)) >> 1;
+        out.d = static_cast<uint32_t>(static_cast<int>(p.dim) - dot) >> 1;
         out.rk = best_rk;
         out.ad = best_ad;
       }
@@ -700,6 +742,9 @@ static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, u
     auto* d_list = d_start + n_tiles + 1;
     HB_CUDA(ctx, cudaMemcpyAsync(d_items, h_items, plan_bytes, cudaMemcpyHostToDevice, ctx->stream));
     HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], std::max<size_t>(1, n_items) * kTcM * sizeof(Cand)));
+    HB_TRY(ensure(ctx, ctx->scratch[kScrTcBest], q_rows * sizeof(int)));
+    // every byte 0x80: a dot no candidate can be below
+    HB_CUDA(ctx, cudaMemsetAsync(ctx->scratch[kScrTcBest].p, 0x80, q_rows * sizeof(int), ctx->stream));
 
     // 4. search + reduce
     if (n_items > 0) {
@@ -721,6 +766,7 @@ static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, u
       tp.lib_rank = lib.d_id_rank_local.as<uint32_t>();
       tp.n = nb;
       tp.partial = ctx->scratch[kScrTcPartial].as<Cand>();
+      tp.gbest = ctx->scratch[kScrTcBest].as<int>();
       const int grid = static_cast<int>(std::min<uint32_t>(n_items, static_cast<uint32_t>(ctx->sm_count)));
       {
         KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
