@@ -11,7 +11,7 @@ import re
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_ROOT = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "libhoms_b200.so")
+LIB_PATH = os.environ.get("HOMS_B200_LIB") or os.path.join(PKG_DIR, "libhoms_b200.so")  # env: development A/B builds
 HEADER_PATH = os.path.join(REPO_ROOT, "include", "homs_b200.h")
 
 OK, ERR_CONFIG, ERR_INVARIANT, ERR_CUDA, ERR_ARGUMENT, ERR_STATE = range(6)

@@ -106,6 +106,7 @@ struct homs_b200_ctx {
   size_t pinned_cap = 0;
   void* pinned_plan = nullptr;  // pinned block of the tensor engine's host planner
   size_t pinned_plan_cap = 0;
+  cudaEvent_t plan_event = nullptr;  // host planner waits on this instead of the whole stream
   // optional per-kernel timing (homs_b200_ctx_profile)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[3];

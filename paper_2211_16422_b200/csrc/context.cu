@@ -160,6 +160,7 @@ void homs_b200_ctx_destroy(homs_b200_ctx* ctx) {
     release(*b);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned_plan) cudaFreeHost(ctx->pinned_plan);
+  if (ctx->plan_event) cudaEventDestroy(ctx->plan_event);
   cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }

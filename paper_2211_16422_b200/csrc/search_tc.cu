@@ -41,7 +41,6 @@ namespace hb {
 
 constexpr int kTcM = 128;      // queries per tile == TMEM lanes
 constexpr int kTcKB = 128;     // K bytes per pipeline stage == one swizzle atom
-constexpr int kTcStages = 4;
 constexpr uint32_t kTcABytes = kTcM * kTcKB;  // 16 KB
 constexpr int kTcThreads = 192;
 constexpr uint32_t kTcBarBytes = 256;
@@ -51,15 +50,21 @@ constexpr uint32_t kTcTmemCols = 512;  // two accumulators (+ the scale-factor c
 //   int8 (kind::i8):   1 byte per dimension, 128 dimensions per stage row, N = 256, int32 accumulate
 //   fp4  (kind::mxf4): e2m1 nibbles (+1.0 = 0x2, -1.0 = 0xA), 256 dimensions per stage row, block
 //                      scale factors all 1.0 (UE8M0 0x7F), fp32 accumulate (exact: |dot| <= D < 2^24);
-//                      twice the MACs per byte and per tensor-pipe cycle.  N = 240 leaves 32 TMEM
-//                      columns for the (constant) scale factors next to two accumulators.
+//                      twice the MACs per byte and per tensor-pipe cycle.  N = 224 leaves room in
+//                      TMEM for the (constant) scale factors next to two accumulators and in
+//                      shared memory for a 5-stage ring (220 KB).
 template <bool kFp4>
 struct TcMode {
-  static constexpr int N = kFp4 ? 240 : 256;              // library rows per MMA tile
+#ifndef HB_TC_FP4_N
+#define HB_TC_FP4_N 224      // measured: 224 rows x 5 stages beats 240 x 4 and 208 x 5 (profiles/)
+#define HB_TC_FP4_STAGES 5
+#endif
+  static constexpr int N = kFp4 ? HB_TC_FP4_N : 256;      // library rows per MMA tile
+  static constexpr int Stages = kFp4 ? HB_TC_FP4_STAGES : 4;  // depth of the smem ring
   static constexpr int kDims = kFp4 ? 256 : 128;          // dimensions per 128-byte stage row
   static constexpr uint32_t BBytes = N * kTcKB;
   static constexpr uint32_t StageBytes = kTcABytes + BBytes;  // multiple of 1024
-  static constexpr uint32_t SmemBytes = kTcStages * StageBytes + 1024 + kTcBarBytes;
+  static constexpr uint32_t SmemBytes = Stages * StageBytes + 1024 + kTcBarBytes;
   static constexpr uint32_t SfCol = 480;                  // fp4: scale-factor columns [480, 512)
 };
 constexpr uint32_t kTcGroupTiles = 12;  // query tiles per L2 group
@@ -360,23 +365,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   using Acc = TcAcc<kFp4>;
   using AccT = typename Acc::T;
   constexpr int kN = Mode::N;
+  constexpr int kStages = Mode::Stages;
   extern __shared__ unsigned char tc_smem_raw[];
   const uint32_t raw = smem_u32(tc_smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-byte alignment
   unsigned char* gen_base = tc_smem_raw + (base - raw);
-  const uint32_t bar0 = base + kTcStages * Mode::StageBytes;
+  const uint32_t bar0 = base + kStages * Mode::StageBytes;
   // barriers: full[4], empty[4], tfull[2], tempty[2]; then the TMEM base address
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
-  auto empty_bar = [&](int s) { return bar0 + 8u * (kTcStages + s); };
-  auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kTcStages + a); };
-  auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kTcStages + 2 + a); };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
+  auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kStages + a); };
+  auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kStages + 2 + a); };
   volatile uint32_t* tmem_slot =
-      reinterpret_cast<volatile uint32_t*>(gen_base + kTcStages * Mode::StageBytes + 8 * (2 * kTcStages + 4));
+      reinterpret_cast<volatile uint32_t*>(gen_base + kStages * Mode::StageBytes + 8 * (2 * kStages + 4));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTcStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
@@ -424,7 +430,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
             mbar_expect_tx(full_bar(stage), Mode::StageBytes);
             bulk_g2s(sa, a_src + uint64_t(kc) * p.q_rows * kTcKB, kTcABytes, full_bar(stage));
             bulk_g2s(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, Mode::BBytes, full_bar(stage));
-            if (++stage == kTcStages) {
+            if (++stage == kStages) {
               stage = 0;
               phase ^= 1u;
             }
@@ -459,7 +465,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
                 tc_mma_i8(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescI8, (kc | k) != 0u);
             }
             tc_commit(empty_bar(stage));  // stage reusable once these MMAs have read it
-            if (++stage == kTcStages) {
+            if (++stage == kStages) {
               stage = 0;
               phase ^= 1u;
             }
@@ -559,20 +565,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           if (best_row != kNone) bar = best_dot;
         };
 
-        // the last chunk of a 240-column accumulator also reads 16 columns of its neighbour
-        // (other accumulator or scale factors): harmless, c1 <= kN masks them
-        int va[32], vb[32];
-        static_assert(kChunks % 2 == 0, "the drain loop handles chunk pairs");
+                int va[32], vb[32];
         tc_ld32_issue(taddr, va);
         tc_ld_wait(va);
 #pragma unroll 1
         for (int ch = 0; ch < kChunks; ch += 2) {
-          tc_ld32_issue(taddr + (ch + 1) * 32, vb);
+          if (ch + 1 < kChunks) tc_ld32_issue(taddr + (ch + 1) * 32, vb);
           reduce_chunk(va, ch * 32);
-          tc_ld_wait(vb);
-          if (ch + 2 < kChunks) tc_ld32_issue(taddr + (ch + 2) * 32, va);
-          reduce_chunk(vb, (ch + 1) * 32);
-          if (ch + 2 < kChunks) tc_ld_wait(va);
+          if (ch + 1 < kChunks) {
+            tc_ld_wait(vb);
+            if (ch + 2 < kChunks) tc_ld32_issue(taddr + (ch + 2) * 32, va);
+            reduce_chunk(vb, (ch + 1) * 32);
+            if (ch + 2 < kChunks) tc_ld_wait(va);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -668,41 +673,47 @@ static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, u
     const uint32_t n_tiles = static_cast<uint32_t>((nb + kTcM - 1) / kTcM);
     const uint64_t q_rows = uint64_t(n_tiles) * kTcM;
 
-    // 1. union window of every query tile -> host
+    // 1. union window of every query tile -> host (the event lets the host plan while the
+    //    query expansion of step 2 is still running)
     HB_TRY(ensure(ctx, ctx->scratch[kScrTcTiles], size_t(n_tiles) * sizeof(uint2)));
     auto* d_ranges = ctx->scratch[kScrTcTiles].as<uint2>();
     tc_tile_ranges_kernel<<<(n_tiles * 32 + 255) / 256, 256, 0, ctx->stream>>>(nb, d_keys + b0, n_tiles, d_ranges);
     HB_LAUNCHED(ctx);
-    // 2. expand the batch's queries in sorted order (overlaps with the host planning below)
+    HB_TRY(ensure_pinned_plan(ctx, size_t(n_tiles) * sizeof(uint2)));
+    HB_CUDA(ctx, cudaMemcpyAsync(ctx->pinned_plan, d_ranges, size_t(n_tiles) * sizeof(uint2), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    if (!ctx->plan_event) HB_CUDA(ctx, cudaEventCreateWithFlags(&ctx->plan_event, cudaEventDisableTiming));
+    HB_CUDA(ctx, cudaEventRecord(ctx->plan_event, ctx->stream));
+    // 2. expand the batch's queries in sorted order
     HB_TRY(ensure(ctx, ctx->scratch[kScrTcQx], size_t(lib.n_kc) * q_rows * kTcKB));
     HB_TRY(expand_launch<kFp4>(ctx, q_rows, nb, d_vals, d_subset, b0, q.d_words.as<uint64_t>(), q_stride, q.dim,
                                lib.n_kc, ctx->scratch[kScrTcQx].as<uint8_t>()));
-    // tuning knobs (development): query tiles per L2 group, work items per SM
-    uint32_t group_tiles = kTcGroupTiles, items_per_sm = 400;
-    if (const char* e = getenv("HOMS_B200_TC_GROUP")) group_tiles = std::max(1, atoi(e));
-    if (const char* e = getenv("HOMS_B200_TC_ITEMS_PER_SM")) items_per_sm = std::max(1, atoi(e));
-    const size_t plan_cap_items = size_t(ctx->sm_count) * (items_per_sm + 8) + 2 * size_t(n_tiles) + 64;
-    const size_t pinned_bytes = size_t(n_tiles) * sizeof(uint2) + plan_cap_items * (sizeof(TcItem) + 4) +
-                                (size_t(n_tiles) + 1) * 4 + 256;
-    HB_TRY(ensure_pinned_plan(ctx, pinned_bytes));
-    auto* h_ranges = static_cast<uint2*>(ctx->pinned_plan);
-    HB_CUDA(ctx, cudaMemcpyAsync(h_ranges, d_ranges, size_t(n_tiles) * sizeof(uint2), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
-    HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    HB_CUDA(ctx, cudaEventSynchronize(ctx->plan_event));
 
     // 3. plan: strips of row tiles at absolute multiples of `strip` tiles; items ordered
-    //    (query-tile group, strip, tile) so that concurrently running CTAs share operands in L2
+    //    (query-tile group, strip, tile) so that concurrently running CTAs share operands in L2.
+    //    Short strips (<= 8 row tiles, about 400 items per SM on config 2) keep co-running CTAs in
+    //    step, which is what makes the L2 sharing work (ncu: DRAM 261 GB -> 30 GB per launch).
+    uint32_t group_tiles = kTcGroupTiles, items_per_sm = 400, max_strip = 8;  // env: development knobs
+    if (const char* e = getenv("HOMS_B200_TC_GROUP")) group_tiles = std::max(1, atoi(e));
+    if (const char* e = getenv("HOMS_B200_TC_ITEMS_PER_SM")) items_per_sm = std::max(1, atoi(e));
+    if (const char* e = getenv("HOMS_B200_TC_MAX_STRIP")) max_strip = std::max(1, atoi(e));
     std::vector<uint32_t> t_lo(n_tiles), t_hi(n_tiles);  // in row tiles of kN rows
     uint64_t work = 0;
-    for (uint32_t t = 0; t < n_tiles; ++t) {
-      t_lo[t] = h_ranges[t].x / kN;
-      t_hi[t] = h_ranges[t].y > h_ranges[t].x ? (h_ranges[t].y + kN - 1) / kN : t_lo[t];
-      work += t_hi[t] - t_lo[t];
+    {
+      const auto* h_ranges = static_cast<const uint2*>(ctx->pinned_plan);
+      for (uint32_t t = 0; t < n_tiles; ++t) {
+        t_lo[t] = h_ranges[t].x / kN;
+        t_hi[t] = h_ranges[t].y > h_ranges[t].x ? (h_ranges[t].y + kN - 1) / kN : t_lo[t];
+        work += t_hi[t] - t_lo[t];
+      }
     }
     const uint64_t target = uint64_t(ctx->sm_count) * items_per_sm;
-    const uint32_t strip = static_cast<uint32_t>(std::max<uint64_t>(1, (work + target - 1) / target));
+    const uint32_t strip = static_cast<uint32_t>(
+        std::min<uint64_t>(max_strip, std::max<uint64_t>(1, (work + target - 1) / target)));
     std::vector<TcItem> items;
-    std::vector<std::vector<uint32_t>> per_tile(n_tiles);
+    items.reserve(work / strip + 2 * size_t(n_tiles) + 16);
+    std::vector<uint32_t> tile_count(n_tiles + 1, 0);
     for (uint32_t g0 = 0; g0 < n_tiles; g0 += group_tiles) {
       const uint32_t g1 = std::min(n_tiles, g0 + group_tiles);
       uint32_t lo = ~0u, hi = 0;
@@ -717,23 +728,27 @@ static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, u
           const uint32_t a = std::max<uint32_t>(t_lo[t], s * strip);
           const uint32_t b = std::min<uint64_t>(t_hi[t], (uint64_t(s) + 1) * strip);
           if (b <= a) continue;
-          per_tile[t].push_back(static_cast<uint32_t>(items.size()));
+          ++tile_count[t];
           items.push_back(TcItem{t, a * kN, b * kN, 0});
         }
     }
     const uint32_t n_items = static_cast<uint32_t>(items.size());
-    HB_REQUIRE(ctx, n_items <= plan_cap_items, HOMS_B200_ERR_STATE, "tensor search: plan overflow");
-    auto* h_items = reinterpret_cast<TcItem*>(static_cast<unsigned char*>(ctx->pinned_plan) +
-                                              (size_t(n_tiles) * sizeof(uint2) + 15) / 16 * 16);
+    const size_t plan_cap_items = n_items;
+    // pinned layout: items | per-tile CSR start | per-tile item list
+    const size_t pinned_bytes = plan_cap_items * (sizeof(TcItem) + 4) + (size_t(n_tiles) + 1) * 4 + 64;
+    HB_TRY(ensure_pinned_plan(ctx, pinned_bytes));
+    auto* h_items = static_cast<TcItem*>(ctx->pinned_plan);
     auto* h_start = reinterpret_cast<uint32_t*>(h_items + plan_cap_items);
     auto* h_list = h_start + n_tiles + 1;
-    std::memcpy(h_items, items.data(), size_t(n_items) * sizeof(TcItem));
+    if (n_items) std::memcpy(h_items, items.data(), size_t(n_items) * sizeof(TcItem));
     uint32_t cursor = 0;
     for (uint32_t t = 0; t < n_tiles; ++t) {
       h_start[t] = cursor;
-      for (uint32_t i : per_tile[t]) h_list[cursor++] = i;
+      cursor += tile_count[t];
+      tile_count[t] = h_start[t];  // becomes the fill cursor of tile t
     }
     h_start[n_tiles] = cursor;
+    for (uint32_t i = 0; i < n_items; ++i) h_list[tile_count[items[i].tile]++] = i;
 
     const size_t plan_bytes = plan_cap_items * (sizeof(TcItem) + 4) + (size_t(n_tiles) + 1) * 4;
     HB_TRY(ensure(ctx, ctx->scratch[kScrTcPlan], plan_bytes));
