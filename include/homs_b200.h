@@ -41,7 +41,10 @@ enum {
   HOMS_B200_ERR_INVARIANT = 2, /* homs::InvariantError */
   HOMS_B200_ERR_CUDA = 3,      /* CUDA runtime failure (message carries cudaGetErrorString) */
   HOMS_B200_ERR_ARGUMENT = 4,  /* null pointer / size out of the supported range */
-  HOMS_B200_ERR_STATE = 5      /* call order (e.g. search before library upload) */
+  HOMS_B200_ERR_STATE = 5,     /* call order (e.g. search before library upload) */
+  HOMS_B200_ERR_CACHE_FORMAT = 6,  /* homs::CacheFormatError  (bad magic / version) */
+  HOMS_B200_ERR_CACHE_STALE = 7,   /* homs::StaleCacheError   (profile block differs) */
+  HOMS_B200_ERR_CACHE_CORRUPT = 8  /* homs::CacheCorruptError (truncated / bad string / checksum) */
 };
 
 enum { HOMS_B200_TOL_PPM = 0, HOMS_B200_TOL_DALTON = 1 };
@@ -204,6 +207,53 @@ int homs_b200_library_bucket_info(const homs_b200_ctx* ctx, uint32_t which, uint
  * words for the resident slice only.  Any pointer may be NULL. */
 int homs_b200_library_bucket_export(homs_b200_ctx* ctx, uint32_t which, double* out_mz,
                                     uint32_t* out_ordinal, uint64_t* out_words);
+
+/* ---- encoded-library cache (src/cache.cpp:98-211; format include/homs/cache.hpp:48-57) ------- */
+
+/* Where things are inside a cache image. */
+typedef struct {
+  uint64_t count;         /* entries */
+  uint64_t hv_offset;     /* byte offset of the hypervector block */
+  uint64_t hv_bytes;      /* count * ceil(dim/64) * 8 */
+  uint64_t stored_digest; /* the FNV-1a-64 the file carries for that block */
+  uint64_t id_bytes, peptide_bytes; /* total string bytes */
+} homs_b200_cache_layout;
+
+/* FNV-1a-64 exactly as cache.cpp:18-29 (state 1469598103934665603, prime 1099511628211), computed
+ * ON THE DEVICE by a chunked parallel formulation of the serial chain (csrc/cache.cu).  _dev takes
+ * device bytes, the plain form uploads host bytes first.  Blocking. */
+int homs_b200_fnv1a64_dev(homs_b200_ctx* ctx, const void* d_bytes, uint64_t n_bytes, uint64_t* out_digest);
+int homs_b200_fnv1a64(homs_b200_ctx* ctx, const void* bytes, uint64_t n_bytes, uint64_t* out_digest);
+
+/* Header and per-entry metadata of read_cache (cache.cpp:158-190), host only, no checksum: checks
+ * magic / version (ERR_CACHE_FORMAT), the 61-byte profile block against pre+enc (ERR_CACHE_STALE),
+ * truncation and string lengths (ERR_CACHE_CORRUPT).  Output arrays are nullable; strings are
+ * returned as (position, length) inside the image. */
+int homs_b200_cache_parse(const void* image, uint64_t n_bytes, const homs_b200_preprocess_config* pre,
+                          const homs_b200_encoder_config* enc, homs_b200_cache_layout* out_layout,
+                          double* mz, uint8_t* charge, uint8_t* is_decoy, uint64_t* id_pos, uint32_t* id_len,
+                          uint64_t* peptide_pos, uint32_t* peptide_len);
+
+/* read_cache + build_index in one call (pipeline.cpp:121-122): the hypervector block of the image
+ * goes straight to the device, its checksum is verified there (ERR_CACHE_CORRUPT on mismatch), ids
+ * are ranked from the image, and the resident index is built as by homs_b200_library_upload_dev. */
+int homs_b200_library_load_cache(homs_b200_ctx* ctx, const void* image, uint64_t n_bytes,
+                                 const homs_b200_preprocess_config* pre, const homs_b200_encoder_config* enc,
+                                 uint32_t shard_index, uint32_t shard_count, uint64_t* out_count);
+
+/* write_cache (cache.cpp:122-156) into a caller buffer, byte-identical to the reference's file.
+ * Strings travel as a blob + u64 offsets[n+1] (NULL: empty).  out == NULL: only *out_size is set.
+ * _dev: the rows (dense u64[n][W]) are on the device, e.g. straight from encode_batch_dev. */
+int homs_b200_cache_write(homs_b200_ctx* ctx, const homs_b200_preprocess_config* pre,
+                          const homs_b200_encoder_config* enc, uint64_t n, const uint64_t* words, const double* mz,
+                          const uint8_t* charge, const uint8_t* is_decoy, const char* id_blob,
+                          const uint64_t* id_off, const char* peptide_blob, const uint64_t* peptide_off, void* out,
+                          uint64_t out_cap, uint64_t* out_size);
+int homs_b200_cache_write_dev(homs_b200_ctx* ctx, const homs_b200_preprocess_config* pre,
+                              const homs_b200_encoder_config* enc, uint64_t n, const uint64_t* d_words,
+                              const double* mz, const uint8_t* charge, const uint8_t* is_decoy, const char* id_blob,
+                              const uint64_t* id_off, const char* peptide_blob, const uint64_t* peptide_off,
+                              void* out, uint64_t out_cap, uint64_t* out_size);
 
 /* ---- search (src/search.cpp:62-183) -------------------------------------------------------- */
 

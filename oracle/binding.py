@@ -60,6 +60,16 @@ class PreCfg(C.Structure):
                          scaling, 0)
 
 
+class EncCfg(C.Structure):
+    """POD mirror of EncoderConfig (reference codebook.hpp:12-23)."""
+
+    _fields_ = [("dim", C.c_uint32), ("step_flips", C.c_uint32), ("levels", C.c_uint32),
+                ("pad_", C.c_uint32), ("seed", C.c_uint64)]
+
+    def __init__(self, dim=8192, step_flips=4096, levels=16, seed=1):
+        super().__init__(dim, step_flips, levels, 0, seed)
+
+
 class SynthCfg(C.Structure):
     """POD mirror of SynthConfig (reference synth.hpp:17-33)."""
 
@@ -210,6 +220,11 @@ class Oracle:
         self._synth_export = f("synth_export", None, [VP, I, P(U64), P(F64), P(F64), P(F64),
                                                       P(U8), P(U8), C.c_char_p, P(U64)])
         self._synth_truth = f("synth_truth", None, [VP, P(U64), P(U8)])
+        UC = P(C.c_ubyte)
+        self._cache_write = f("cache_write", LL, [P(PreCfg), P(EncCfg), U64, P(U64), P(F64), P(U8), P(U8),
+                                                  C.c_char_p, P(U64), C.c_char_p, P(U64), UC, U64])
+        self._cache_read = f("cache_read", LL, [UC, U64, P(PreCfg), P(EncCfg), P(U64), P(F64), P(U8), P(U8),
+                                                C.c_char_p, P(U64), C.c_char_p, P(U64)])
         if self.kind == "port":
             self._topk = f("search_topk", LL, [VP, U64, P(U64), P(F64), P(U8), I, F64, U32,
                                                P(U32), P(U32)])
@@ -315,6 +330,44 @@ class Oracle:
         self._check(self._fdr(n, _p(score, C.c_double), _p(is_decoy, C.c_uint8),
                               _p(order, C.c_uint64), _p(fdr, C.c_double), _p(q, C.c_double)))
         return order, fdr, q
+
+    # -- encoded-library cache (reference cache.cpp:122-211) ---------------------------------
+    def cache_write(self, pre: PreCfg, enc: "EncCfg", words, mz, charge, is_decoy, ids, peptides) -> bytes:
+        words, mz, charge, dec = _u64(words), _f64(mz), _u8(charge), _u8(is_decoy)
+        n = len(mz)
+        iblob, ioff = encode_ids(ids)
+        pblob, poff = encode_ids(peptides)
+        args = (C.byref(pre), C.byref(enc), n, _p(words, C.c_uint64), _p(mz, C.c_double),
+                _p(charge, C.c_uint8), _p(dec, C.c_uint8), iblob, _p(ioff, C.c_uint64), pblob,
+                _p(poff, C.c_uint64))
+        size = self._check(self._cache_write(*args, None, 0))
+        buf = (C.c_ubyte * size)()
+        self._check(self._cache_write(*args, buf, size))
+        return bytes(buf)
+
+    def cache_read(self, image: bytes, pre: PreCfg, enc: "EncCfg") -> dict:
+        """-> dict(words, mz, charge, is_decoy, ids, peptides); raises OracleError naming the
+        reference exception class (CacheFormatError / StaleCacheError / CacheCorruptError)."""
+        n_bytes = len(image)
+        buf = (C.c_ubyte * max(1, n_bytes)).from_buffer_copy(image if n_bytes else b"\0")
+        nul = (None,) * 8
+        n = self._check(self._cache_read(buf, n_bytes, C.byref(pre), C.byref(enc), *nul))
+        W = words_for(enc.dim)
+        words = np.zeros((n, W), np.uint64)
+        mz = np.zeros(n, np.float64)
+        charge = np.zeros(n, np.uint8)
+        dec = np.zeros(n, np.uint8)
+        iblob = C.create_string_buffer(max(1, n_bytes))
+        pblob = C.create_string_buffer(max(1, n_bytes))
+        ioff = np.zeros(n + 1, np.uint64)
+        poff = np.zeros(n + 1, np.uint64)
+        self._check(self._cache_read(buf, n_bytes, C.byref(pre), C.byref(enc), _p(words, C.c_uint64),
+                                     _p(mz, C.c_double), _p(charge, C.c_uint8), _p(dec, C.c_uint8), iblob,
+                                     _p(ioff, C.c_uint64), pblob, _p(poff, C.c_uint64)))
+        iraw, praw = iblob.raw, pblob.raw  # .raw copies the whole buffer: take it once
+        ids = [iraw[int(ioff[i]):int(ioff[i + 1])].decode() for i in range(n)]
+        peps = [praw[int(poff[i]):int(poff[i + 1])].decode() for i in range(n)]
+        return dict(words=words, mz=mz, charge=charge, is_decoy=dec, ids=ids, peptides=peps)
 
     # -- synth ------------------------------------------------------------------------------
     def synth(self, cfg: SynthCfg) -> dict:

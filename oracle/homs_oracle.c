@@ -1115,3 +1115,186 @@ void ho_synth_truth(const void* h, uint64_t* source_index, uint8_t* modified) {
   memcpy(source_index, s->truth_src, s->qry.n * 8);
   memcpy(modified, s->truth_mod, s->qry.n);
 }
+
+/* ---- encoded-library cache: src/cache.cpp ------------------------------------------------- */
+
+/* little-endian writers into a growing cursor (cache.cpp:31-57); out may be NULL (sizing pass) */
+typedef struct {
+  unsigned char* p;
+  uint64_t cap, at;
+  int overflow;
+} wcur;
+
+static void w_bytes(wcur* c, const void* d, uint64_t n) {
+  if (c->p) {
+    if (c->at + n > c->cap) c->overflow = 1;
+    else memcpy(c->p + c->at, d, n);
+  }
+  c->at += n;
+}
+static void w_u8(wcur* c, uint8_t v) { w_bytes(c, &v, 1); }
+static void w_u32(wcur* c, uint32_t v) {
+  unsigned char b[4];
+  for (int i = 0; i < 4; ++i) b[i] = (unsigned char)(v >> (8 * i));
+  w_bytes(c, b, 4);
+}
+static void w_u64(wcur* c, uint64_t v) {
+  unsigned char b[8];
+  for (int i = 0; i < 8; ++i) b[i] = (unsigned char)(v >> (8 * i));
+  w_bytes(c, b, 8);
+}
+static void w_f64(wcur* c, double v) {
+  uint64_t u;
+  memcpy(&u, &v, 8);
+  w_u64(c, u);
+}
+static void w_str(wcur* c, const char* blob, const uint64_t* off, uint64_t i) { /* cache.cpp:54-57 */
+  const uint64_t n = blob && off ? off[i + 1] - off[i] : 0;
+  w_u32(c, (uint32_t)n);
+  if (n) w_bytes(c, blob + off[i], n);
+}
+/* put_profile, cache.cpp:98-110: 61 bytes */
+static void w_profile(wcur* c, const ho_precfg* pre, const ho_enccfg* enc) {
+  w_f64(c, pre->min_mz);
+  w_f64(c, pre->max_mz);
+  w_f64(c, pre->bin_size);
+  w_u32(c, pre->max_peaks);
+  w_u32(c, pre->min_peaks);
+  w_f64(c, pre->intensity_floor);
+  w_u8(c, (uint8_t)pre->scaling);
+  w_u32(c, enc->dim);
+  w_u32(c, enc->step_flips);
+  w_u32(c, enc->levels);
+  w_u64(c, enc->seed);
+}
+
+long long ho_cache_write(const ho_precfg* pre, const ho_enccfg* enc, uint64_t n, const uint64_t* words,
+                         const double* mz, const uint8_t* charge, const uint8_t* is_decoy,
+                         const char* id_blob, const uint64_t* id_off, const char* pep_blob,
+                         const uint64_t* pep_off, unsigned char* out, uint64_t out_cap) {
+  /* write_cache, cache.cpp:122-156 */
+  wcur c = {out, out_cap, 0, 0};
+  const uint64_t W = ((uint64_t)enc->dim + 63) / 64;
+  w_bytes(&c, "HOMS", 4);
+  w_u32(&c, 1);
+  w_profile(&c, pre, enc);
+  w_u64(&c, n);
+  for (uint64_t i = 0; i < n; ++i) {
+    w_str(&c, id_blob, id_off, i);
+    w_f64(&c, mz[i]);
+    w_u8(&c, charge[i]);
+    w_u8(&c, is_decoy[i] ? 1 : 0);
+    w_str(&c, pep_blob, pep_off, i);
+  }
+  const uint64_t block = c.at;
+  for (uint64_t i = 0; i < n * W; ++i) w_u64(&c, words[i]);
+  uint64_t digest = 1469598103934665603ULL; /* of the little-endian block bytes */
+  if (out && !c.overflow) digest = ho_fnv1a64(out + block, n * W * 8);
+  w_u64(&c, digest);
+  if (c.overflow) return fail("Error", "ho_cache_write: buffer too small");
+  return (long long)c.at;
+}
+
+typedef struct {
+  const unsigned char* p;
+  uint64_t n, at;
+  int truncated;
+} rcur;
+
+static int r_bytes(rcur* c, void* d, uint64_t n) { /* get_bytes, cache.cpp:59-64 */
+  if (c->truncated || c->at + n > c->n) {
+    c->truncated = 1;
+    memset(d, 0, n);
+    return 0;
+  }
+  memcpy(d, c->p + c->at, n);
+  c->at += n;
+  return 1;
+}
+static uint32_t r_u32(rcur* c) {
+  unsigned char b[4];
+  r_bytes(c, b, 4);
+  uint32_t v = 0;
+  for (int i = 0; i < 4; ++i) v |= (uint32_t)b[i] << (8 * i);
+  return v;
+}
+static uint64_t r_u64(rcur* c) {
+  unsigned char b[8];
+  r_bytes(c, b, 8);
+  uint64_t v = 0;
+  for (int i = 0; i < 8; ++i) v |= (uint64_t)b[i] << (8 * i);
+  return v;
+}
+
+long long ho_cache_read(const unsigned char* image, uint64_t n_bytes, const ho_precfg* pre,
+                        const ho_enccfg* enc, uint64_t* words, double* mz, uint8_t* charge,
+                        uint8_t* is_decoy, char* id_blob, uint64_t* id_off, char* pep_blob,
+                        uint64_t* pep_off) {
+  /* read_cache, cache.cpp:158-211; error classes in the reference's order of checks */
+  rcur c = {image, n_bytes, 0, 0};
+  char magic[4];
+  if (!r_bytes(&c, magic, 4)) return fail("CacheCorruptError", "cache stream truncated");
+  if (memcmp(magic, "HOMS", 4) != 0) return fail("CacheFormatError", "not a spectral library cache (bad magic)");
+  const uint32_t version = r_u32(&c);
+  if (c.truncated) return fail("CacheCorruptError", "cache stream truncated");
+  if (version != 1) return fail("CacheFormatError", "unsupported cache version");
+  unsigned char stored[61], want[61];
+  if (!r_bytes(&c, stored, 61)) return fail("CacheCorruptError", "cache stream truncated");
+  wcur w = {want, 61, 0, 0};
+  w_profile(&w, pre, enc);
+  if (memcmp(stored, want, 61) != 0)
+    return fail("StaleCacheError", "cache was encoded with different parameters than this run requests");
+  const uint64_t count = r_u64(&c);
+  if (c.truncated) return fail("CacheCorruptError", "cache stream truncated");
+  /* std::vector<EncodedSpectrum> entries(count) would throw bad_alloc on absurd counts; an image
+   * cannot hold more entries than it has bytes for their fixed fields */
+  if (count > n_bytes / 18) return fail("CacheCorruptError", "cache stream truncated");
+  const uint64_t W = ((uint64_t)enc->dim + 63) / 64;
+  uint64_t io = 0, po = 0;
+  for (uint64_t i = 0; i < count; ++i) {
+    for (int which = 0; which < 2; ++which) {
+      if (which == 1) { /* between the strings: precursor f64, charge u8, decoy u8 */
+        const uint64_t u = r_u64(&c);
+        unsigned char cd[2];
+        r_bytes(&c, cd, 2);
+        if (c.truncated) return fail("CacheCorruptError", "cache stream truncated");
+        if (words) {
+          memcpy(&mz[i], &u, 8);
+          charge[i] = cd[0];
+          is_decoy[i] = cd[1] != 0;
+        }
+      }
+      const uint32_t len = r_u32(&c);
+      if (c.truncated) return fail("CacheCorruptError", "cache stream truncated");
+      if (len > (1u << 20)) return fail("CacheCorruptError", "cache string length out of range");
+      if (c.at + len > c.n) return fail("CacheCorruptError", "cache stream truncated");
+      if (words) {
+        char* blob = which == 0 ? id_blob : pep_blob;
+        uint64_t* off = which == 0 ? id_off : pep_off;
+        uint64_t* cur = which == 0 ? &io : &po;
+        off[i] = *cur;
+        memcpy(blob + *cur, c.p + c.at, len);
+        *cur += len;
+      }
+      c.at += len;
+    }
+  }
+  if (words) {
+    id_off[count] = io;
+    pep_off[count] = po;
+  }
+  const uint64_t block = count * W * 8;
+  if (c.at + block > c.n) return fail("CacheCorruptError", "cache stream truncated");
+  const uint64_t digest = ho_fnv1a64(c.p + c.at, block);
+  if (words)
+    for (uint64_t i = 0; i < count * W; ++i) {
+      uint64_t v = 0;
+      for (int b = 0; b < 8; ++b) v |= (uint64_t)c.p[c.at + i * 8 + b] << (8 * b);
+      words[i] = v;
+    }
+  c.at += block;
+  const uint64_t stored_digest = r_u64(&c);
+  if (c.truncated) return fail("CacheCorruptError", "cache stream truncated");
+  if (stored_digest != digest) return fail("CacheCorruptError", "cache hypervector block failed its checksum");
+  return (long long)count;
+}

@@ -100,6 +100,20 @@ void ho_synth_export(const void* h, int which, uint64_t* offsets, double* mz, do
                      uint64_t* id_off);
 void ho_synth_truth(const void* h, uint64_t* source_index, uint8_t* modified);
 
+/* encoded-library cache, src/cache.cpp:98-211 (format: include/homs/cache.hpp:48-57) */
+typedef struct {
+  uint32_t dim, step_flips, levels, pad_;
+  uint64_t seed;
+} ho_enccfg;
+long long ho_cache_write(const ho_precfg* pre, const ho_enccfg* enc, uint64_t n, const uint64_t* words,
+                         const double* mz, const uint8_t* charge, const uint8_t* is_decoy,
+                         const char* id_blob, const uint64_t* id_off, const char* pep_blob,
+                         const uint64_t* pep_off, unsigned char* out, uint64_t out_cap);
+long long ho_cache_read(const unsigned char* image, uint64_t n_bytes, const ho_precfg* pre,
+                        const ho_enccfg* enc, uint64_t* words, double* mz, uint8_t* charge,
+                        uint8_t* is_decoy, char* id_blob, uint64_t* id_off, char* pep_blob,
+                        uint64_t* pep_off);
+
 #ifdef __cplusplus
 }
 #endif

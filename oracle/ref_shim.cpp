@@ -26,6 +26,7 @@
 #include <iterator>
 #include <memory>
 #include <optional>
+#include <sstream>
 #include <string>
 #include <typeinfo>
 #include <vector>
@@ -53,6 +54,12 @@ long long guarded(Fn&& fn) {
     g_error = std::string("ConfigError: ") + e.what();
   } catch (const homs::InvariantError& e) {
     g_error = std::string("InvariantError: ") + e.what();
+  } catch (const homs::CacheFormatError& e) {
+    g_error = std::string("CacheFormatError: ") + e.what();
+  } catch (const homs::StaleCacheError& e) {
+    g_error = std::string("StaleCacheError: ") + e.what();
+  } catch (const homs::CacheCorruptError& e) {
+    g_error = std::string("CacheCorruptError: ") + e.what();
   } catch (const homs::Error& e) {
     g_error = std::string("Error: ") + e.what();
   } catch (const std::exception& e) {
@@ -494,6 +501,84 @@ void hr_synth_truth(const void* h, std::uint64_t* source_index, std::uint8_t* mo
     source_index[i] = parse_index(s->truth[i].source_id.substr(4)) - 1;
     modified[i] = s->truth[i].modified;
   }
+}
+
+// ---- encoded-library cache (src/cache.cpp:122-211) ---------------------------------------------
+
+struct EncCfgPod {
+  std::uint32_t dim, step_flips, levels, pad_;
+  std::uint64_t seed;
+};
+
+static homs::EncodingProfile to_profile(const PreCfgPod* pre, const EncCfgPod* enc) {
+  homs::EncodingProfile p;
+  p.preprocess = to_cfg(pre);
+  p.encoder.dim = enc->dim;
+  p.encoder.step_flips = enc->step_flips;
+  p.encoder.levels = enc->levels;
+  p.encoder.seed = enc->seed;
+  return p;
+}
+
+// write_cache into a caller buffer; returns the image size (call with out == NULL to size it)
+long long hr_cache_write(const PreCfgPod* pre, const EncCfgPod* enc, std::uint64_t n,
+                         const std::uint64_t* words, const double* mz, const std::uint8_t* charge,
+                         const std::uint8_t* is_decoy, const char* id_blob, const std::uint64_t* id_off,
+                         const char* pep_blob, const std::uint64_t* pep_off, unsigned char* out,
+                         std::uint64_t out_cap) {
+  return guarded([&]() -> long long {
+    const homs::EncodingProfile profile = to_profile(pre, enc);
+    const std::size_t W = homs::Hypervector::words_for(enc->dim);
+    std::vector<homs::EncodedSpectrum> entries(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      entries[i].meta.id = str_at(id_blob, id_off, i);
+      entries[i].meta.precursor_mz = mz[i];
+      entries[i].meta.charge = charge[i];
+      entries[i].meta.is_decoy = is_decoy[i] != 0;
+      entries[i].meta.peptide = str_at(pep_blob, pep_off, i);
+      entries[i].hv = hv_from(words + i * W, enc->dim);
+    }
+    std::ostringstream os(std::ios::binary);
+    homs::write_cache(os, entries, profile);
+    const std::string image = std::move(os).str();
+    if (out != nullptr) {
+      if (image.size() > out_cap) throw homs::Error("hr_cache_write: buffer too small");
+      std::memcpy(out, image.data(), image.size());
+    }
+    return static_cast<long long>(image.size());
+  });
+}
+
+// read_cache from a byte image; returns the entry count.  With words == NULL only validates.
+// Strings come back as blobs with offsets (capacity: the image size is always enough).
+long long hr_cache_read(const unsigned char* image, std::uint64_t n_bytes, const PreCfgPod* pre,
+                        const EncCfgPod* enc, std::uint64_t* words, double* mz, std::uint8_t* charge,
+                        std::uint8_t* is_decoy, char* id_blob, std::uint64_t* id_off, char* pep_blob,
+                        std::uint64_t* pep_off) {
+  return guarded([&]() -> long long {
+    std::istringstream is(std::string(reinterpret_cast<const char*>(image), n_bytes), std::ios::binary);
+    const std::vector<homs::EncodedSpectrum> entries = homs::read_cache(is, to_profile(pre, enc));
+    if (words != nullptr) {
+      const std::size_t W = homs::Hypervector::words_for(enc->dim);
+      std::uint64_t io = 0, po = 0;
+      for (std::size_t i = 0; i < entries.size(); ++i) {
+        const auto& e = entries[i];
+        std::memcpy(words + i * W, e.hv.words().data(), W * 8);
+        mz[i] = e.meta.precursor_mz;
+        charge[i] = e.meta.charge;
+        is_decoy[i] = e.meta.is_decoy;
+        id_off[i] = io;
+        std::memcpy(id_blob + io, e.meta.id.data(), e.meta.id.size());
+        io += e.meta.id.size();
+        pep_off[i] = po;
+        std::memcpy(pep_blob + po, e.meta.peptide.data(), e.meta.peptide.size());
+        po += e.meta.peptide.size();
+      }
+      id_off[entries.size()] = io;
+      pep_off[entries.size()] = po;
+    }
+    return static_cast<long long>(entries.size());
+  });
 }
 
 }  // extern "C"

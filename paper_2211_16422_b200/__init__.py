@@ -6,13 +6,14 @@ it without the built library raises ImportError: there is no CPU fallback.
 """
 from . import capi  # noqa: F401  (raises if the CUDA library is missing)
 from .host import (  # noqa: F401
-    Codebook, ConfigError, Context, CudaError, EncodeOutcome, EncoderConfig, HomsError,
-    InvariantError, Match, PreprocessConfig, Tolerance, compute_fdr_curve, dimension, id_ranks,
-    make_codebook, quantize_intensity, words_for,
+    CacheCorruptError, CacheFormatError, Codebook, ConfigError, Context, CudaError, EncodeOutcome,
+    EncoderConfig, HomsError, InvariantError, Match, PreprocessConfig, StaleCacheError, Tolerance,
+    cache_parse, compute_fdr_curve, dimension, id_ranks, make_codebook, quantize_intensity, words_for,
 )
 
 __all__ = [
-    "Codebook", "ConfigError", "Context", "CudaError", "EncodeOutcome", "EncoderConfig",
-    "HomsError", "InvariantError", "Match", "PreprocessConfig", "Tolerance", "compute_fdr_curve",
-    "dimension", "id_ranks", "make_codebook", "quantize_intensity", "words_for",
+    "CacheCorruptError", "CacheFormatError", "Codebook", "ConfigError", "Context", "CudaError",
+    "EncodeOutcome", "EncoderConfig", "HomsError", "InvariantError", "Match", "PreprocessConfig",
+    "StaleCacheError", "Tolerance", "cache_parse", "compute_fdr_curve", "dimension", "id_ranks",
+    "make_codebook", "quantize_intensity", "words_for",
 ]

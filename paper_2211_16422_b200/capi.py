@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("HOMS_B200_LIB") or os.path.join(PKG_DIR, "libhoms_b20
 HEADER_PATH = os.path.join(REPO_ROOT, "include", "homs_b200.h")
 
 OK, ERR_CONFIG, ERR_INVARIANT, ERR_CUDA, ERR_ARGUMENT, ERR_STATE = range(6)
+ERR_CACHE_FORMAT, ERR_CACHE_STALE, ERR_CACHE_CORRUPT = 6, 7, 8
 TOL_PPM, TOL_DALTON = 0, 1
 NO_HIT = 0xFFFFFFFF
 MAX_TOPK = 64
@@ -30,6 +31,11 @@ class PreprocessConfigPod(C.Structure):
 class EncoderConfigPod(C.Structure):
     _fields_ = [("dim", C.c_uint32), ("step_flips", C.c_uint32), ("levels", C.c_uint32),
                 ("reserved", C.c_uint32), ("seed", C.c_uint64)]
+
+
+class CacheLayoutPod(C.Structure):
+    _fields_ = [("count", C.c_uint64), ("hv_offset", C.c_uint64), ("hv_bytes", C.c_uint64),
+                ("stored_digest", C.c_uint64), ("id_bytes", C.c_uint64), ("peptide_bytes", C.c_uint64)]
 
 
 class TolerancePod(C.Structure):
@@ -115,3 +121,17 @@ candidates_decode = _decl("homs_b200_candidates_decode", _I, [_VP, _U64, _U32, _
 cascade_search = _decl("homs_b200_cascade_search", _I,
                        [_VP, _U32, _U64, _VP, _VP, _VP, _P(TolerancePod), _P(TolerancePod), _F64,
                         _VP, _VP, _VP, _VP, _VP, _VP, _P(_U64)])
+
+fnv1a64_dev = _decl("homs_b200_fnv1a64_dev", _I, [_VP, _VP, _U64, _P(_U64)])
+fnv1a64 = _decl("homs_b200_fnv1a64", _I, [_VP, _VP, _U64, _P(_U64)])
+cache_parse = _decl("homs_b200_cache_parse", _I,
+                    [_VP, _U64, _P(PreprocessConfigPod), _P(EncoderConfigPod), _P(CacheLayoutPod),
+                     _VP, _VP, _VP, _VP, _VP, _VP, _VP])
+library_load_cache = _decl("homs_b200_library_load_cache", _I,
+                           [_VP, _VP, _U64, _P(PreprocessConfigPod), _P(EncoderConfigPod), _U32, _U32, _P(_U64)])
+cache_write = _decl("homs_b200_cache_write", _I,
+                    [_VP, _P(PreprocessConfigPod), _P(EncoderConfigPod), _U64, _VP, _VP, _VP, _VP, _VP, _VP,
+                     _VP, _VP, _VP, _U64, _P(_U64)])
+cache_write_dev = _decl("homs_b200_cache_write_dev", _I,
+                        [_VP, _P(PreprocessConfigPod), _P(EncoderConfigPod), _U64, _VP, _VP, _VP, _VP, _VP, _VP,
+                         _VP, _VP, _VP, _U64, _P(_U64)])

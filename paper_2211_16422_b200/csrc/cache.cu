@@ -1,0 +1,525 @@
+// Encoded-library cache <-> device: the reference's `read_cache` +
+// `build_index` pair (src/cache.cpp:158-211, src/pipeline.cpp:121-122) as ONE call that moves the
+// hypervector block of the file image straight to HBM, verifies its FNV-1a-64 checksum ON THE
+// DEVICE, and builds the resident index there; and `write_cache` (cache.cpp:122-156) producing a
+// byte-identical file from rows that may still be on the device.  File format
+// (include/homs/cache.hpp:48-57, all little-endian):
+//   "HOMS" | u32 version = 1 | 61-byte profile | u64 count |
+//   count x { u32 len, id | f64 precursor | u8 charge | u8 decoy | u32 len, peptide } |
+//   count x W u64 hypervector words | u64 FNV-1a-64 of that block
+//
+// FNV-1a is a serial chain  s <- (s ^ b) * P  (mod 2^64), which the reference walks one byte at a
+// time (~1 GB/s, 1.3 s for the 1.23 GB block of config 2).  It parallelises exactly:
+//   * XOR with a byte only touches the low byte of s, and the low byte of the next state depends
+//     only on the low byte of the current one:  l' = ((l ^ b) * 0xB3) & 0xFF.  The low bytes are
+//     therefore an 8-bit automaton; per 16 KiB chunk we tabulate its 256 -> 256 transition
+//     (fnv_table_kernel, 4 states per 32-bit lane), compose the tables group-wise, and obtain the
+//     true low byte at every chunk start.
+//   * with l known, s ^ b = s + e where e = (l ^ b) - l is a known small integer, so
+//     s' = (s + e) * P is AFFINE in s:  over a chunk  s_end = s * P^len + A,  A = sum e_i P^(len-i).
+//     Chunks give (P^len, A) pairs (fnv_affine_kernel) that are folded in order.
+#include <algorithm>
+#include <cstring>
+#include <string_view>
+
+#include "common.cuh"
+
+namespace hb {
+
+constexpr uint64_t kFnvPrime = 1099511628211ULL;          // cache.cpp:24
+constexpr uint64_t kFnvBasis = 1469598103934665603ULL;    // cache.cpp:19 (the reference's constant)
+constexpr uint32_t kFnvChunk = 16384;                     // bytes per chunk
+constexpr uint32_t kFnvGroup = 256;                       // chunks per group
+constexpr size_t kProfileBytes = 61;                      // cache.cpp:112
+
+// ---- device FNV-1a-64 -------------------------------------------------------------------------
+
+__host__ __device__ __forceinline__ uint64_t min_u64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ uint32_t fnv_low4(uint32_t x, uint32_t b) {  // 4 automaton states at once
+  x ^= b * 0x01010101u;
+  const uint32_t lo = ((x & 0x00FF00FFu) * 0xB3u) & 0x00FF00FFu;
+  const uint32_t hi = (((x >> 8) & 0x00FF00FFu) * 0xB3u) & 0x00FF00FFu;
+  return lo | (hi << 8);
+}
+
+// block = one chunk, 64 threads; thread t carries start states 4t .. 4t+3
+__global__ void __launch_bounds__(64) fnv_table_kernel(const uint8_t* __restrict__ bytes, uint64_t n,
+                                                       uint8_t* __restrict__ tables) {
+  __shared__ uint32_t s_words[kFnvChunk / 4];
+  const uint64_t c = blockIdx.x;
+  const uint64_t begin = c * kFnvChunk;
+  const uint32_t len = static_cast<uint32_t>(min_u64(kFnvChunk, n - begin));
+  // stage the chunk (byte loads keep any alignment legal; the block is read once)
+  for (uint32_t i = threadIdx.x; i < kFnvChunk / 4; i += 64) {
+    uint32_t w = 0;
+    const uint32_t o = i * 4;
+    if (o + 4 <= len && ((reinterpret_cast<uintptr_t>(bytes) + begin) & 3) == 0) {
+      w = *reinterpret_cast<const uint32_t*>(bytes + begin + o);
+    } else {
+      for (uint32_t k = 0; k < 4 && o + k < len; ++k) w |= uint32_t(bytes[begin + o + k]) << (8 * k);
+    }
+    s_words[i] = w;
+  }
+  __syncthreads();
+  const uint32_t t = threadIdx.x;
+  uint32_t x = (4 * t) | ((4 * t + 1) << 8) | ((4 * t + 2) << 16) | ((4 * t + 3) << 24);
+  const uint32_t full = len / 4;
+  for (uint32_t i = 0; i < full; ++i) {
+    const uint32_t w = s_words[i];  // same address for every thread: broadcast
+    x = fnv_low4(x, w & 0xFFu);
+    x = fnv_low4(x, (w >> 8) & 0xFFu);
+    x = fnv_low4(x, (w >> 16) & 0xFFu);
+    x = fnv_low4(x, w >> 24);
+  }
+  for (uint32_t k = full * 4; k < len; ++k) x = fnv_low4(x, (s_words[k >> 2] >> (8 * (k & 3))) & 0xFFu);
+  reinterpret_cast<uint32_t*>(tables + c * 256)[t] = x;
+}
+
+// block = one group of chunks, thread x follows start state x through the group's tables
+__global__ void __launch_bounds__(256) fnv_group_kernel(const uint8_t* __restrict__ tables, uint64_t n_chunks,
+                                                        uint8_t* __restrict__ group_tables) {
+  const uint64_t g = blockIdx.x;
+  const uint64_t c0 = g * kFnvGroup, c1 = min_u64(n_chunks, c0 + kFnvGroup);
+  uint32_t s = threadIdx.x;
+  for (uint64_t c = c0; c < c1; ++c) s = tables[c * 256 + s];
+  group_tables[g * 256 + threadIdx.x] = static_cast<uint8_t>(s);
+}
+
+// one thread: low byte at the start of every group
+__global__ void fnv_group_scan_kernel(const uint8_t* __restrict__ group_tables, uint64_t n_groups,
+                                      uint8_t* __restrict__ group_start) {
+  if (blockIdx.x || threadIdx.x) return;
+  uint32_t l = static_cast<uint32_t>(kFnvBasis & 0xFFu);
+  for (uint64_t g = 0; g < n_groups; ++g) {
+    group_start[g] = static_cast<uint8_t>(l);
+    l = group_tables[g * 256 + l];
+  }
+}
+
+// thread per group: low byte at the start of every chunk of the group
+__global__ void fnv_chunk_start_kernel(const uint8_t* __restrict__ tables, uint64_t n_chunks, uint64_t n_groups,
+                                       const uint8_t* __restrict__ group_start, uint8_t* __restrict__ chunk_start) {
+  const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= n_groups) return;
+  const uint64_t c0 = g * kFnvGroup, c1 = min_u64(n_chunks, c0 + kFnvGroup);
+  uint32_t l = group_start[g];
+  for (uint64_t c = c0; c < c1; ++c) {
+    chunk_start[c] = static_cast<uint8_t>(l);
+    l = tables[c * 256 + l];
+  }
+}
+
+// thread per chunk: A = sum e_i * P^(len - i) with the now-known low bytes
+__global__ void fnv_affine_kernel(const uint8_t* __restrict__ bytes, uint64_t n, uint64_t n_chunks,
+                                  const uint8_t* __restrict__ chunk_start, uint64_t* __restrict__ affine) {
+  const uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= n_chunks) return;
+  const uint64_t begin = c * kFnvChunk;
+  const uint32_t len = static_cast<uint32_t>(min_u64(kFnvChunk, n - begin));
+  const uint8_t* p = bytes + begin;
+  uint32_t l = chunk_start[c];
+  uint64_t acc = 0;
+  auto step = [&](uint32_t b) {
+    const uint32_t t = l ^ b;
+    acc = (acc + static_cast<uint64_t>(static_cast<int64_t>(static_cast<int32_t>(t) - static_cast<int32_t>(l)))) *
+          kFnvPrime;
+    l = (t * 0xB3u) & 0xFFu;
+  };
+  uint32_t i = 0;
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+    for (; i + 16 <= len; i += 16) {
+      const uint4 v = *reinterpret_cast<const uint4*>(p + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        step(w[k] & 0xFFu);
+        step((w[k] >> 8) & 0xFFu);
+        step((w[k] >> 16) & 0xFFu);
+        step(w[k] >> 24);
+      }
+    }
+  }
+  for (; i < len; ++i) step(p[i]);
+  affine[c] = acc;
+}
+
+// thread per group folds its chunks into one affine map (M, A); thread 0 of block 0 is not special
+__global__ void fnv_fold_groups_kernel(const uint64_t* __restrict__ affine, uint64_t n, uint64_t n_chunks,
+                                       uint64_t n_groups, uint64_t p_chunk, uint64_t p_last,
+                                       uint64_t* __restrict__ group_m, uint64_t* __restrict__ group_a) {
+  const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= n_groups) return;
+  const uint64_t c0 = g * kFnvGroup, c1 = min_u64(n_chunks, c0 + kFnvGroup);
+  uint64_t m = 1, a = 0;
+  for (uint64_t c = c0; c < c1; ++c) {
+    const uint64_t pc = (c + 1 == n_chunks && (n % kFnvChunk) != 0) ? p_last : p_chunk;
+    a = a * pc + affine[c];
+    m = m * pc;
+  }
+  group_m[g] = m;
+  group_a[g] = a;
+}
+
+__global__ void fnv_final_kernel(const uint64_t* __restrict__ group_m, const uint64_t* __restrict__ group_a,
+                                 uint64_t n_groups, uint64_t* __restrict__ out) {
+  if (blockIdx.x || threadIdx.x) return;
+  uint64_t s = kFnvBasis;
+  for (uint64_t g = 0; g < n_groups; ++g) s = s * group_m[g] + group_a[g];
+  *out = s;
+}
+
+static uint64_t pow_u64(uint64_t base, uint64_t e) {
+  uint64_t r = 1;
+  while (e) {
+    if (e & 1) r *= base;
+    base *= base;
+    e >>= 1;
+  }
+  return r;
+}
+
+// digest of n device bytes -> *h_out (blocking)
+static int fnv1a64_device(homs_b200_ctx* ctx, const uint8_t* d_bytes, uint64_t n, uint64_t* h_out) {
+  if (n == 0) {
+    *h_out = kFnvBasis;
+    return HOMS_B200_OK;
+  }
+  const uint64_t n_chunks = (n + kFnvChunk - 1) / kFnvChunk;
+  const uint64_t n_groups = (n_chunks + kFnvGroup - 1) / kFnvGroup;
+  HB_REQUIRE(ctx, n_chunks < 0x7FFFFFFFull, HOMS_B200_ERR_ARGUMENT, "fnv1a64: input above 32 TiB");
+  // scratch: tables | group tables | group start | chunk start | affine | group m | group a | out
+  const size_t o_tab = 0, o_gtab = o_tab + n_chunks * 256, o_gst = o_gtab + n_groups * 256,
+               o_cst = (o_gst + n_groups + 255) / 256 * 256, o_aff = (o_cst + n_chunks + 255) / 256 * 256,
+               o_gm = o_aff + n_chunks * 8, o_ga = o_gm + n_groups * 8, o_out = o_ga + n_groups * 8;
+  HB_TRY(ensure(ctx, ctx->scratch[kScrFnv], o_out + 8));
+  auto* base = ctx->scratch[kScrFnv].as<uint8_t>();
+  cudaStream_t st = ctx->stream;
+  fnv_table_kernel<<<static_cast<unsigned>(n_chunks), 64, 0, st>>>(d_bytes, n, base + o_tab);
+  HB_LAUNCHED(ctx);
+  fnv_group_kernel<<<static_cast<unsigned>(n_groups), 256, 0, st>>>(base + o_tab, n_chunks, base + o_gtab);
+  HB_LAUNCHED(ctx);
+  fnv_group_scan_kernel<<<1, 32, 0, st>>>(base + o_gtab, n_groups, base + o_gst);
+  HB_LAUNCHED(ctx);
+  fnv_chunk_start_kernel<<<static_cast<unsigned>((n_groups + 63) / 64), 64, 0, st>>>(
+      base + o_tab, n_chunks, n_groups, base + o_gst, base + o_cst);
+  HB_LAUNCHED(ctx);
+  fnv_affine_kernel<<<static_cast<unsigned>((n_chunks + 63) / 64), 64, 0, st>>>(
+      d_bytes, n, n_chunks, base + o_cst, reinterpret_cast<uint64_t*>(base + o_aff));
+  HB_LAUNCHED(ctx);
+  const uint64_t p_chunk = pow_u64(kFnvPrime, kFnvChunk), p_last = pow_u64(kFnvPrime, n % kFnvChunk);
+  fnv_fold_groups_kernel<<<static_cast<unsigned>((n_groups + 63) / 64), 64, 0, st>>>(
+      reinterpret_cast<uint64_t*>(base + o_aff), n, n_chunks, n_groups, p_chunk, p_last,
+      reinterpret_cast<uint64_t*>(base + o_gm), reinterpret_cast<uint64_t*>(base + o_ga));
+  HB_LAUNCHED(ctx);
+  fnv_final_kernel<<<1, 32, 0, st>>>(reinterpret_cast<uint64_t*>(base + o_gm),
+                                     reinterpret_cast<uint64_t*>(base + o_ga), n_groups,
+                                     reinterpret_cast<uint64_t*>(base + o_out));
+  HB_LAUNCHED(ctx);
+  HB_CUDA(ctx, cudaMemcpyAsync(h_out, base + o_out, 8, cudaMemcpyDeviceToHost, st));
+  HB_CUDA(ctx, cudaStreamSynchronize(st));
+  return HOMS_B200_OK;
+}
+
+// ---- host: cache image parsing / writing ------------------------------------------------------
+
+struct Reader {  // get_* of cache.cpp:59-96 over a memory image
+  const unsigned char* p;
+  uint64_t n, at = 0;
+  bool truncated = false;
+  bool bytes(void* dst, uint64_t len) {
+    if (truncated || at + len > n || at + len < at) {
+      truncated = true;
+      return false;
+    }
+    std::memcpy(dst, p + at, len);
+    at += len;
+    return true;
+  }
+  uint32_t u32() {
+    unsigned char b[4] = {0, 0, 0, 0};
+    bytes(b, 4);
+    return uint32_t(b[0]) | uint32_t(b[1]) << 8 | uint32_t(b[2]) << 16 | uint32_t(b[3]) << 24;
+  }
+  uint64_t u64() {
+    unsigned char b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bytes(b, 8);
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= uint64_t(b[i]) << (8 * i);
+    return v;
+  }
+};
+
+struct Writer {  // put_* of cache.cpp:31-57 into a caller buffer (nullptr: sizing pass)
+  unsigned char* p;
+  uint64_t cap, at = 0;
+  bool overflow = false;
+  void bytes(const void* src, uint64_t len) {
+    if (p) {
+      if (at + len > cap) overflow = true;
+      else std::memcpy(p + at, src, len);
+    }
+    at += len;
+  }
+  void u8(uint8_t v) { bytes(&v, 1); }
+  void u32(uint32_t v) {
+    unsigned char b[4];
+    for (int i = 0; i < 4; ++i) b[i] = static_cast<unsigned char>(v >> (8 * i));
+    bytes(b, 4);
+  }
+  void u64(uint64_t v) {
+    unsigned char b[8];
+    for (int i = 0; i < 8; ++i) b[i] = static_cast<unsigned char>(v >> (8 * i));
+    bytes(b, 8);
+  }
+  void f64(double v) {
+    uint64_t u;
+    std::memcpy(&u, &v, 8);
+    u64(u);
+  }
+};
+
+static void put_profile(Writer& w, const homs_b200_preprocess_config& pre, const homs_b200_encoder_config& enc) {
+  w.f64(pre.min_mz);  // cache.cpp:98-110
+  w.f64(pre.max_mz);
+  w.f64(pre.bin_size);
+  w.u32(pre.max_peaks);
+  w.u32(pre.min_peaks);
+  w.f64(pre.intensity_floor);
+  w.u8(static_cast<uint8_t>(pre.scaling));
+  w.u32(enc.dim);
+  w.u32(enc.step_flips);
+  w.u32(enc.levels);
+  w.u64(enc.seed);
+}
+
+static int parse_image(const homs_b200_ctx* ctx, const void* image, uint64_t n_bytes,
+                       const homs_b200_preprocess_config* pre, const homs_b200_encoder_config* enc,
+                       homs_b200_cache_layout* lay, double* mz, uint8_t* charge, uint8_t* is_decoy,
+                       uint64_t* id_pos, uint32_t* id_len, uint64_t* pep_pos, uint32_t* pep_len) {
+  const char* kTrunc = "cache stream truncated";  // get_bytes, cache.cpp:59-64
+  Reader r{static_cast<const unsigned char*>(image), n_bytes};
+  char magic[4];
+  if (!r.bytes(magic, 4)) return set_error(ctx, HOMS_B200_ERR_CACHE_CORRUPT, kTrunc);
+  if (std::memcmp(magic, "HOMS", 4) != 0)  // cache.cpp:161-164
+    return set_error(ctx, HOMS_B200_ERR_CACHE_FORMAT, "not a spectral library cache (bad magic)");
+  const uint32_t version = r.u32();
+  if (r.truncated) return set_error(ctx, HOMS_B200_ERR_CACHE_CORRUPT, kTrunc);
+  if (version != 1)  // :165-168
+    return set_error(ctx, HOMS_B200_ERR_CACHE_FORMAT, "unsupported cache version " + std::to_string(version));
+  unsigned char stored[kProfileBytes], want[kProfileBytes];
+  if (!r.bytes(stored, kProfileBytes)) return set_error(ctx, HOMS_B200_ERR_CACHE_CORRUPT, kTrunc);
+  Writer w{want, kProfileBytes};
+  put_profile(w, *pre, *enc);
+  if (std::memcmp(stored, want, kProfileBytes) != 0)  // :170-176
+    return set_error(ctx, HOMS_B200_ERR_CACHE_STALE,
+                     "cache was encoded with different parameters than this run requests; re-encode the library");
+  const uint64_t count = r.u64();
+  if (r.truncated || count > n_bytes / 18) return set_error(ctx, HOMS_B200_ERR_CACHE_CORRUPT, kTrunc);
+  uint64_t id_total = 0, pep_total = 0;
+  for (uint64_t i = 0; i < count; ++i) {  // :183-189
+    for (int which = 0; which < 2; ++which) {
+      if (which == 1) {
+        const uint64_t u = r.u64();
+        unsigned char cd[2] = {0, 0};
+        r.bytes(cd, 2);
+        if (r.truncated) return set_error(ctx, HOMS_B200_ERR_CACHE_CORRUPT, kTrunc);
+        if (mz) std::memcpy(&mz[i], &u, 8);
+        if (charge) charge[i] = cd[0];
+        if (is_decoy) is_decoy[i] = cd[1] != 0;
+      }
+      const uint32_t len = r.u32();
+      if (r.truncated) return set_error(ctx, HOMS_B200_ERR_CACHE_CORRUPT, kTrunc);
+      if (len > (1u << 20))  // :91-93
+        return set_error(ctx, HOMS_B200_ERR_CACHE_CORRUPT, "cache string length out of range");
+      if (r.at + len > r.n) return set_error(ctx, HOMS_B200_ERR_CACHE_CORRUPT, kTrunc);
+      if (which == 0) {
+        if (id_pos) id_pos[i] = r.at;
+        if (id_len) id_len[i] = len;
+        id_total += len;
+      } else {
+        if (pep_pos) pep_pos[i] = r.at;
+        if (pep_len) pep_len[i] = len;
+        pep_total += len;
+      }
+      r.at += len;
+    }
+  }
+  const uint64_t W = (uint64_t(enc->dim) + 63) / 64;
+  const uint64_t block = count * W * 8;
+  if (r.at + block + 8 > r.n || r.at + block + 8 < r.at) return set_error(ctx, HOMS_B200_ERR_CACHE_CORRUPT, kTrunc);
+  lay->count = count;
+  lay->hv_offset = r.at;
+  lay->hv_bytes = block;
+  r.at += block;
+  lay->stored_digest = r.u64();
+  lay->id_bytes = id_total;
+  lay->peptide_bytes = pep_total;
+  return HOMS_B200_OK;
+}
+
+static int check_profile_args(const homs_b200_ctx* ctx, const homs_b200_preprocess_config* pre,
+                              const homs_b200_encoder_config* enc) {
+  HB_REQUIRE(ctx, pre && enc, HOMS_B200_ERR_ARGUMENT, "cache: null encoding profile");
+  HB_REQUIRE(ctx, enc->dim >= 1, HOMS_B200_ERR_ARGUMENT, "cache: dim must be positive");
+  return HOMS_B200_OK;
+}
+
+// header + metadata of write_cache (cache.cpp:131-142); returns the offset of the block
+static void write_head(Writer& w, const homs_b200_preprocess_config& pre, const homs_b200_encoder_config& enc,
+                       uint64_t n, const double* mz, const uint8_t* charge, const uint8_t* is_decoy,
+                       const char* id_blob, const uint64_t* id_off, const char* pep_blob, const uint64_t* pep_off) {
+  w.bytes("HOMS", 4);
+  w.u32(1);
+  put_profile(w, pre, enc);
+  w.u64(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t il = id_blob && id_off ? id_off[i + 1] - id_off[i] : 0;
+    w.u32(static_cast<uint32_t>(il));
+    if (il) w.bytes(id_blob + id_off[i], il);
+    w.f64(mz[i]);
+    w.u8(charge[i]);
+    w.u8(is_decoy && is_decoy[i] ? 1 : 0);
+    const uint64_t pl = pep_blob && pep_off ? pep_off[i + 1] - pep_off[i] : 0;
+    w.u32(static_cast<uint32_t>(pl));
+    if (pl) w.bytes(pep_blob + pep_off[i], pl);
+  }
+}
+
+int library_build_from_device(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* d_words,
+                              const double* mz, const uint8_t* charge, const uint32_t* id_rank,
+                              uint32_t shard_index, uint32_t shard_count);  // library.cu
+
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" {
+
+int homs_b200_fnv1a64_dev(homs_b200_ctx* ctx, const void* d_bytes, uint64_t n_bytes, uint64_t* out_digest) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_REQUIRE(ctx, out_digest && (n_bytes == 0 || d_bytes), HOMS_B200_ERR_ARGUMENT, "fnv1a64: null argument");
+  return fnv1a64_device(ctx, static_cast<const uint8_t*>(d_bytes), n_bytes, out_digest);
+}
+
+int homs_b200_fnv1a64(homs_b200_ctx* ctx, const void* bytes, uint64_t n_bytes, uint64_t* out_digest) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_REQUIRE(ctx, out_digest && (n_bytes == 0 || bytes), HOMS_B200_ERR_ARGUMENT, "fnv1a64: null argument");
+  HB_TRY(ensure(ctx, ctx->scratch[kScrCacheBlock], n_bytes));
+  if (n_bytes)
+    HB_CUDA(ctx, cudaMemcpyAsync(ctx->scratch[kScrCacheBlock].p, bytes, n_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return fnv1a64_device(ctx, ctx->scratch[kScrCacheBlock].as<uint8_t>(), n_bytes, out_digest);
+}
+
+int homs_b200_cache_parse(const void* image, uint64_t n_bytes, const homs_b200_preprocess_config* pre,
+                          const homs_b200_encoder_config* enc, homs_b200_cache_layout* out_layout,
+                          double* mz, uint8_t* charge, uint8_t* is_decoy, uint64_t* id_pos, uint32_t* id_len,
+                          uint64_t* peptide_pos, uint32_t* peptide_len) {
+  HB_TRY(check_profile_args(nullptr, pre, enc));
+  if (!out_layout || (!image && n_bytes)) return set_error(nullptr, HOMS_B200_ERR_ARGUMENT, "cache_parse: null argument");
+  return parse_image(nullptr, image, n_bytes, pre, enc, out_layout, mz, charge, is_decoy, id_pos, id_len,
+                     peptide_pos, peptide_len);
+}
+
+int homs_b200_library_load_cache(homs_b200_ctx* ctx, const void* image, uint64_t n_bytes,
+                                 const homs_b200_preprocess_config* pre, const homs_b200_encoder_config* enc,
+                                 uint32_t shard_index, uint32_t shard_count, uint64_t* out_count) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_TRY(check_profile_args(ctx, pre, enc));
+  HB_REQUIRE(ctx, image || n_bytes == 0, HOMS_B200_ERR_ARGUMENT, "load_cache: null image");
+  homs_b200_cache_layout lay{};
+  HB_TRY(parse_image(ctx, image, n_bytes, pre, enc, &lay, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr));
+  const uint64_t n = lay.count;
+  std::vector<double> mz(n);
+  std::vector<uint8_t> charge(n);
+  std::vector<uint64_t> id_pos(n);
+  std::vector<uint32_t> id_len(n);
+  HB_TRY(parse_image(ctx, image, n_bytes, pre, enc, &lay, mz.data(), charge.data(), nullptr, id_pos.data(),
+                     id_len.data(), nullptr, nullptr));
+  // hypervector block: image -> device, checksum on the device (cache.cpp:192-209)
+  const auto* bytes = static_cast<const unsigned char*>(image);
+  HB_TRY(ensure(ctx, ctx->scratch[kScrCacheBlock], lay.hv_bytes));
+  if (lay.hv_bytes)
+    HB_CUDA(ctx, cudaMemcpyAsync(ctx->scratch[kScrCacheBlock].p, bytes + lay.hv_offset, lay.hv_bytes,
+                                 cudaMemcpyHostToDevice, ctx->stream));
+  uint64_t digest = 0;
+  HB_TRY(fnv1a64_device(ctx, ctx->scratch[kScrCacheBlock].as<uint8_t>(), lay.hv_bytes, &digest));
+  HB_REQUIRE(ctx, digest == lay.stored_digest, HOMS_B200_ERR_CACHE_CORRUPT,
+             "cache hypervector block failed its checksum");
+  if (out_count) *out_count = n;
+  // build_index (search.cpp:17-60): id ranks from the ids inside the image
+  std::vector<uint32_t> order(n), rank(n);
+  for (uint64_t i = 0; i < n; ++i) order[i] = static_cast<uint32_t>(i);
+  const char* chars = static_cast<const char*>(image);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    return std::string_view(chars + id_pos[a], id_len[a]) < std::string_view(chars + id_pos[b], id_len[b]);
+  });
+  for (uint64_t p = 0; p < n; ++p) rank[order[p]] = static_cast<uint32_t>(p);
+  // the block is dense little-endian u64 rows == the layout library_upload_dev takes
+  const int rc = library_build_from_device(ctx, enc->dim, n, ctx->scratch[kScrCacheBlock].as<uint64_t>(),
+                                           mz.data(), charge.data(), rank.data(), shard_index, shard_count);
+  release(ctx->scratch[kScrCacheBlock]);  // up to several GB: do not keep it as scratch
+  return rc;
+}
+
+static int cache_write_common(homs_b200_ctx* ctx, const homs_b200_preprocess_config* pre,
+                              const homs_b200_encoder_config* enc, uint64_t n, const uint64_t* words,
+                              bool words_on_device, const double* mz, const uint8_t* charge,
+                              const uint8_t* is_decoy, const char* id_blob, const uint64_t* id_off,
+                              const char* pep_blob, const uint64_t* pep_off, void* out, uint64_t out_cap,
+                              uint64_t* out_size) {
+  HB_TRY(check_profile_args(ctx, pre, enc));
+  HB_REQUIRE(ctx, out_size && (n == 0 || (mz && charge)), HOMS_B200_ERR_ARGUMENT, "cache_write: null argument");
+  const uint64_t W = (uint64_t(enc->dim) + 63) / 64, block = n * W * 8;
+  Writer w{static_cast<unsigned char*>(out), out_cap};
+  write_head(w, *pre, *enc, n, mz, charge, is_decoy, id_blob, id_off, pep_blob, pep_off);
+  const uint64_t block_at = w.at;
+  *out_size = block_at + block + 8;
+  if (!out) return HOMS_B200_OK;  // sizing pass
+  HB_REQUIRE(ctx, !w.overflow && *out_size <= out_cap, HOMS_B200_ERR_ARGUMENT, "cache_write: buffer too small");
+  HB_REQUIRE(ctx, block == 0 || words, HOMS_B200_ERR_ARGUMENT, "cache_write: null hypervector rows");
+  unsigned char* dst = static_cast<unsigned char*>(out) + block_at;
+  const uint8_t* d_block = reinterpret_cast<const uint8_t*>(words);
+  if (!words_on_device) {  // rows are already little-endian u64 on an x86-64 host: copy, then hash on the GPU
+    std::memcpy(dst, words, block);
+    HB_TRY(ensure(ctx, ctx->scratch[kScrCacheBlock], block));
+    if (block)
+      HB_CUDA(ctx, cudaMemcpyAsync(ctx->scratch[kScrCacheBlock].p, words, block, cudaMemcpyHostToDevice, ctx->stream));
+    d_block = ctx->scratch[kScrCacheBlock].as<uint8_t>();
+  } else if (block) {
+    HB_CUDA(ctx, cudaMemcpyAsync(dst, words, block, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  uint64_t digest = 0;
+  HB_TRY(fnv1a64_device(ctx, d_block, block, &digest));  // synchronises: the D2H above has landed
+  Writer tail{static_cast<unsigned char*>(out) + block_at + block, 8};
+  tail.u64(digest);
+  if (!words_on_device) release(ctx->scratch[kScrCacheBlock]);
+  return HOMS_B200_OK;
+}
+
+int homs_b200_cache_write(homs_b200_ctx* ctx, const homs_b200_preprocess_config* pre,
+                          const homs_b200_encoder_config* enc, uint64_t n, const uint64_t* words, const double* mz,
+                          const uint8_t* charge, const uint8_t* is_decoy, const char* id_blob,
+                          const uint64_t* id_off, const char* peptide_blob, const uint64_t* peptide_off, void* out,
+                          uint64_t out_cap, uint64_t* out_size) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  return cache_write_common(ctx, pre, enc, n, words, false, mz, charge, is_decoy, id_blob, id_off, peptide_blob,
+                            peptide_off, out, out_cap, out_size);
+}
+
+int homs_b200_cache_write_dev(homs_b200_ctx* ctx, const homs_b200_preprocess_config* pre,
+                              const homs_b200_encoder_config* enc, uint64_t n, const uint64_t* d_words,
+                              const double* mz, const uint8_t* charge, const uint8_t* is_decoy, const char* id_blob,
+                              const uint64_t* id_off, const char* peptide_blob, const uint64_t* peptide_off,
+                              void* out, uint64_t out_cap, uint64_t* out_size) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  return cache_write_common(ctx, pre, enc, n, d_words, true, mz, charge, is_decoy, id_blob, id_off, peptide_blob,
+                            peptide_off, out, out_cap, out_size);
+}
+
+}  // extern "C"

@@ -170,7 +170,7 @@ enum Scratch {
   kScrOffsets = 0, kScrMz, kScrInt, kScrSvBins, kScrSvLev, kScrSvCount, kScrEncOut, kScrEncOk,
   kScrQFirst, kScrQLast, kScrKeys, kScrKeysAlt, kScrVals, kScrValsAlt, kScrCub, kScrPlan,
   kScrPartial, kScrRecords, kScrSubset, kScrDecode, kScrMisc, kScrMisc2, kScrRecords2, kScrHas,
-  kScrTcQx, kScrTcPlan, kScrTcPartial, kScrTcTiles, kScrTcBest
+  kScrTcQx, kScrTcPlan, kScrTcPartial, kScrTcTiles, kScrTcBest, kScrFnv, kScrCacheBlock
 };
 
 // Tensor-core engine (search_tc.cu).  expand: packed rows -> +-1 int8 swizzled image.

@@ -185,6 +185,12 @@ static int build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h
   return HOMS_B200_OK;
 }
 
+int library_build_from_device(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* d_words,
+                              const double* mz, const uint8_t* charge, const uint32_t* id_rank,
+                              uint32_t shard_index, uint32_t shard_count) {
+  return build(ctx, dim, n, nullptr, d_words, mz, charge, id_rank, shard_index, shard_count);
+}
+
 }  // namespace hb
 
 using namespace hb;

@@ -38,8 +38,22 @@ class CudaError(HomsError):
     pass
 
 
+class CacheFormatError(HomsError):
+    """homs::CacheFormatError (errors.hpp:33-36)."""
+
+
+class StaleCacheError(HomsError):
+    """homs::StaleCacheError (errors.hpp:38-41)."""
+
+
+class CacheCorruptError(HomsError):
+    """homs::CacheCorruptError (errors.hpp:43-46)."""
+
+
 _ERRORS = {capi.ERR_CONFIG: ConfigError, capi.ERR_INVARIANT: InvariantError,
-           capi.ERR_CUDA: CudaError, capi.ERR_ARGUMENT: HomsError, capi.ERR_STATE: HomsError}
+           capi.ERR_CUDA: CudaError, capi.ERR_ARGUMENT: HomsError, capi.ERR_STATE: HomsError,
+           capi.ERR_CACHE_FORMAT: CacheFormatError, capi.ERR_CACHE_STALE: StaleCacheError,
+           capi.ERR_CACHE_CORRUPT: CacheCorruptError}
 
 
 def _check(rc: int, ctx=None) -> None:
@@ -148,6 +162,35 @@ def compute_fdr_curve(score, is_decoy):
     q = np.zeros(n, np.float64)
     _check(capi.compute_fdr_curve(n, _ptr(score), _ptr(is_decoy), _ptr(order), _ptr(fdr), _ptr(q)))
     return order, fdr, q
+
+
+def _blob(strings):
+    enc = [x.encode() if isinstance(x, str) else bytes(x) for x in strings]
+    off = np.zeros(len(enc) + 1, np.uint64)
+    if enc:
+        off[1:] = np.cumsum([len(e) for e in enc])
+    return np.frombuffer(b"".join(enc) + b"\0", np.uint8).copy(), off
+
+
+def cache_parse(image: bytes, preprocess: PreprocessConfig, encoder: EncoderConfig) -> dict:
+    """Header + metadata of a cache image (cache.cpp:158-190); host only, no checksum.  Raises
+    CacheFormatError / StaleCacheError / CacheCorruptError like read_cache."""
+    buf = np.frombuffer(image, np.uint8)
+    lay = capi.CacheLayoutPod()
+    args = (_ptr(buf) if len(buf) else 0, len(buf), C.byref(preprocess.pod()), C.byref(encoder.pod()), C.byref(lay))
+    _check(capi.cache_parse(*args, 0, 0, 0, 0, 0, 0, 0))
+    n = lay.count
+    mz = np.zeros(n, np.float64)
+    charge = np.zeros(n, np.uint8)
+    decoy = np.zeros(n, np.uint8)
+    ipos, ppos = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
+    ilen, plen = np.zeros(n, np.uint32), np.zeros(n, np.uint32)
+    _check(capi.cache_parse(*args, _ptr(mz), _ptr(charge), _ptr(decoy), _ptr(ipos), _ptr(ilen), _ptr(ppos),
+                            _ptr(plen)))
+    ids = [bytes(image[int(p):int(p) + int(l)]).decode() for p, l in zip(ipos, ilen)]
+    peps = [bytes(image[int(p):int(p) + int(l)]).decode() for p, l in zip(ppos, plen)]
+    return dict(count=n, hv_offset=lay.hv_offset, hv_bytes=lay.hv_bytes, stored_digest=lay.stored_digest,
+                precursor_mz=mz, charge=charge, is_decoy=decoy, ids=ids, peptides=peps)
 
 
 def id_ranks(ids) -> np.ndarray:
@@ -340,6 +383,45 @@ class Context:
         self.lib_dim, self.lib_n = dim, n
         self.lib_is_decoy = (_arr(is_decoy, np.uint8) if is_decoy is not None
                              else np.zeros(n, np.uint8))
+
+    def load_cache(self, image: bytes, preprocess: PreprocessConfig, encoder: EncoderConfig,
+                   shard_index: int = 0, shard_count: int = 1) -> dict:
+        """read_cache + build_index (pipeline.cpp:121-122): cache image -> resident index, checksum
+        verified on the device.  Returns the parsed metadata (ids, peptides, ...)."""
+        meta = cache_parse(image, preprocess, encoder)
+        buf = np.frombuffer(image, np.uint8)
+        cnt = C.c_uint64()
+        _check(capi.library_load_cache(self._h, _ptr(buf), len(buf), C.byref(preprocess.pod()),
+                                       C.byref(encoder.pod()), shard_index, shard_count, C.byref(cnt)), self._h)
+        self._set_lib(encoder.dim, cnt.value, meta["is_decoy"])
+        return meta
+
+    def cache_write(self, preprocess: PreprocessConfig, encoder: EncoderConfig, words, precursor_mz, charge,
+                    is_decoy, ids, peptides, d_words: int = 0) -> bytes:
+        """write_cache (cache.cpp:122-156): the byte image of the cache file.  `d_words` != 0: the
+        rows are on the device (dense u64[n, W]) and `words` is ignored."""
+        mz = _arr(precursor_mz, np.float64)
+        ch = _arr(charge, np.uint8)
+        dec = _arr(is_decoy, np.uint8)
+        n = len(mz)
+        iblob, ioff = _blob(ids)
+        pblob, poff = _blob(peptides)
+        w = None if d_words else _arr(words, np.uint64)
+        fn = capi.cache_write_dev if d_words else capi.cache_write
+        args = (self._h, C.byref(preprocess.pod()), C.byref(encoder.pod()), n, d_words or _ptr(w), _ptr(mz),
+                _ptr(ch), _ptr(dec), _ptr(iblob), _ptr(ioff), _ptr(pblob), _ptr(poff))
+        size = C.c_uint64()
+        _check(fn(*args, 0, 0, C.byref(size)), self._h)
+        out = np.zeros(size.value, np.uint8)
+        _check(fn(*args, _ptr(out), size.value, C.byref(size)), self._h)
+        return out.tobytes()
+
+    def fnv1a64(self, data) -> int:
+        """FNV-1a-64 of host bytes, computed on the device (cache.cpp:18-29)."""
+        buf = np.frombuffer(data, np.uint8) if not isinstance(data, np.ndarray) else data.view(np.uint8).ravel()
+        out = C.c_uint64()
+        _check(capi.fnv1a64(self._h, _ptr(buf) if len(buf) else 0, len(buf), C.byref(out)), self._h)
+        return out.value
 
     def buckets(self):
         cnt = C.c_uint32()

@@ -12,6 +12,7 @@ Outputs (tests/golden/):
   fingerprints.json   codebook / config-1 FNV-1a fingerprints and counts
   encode_cases.npz    spectra -> (ok, hypervector words, bins, levels) for several configs
   search_cases.npz    small libraries with clones / mirror pairs -> windows, top-1, cascade
+  cache_small.homs    a cache file written by the reference's write_cache (+ cache_small.npz: its entries)
 """
 from __future__ import annotations
 
@@ -24,7 +25,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
-from oracle.binding import Oracle, PreCfg, SynthCfg, fnv1a64_words, words_for  # noqa: E402
+from oracle.binding import EncCfg, Oracle, PreCfg, SynthCfg, fnv1a64_words, words_for  # noqa: E402
 
 
 def csr(spectra):
@@ -244,9 +245,44 @@ def fingerprints(ref: Oracle):
     return out
 
 
+def cache_case(ref: Oracle):
+    """A cache file exactly as the reference writes it (cache.cpp:122-156): odd dimension count,
+    empty / non-ASCII / long strings, unknown charge, decoys."""
+    rng = np.random.default_rng(2211)
+    n, dim = 37, 320
+    words = rng.integers(0, 2**64, (n, words_for(dim)), dtype=np.uint64)
+    mz = np.round(rng.uniform(300.0, 1400.0, n), 4)
+    charge = rng.integers(0, 5, n).astype(np.uint8)
+    decoy = (rng.uniform(0, 1, n) < 0.4).astype(np.uint8)
+    ids = [f"LIB_{i:05d}" if i % 5 else "" for i in range(n)]
+    ids[3], ids[4] = "d\u00e9j\u00e0-vu", "x" * 300
+    peps = ["PEPTIDEK"[: 1 + i % 8] if i % 3 else "" for i in range(n)]
+    pre = PreCfg(min_mz=100.5, max_peaks=64, min_peaks=3, scaling=1)
+    enc = EncCfg(dim, 99, 7, 12345)
+    image = ref.cache_write(pre, enc, words, mz, charge, decoy, ids, peps)
+    back = ref.cache_read(image, pre, enc)
+    assert np.array_equal(back["words"], words) and back["ids"] == ids and back["peptides"] == peps
+    with open(os.path.join(HERE, "cache_small.homs"), "wb") as f:
+        f.write(image)
+    np.savez_compressed(os.path.join(HERE, "cache_small.npz"), words=words, mz=mz, charge=charge, decoy=decoy,
+                        ids=np.array([x.encode() for x in ids], dtype="S"),
+                        peptides=np.array([x.encode() for x in peps], dtype="S"),
+                        pre=np.array([100.5, 1500.0, 0.05, 64, 3, 0.01, 1]), enc=np.array([dim, 99, 7, 12345]))
+    return dict(bytes=len(image), fnv_of_file=f"{fnv1a64_words(np.frombuffer(image + bytes(-len(image) % 8), np.uint64)):016x}")
+
+
 def main():
     ref = Oracle("ref")
+    if "--cache-only" in sys.argv:  # adds the cache fixture without regenerating the others
+        with open(os.path.join(HERE, "fingerprints.json")) as f:
+            fp = json.load(f)
+        fp["cache_small"] = cache_case(ref)
+        with open(os.path.join(HERE, "fingerprints.json"), "w") as f:
+            json.dump(fp, f, indent=1, sort_keys=True)
+        print(fp["cache_small"])
+        return
     fp = fingerprints(ref)
+    fp["cache_small"] = cache_case(ref)
     fp["encode_cases_ok"] = encode_cases(ref)
     fp["search_cases_hits"] = search_cases(ref)
     with open(os.path.join(HERE, "fingerprints.json"), "w") as f:
