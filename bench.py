@@ -196,10 +196,18 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # HOMS_BENCH_BACKEND=gloo: development smoke of the world > 1 path on a box with fewer GPUs than
+    # ranks (ranks share devices, the gather is staged through the host); the product path is NCCL
+    backend = os.environ.get("HOMS_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local_rank = local_rank % torch.cuda.device_count()
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", rank=rank, world_size=world,
-                                device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", rank=rank, world_size=world,
+                                    device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend, rank=rank, world_size=world)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
 
@@ -271,7 +279,13 @@ def run_ours(args) -> None:
     def step():
         ctx.search_resident_dev(tol, k, rec.data_ptr())
         if world > 1:
-            dist.all_gather_into_tensor(gathered, rec)
+            if backend == "nccl":
+                dist.all_gather_into_tensor(gathered, rec)
+            else:
+                stream.synchronize()
+                parts = [torch.empty(rec.numel(), dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(parts, rec.cpu())
+                gathered.copy_(torch.cat(parts))
             ctx.merge_candidates_dev(nq, k, world, gathered.data_ptr(), merged.data_ptr())
 
     def sync_all():
@@ -298,7 +312,7 @@ def run_ours(args) -> None:
     ctx.profile(False)
     launches = ctx.launch_count() - launches0
     if world > 1:
-        tmax = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        tmax = torch.tensor([ms_total], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         ms_total = float(tmax.item())
     ms_step = ms_total / args.steps
@@ -307,6 +321,8 @@ def run_ours(args) -> None:
     # results of the device-resident path (for the parity check below)
     final = merged if world > 1 else rec
     dev_score, dev_ord = ctx.candidates_decode(nq, k, final.data_ptr())
+    import hashlib
+    result_digest = hashlib.sha256(dev_ord.tobytes() + dev_score.tobytes()).hexdigest()[:16]  # same at every N
 
     # ---- end to end through the public host-buffer call ----------------------------------
     h_words = torch.empty((nq, W), dtype=torch.int64).pin_memory()
@@ -327,7 +343,7 @@ def run_ours(args) -> None:
             e2e_result = ctx.candidates_decode(nq, k, merged.data_ptr())
         dt = time.perf_counter() - t0
         if world > 1:
-            tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+            tt = torch.tensor([dt], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
         if i >= args.warmup:
@@ -406,6 +422,7 @@ def run_ours(args) -> None:
                                       "all-gather + merge of 16-byte candidates" if world > 1 else "single GPU"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "result_digest": result_digest,
             "encode": {"spectra_per_s": n_lib / ((pre_ms + enc_ms) * 1e-3), "preprocess_ms": pre_ms,
                        "encode_ms": enc_ms, "spectra": n_lib, "peaks": lib["peaks"]},
         }
