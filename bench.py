@@ -54,7 +54,7 @@ def measured_peak_tensor_i8():
         return 2.0 * float(j.get("bf16_tflops_sustained") or j["bf16_tflops"]), \
             "2 x measured sustained dense bf16 (MEASURED_PEAKS.json)"
     except Exception:
-        return 2.0 * 1500.0, "fallback: 2 x 1500 TFLOP/s bf16 (B200_PROFILING.md)"
+        return 2.0 * 1400.0, "fallback: 2 x 1400 TFLOP/s sustained dense bf16 (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
 
 
 class ClockSampler:
@@ -382,8 +382,14 @@ def run_ours(args) -> None:
         if fp4:  # 4-bit operands: twice the 8-bit rate (9 vs 4.5 PFLOP/s nominal)
             tpeak, tsrc = 2.0 * tpeak, tsrc.replace("2 x", "4 x")
         ach = ops / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else 0.0
+        # the same MMA shape issued back to back with no memory traffic, on this box, right now
+        probe_ops, probe_ms = ctx.tensor_peak_probe("tensor_fp4" if fp4 else "tensor", 0.5)
+        probe = {"value": probe_ops / 1e12, "unit": "TFLOP/s", "frac": ach / (probe_ops / 1e12),
+                 "source": "in-situ probe: bare tcgen05.mma issue loop of the kernel's shape on all SMs, "
+                           f"no memory traffic, {probe_ms:.0f} ms under the power cap "
+                           "(homs_b200_tensor_peak_probe)"}
         roofline = {"bound": "tensor", "achieved": ach, "peak": tpeak, "unit": "TFLOP/s", "frac": ach / tpeak,
-                    "traffic": traffic, "traffic_source": traffic_src, "peak_source": tsrc, "kernel": "tc_search_kernel",
+                    "traffic": traffic, "traffic_source": traffic_src, "peak_source": tsrc, "peak_probe": probe, "kernel": "tc_search_kernel",
                     "kernel_ms_per_launch": kernel_ms,
                     "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
                     "algorithmic_ops_per_launch": ops, "pairs_per_launch": n_pairs / world,

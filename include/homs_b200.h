@@ -119,6 +119,11 @@ int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine);
 int homs_b200_ctx_profile(homs_b200_ctx* ctx, int enable);
 int homs_b200_ctx_kernel_time(homs_b200_ctx* ctx, int which, double* out_total_ms,
                               uint64_t* out_launches);
+/* Measurement aid (no reference counterpart): sustained issue rate of the tensor engine's MMA shape
+ * on this device with every SM busy and no memory traffic -- the ceiling bench.py quotes the search
+ * kernel against.  engine: HOMS_B200_ENGINE_TENSOR or _TENSOR_FP4; runs for about `seconds`. */
+int homs_b200_tensor_peak_probe(homs_b200_ctx* ctx, int engine, double seconds, double* out_ops_per_s,
+                                double* out_kernel_ms);
 
 /* ---- host-side configuration (no device work) ----------------------------------------------- */
 

@@ -81,6 +81,7 @@ ENGINE_AUTO, ENGINE_POPC, ENGINE_TENSOR, ENGINE_TENSOR_FP4 = 0, 1, 2, 3
 ctx_profile = _decl("homs_b200_ctx_profile", _I, [_VP, _I])
 ctx_kernel_time = _decl("homs_b200_ctx_kernel_time", _I, [_VP, _I, _P(_F64), _P(_U64)])
 KERNEL_SEARCH, KERNEL_ENCODE, KERNEL_PREPROCESS = 0, 1, 2
+tensor_peak_probe = _decl("homs_b200_tensor_peak_probe", _I, [_VP, _I, _F64, _P(_F64), _P(_F64)])
 
 preprocess_validate = _decl("homs_b200_preprocess_validate", _I, [_P(PreprocessConfigPod)])
 dimension = _decl("homs_b200_dimension", _U32, [_P(PreprocessConfigPod)])

@@ -386,10 +386,6 @@ static void write_head(Writer& w, const homs_b200_preprocess_config& pre, const 
   }
 }
 
-int library_build_from_device(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* d_words,
-                              const double* mz, const uint8_t* charge, const uint32_t* id_rank,
-                              uint32_t shard_index, uint32_t shard_count);  // library.cu
-
 }  // namespace hb
 
 using namespace hb;

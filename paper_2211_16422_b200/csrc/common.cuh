@@ -99,7 +99,7 @@ struct homs_b200_ctx {
   hb::Library lib;
   hb::Queries q;
   // grow-only scratch, keyed by purpose
-  enum { kScratchSlots = 32 };
+  enum { kScratchSlots = 40 };
   hb::DevBuf scratch[kScratchSlots];
   int engine = HOMS_B200_ENGINE_AUTO;  // homs_b200_ctx_set_engine
   void* pinned = nullptr;  // small pinned staging block
@@ -107,6 +107,11 @@ struct homs_b200_ctx {
   void* pinned_plan = nullptr;  // pinned block of the tensor engine's host planner
   size_t pinned_plan_cap = 0;
   cudaEvent_t plan_event = nullptr;  // host planner waits on this instead of the whole stream
+  // chunked host <-> device pipeline of the encoder (encode.cu:encode_pipeline): copy-in and
+  // copy-out streams beside the compute stream, per-slot events, created on first use
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaEvent_t pipe_in_ready[2] = {nullptr, nullptr}, pipe_done[2] = {nullptr, nullptr},
+              pipe_out_free[2] = {nullptr, nullptr};
   // optional per-kernel timing (homs_b200_ctx_profile)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[3];
@@ -170,7 +175,8 @@ enum Scratch {
   kScrOffsets = 0, kScrMz, kScrInt, kScrSvBins, kScrSvLev, kScrSvCount, kScrEncOut, kScrEncOk,
   kScrQFirst, kScrQLast, kScrKeys, kScrKeysAlt, kScrVals, kScrValsAlt, kScrCub, kScrPlan,
   kScrPartial, kScrRecords, kScrSubset, kScrDecode, kScrMisc, kScrMisc2, kScrRecords2, kScrHas,
-  kScrTcQx, kScrTcPlan, kScrTcPartial, kScrTcTiles, kScrTcBest, kScrFnv, kScrCacheBlock
+  kScrTcQx, kScrTcPlan, kScrTcPartial, kScrTcTiles, kScrTcBest, kScrFnv, kScrCacheBlock,
+  kScrPipeIn0, kScrPipeIn1, kScrPipeOut0, kScrPipeOut1, kScrFusedRows, kScrFusedOk
 };
 
 // Tensor-core engine (search_tc.cu).  expand: packed rows -> +-1 int8 swizzled image.
@@ -179,6 +185,7 @@ int tc_expand_library(homs_b200_ctx* ctx);
 int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
                      const uint32_t* d_vals, Cand* d_out, uint32_t k_stride);
 bool tc_available(const homs_b200_ctx* ctx);
+int tc_peak_probe(homs_b200_ctx* ctx, int fp4, double seconds, double* out_ops_per_s, double* out_ms);
 
 // dense host rows (W words) -> padded device rows (S words), zero padded.  Async on ctx->stream.
 int upload_rows(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* h_src, uint64_t n, uint32_t W,
@@ -188,6 +195,19 @@ int download_rows(homs_b200_ctx* ctx, uint64_t* h_dst, const uint64_t* d_src, ui
 // dense device rows -> padded device rows
 int repack_rows_dev(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src, uint64_t n,
                     uint32_t W, uint32_t S);
+
+// Chunked, double-buffered encoder pipeline over HOST spectra (CSR): H2D of chunk c+1 and D2H of
+// chunk c-1 overlap the kernels of chunk c.  Hypervector rows go to d_keep (dense u64[n][W] on the
+// device, may be null) and/or h_words (host, may be null); ok flags likewise.
+int encode_pipeline(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint64_t n,
+                    const uint64_t* offsets, const double* mz, const double* intensity, uint64_t* d_keep,
+                    uint8_t* d_keep_ok, uint64_t* h_words, uint8_t* h_ok);
+// build_index over rows already on the device; row_of_entry (host, may be null) maps entry i of the
+// metadata arrays to its row in d_words
+int library_build_from_device(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* d_words,
+                              const double* mz, const uint8_t* charge, const uint32_t* id_rank,
+                              uint32_t shard_index, uint32_t shard_count,
+                              const uint32_t* row_of_entry = nullptr);
 
 struct Lock {
   explicit Lock(homs_b200_ctx* c) : g(c->mu) { cudaSetDevice(c->device); }

@@ -161,6 +161,11 @@ void homs_b200_ctx_destroy(homs_b200_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned_plan) cudaFreeHost(ctx->pinned_plan);
   if (ctx->plan_event) cudaEventDestroy(ctx->plan_event);
+  for (int i = 0; i < 2; ++i)
+    for (cudaEvent_t e : {ctx->pipe_in_ready[i], ctx->pipe_done[i], ctx->pipe_out_free[i]})
+      if (e) cudaEventDestroy(e);
+  if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
+  if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
   cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -224,6 +229,17 @@ int homs_b200_ctx_kernel_time(homs_b200_ctx* ctx, int which, double* out_total_m
   if (out_launches) *out_launches = ctx->prof[which].size();
   ctx->prof[which].clear();
   return HOMS_B200_OK;
+}
+
+int homs_b200_tensor_peak_probe(homs_b200_ctx* ctx, int engine, double seconds, double* out_ops_per_s,
+                                double* out_kernel_ms) {
+  if (!ctx || !out_ops_per_s) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_REQUIRE(ctx, engine == HOMS_B200_ENGINE_TENSOR || engine == HOMS_B200_ENGINE_TENSOR_FP4,
+             HOMS_B200_ERR_ARGUMENT, "tensor_peak_probe: engine must be TENSOR or TENSOR_FP4");
+  HB_REQUIRE(ctx, seconds > 0.0 && seconds <= 10.0, HOMS_B200_ERR_ARGUMENT,
+             "tensor_peak_probe: seconds must be in (0, 10]");
+  return tc_peak_probe(ctx, engine == HOMS_B200_ENGINE_TENSOR_FP4, seconds, out_ops_per_s, out_kernel_ms);
 }
 
 // ---- host-only configuration --------------------------------------------------------------

@@ -16,6 +16,7 @@
 //     coalesced 128-bit stores.
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 
@@ -197,22 +198,25 @@ __device__ __forceinline__ U4 ld_global_u4(const uint4* p) {
 //   strided mode (sv_offsets == nullptr): sv_bins[i*stride .. +sv_count[i])
 //   CSR mode:                              sv_bins[sv_offsets[i] .. sv_offsets[i+1])
 // NP = number of vertical counter planes (counts < 2^NP).
-template <int NP>
-__global__ void __launch_bounds__(256)
+#ifndef HB_ENC_MINB
+#define HB_ENC_MINB 2   // resident CTAs per SM the register budget is sized for (A/B: profiles/)
+#define HB_ENC_WARPS 8  // warps (= spectra in flight) per CTA
+#endif
+template <int NP, bool kLvlSmem>
+__global__ void __launch_bounds__(HB_ENC_WARPS * 32, HB_ENC_MINB)
 encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stride,
               const uint32_t* __restrict__ sv_bins, const uint32_t* __restrict__ sv_levels,
               const uint32_t* __restrict__ sv_count, const uint4* __restrict__ pos,
               const uint4* __restrict__ lvl_global, uint32_t n_level_rows, uint32_t row_u4,
-              uint32_t dim, uint32_t W, int lvl_in_smem, int vec_store,
+              uint32_t dim, uint32_t W, int vec_store,
               uint64_t* __restrict__ out_words,
               uint8_t* __restrict__ out_ok) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const uint4* lvl = lvl_global;
-  if (lvl_in_smem) {
-    uint4* s_lvl = reinterpret_cast<uint4*>(smem_raw);
+  // level rows: shared memory when they fit (LDS with a 32-bit address), else global through L1
+  uint4* s_lvl = reinterpret_cast<uint4*>(smem_raw);
+  if constexpr (kLvlSmem) {
     for (uint32_t i = threadIdx.x; i < n_level_rows * row_u4; i += blockDim.x) s_lvl[i] = lvl_global[i];
     __syncthreads();
-    lvl = s_lvl;
   }
   const int lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
@@ -244,52 +248,74 @@ encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stri
 #pragma unroll
       for (int b = 0; b < NP; ++b) c[b] = U4{{0, 0, 0, 0}};
 
-      for (uint32_t k0 = 0; k0 < nb; k0 += 7) {
-        U4 x[7];
-#pragma unroll
-        for (int j = 0; j < 7; ++j) {
-          x[j] = U4{{0, 0, 0, 0}};
-          if (k0 + j < nb && active) {
-            const uint32_t bin = sv_bins[start + k0 + j];    // warp-uniform: broadcast
-            const uint32_t lev = sv_levels[start + k0 + j];
-            const U4 pw = ld_global_u4(pos + size_t(bin) * row_u4 + u);
-            const uint4 lw4 = lvl[size_t(lev) * row_u4 + u];
-            x[j].v[0] = ~(pw.v[0] ^ lw4.x);  // encoder.cpp:41 agree = ~(pos ^ lvl)
-            x[j].v[1] = ~(pw.v[1] ^ lw4.y);
-            x[j].v[2] = ~(pw.v[2] ^ lw4.z);
-            x[j].v[3] = ~(pw.v[3] ^ lw4.w);
-          }
+      // The (bin, level) list is staged through registers 32 entries at a time (lane j holds entry
+      // c0 + j: one coalesced load per warp, the next block prefetched) and broadcast by shuffle,
+      // so the position-row gathers depend on no other memory access.  Votes are summed by a
+      // Harley-Seal tree: c[0..3] are carry-save accumulators of weight 1, 2, 4, 8 (and, being
+      // single bits per position, ARE planes 0..3 of the count); every 16 inputs emit one carry
+      // of weight 16 into the half-adder chain c[4..NP).  15 CSAs + NP-4 half adders per 16 inputs.
+      // Groups of 8 run in a real loop: 8 gathers in flight per lane, bounded registers.
+      const uint32_t uu = active ? u : row_u4 - 1;  // idle lanes gather a valid slab and store nothing
+      const uint4* pos_u = pos + uu;
+      uint32_t nxt_bin = 0, nxt_lev = 0;
+      if (lane < nb) {
+        nxt_bin = sv_bins[start + lane];
+        nxt_lev = sv_levels[start + lane];
+      }
+      for (uint32_t c0 = 0; c0 < nb; c0 += 32) {
+        const uint32_t my_bin = nxt_bin, my_lev = nxt_lev;
+        nxt_bin = nxt_lev = 0;  // entries beyond the list read row 0 and are masked to zero votes
+        if (c0 + 32 + lane < nb) {
+          nxt_bin = sv_bins[start + c0 + 32 + lane];
+          nxt_lev = sv_levels[start + c0 + 32 + lane];
         }
-        // 7:3 compressor
-        U4 s1, k1, s2, k2, ones, k3, twos, fours;
-        HB_CSA(s1, k1, x[0], x[1], x[2]);
-        HB_CSA(s2, k2, x[3], x[4], x[5]);
-        HB_CSA(ones, k3, s1, s2, x[6]);
-        HB_CSA(twos, fours, k1, k2, k3);
-        // add the 3-bit number (fours twos ones) into the vertical counters
+        const uint32_t cn = min(32u, nb - c0);
+        const uint32_t n_groups = 2 * ((cn + 15) / 16);  // groups of 8, an even number of them
+        U4 pend{{0, 0, 0, 0}};
+#pragma unroll 1
+        for (uint32_t g = 0; g < n_groups; ++g) {
+          U4 x[8];
+          uint32_t lev[8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint32_t carry;
-          {
-            const uint32_t a = c[0].v[i], o = ones.v[i];
-            c[0].v[i] = a ^ o;
-            carry = a & o;
+          for (int j = 0; j < 8; ++j) {  // 8 position-row gathers in flight
+            const uint32_t k = 8 * g + j;
+            const uint32_t bin = __shfl_sync(0xffffffffu, my_bin, k);
+            lev[j] = __shfl_sync(0xffffffffu, my_lev, k) * row_u4;
+            x[j] = ld_global_u4(pos_u + size_t(bin) * row_u4);
           }
-          if (NP > 1) {
-            const uint32_t a = c[1].v[i], t = twos.v[i];
-            c[1].v[i] = a ^ t ^ carry;
-            carry = (a & t) | (a & carry) | (t & carry);
-          }
-          if (NP > 2) {
-            const uint32_t a = c[2].v[i], f = fours.v[i];
-            c[2].v[i] = a ^ f ^ carry;
-            carry = (a & f) | (a & carry) | (f & carry);
-          }
+          asm volatile("" ::: "memory");  // level rows (shared memory) are fetched only as the gathers land
 #pragma unroll
-          for (int b = 3; b < NP; ++b) {
-            const uint32_t a = c[b].v[i];
-            c[b].v[i] = a ^ carry;
-            carry = a & carry;
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t m = 8 * g + j < cn ? 0xffffffffu : 0u;
+            const uint4 lw4 = kLvlSmem ? s_lvl[lev[j] + uu] : __ldg(lvl_global + lev[j] + uu);
+            x[j].v[0] = ~(x[j].v[0] ^ lw4.x) & m;  // encoder.cpp:41 agree = ~(pos ^ lvl)
+            x[j].v[1] = ~(x[j].v[1] ^ lw4.y) & m;
+            x[j].v[2] = ~(x[j].v[2] ^ lw4.z) & m;
+            x[j].v[3] = ~(x[j].v[3] ^ lw4.w) & m;
+          }
+          // 8 inputs -> c[0..2] updated, one carry e of weight 8
+          U4 ta, tb, fa, fb, e;
+          HB_CSA(c[0], ta, c[0], x[0], x[1]);
+          HB_CSA(c[0], tb, c[0], x[2], x[3]);
+          HB_CSA(c[1], fa, c[1], ta, tb);
+          HB_CSA(c[0], ta, c[0], x[4], x[5]);
+          HB_CSA(c[0], tb, c[0], x[6], x[7]);
+          HB_CSA(c[1], fb, c[1], ta, tb);
+          HB_CSA(c[2], e, c[2], fa, fb);
+          if ((g & 1u) == 0) {
+            pend = e;
+          } else {  // the carries of an even/odd pair meet in c[3] and ripple into the upper planes
+            U4 carry;
+            HB_CSA(c[3], carry, c[3], pend, e);
+#pragma unroll
+            for (int b = 4; b < NP; ++b) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const uint32_t a = c[b].v[i];
+                c[b].v[i] = a ^ carry.v[i];
+                carry.v[i] = a & carry.v[i];
+              }
+            }
           }
         }
       }
@@ -416,26 +442,31 @@ static int launch_encode(homs_b200_ctx* ctx, uint64_t n, const uint64_t* d_sv_of
   const size_t lvl_bytes = size_t(cb.levels + 1) * cb.S * 8;
   const int lvl_in_smem = lvl_bytes <= 96 * 1024;
   const size_t smem = lvl_in_smem ? lvl_bytes : 0;
-  const int warps = 8;
+  const int warps = HB_ENC_WARPS;
   const uint64_t want = (n + warps - 1) / warps;
-  const int grid = static_cast<int>(std::min<uint64_t>(want, uint64_t(ctx->sm_count) * 8));
+  const int grid = static_cast<int>(std::min<uint64_t>(want, uint64_t(ctx->sm_count) * HB_ENC_MINB * 4));
   // 128-bit stores need an even word count and a 16-byte aligned destination
   const int vec_store = (cb.W % 2 == 0) && (reinterpret_cast<uintptr_t>(d_out) % 16 == 0);
   HB_REQUIRE(ctx, max_count <= 65535, HOMS_B200_ERR_ARGUMENT,
              "encode: more than 65535 bins per spectrum is not supported by the device path");
-#define HB_ENC_LAUNCH(NP)                                                                        \
+#define HB_ENC_LAUNCH(NP, SM)                                                                    \
   do {                                                                                           \
-    HB_CUDA(ctx, cudaFuncSetAttribute(encode_kernel<NP>,                                         \
+    HB_CUDA(ctx, cudaFuncSetAttribute(encode_kernel<NP, SM>,                                     \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,               \
                                       static_cast<int>(smem)));                                  \
-    encode_kernel<NP><<<grid, warps * 32, smem, ctx->stream>>>(                                  \
+    encode_kernel<NP, SM><<<grid, warps * 32, smem, ctx->stream>>>(                              \
         n, d_sv_off, stride, d_bins, d_lev, d_count, cb.d_pos.as<uint4>(), cb.d_lvl.as<uint4>(), \
-        cb.levels + 1, row_u4, cb.dim, cb.W, lvl_in_smem, vec_store, d_out, d_ok);                          \
+        cb.levels + 1, row_u4, cb.dim, cb.W, vec_store, d_out, d_ok);                            \
   } while (0)
   {
     KernelTimer timer(ctx, HOMS_B200_KERNEL_ENCODE);
-    if (max_count <= 255) HB_ENC_LAUNCH(8);
-    else HB_ENC_LAUNCH(16);
+    if (max_count <= 255) {
+      if (lvl_in_smem) HB_ENC_LAUNCH(8, true);
+      else HB_ENC_LAUNCH(8, false);
+    } else {
+      if (lvl_in_smem) HB_ENC_LAUNCH(16, true);
+      else HB_ENC_LAUNCH(16, false);
+    }
   }
 #undef HB_ENC_LAUNCH
   HB_LAUNCHED(ctx);
@@ -461,6 +492,109 @@ static int encode_dev_locked(homs_b200_ctx* ctx, const homs_b200_preprocess_conf
   uint32_t* d_cnt = ctx->scratch[kScrSvCount].as<uint32_t>();
   HB_TRY(launch_preprocess(ctx, p, n, d_off, d_mz, d_int, d_bins, d_lev, d_cnt));
   HB_TRY(launch_encode(ctx, n, nullptr, p.max_peaks, d_bins, d_lev, d_cnt, p.max_peaks, d_out, d_ok));
+  return HOMS_B200_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// chunked host <-> device pipeline (pipeline.cpp:60-85 fans spectra out to threads; here chunks
+// of the CSR stream through three streams so that PCIe and the kernels overlap)
+// ------------------------------------------------------------------------------------------
+
+static int pipeline_resources(homs_b200_ctx* ctx) {
+  if (ctx->copy_in) return HOMS_B200_OK;
+  HB_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
+  HB_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    HB_CUDA(ctx, cudaEventCreateWithFlags(&ctx->pipe_in_ready[i], cudaEventDisableTiming));
+    HB_CUDA(ctx, cudaEventCreateWithFlags(&ctx->pipe_done[i], cudaEventDisableTiming));
+    HB_CUDA(ctx, cudaEventCreateWithFlags(&ctx->pipe_out_free[i], cudaEventDisableTiming));
+  }
+  return HOMS_B200_OK;
+}
+
+int encode_pipeline(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint64_t n,
+                    const uint64_t* offsets, const double* mz, const double* intensity, uint64_t* d_keep,
+                    uint8_t* d_keep_ok, uint64_t* h_words, uint8_t* h_ok) {
+  HB_REQUIRE(ctx, ctx->cb.ready, HOMS_B200_ERR_STATE, "encode: no codebook uploaded");
+  PreParams p;
+  HB_TRY(fill_pre_params(ctx, cfg, ctx->cb.levels, &p));
+  HB_REQUIRE(ctx, p.dims == ctx->cb.n_bins, HOMS_B200_ERR_INVARIANT,
+             "encode: spectrum vector dims do not match codebook");
+  if (n == 0) return HOMS_B200_OK;
+  HB_REQUIRE(ctx, offsets != nullptr, HOMS_B200_ERR_ARGUMENT, "encode: null offsets");
+  const uint64_t total = offsets[n] - offsets[0];
+  HB_REQUIRE(ctx, total == 0 || (mz && intensity), HOMS_B200_ERR_ARGUMENT, "encode: null peaks");
+  const uint32_t W = ctx->cb.W;
+
+  // chunks: at most 64 Ki spectra and about 4 Mi peaks (64 MB of m/z + intensity) each
+  constexpr uint64_t kMaxSpectra = 64 * 1024, kMaxPeaks = 4ull << 20;
+  std::vector<uint64_t> cuts{0};
+  uint64_t max_n = 0, max_peaks = 0;
+  for (uint64_t a = 0; a < n;) {
+    uint64_t b = a + 1;
+    while (b < n && b - a < kMaxSpectra && offsets[b + 1] - offsets[a] <= kMaxPeaks) ++b;
+    HB_REQUIRE(ctx, offsets[b] >= offsets[a], HOMS_B200_ERR_ARGUMENT, "encode: offsets must be non-decreasing");
+    max_n = std::max(max_n, b - a);
+    max_peaks = std::max(max_peaks, offsets[b] - offsets[a]);
+    cuts.push_back(b);
+    a = b;
+  }
+  const bool to_host = h_words != nullptr || h_ok != nullptr;
+  const bool out_slots = d_keep == nullptr;  // rows live in a slot only until they are copied out
+  HB_TRY(pipeline_resources(ctx));
+  const size_t in_bytes = (max_n + 1) * 8 + max_peaks * 16;
+  const size_t out_bytes = out_slots ? max_n * W * 8 + max_n : (d_keep_ok ? 0 : max_n);
+  for (int s = 0; s < 2; ++s) {
+    HB_TRY(ensure(ctx, ctx->scratch[kScrPipeIn0 + s], in_bytes));
+    if (out_bytes) HB_TRY(ensure(ctx, ctx->scratch[kScrPipeOut0 + s], out_bytes));
+  }
+  // sized once so that no chunk reallocates under the pipeline
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvBins], size_t(max_n) * p.max_peaks * 4));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvLev], size_t(max_n) * p.max_peaks * 4));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrSvCount], size_t(max_n) * 4));
+
+  cudaStream_t cs = ctx->stream, in = ctx->copy_in, out = ctx->copy_out;
+  for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+    const int s = static_cast<int>(c & 1);
+    const uint64_t a = cuts[c], b = cuts[c + 1], cn = b - a;
+    const uint64_t p0 = offsets[a], np = offsets[b] - p0;
+    auto* d_off = ctx->scratch[kScrPipeIn0 + s].as<uint64_t>();
+    auto* d_mz = reinterpret_cast<double*>(d_off + (max_n + 1));
+    auto* d_int = d_mz + max_peaks;
+    if (c >= 2) HB_CUDA(ctx, cudaStreamWaitEvent(in, ctx->pipe_done[s], 0));  // slot inputs consumed
+    HB_CUDA(ctx, cudaMemcpyAsync(d_off, offsets + a, (cn + 1) * 8, cudaMemcpyHostToDevice, in));
+    if (np) {
+      HB_CUDA(ctx, cudaMemcpyAsync(d_mz, mz + p0, np * 8, cudaMemcpyHostToDevice, in));
+      HB_CUDA(ctx, cudaMemcpyAsync(d_int, intensity + p0, np * 8, cudaMemcpyHostToDevice, in));
+    }
+    HB_CUDA(ctx, cudaEventRecord(ctx->pipe_in_ready[s], in));
+
+    uint64_t* d_rows;
+    uint8_t* d_ok;
+    if (out_slots) {
+      d_rows = ctx->scratch[kScrPipeOut0 + s].as<uint64_t>();
+      d_ok = reinterpret_cast<uint8_t*>(d_rows + max_n * W);
+    } else {
+      d_rows = d_keep + a * W;
+      d_ok = d_keep_ok ? d_keep_ok + a : ctx->scratch[kScrPipeOut0 + s].as<uint8_t>();
+    }
+    HB_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->pipe_in_ready[s], 0));
+    if (to_host && c >= 2) HB_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->pipe_out_free[s], 0));
+    // the kernels index peaks with the absolute offsets: shift the slot pointers by -p0
+    HB_TRY(encode_dev_locked(ctx, cfg, cn, d_off, d_mz - p0, d_int - p0, d_rows, d_ok));
+    HB_CUDA(ctx, cudaEventRecord(ctx->pipe_done[s], cs));
+
+    if (to_host) {
+      HB_CUDA(ctx, cudaStreamWaitEvent(out, ctx->pipe_done[s], 0));
+      if (h_words)
+        HB_CUDA(ctx, cudaMemcpyAsync(h_words + a * W, d_rows, cn * W * 8, cudaMemcpyDeviceToHost, out));
+      if (h_ok) HB_CUDA(ctx, cudaMemcpyAsync(h_ok + a, d_ok, cn, cudaMemcpyDeviceToHost, out));
+      HB_CUDA(ctx, cudaEventRecord(ctx->pipe_out_free[s], out));
+    }
+  }
+  HB_CUDA(ctx, cudaStreamSynchronize(in));
+  HB_CUDA(ctx, cudaStreamSynchronize(cs));
+  HB_CUDA(ctx, cudaStreamSynchronize(out));
   return HOMS_B200_OK;
 }
 
@@ -510,39 +644,10 @@ int homs_b200_encode_batch(homs_b200_ctx* ctx, const homs_b200_preprocess_config
                            uint64_t* out_words, uint8_t* out_ok) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
-  HB_REQUIRE(ctx, ctx->cb.ready, HOMS_B200_ERR_STATE, "encode: no codebook uploaded");
-  if (n == 0) {
-    PreParams p;
-    HB_TRY(fill_pre_params(ctx, cfg, ctx->cb.levels, &p));
-    HB_REQUIRE(ctx, p.dims == ctx->cb.n_bins, HOMS_B200_ERR_INVARIANT,
-               "encode: spectrum vector dims do not match codebook");
-    return HOMS_B200_OK;
-  }
-  HB_REQUIRE(ctx, offsets && out_words && out_ok, HOMS_B200_ERR_ARGUMENT, "encode_batch: null argument");
-  const uint64_t total = offsets[n] - offsets[0];
-  HB_REQUIRE(ctx, total == 0 || (mz && intensity), HOMS_B200_ERR_ARGUMENT, "encode_batch: null peaks");
-  HB_REQUIRE(ctx, offsets[0] == 0, HOMS_B200_ERR_ARGUMENT, "encode_batch: offsets[0] must be 0");
-  const uint32_t W = ctx->cb.W;
-  HB_TRY(ensure(ctx, ctx->scratch[kScrOffsets], (n + 1) * 8));
-  HB_TRY(ensure(ctx, ctx->scratch[kScrMz], total * 8));
-  HB_TRY(ensure(ctx, ctx->scratch[kScrInt], total * 8));
-  HB_TRY(ensure(ctx, ctx->scratch[kScrEncOut], n * W * 8));
-  HB_TRY(ensure(ctx, ctx->scratch[kScrEncOk], n));
-  auto* d_off = ctx->scratch[kScrOffsets].as<uint64_t>();
-  auto* d_mz = ctx->scratch[kScrMz].as<double>();
-  auto* d_int = ctx->scratch[kScrInt].as<double>();
-  auto* d_out = ctx->scratch[kScrEncOut].as<uint64_t>();
-  auto* d_ok = ctx->scratch[kScrEncOk].as<uint8_t>();
-  HB_CUDA(ctx, cudaMemcpyAsync(d_off, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
-  if (total) {
-    HB_CUDA(ctx, cudaMemcpyAsync(d_mz, mz, total * 8, cudaMemcpyHostToDevice, ctx->stream));
-    HB_CUDA(ctx, cudaMemcpyAsync(d_int, intensity, total * 8, cudaMemcpyHostToDevice, ctx->stream));
-  }
-  HB_TRY(encode_dev_locked(ctx, cfg, n, d_off, d_mz, d_int, d_out, d_ok));
-  HB_CUDA(ctx, cudaMemcpyAsync(out_words, d_out, n * W * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  HB_CUDA(ctx, cudaMemcpyAsync(out_ok, d_ok, n, cudaMemcpyDeviceToHost, ctx->stream));
-  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  return HOMS_B200_OK;
+  HB_REQUIRE(ctx, n == 0 || (offsets && out_words && out_ok), HOMS_B200_ERR_ARGUMENT,
+             "encode_batch: null argument");
+  HB_REQUIRE(ctx, n == 0 || offsets[0] == 0, HOMS_B200_ERR_ARGUMENT, "encode_batch: offsets[0] must be 0");
+  return encode_pipeline(ctx, cfg, n, offsets, mz, intensity, nullptr, nullptr, out_words, out_ok);
 }
 
 int homs_b200_preprocess_batch(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg,

@@ -31,7 +31,8 @@ __global__ void gather_rows_kernel(uint64_t n_rows, const uint32_t* __restrict__
 
 static int build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h_words,
                  const uint64_t* d_words_in, const double* mz, const uint8_t* charge,
-                 const uint32_t* id_rank, uint32_t shard_index, uint32_t shard_count) {
+                 const uint32_t* id_rank, uint32_t shard_index, uint32_t shard_count,
+                 const uint32_t* row_of_entry = nullptr) {
   HB_REQUIRE(ctx, n >= 1, HOMS_B200_ERR_INVARIANT, "build_index: library is empty");  // search.cpp:18
   HB_REQUIRE(ctx, dim >= 1, HOMS_B200_ERR_ARGUMENT, "build_index: dim must be positive");
   HB_REQUIRE(ctx, n < 0xFFFFFFFFull, HOMS_B200_ERR_ARGUMENT, "build_index: more than 2^32-2 entries");
@@ -107,7 +108,7 @@ static int build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h
   for (const BucketDev& b : lib.buckets)
     for (uint64_t i = b.shard_begin; i < b.shard_end; ++i) {
       const uint64_t l = b.local_offset + (i - b.shard_begin), g = b.begin + i;
-      local_src[l] = order[g];
+      local_src[l] = row_of_entry ? row_of_entry[order[g]] : order[g];
       local_mz[l] = lib.h_mz[g];
       local_rank[l] = rank_sorted[g];
     }
@@ -187,8 +188,8 @@ static int build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h
 
 int library_build_from_device(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* d_words,
                               const double* mz, const uint8_t* charge, const uint32_t* id_rank,
-                              uint32_t shard_index, uint32_t shard_count) {
-  return build(ctx, dim, n, nullptr, d_words, mz, charge, id_rank, shard_index, shard_count);
+                              uint32_t shard_index, uint32_t shard_count, const uint32_t* row_of_entry) {
+  return build(ctx, dim, n, nullptr, d_words, mz, charge, id_rank, shard_index, shard_count, row_of_entry);
 }
 
 }  // namespace hb

@@ -797,14 +797,20 @@ int homs_b200_search_batch(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq,
   return decode_locked(ctx, nq * k, d_rec, out_raw_score, out_ordinal);
 }
 
-int homs_b200_cascade_search(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq,
-                             const uint64_t* q_words, const double* q_mz, const uint8_t* q_charge,
-                             const homs_b200_tolerance* narrow, const homs_b200_tolerance* wide,
-                             double fdr_q, const uint8_t* lib_is_decoy, uint64_t* out_query,
-                             uint32_t* out_ordinal, uint8_t* out_stage, uint32_t* out_raw_score,
-                             double* out_q_value, uint64_t* out_count) {
-  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
-  Lock lock(ctx);
+}  // extern "C"
+
+// cascade over the RESIDENT queries (q_words == nullptr) or over host queries uploaded first
+static int cascade_locked(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq, const uint64_t* q_words,
+                          const double* q_mz, const uint8_t* q_charge, const homs_b200_tolerance* narrow,
+                          const homs_b200_tolerance* wide, double fdr_q, const uint8_t* lib_is_decoy,
+                          uint64_t* out_query, uint32_t* out_ordinal, uint8_t* out_stage,
+                          uint32_t* out_raw_score, double* out_q_value, uint64_t* out_count) {
+  const bool resident = q_words == nullptr && q_mz == nullptr && q_charge == nullptr;
+  if (resident) {
+    HB_REQUIRE(ctx, ctx->q.ready, HOMS_B200_ERR_STATE, "cascade_resident: no resident queries");
+    query_dim = ctx->q.dim;
+    nq = ctx->q.nq;
+  }
   HB_REQUIRE(ctx, ctx->lib.ready, HOMS_B200_ERR_STATE, "cascade_search: no library uploaded");
   HB_REQUIRE(ctx, ctx->lib.shard_count == 1, HOMS_B200_ERR_STATE, "cascade_search: sharded library");
   HB_TRY(check_tol(ctx, narrow));
@@ -819,7 +825,7 @@ int homs_b200_cascade_search(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq
              "search_one: query dimensionality does not match index");
   HB_REQUIRE(ctx, lib_is_decoy && out_query && out_ordinal && out_stage && out_raw_score && out_q_value,
              HOMS_B200_ERR_ARGUMENT, "cascade_search: null argument");
-  HB_TRY(queries_set_locked(ctx, query_dim, nq, q_words, q_mz, q_charge, false));
+  if (!resident) HB_TRY(queries_set_locked(ctx, query_dim, nq, q_words, q_mz, q_charge, false));
   HB_TRY(ensure(ctx, ctx->scratch[kScrRecords], nq * sizeof(Cand)));
   Cand* d_rec = ctx->scratch[kScrRecords].as<Cand>();
 
@@ -892,6 +898,68 @@ int homs_b200_cascade_search(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq
       }
   *out_count = m;
   return HOMS_B200_OK;
+}
+
+extern "C" {
+
+int homs_b200_cascade_search(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq,
+                             const uint64_t* q_words, const double* q_mz, const uint8_t* q_charge,
+                             const homs_b200_tolerance* narrow, const homs_b200_tolerance* wide,
+                             double fdr_q, const uint8_t* lib_is_decoy, uint64_t* out_query,
+                             uint32_t* out_ordinal, uint8_t* out_stage, uint32_t* out_raw_score,
+                             double* out_q_value, uint64_t* out_count) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_REQUIRE(ctx, nq == 0 || (q_words && q_mz && q_charge), HOMS_B200_ERR_ARGUMENT,
+             "cascade_search: null argument");
+  if (nq == 0) {  // keep the validation order of the host-query form
+    static const uint64_t none = 0;
+    q_words = &none;
+  }
+  return cascade_locked(ctx, query_dim, nq, q_words, q_mz, q_charge, narrow, wide, fdr_q, lib_is_decoy, out_query,
+                        out_ordinal, out_stage, out_raw_score, out_q_value, out_count);
+}
+
+int homs_b200_cascade_resident(homs_b200_ctx* ctx, const homs_b200_tolerance* narrow,
+                               const homs_b200_tolerance* wide, double fdr_q, const uint8_t* lib_is_decoy,
+                               uint64_t* out_query, uint32_t* out_ordinal, uint8_t* out_stage,
+                               uint32_t* out_raw_score, double* out_q_value, uint64_t* out_count) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  return cascade_locked(ctx, 0, 0, nullptr, nullptr, nullptr, narrow, wide, fdr_q, lib_is_decoy, out_query,
+                        out_ordinal, out_stage, out_raw_score, out_q_value, out_count);
+}
+
+int homs_b200_search_resident(homs_b200_ctx* ctx, const homs_b200_tolerance* tol, uint32_t k,
+                              uint32_t* out_raw_score, uint32_t* out_ordinal, uint64_t* out_first,
+                              uint64_t* out_last) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_REQUIRE(ctx, ctx->lib.ready, HOMS_B200_ERR_STATE, "search_resident: no library uploaded");
+  HB_REQUIRE(ctx, ctx->q.ready, HOMS_B200_ERR_STATE, "search_resident: no resident queries");
+  HB_REQUIRE(ctx, ctx->lib.shard_count == 1, HOMS_B200_ERR_STATE,
+             "search_resident: sharded library; use search_resident_dev + merge_candidates_dev");
+  HB_REQUIRE(ctx, ctx->q.dim == ctx->lib.dim, HOMS_B200_ERR_INVARIANT,
+             "search_one: query dimensionality does not match index");
+  HB_TRY(check_tol(ctx, tol));
+  HB_REQUIRE(ctx, k >= 1 && k <= HOMS_B200_MAX_TOPK, HOMS_B200_ERR_ARGUMENT, "search: k must be in [1, 64]");
+  const uint64_t nq = ctx->q.nq;
+  if (nq == 0) return HOMS_B200_OK;
+  HB_REQUIRE(ctx, out_raw_score && out_ordinal, HOMS_B200_ERR_ARGUMENT, "search_resident: null output");
+  HB_TRY(ensure(ctx, ctx->scratch[kScrRecords], nq * k * sizeof(Cand)));
+  uint64_t* d_first = nullptr;
+  uint64_t* d_last = nullptr;
+  if (out_first || out_last) {
+    HB_TRY(ensure(ctx, ctx->scratch[kScrQFirst], nq * 8));
+    HB_TRY(ensure(ctx, ctx->scratch[kScrQLast], nq * 8));
+    d_first = ctx->scratch[kScrQFirst].as<uint64_t>();
+    d_last = ctx->scratch[kScrQLast].as<uint64_t>();
+  }
+  Cand* d_rec = ctx->scratch[kScrRecords].as<Cand>();
+  HB_TRY(search_dev_locked(ctx, nullptr, nq, tol, k, d_rec, d_first, d_last, nullptr));
+  if (out_first) HB_CUDA(ctx, cudaMemcpyAsync(out_first, d_first, nq * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (out_last) HB_CUDA(ctx, cudaMemcpyAsync(out_last, d_last, nq * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  return decode_locked(ctx, nq * k, d_rec, out_raw_score, out_ordinal);
 }
 
 }  // extern "C"

@@ -804,4 +804,114 @@ int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, c
                         : tc_search_sorted_mode<false>(ctx, d_subset, n, d_keys, d_vals, d_out, k_stride);
 }
 
+// ---- tensor-pipe ceiling probe ----------------------------------------------------------------
+// The issue loop of tc_search_kernel with everything else removed: one thread per SM issues the same
+// MMA shape back to back on whatever bytes shared memory holds (no global traffic, no drain), in
+// groups of 4 per commit with `depth` groups in flight.  bench.py times it on the same box in the same run and
+// reports the search kernel against it: MEASURED_PEAKS.json holds a bf16 figure only, and the
+// sustained rate of the 4-bit / 8-bit kinds under the power cap is not a fixed multiple of it.
+template <bool kFp4>
+__global__ void __launch_bounds__(kTcThreads, 1) tc_peak_kernel(uint32_t groups) {
+  using Mode = TcMode<kFp4>;
+  constexpr int kN = Mode::N;
+  constexpr int kDepth = 4;
+  extern __shared__ unsigned char tc_smem_raw[];
+  const uint32_t raw = smem_u32(tc_smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  unsigned char* gen_base = tc_smem_raw + (base - raw);
+  const uint32_t bar0 = base + Mode::Stages * Mode::StageBytes;
+  volatile uint32_t* tmem_slot =
+      reinterpret_cast<volatile uint32_t*>(gen_base + Mode::Stages * Mode::StageBytes + 8 * kDepth);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // operands: any finite pattern will do; e2m1 / int8 have no NaN or Inf encodings
+  for (uint32_t i = threadIdx.x; i < Mode::StageBytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(gen_base)[i] = make_uint4(0x2A2A2A2Au, 0xA2A2A2A2u, 0x22AA22AAu, 0xAAAA2222u);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kDepth; ++s) mbar_init(bar0 + 8u * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(const_cast<uint32_t*>(tmem_slot))),
+                 "r"(kTcTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if constexpr (kFp4) {
+    if (warp >= 2) tc_st32_fill(tmem_base + (uint32_t((warp & 3) * 32) << 16) + Mode::SfCol, 0x7F7F7F7Fu);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  if (warp == 1 && lane == 0) {
+    const uint64_t adesc = tc_smem_desc(base);
+    const uint64_t bdesc = tc_smem_desc(base + kTcABytes);
+    for (uint32_t g = 0; g < groups; ++g) {
+      const uint32_t slot = g % kDepth;
+      if (g >= kDepth) mbar_wait(bar0 + 8u * slot, ((g / kDepth) - 1u) & 1u);
+      const uint32_t tmem_d = tmem_base + (g & 1u) * kN;
+#pragma unroll
+      for (uint32_t k = 0; k < kTcKB / 32; ++k) {
+        if constexpr (kFp4)
+          tc_mma_fp4(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescFp4, tmem_base + Mode::SfCol,
+                     tmem_base + Mode::SfCol + 16, 1u);
+        else
+          tc_mma_i8(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescI8, 1u);
+      }
+      tc_commit(bar0 + 8u * slot);
+    }
+    for (uint32_t g = groups > kDepth ? groups - kDepth : 0; g < groups; ++g)
+      mbar_wait(bar0 + 8u * (g % kDepth), (g / kDepth) & 1u);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcTmemCols)
+                 : "memory");
+  }
+}
+
+template <bool kFp4>
+static int tc_peak_probe_mode(homs_b200_ctx* ctx, double seconds, double* out_ops_per_s, double* out_ms) {
+  using Mode = TcMode<kFp4>;
+  HB_CUDA(ctx, cudaFuncSetAttribute(tc_peak_kernel<kFp4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(Mode::SmemBytes)));
+  cudaEvent_t e0, e1;
+  HB_CUDA(ctx, cudaEventCreate(&e0));
+  HB_CUDA(ctx, cudaEventCreate(&e1));
+  // ops of one group: 4 MMAs of M128 x N x (32 bytes of K)
+  const double ops_group = 2.0 * kTcM * Mode::N * Mode::kDims;
+  uint32_t groups = 1u << 14;
+  float ms = 0.f;
+  for (int pass = 0; pass < 3; ++pass) {  // calibrate, warm (reach the power-capped clock), measure
+    HB_CUDA(ctx, cudaEventRecord(e0, ctx->stream));
+    tc_peak_kernel<kFp4><<<ctx->sm_count, kTcThreads, Mode::SmemBytes, ctx->stream>>>(groups);
+    HB_LAUNCHED(ctx);
+    HB_CUDA(ctx, cudaEventRecord(e1, ctx->stream));
+    HB_CUDA(ctx, cudaEventSynchronize(e1));
+    HB_CUDA(ctx, cudaEventElapsedTime(&ms, e0, e1));
+    if (pass == 0) {
+      const double want = seconds * 1e3 / std::max(1e-3f, ms) * groups;
+      groups = static_cast<uint32_t>(std::min(want, 4.0e9));
+      groups = std::max(groups, 1u << 10);
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *out_ops_per_s = ops_group * groups * ctx->sm_count / (ms * 1e-3);
+  if (out_ms) *out_ms = ms;
+  return HOMS_B200_OK;
+}
+
+int tc_peak_probe(homs_b200_ctx* ctx, int fp4, double seconds, double* out_ops_per_s, double* out_ms) {
+  return fp4 ? tc_peak_probe_mode<true>(ctx, seconds, out_ops_per_s, out_ms)
+             : tc_peak_probe_mode<false>(ctx, seconds, out_ops_per_s, out_ms);
+}
+
 }  // namespace hb

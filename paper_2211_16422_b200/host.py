@@ -285,6 +285,13 @@ class Context:
         _check(capi.ctx_kernel_time(self._h, which, C.byref(ms), C.byref(cnt)), self._h)
         return ms.value, cnt.value
 
+    def tensor_peak_probe(self, engine: str = "tensor_fp4", seconds: float = 0.5):
+        """(ops/s, kernel ms) of the tensor engine's bare MMA issue loop on this device."""
+        eng = {"tensor": capi.ENGINE_TENSOR, "tensor_fp4": capi.ENGINE_TENSOR_FP4}[engine]
+        ops, ms = C.c_double(), C.c_double()
+        _check(capi.tensor_peak_probe(self._h, eng, float(seconds), C.byref(ops), C.byref(ms)), self._h)
+        return ops.value, ms.value
+
     # -- encoding ---------------------------------------------------------------------------
     def upload_codebook(self, cb: Codebook) -> None:
         pos = _arr(cb.position, np.uint64)
