@@ -508,10 +508,12 @@ def run_encode(args) -> None:
     h_off = torch.from_numpy(offs[:m + 1].astype(np.int64)).pin_memory().numpy().view(np.uint64)
     h_mz = torch.from_numpy(spec["mz"][:p1]).pin_memory().numpy()
     h_int = torch.from_numpy(spec["intensity"][:p1]).pin_memory().numpy()
+    h_words = torch.empty((m, W), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    h_ok = torch.empty(m, dtype=torch.uint8).pin_memory().numpy()
     times = []
     for i in range(2 + args.steps):
         t0 = time.perf_counter()
-        hw, hok = ctx.encode_batch(h_off, h_mz, h_int, pre)
+        hw, hok = ctx.encode_batch(h_off, h_mz, h_int, pre, out=(h_words, h_ok))
         if i >= 2:
             times.append(time.perf_counter() - t0)
     e2e_value = m / (sum(times) / len(times))

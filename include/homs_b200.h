@@ -300,6 +300,42 @@ int homs_b200_candidates_decode(homs_b200_ctx* ctx, uint64_t n, uint32_t k,
                                 const homs_b200_candidate* d_records, uint32_t* out_raw_score,
                                 uint32_t* out_ordinal);
 
+/* ---- fused raw-spectra entry points (no single reference counterpart) -------
+ * The reference composes these from its public calls and moves every hypervector through host
+ * vectors in between; here the rows never leave the device.
+ *
+ * library_build_from_spectra == build_index(encode_spectra(spectra).encoded)
+ *   (src/pipeline.cpp:60-85 then src/search.cpp:17-60; `homs encode` + index load,
+ *   pipeline.cpp:97-99,121).  Unprocessable spectra are dropped in order exactly as
+ *   pipeline.cpp:75-83 does, so the library ordinals a search reports count PROCESSABLE spectra
+ *   only.  precursor_mz / charge / id_rank are indexed by raw spectrum; id_rank (may be NULL =
+ *   input order) is a permutation of 0..n-1 over the raw list.  out_ok[n] (may be NULL) receives
+ *   1 for encoded, 0 for dropped; *out_n_encoded the library size.  Fails with ERR_INVARIANT
+ *   ("library is empty", search.cpp:18) when nothing survives.  The codebook must be uploaded to
+ *   THIS context. */
+int homs_b200_library_build_from_spectra(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg,
+                                         uint64_t n, const uint64_t* offsets, const double* mz,
+                                         const double* intensity, const double* precursor_mz,
+                                         const uint8_t* charge, const uint32_t* id_rank,
+                                         uint32_t shard_index, uint32_t shard_count, uint8_t* out_ok,
+                                         uint64_t* out_n_encoded);
+/* queries_from_spectra == the encode_spectra step of run_search (pipeline.cpp:121-122) with the
+ * result left resident: query e of the resident set is the e-th processable spectrum. */
+int homs_b200_queries_from_spectra(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint64_t n,
+                                   const uint64_t* offsets, const double* mz, const double* intensity,
+                                   const double* precursor_mz, const uint8_t* charge, uint8_t* out_ok,
+                                   uint64_t* out_n_encoded);
+/* search_batch (search.cpp:171-183) / cascade_search (search.cpp:219-248) over the RESIDENT
+ * queries (queries_upload*, queries_from_spectra); outputs as in the host-query forms, sized by
+ * the resident query count. */
+int homs_b200_search_resident(homs_b200_ctx* ctx, const homs_b200_tolerance* tol, uint32_t k,
+                              uint32_t* out_raw_score, uint32_t* out_ordinal, uint64_t* out_first,
+                              uint64_t* out_last);
+int homs_b200_cascade_resident(homs_b200_ctx* ctx, const homs_b200_tolerance* narrow,
+                               const homs_b200_tolerance* wide, double fdr_q, const uint8_t* lib_is_decoy,
+                               uint64_t* out_query, uint32_t* out_ordinal, uint8_t* out_stage,
+                               uint32_t* out_raw_score, double* out_q_value, uint64_t* out_count);
+
 /* cascade_search, src/search.cpp:219-248 (run_stage :188-215): narrow stage on all queries,
  * target-decoy FDR, wide stage on the not-accepted rest, FDR again.  lib_is_decoy is indexed by
  * library ordinal.  Outputs need room for nq entries; accepted matches come narrow block first,

@@ -123,6 +123,15 @@ cascade_search = _decl("homs_b200_cascade_search", _I,
                        [_VP, _U32, _U64, _VP, _VP, _VP, _P(TolerancePod), _P(TolerancePod), _F64,
                         _VP, _VP, _VP, _VP, _VP, _VP, _P(_U64)])
 
+library_build_from_spectra = _decl("homs_b200_library_build_from_spectra", _I,
+                                   [_VP, _P(PreprocessConfigPod), _U64, _VP, _VP, _VP, _VP, _VP, _VP, _U32, _U32,
+                                    _VP, _P(_U64)])
+queries_from_spectra = _decl("homs_b200_queries_from_spectra", _I,
+                             [_VP, _P(PreprocessConfigPod), _U64, _VP, _VP, _VP, _VP, _VP, _VP, _P(_U64)])
+search_resident = _decl("homs_b200_search_resident", _I, [_VP, _P(TolerancePod), _U32, _VP, _VP, _VP, _VP])
+cascade_resident = _decl("homs_b200_cascade_resident", _I,
+                         [_VP, _P(TolerancePod), _P(TolerancePod), _F64, _VP, _VP, _VP, _VP, _VP, _VP, _P(_U64)])
+
 fnv1a64_dev = _decl("homs_b200_fnv1a64_dev", _I, [_VP, _VP, _U64, _P(_U64)])
 fnv1a64 = _decl("homs_b200_fnv1a64", _I, [_VP, _VP, _U64, _P(_U64)])
 cache_parse = _decl("homs_b200_cache_parse", _I,

@@ -300,16 +300,23 @@ class Context:
                                     _ptr(pos), _ptr(lvl)), self._h)
         self.codebook = cb
 
-    def encode_batch(self, offsets, mz, intensity, preprocess: PreprocessConfig):
+    def encode_batch(self, offsets, mz, intensity, preprocess: PreprocessConfig, out=None):
         """Flat form of encode_spectra: (words u64[n, W] with zero rows for unprocessable
-        spectra, ok u8[n])."""
+        spectra, ok u8[n]).  `out` = (words, ok) reuses caller arrays (e.g. pinned memory: the
+        chunked H2D / kernel / D2H pipeline then overlaps fully)."""
         offsets = _arr(offsets, np.uint64)
         mz = _arr(mz, np.float64)
         intensity = _arr(intensity, np.float64)
         n = len(offsets) - 1
         W = words_for(self.codebook.config.dim) if self.codebook else 0
-        words = np.zeros((n, W), np.uint64)
-        ok = np.zeros(n, np.uint8)
+        if out is not None:
+            words, ok = out
+            if words.dtype != np.uint64 or words.shape != (n, W) or ok.dtype != np.uint8 or ok.shape != (n,) \
+                    or not words.flags.c_contiguous:
+                raise ValueError("encode_batch: out must be (uint64[n, W] C-contiguous, uint8[n])")
+        else:
+            words = np.empty((n, W), np.uint64)
+            ok = np.empty(n, np.uint8)
         _check(capi.encode_batch(self._h, C.byref(preprocess.pod()), n, _ptr(offsets), _ptr(mz),
                                  _ptr(intensity), _ptr(words), _ptr(ok)), self._h)
         return words, ok
@@ -501,6 +508,74 @@ class Context:
         return dict(query=query[:m].copy(), ordinal=ordinal[:m].copy(), stage=stage[:m].copy(),
                     raw_score=score[:m].copy(), q_value=qv[:m].copy())
 
+    # -- fused raw-spectra paths ---------------------------------------------
+    def build_index_from_spectra(self, offsets, mz, intensity, preprocess: PreprocessConfig, precursor_mz,
+                                 charge, ids=None, is_decoy=None, shard_index: int = 0, shard_count: int = 1,
+                                 id_rank=None):
+        """build_index(encode_spectra(spectra).encoded) without moving a hypervector to the host.
+        Returns ok u8[n]; library ordinals count the processable spectra only (pipeline.cpp:75-83)."""
+        offsets = _arr(offsets, np.uint64)
+        mz = _arr(mz, np.float64)
+        intensity = _arr(intensity, np.float64)
+        precursor_mz = _arr(precursor_mz, np.float64)
+        charge = _arr(charge, np.uint8)
+        n = len(offsets) - 1
+        if id_rank is None and ids is not None:
+            id_rank = id_ranks(ids)
+        rank = _arr(id_rank, np.uint32) if id_rank is not None else None
+        ok = np.zeros(n, np.uint8)
+        cnt = C.c_uint64()
+        _check(capi.library_build_from_spectra(self._h, C.byref(preprocess.pod()), n, _ptr(offsets), _ptr(mz),
+                                               _ptr(intensity), _ptr(precursor_mz), _ptr(charge), _ptr(rank),
+                                               shard_index, shard_count, _ptr(ok), C.byref(cnt)), self._h)
+        kept = np.flatnonzero(ok)
+        dec = _arr(is_decoy, np.uint8)[kept] if is_decoy is not None else None
+        self._set_lib(self.codebook.config.dim, int(cnt.value), dec)
+        return ok
+
+    def queries_from_spectra(self, offsets, mz, intensity, preprocess: PreprocessConfig, precursor_mz, charge):
+        """encode_spectra with the result left resident as the query set.  Returns ok u8[n]."""
+        offsets = _arr(offsets, np.uint64)
+        mz = _arr(mz, np.float64)
+        intensity = _arr(intensity, np.float64)
+        precursor_mz = _arr(precursor_mz, np.float64)
+        charge = _arr(charge, np.uint8)
+        n = len(offsets) - 1
+        ok = np.zeros(n, np.uint8)
+        cnt = C.c_uint64()
+        _check(capi.queries_from_spectra(self._h, C.byref(preprocess.pod()), n, _ptr(offsets), _ptr(mz),
+                                         _ptr(intensity), _ptr(precursor_mz), _ptr(charge), _ptr(ok),
+                                         C.byref(cnt)), self._h)
+        self.resident_queries = int(cnt.value)
+        return ok
+
+    def search_resident(self, tol: Tolerance, k: int = 1, nq: int | None = None) -> Match:
+        """search_batch over the resident queries."""
+        nq = self.resident_queries if nq is None else nq
+        score = np.zeros((nq, k), np.uint32)
+        ordinal = np.full((nq, k), capi.NO_HIT, np.uint32)
+        first = np.zeros(nq, np.uint64)
+        last = np.zeros(nq, np.uint64)
+        _check(capi.search_resident(self._h, C.byref(tol.pod()), k, _ptr(score), _ptr(ordinal), _ptr(first),
+                                    _ptr(last)), self._h)
+        return Match(ordinal != capi.NO_HIT, score, ordinal, first, last)
+
+    def cascade_resident(self, narrow: Tolerance, wide: Tolerance, fdr_q: float, nq: int | None = None) -> dict:
+        """cascade_search over the resident queries."""
+        nq = self.resident_queries if nq is None else nq
+        query = np.zeros(nq, np.uint64)
+        ordinal = np.zeros(nq, np.uint32)
+        stage = np.zeros(nq, np.uint8)
+        score = np.zeros(nq, np.uint32)
+        qv = np.zeros(nq, np.float64)
+        cnt = C.c_uint64()
+        _check(capi.cascade_resident(self._h, C.byref(narrow.pod()), C.byref(wide.pod()), float(fdr_q),
+                                     _ptr(self.lib_is_decoy), _ptr(query), _ptr(ordinal), _ptr(stage),
+                                     _ptr(score), _ptr(qv), C.byref(cnt)), self._h)
+        m = cnt.value
+        return dict(query=query[:m].copy(), ordinal=ordinal[:m].copy(), stage=stage[:m].copy(),
+                    raw_score=score[:m].copy(), q_value=qv[:m].copy())
+
     # -- device-resident pieces (multi-GPU composition, benchmarks) -------------------------
     def queries_upload(self, dim: int, q_words, q_mz, q_charge) -> int:
         q_mz = _arr(q_mz, np.float64)
@@ -509,6 +584,7 @@ class Context:
         q_words = _arr(q_words, np.uint64)
         _check(capi.queries_upload(self._h, dim, nq, _ptr(q_words), _ptr(q_mz), _ptr(q_charge)),
                self._h)
+        self.resident_queries = nq
         return nq
 
     def queries_upload_dev(self, dim: int, nq: int, d_words: int, d_mz: int, d_charge: int) -> None:
