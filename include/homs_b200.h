@@ -44,7 +44,8 @@ enum {
   HOMS_B200_ERR_STATE = 5,     /* call order (e.g. search before library upload) */
   HOMS_B200_ERR_CACHE_FORMAT = 6,  /* homs::CacheFormatError  (bad magic / version) */
   HOMS_B200_ERR_CACHE_STALE = 7,   /* homs::StaleCacheError   (profile block differs) */
-  HOMS_B200_ERR_CACHE_CORRUPT = 8  /* homs::CacheCorruptError (truncated / bad string / checksum) */
+  HOMS_B200_ERR_CACHE_CORRUPT = 8, /* homs::CacheCorruptError (truncated / bad string / checksum) */
+  HOMS_B200_ERR_PARSE = 9          /* homs::ParseError (message: "line N: ...", errors.hpp:22-32) */
 };
 
 enum { HOMS_B200_TOL_PPM = 0, HOMS_B200_TOL_DALTON = 1 };
@@ -335,6 +336,32 @@ int homs_b200_cascade_resident(homs_b200_ctx* ctx, const homs_b200_tolerance* na
                                const homs_b200_tolerance* wide, double fdr_q, const uint8_t* lib_is_decoy,
                                uint64_t* out_query, uint32_t* out_ordinal, uint8_t* out_stage,
                                uint32_t* out_raw_score, double* out_q_value, uint64_t* out_count);
+
+/* ---- MGF text -> CSR spectra on the device ----------------------------------
+ * parse_mgf, src/mgf.cpp:93-181 (finalize_block :66-89): BEGIN IONS / END IONS blocks, KEY=VALUE
+ * headers (PEPMASS required; CHARGE, TITLE, SEQ interpreted, last one wins), "mz intensity" peak
+ * lines, peaks stable-sorted by m/z with exact duplicates merged by intensity sum.  Numbers are
+ * std::from_chars doubles: the results are the same bits.  A grammar violation returns
+ * HOMS_B200_ERR_PARSE with the reference's ParseError text ("line N: message") and the first
+ * offending line in info->error_line, exactly the error the sequential parser stops at.
+ * The CSR stays resident in the context (until the next mgf_parse) so it can be handed to
+ * encode_batch_dev without touching the host; mgf_fetch copies any of it out.  TITLE / SEQ values
+ * are returned as (offset, length) into the image; length 0 = absent (the caller synthesises
+ * "spectrum_<ordinal>" ids and applies the decoy prefix as mgf.cpp:68-76 does).  charge 0 =
+ * unknown (spectrum.hpp:10).  Images must be smaller than 4 GiB. */
+typedef struct {
+  uint64_t n_lines, n_spectra, n_peaks;
+  uint64_t n_hard_numbers; /* tokens that needed the exact big-integer conversion */
+  uint64_t error_line;     /* 1-based, 0 = none */
+  uint32_t error_code, reserved;
+} homs_b200_mgf_info;
+int homs_b200_mgf_parse(homs_b200_ctx* ctx, const void* image, uint64_t n_bytes, homs_b200_mgf_info* info);
+int homs_b200_mgf_fetch(homs_b200_ctx* ctx, uint64_t* offsets, double* mz, double* intensity,
+                        double* precursor_mz, uint8_t* charge, uint32_t* title_off, uint32_t* title_len,
+                        uint32_t* seq_off, uint32_t* seq_len);
+int homs_b200_mgf_device_csr(homs_b200_ctx* ctx, uint64_t* out_n_spectra, uint64_t* out_n_peaks,
+                             const uint64_t** d_offsets, const double** d_mz, const double** d_intensity,
+                             const double** d_precursor_mz, const uint8_t** d_charge);
 
 /* cascade_search, src/search.cpp:219-248 (run_stage :188-215): narrow stage on all queries,
  * target-decoy FDR, wide stage on the not-accepted rest, FDR again.  lib_is_decoy is indexed by

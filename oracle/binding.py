@@ -225,6 +225,13 @@ class Oracle:
                                                   C.c_char_p, P(U64), C.c_char_p, P(U64), UC, U64])
         self._cache_read = f("cache_read", LL, [UC, U64, P(PreCfg), P(EncCfg), P(U64), P(F64), P(U8), P(U8),
                                                 C.c_char_p, P(U64), C.c_char_p, P(U64)])
+        self._mgf_parse = f("mgf_parse", VP, [C.c_char_p, U64, C.c_char_p])
+        self._mgf_free = f("mgf_free", None, [VP])
+        self._mgf_sizes = f("mgf_sizes", None, [VP, P(U64)])
+        self._mgf_export = f("mgf_export", None, [VP, P(U64), P(F64), P(F64), P(F64), P(U8), P(U8),
+                                                  C.c_char_p, P(U64), C.c_char_p, P(U64)])
+        self._mgf_write = f("mgf_write", LL, [U64, P(U64), P(F64), P(F64), P(F64), P(U8), C.c_char_p, P(U64),
+                                              C.c_char_p, P(U64), C.c_char_p, U64])
         if self.kind == "port":
             self._topk = f("search_topk", LL, [VP, U64, P(U64), P(F64), P(U8), I, F64, U32,
                                                P(U32), P(U32)])
@@ -404,6 +411,50 @@ class Oracle:
         finally:
             self._synth_free(h)
         return out
+
+
+    # -- MGF text (src/mgf.cpp) -----------------------------------------------------------------
+    def mgf_parse(self, text: bytes, decoy_prefix: str = "DECOY_") -> dict:
+        """parse_mgf: CSR peaks + metadata; OracleError("ParseError: line N: ...") on a violation."""
+        h = self._mgf_parse(text, len(text), decoy_prefix.encode())
+        if not h:
+            raise OracleError(self.error())
+        try:
+            sizes = np.zeros(4, np.uint64)
+            self._mgf_sizes(h, _p(sizes, C.c_uint64))
+            n, npk, nid, npep = (int(x) for x in sizes)
+            offsets = np.zeros(n + 1, np.uint64)
+            mz = np.zeros(npk, np.float64)
+            inten = np.zeros(npk, np.float64)
+            prec = np.zeros(n, np.float64)
+            charge = np.zeros(n, np.uint8)
+            decoy = np.zeros(n, np.uint8)
+            iblob, pblob = C.create_string_buffer(max(nid, 1)), C.create_string_buffer(max(npep, 1))
+            ioff, poff = np.zeros(n + 1, np.uint64), np.zeros(n + 1, np.uint64)
+            self._mgf_export(h, _p(offsets, C.c_uint64), _p(mz, C.c_double), _p(inten, C.c_double),
+                             _p(prec, C.c_double), _p(charge, C.c_uint8), _p(decoy, C.c_uint8), iblob,
+                             _p(ioff, C.c_uint64), pblob, _p(poff, C.c_uint64))
+            ri, rp = iblob.raw[:nid], pblob.raw[:npep]
+            ids = [ri[int(ioff[i]):int(ioff[i + 1])] for i in range(n)]
+            peps = [rp[int(poff[i]):int(poff[i + 1])] for i in range(n)]
+            return dict(offsets=offsets, mz=mz, intensity=inten, precursor_mz=prec, charge=charge,
+                        is_decoy=decoy, ids=ids, peptides=peps)
+        finally:
+            self._mgf_free(h)
+
+    def mgf_write(self, offsets, mz, inten, precursor_mz, charge, ids, peptides=None) -> bytes:
+        """write_mgf of the given spectra."""
+        offsets, mz, inten = _u64(offsets), _f64(mz), _f64(inten)
+        prec, charge = _f64(precursor_mz), _u8(charge)
+        n = len(prec)
+        iblob, ioff = encode_ids(ids)
+        pblob, poff = encode_ids(peptides if peptides is not None else [b""] * n)
+        args = (n, _p(offsets, C.c_uint64), _p(mz, C.c_double), _p(inten, C.c_double), _p(prec, C.c_double),
+                _p(charge, C.c_uint8), iblob, _p(ioff, C.c_uint64), pblob, _p(poff, C.c_uint64))
+        size = self._check(self._mgf_write(*args, None, 0))
+        out = C.create_string_buffer(max(size, 1))
+        self._check(self._mgf_write(*args, out, size))
+        return out.raw[:size]
 
 
 class OracleError(RuntimeError):

@@ -1298,3 +1298,346 @@ long long ho_cache_read(const unsigned char* image, uint64_t n_bytes, const ho_p
   if (stored_digest != digest) return fail("CacheCorruptError", "cache hypervector block failed its checksum");
   return (long long)count;
 }
+
+/* ---- MGF text: src/mgf.cpp ---------------------------------------------------------------------- */
+
+static int mg_space(unsigned char c) {  /* std::isspace in the "C" locale (mgf.cpp:18-26) */
+  return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
+}
+static int mg_alpha(unsigned char c) { return (c >= 'A' && c <= 'Z') || (c >= 'a' && c <= 'z'); }
+static int mg_digit(unsigned char c) { return c >= '0' && c <= '9'; }
+static int mg_lower(unsigned char c) { return (c >= 'A' && c <= 'Z') ? c + 32 : c; }
+
+static void mg_strip(const char** p, size_t* n) {
+  while (*n && mg_space((unsigned char)(*p)[0])) ++*p, --*n;
+  while (*n && mg_space((unsigned char)(*p)[*n - 1])) --*n;
+}
+static size_t mg_first_token(const char* p, size_t n) {  /* mgf.cpp:50-54 */
+  size_t i = 0;
+  while (i < n && !mg_space((unsigned char)p[i])) ++i;
+  return i;
+}
+static int mg_ieq(const char* p, size_t n, const char* lit) {
+  size_t m = strlen(lit);
+  if (n != m) return 0;
+  for (size_t i = 0; i < n; ++i)
+    if (mg_lower((unsigned char)p[i]) != lit[i]) return 0;
+  return 1;
+}
+
+/* std::from_chars(first, last, double) in chars_format::general that must consume the whole token
+ * (mgf.cpp:28-33): optional '-', then inf / infinity / nan / nan(n-char-seq), or digits with an
+ * optional '.', and an exponent only when it has digits.  No '+', no hex, no leading blanks.
+ * Out-of-range (overflow, or a nonzero value that rounds to zero) is an error. */
+static int mg_parse_double(const char* p, size_t n, double* out) {
+  size_t i = 0;
+  int neg = 0;
+  if (i < n && p[i] == '-') neg = 1, ++i;
+  if (i < n && mg_alpha((unsigned char)p[i])) {
+    if (mg_ieq(p + i, n - i, "inf") || mg_ieq(p + i, n - i, "infinity")) {
+      *out = neg ? -INFINITY : INFINITY;
+      return 1;
+    }
+    if (n - i >= 3 && mg_ieq(p + i, 3, "nan")) {
+      size_t j = i + 3;
+      if (j < n) {
+        if (p[j] != '(' || p[n - 1] != ')') return 0;
+        for (size_t k = j + 1; k + 1 < n; ++k) {
+          unsigned char c = (unsigned char)p[k];
+          if (!(mg_alpha(c) || mg_digit(c) || c == '_')) return 0;
+        }
+      }
+      *out = NAN;
+      return 1;
+    }
+    return 0;
+  }
+  size_t digits = 0;
+  int nonzero = 0;
+  while (i < n && mg_digit((unsigned char)p[i])) nonzero |= p[i] != '0', ++i, ++digits;
+  if (i < n && p[i] == '.') {
+    ++i;
+    while (i < n && mg_digit((unsigned char)p[i])) nonzero |= p[i] != '0', ++i, ++digits;
+  }
+  if (digits == 0) return 0;
+  if (i < n && (p[i] == 'e' || p[i] == 'E')) {
+    size_t j = i + 1;
+    if (j < n && (p[j] == '+' || p[j] == '-')) ++j;
+    if (j < n && mg_digit((unsigned char)p[j])) {
+      while (j < n && mg_digit((unsigned char)p[j])) ++j;
+      i = j;
+    }
+  }
+  if (i != n) return 0;
+  char stack[128];
+  char* buf = n < sizeof stack ? stack : (char*)malloc(n + 1);
+  memcpy(buf, p, n);
+  buf[n] = 0;
+  const double v = strtod(buf, NULL);  /* glibc: correctly rounded, like from_chars */
+  if (buf != stack) free(buf);
+  if (isinf(v)) return 0;             /* result_out_of_range */
+  if (v == 0.0 && nonzero) return 0;  /* underflow to zero: result_out_of_range */
+  *out = v;
+  return 1;
+}
+
+static int mg_parse_charge(const char* p, size_t n, uint8_t* out) {  /* mgf.cpp:35-48 */
+  if (n == 0) return 0;
+  if (p[0] == '+') ++p, --n;
+  else if (p[n - 1] == '+') --n;
+  if (n == 0) return 0;
+  unsigned long long v = 0;
+  for (size_t i = 0; i < n; ++i) {
+    if (!mg_digit((unsigned char)p[i])) return 0;
+    v = v * 10 + (unsigned)(p[i] - '0');
+    if (v > 0xFFFFFFFFull) return 0;  /* from_chars<unsigned>: result_out_of_range */
+  }
+  if (v < 1 || v > 99) return 0;
+  *out = (uint8_t)v;
+  return 1;
+}
+
+typedef struct {
+  double mz, inten;
+  size_t seq;
+} mg_peak;
+static int mg_peak_cmp(const void* a, const void* b) {  /* std::stable_sort by m/z (mgf.cpp:78-79) */
+  const mg_peak *x = (const mg_peak*)a, *y = (const mg_peak*)b;
+  if (x->mz < y->mz) return -1;
+  if (y->mz < x->mz) return 1;
+  return x->seq < y->seq ? -1 : (x->seq > y->seq ? 1 : 0);
+}
+
+typedef struct {
+  uint64_t n, n_peaks, cap, peak_cap, id_bytes, pep_bytes;
+  uint64_t* offsets;
+  double *mz, *inten, *precursor;
+  uint8_t *charge, *decoy;
+  char **ids, **peps;
+} mg_set;
+
+void ho_mgf_free(void* h) {
+  mg_set* s = (mg_set*)h;
+  if (!s) return;
+  for (uint64_t i = 0; i < s->n; ++i) free(s->ids[i]), free(s->peps[i]);
+  free(s->offsets), free(s->mz), free(s->inten), free(s->precursor), free(s->charge), free(s->decoy);
+  free(s->ids), free(s->peps), free(s);
+}
+
+static void* mg_fail(mg_set* s, mg_peak* pk, size_t line, const char* msg) {
+  char buf[200];
+  snprintf(buf, sizeof buf, "line %zu: %s", line, msg);  /* errors.hpp:25-27 */
+  fail("ParseError", buf);
+  free(pk);
+  ho_mgf_free(s);
+  return NULL;
+}
+
+static char* mg_dup(const char* p, size_t n) {
+  char* d = (char*)malloc(n + 1);
+  memcpy(d, p, n);
+  d[n] = 0;
+  return d;
+}
+
+void* ho_mgf_parse(const char* text, uint64_t n_bytes, const char* decoy_prefix) {
+  mg_set* s = (mg_set*)calloc(1, sizeof *s);
+  s->offsets = (uint64_t*)calloc(1, sizeof(uint64_t));
+  const size_t plen = decoy_prefix ? strlen(decoy_prefix) : 0;
+  mg_peak* pk = NULL;
+  size_t npk = 0, pk_cap = 0;
+  size_t line_no = 0, begin_line = 0, ordinal = 0;
+  int inside = 0, has_pepmass = 0;
+  double pepmass = 0.0;
+  uint8_t charge = 0;
+  const char *title = NULL, *pep = NULL;
+  size_t title_n = 0, pep_n = 0;
+
+  for (uint64_t pos = 0; pos < n_bytes;) {  /* std::getline, mgf.cpp:100 */
+    const char* raw = text + pos;
+    const char* nl = (const char*)memchr(raw, '\n', n_bytes - pos);
+    size_t len = nl ? (size_t)(nl - raw) : (size_t)(n_bytes - pos);
+    pos += len + (nl ? 1 : 0);
+    ++line_no;
+    const char* line = raw;
+    mg_strip(&line, &len);
+
+    if (!inside) {  /* mgf.cpp:104-119 */
+      if (len == 0 || line[0] == '#') continue;
+      if (len == 10 && memcmp(line, "BEGIN IONS", 10) == 0) {
+        inside = 1;
+        begin_line = line_no;
+        ordinal = s->n + 1;
+        has_pepmass = 0, pepmass = 0.0, charge = 0, title = pep = NULL, title_n = pep_n = 0, npk = 0;
+        continue;
+      }
+      if (memchr(line, '=', len) && mg_alpha((unsigned char)line[0])) continue;
+      return mg_fail(s, pk, line_no, "unexpected content outside BEGIN IONS/END IONS");
+    }
+    if (len == 0) continue;
+    if (len == 8 && memcmp(line, "END IONS", 8) == 0) {  /* mgf.cpp:122-129, finalize_block :66-89 */
+      if (!has_pepmass) return mg_fail(s, pk, begin_line, "spectrum block is missing PEPMASS");
+      if (s->n == s->cap) {
+        s->cap = s->cap ? 2 * s->cap : 64;
+        s->offsets = (uint64_t*)realloc(s->offsets, (s->cap + 1) * sizeof(uint64_t));
+        s->precursor = (double*)realloc(s->precursor, s->cap * sizeof(double));
+        s->charge = (uint8_t*)realloc(s->charge, s->cap);
+        s->decoy = (uint8_t*)realloc(s->decoy, s->cap);
+        s->ids = (char**)realloc(s->ids, s->cap * sizeof(char*));
+        s->peps = (char**)realloc(s->peps, s->cap * sizeof(char*));
+      }
+      char idbuf[40];
+      const char* id = title;
+      size_t id_n = title_n;
+      if (title_n == 0) {
+        id_n = (size_t)snprintf(idbuf, sizeof idbuf, "spectrum_%zu", ordinal);
+        id = idbuf;
+      }
+      const uint64_t k = s->n;
+      s->ids[k] = mg_dup(id, id_n);
+      s->peps[k] = mg_dup(pep ? pep : "", pep_n);
+      s->id_bytes += id_n;
+      s->pep_bytes += pep_n;
+      s->precursor[k] = pepmass;
+      s->charge[k] = charge;
+      s->decoy[k] = plen > 0 && ((id_n >= plen && memcmp(id, decoy_prefix, plen) == 0) ||
+                                 (pep_n >= plen && memcmp(pep, decoy_prefix, plen) == 0));
+      for (size_t i = 0; i < npk; ++i) pk[i].seq = i;
+      qsort(pk, npk, sizeof *pk, mg_peak_cmp);
+      if (s->n_peaks + npk > s->peak_cap) {
+        s->peak_cap = 2 * (s->n_peaks + npk) + 64;
+        s->mz = (double*)realloc(s->mz, s->peak_cap * sizeof(double));
+        s->inten = (double*)realloc(s->inten, s->peak_cap * sizeof(double));
+      }
+      uint64_t w = s->n_peaks;
+      for (size_t i = 0; i < npk; ++i) {
+        if (w > s->n_peaks && s->mz[w - 1] == pk[i].mz) {
+          s->inten[w - 1] += pk[i].inten;  /* duplicate m/z: merge */
+        } else {
+          s->mz[w] = pk[i].mz;
+          s->inten[w] = pk[i].inten;
+          ++w;
+        }
+      }
+      s->n_peaks = w;
+      s->offsets[k + 1] = w;
+      s->n = k + 1;
+      inside = 0;
+      continue;
+    }
+    if (len == 10 && memcmp(line, "BEGIN IONS", 10) == 0)
+      return mg_fail(s, pk, line_no, "BEGIN IONS inside an open spectrum block");
+
+    if (mg_alpha((unsigned char)line[0])) {  /* mgf.cpp:134-161 */
+      const char* eq = (const char*)memchr(line, '=', len);
+      if (!eq) return mg_fail(s, pk, line_no, "expected KEY=VALUE header or peak line");
+      const size_t key_n = (size_t)(eq - line);
+      const char* val = eq + 1;
+      size_t val_n = len - key_n - 1;
+      mg_strip(&val, &val_n);
+      if (key_n == 7 && memcmp(line, "PEPMASS", 7) == 0) {
+        double mass = 0.0;
+        if (!mg_parse_double(val, mg_first_token(val, val_n), &mass) || !(mass > 0.0))
+          return mg_fail(s, pk, line_no, "PEPMASS must be a positive number");
+        pepmass = mass;
+        has_pepmass = 1;
+      } else if (key_n == 6 && memcmp(line, "CHARGE", 6) == 0) {
+        if (!mg_parse_charge(val, val_n, &charge))
+          return mg_fail(s, pk, line_no, "CHARGE must be a positive integer like 2+");
+      } else if (key_n == 5 && memcmp(line, "TITLE", 5) == 0) {
+        title = val, title_n = val_n;
+      } else if (key_n == 3 && memcmp(line, "SEQ", 3) == 0) {
+        pep = val, pep_n = val_n;
+      }
+      continue;
+    }
+
+    /* peak line "mz intensity", extra columns ignored (mgf.cpp:163-177) */
+    const size_t mz_n = mg_first_token(line, len);
+    const char* rest = line + mz_n;
+    size_t rest_n = len - mz_n;
+    mg_strip(&rest, &rest_n);
+    const size_t in_n = mg_first_token(rest, rest_n);
+    double m = 0.0, v = 0.0;
+    if (!mg_parse_double(line, mz_n, &m) || !mg_parse_double(rest, in_n, &v))
+      return mg_fail(s, pk, line_no, "peak line must be two numbers: m/z intensity");
+    if (!(m > 0.0)) return mg_fail(s, pk, line_no, "peak m/z must be positive");
+    if (!(v >= 0.0)) return mg_fail(s, pk, line_no, "peak intensity must be non-negative");
+    if (npk == pk_cap) {
+      pk_cap = pk_cap ? 2 * pk_cap : 256;
+      pk = (mg_peak*)realloc(pk, pk_cap * sizeof *pk);
+    }
+    pk[npk].mz = m;
+    pk[npk].inten = v;
+    ++npk;
+  }
+  if (inside) return mg_fail(s, pk, begin_line, "spectrum block not closed by END IONS");
+  free(pk);
+  return s;
+}
+
+void ho_mgf_sizes(const void* h, uint64_t* sizes) {
+  const mg_set* s = (const mg_set*)h;
+  sizes[0] = s->n, sizes[1] = s->n_peaks, sizes[2] = s->id_bytes, sizes[3] = s->pep_bytes;
+}
+
+void ho_mgf_export(const void* h, uint64_t* offsets, double* mz, double* inten, double* precursor,
+                   uint8_t* charge, uint8_t* is_decoy, char* id_blob, uint64_t* id_off, char* pep_blob,
+                   uint64_t* pep_off) {
+  const mg_set* s = (const mg_set*)h;
+  memcpy(offsets, s->offsets, (s->n + 1) * sizeof(uint64_t));
+  if (s->n_peaks) {
+    memcpy(mz, s->mz, s->n_peaks * sizeof(double));
+    memcpy(inten, s->inten, s->n_peaks * sizeof(double));
+  }
+  uint64_t c = 0, q = 0;
+  for (uint64_t i = 0; i < s->n; ++i) {
+    precursor[i] = s->precursor[i];
+    charge[i] = s->charge[i];
+    is_decoy[i] = s->decoy[i];
+    id_off[i] = c;
+    pep_off[i] = q;
+    const size_t a = strlen(s->ids[i]), b = strlen(s->peps[i]);
+    memcpy(id_blob + c, s->ids[i], a);
+    memcpy(pep_blob + q, s->peps[i], b);
+    c += a;
+    q += b;
+  }
+  id_off[s->n] = c;
+  pep_off[s->n] = q;
+}
+
+long long ho_mgf_write(uint64_t n, const uint64_t* offsets, const double* mz, const double* inten,
+                       const double* precursor, const uint8_t* charge, const char* id_blob,
+                       const uint64_t* id_off, const char* pep_blob, const uint64_t* pep_off, char* out,
+                       uint64_t cap) {  /* mgf.cpp:183-208 */
+  uint64_t w = 0;
+  char buf[96];
+#define MG_PUT(ptr, len)                                    \
+  do {                                                      \
+    if (out && w + (len) <= cap) memcpy(out + w, (ptr), (len)); \
+    w += (len);                                             \
+  } while (0)
+  for (uint64_t i = 0; i < n; ++i) {
+    MG_PUT("BEGIN IONS\nTITLE=", 17);
+    MG_PUT(id_blob + id_off[i], id_off[i + 1] - id_off[i]);
+    int k = snprintf(buf, sizeof buf, "\nPEPMASS=%.5f\n", precursor[i]);
+    MG_PUT(buf, (uint64_t)k);
+    if (charge[i] != 0) {
+      k = snprintf(buf, sizeof buf, "CHARGE=%u+\n", (unsigned)charge[i]);
+      MG_PUT(buf, (uint64_t)k);
+    }
+    if (pep_blob && pep_off[i + 1] > pep_off[i]) {
+      MG_PUT("SEQ=", 4);
+      MG_PUT(pep_blob + pep_off[i], pep_off[i + 1] - pep_off[i]);
+      MG_PUT("\n", 1);
+    }
+    for (uint64_t j = offsets[i]; j < offsets[i + 1]; ++j) {
+      k = snprintf(buf, sizeof buf, "%.5f %.6f\n", mz[j], inten[j]);
+      MG_PUT(buf, (uint64_t)k);
+    }
+    MG_PUT("END IONS\n\n", 10);
+  }
+#undef MG_PUT
+  return (long long)w;
+}

@@ -114,6 +114,20 @@ long long ho_cache_read(const unsigned char* image, uint64_t n_bytes, const ho_p
                         uint8_t* is_decoy, char* id_blob, uint64_t* id_off, char* pep_blob,
                         uint64_t* pep_off);
 
+/* MGF text, src/mgf.cpp:93-181 (parse_mgf, finalize_block :66-89) and :183-208 (write_mgf).
+ * parse returns a handle (NULL after a grammar violation: ho_last_error() == "ParseError: line N: ...").
+ * sizes[0] = spectra, [1] = peaks, [2] = id bytes, [3] = peptide bytes. */
+void* ho_mgf_parse(const char* text, uint64_t n_bytes, const char* decoy_prefix);
+void ho_mgf_free(void* h);
+void ho_mgf_sizes(const void* h, uint64_t* sizes);
+void ho_mgf_export(const void* h, uint64_t* offsets, double* mz, double* inten, double* precursor,
+                   uint8_t* charge, uint8_t* is_decoy, char* id_blob, uint64_t* id_off, char* pep_blob,
+                   uint64_t* pep_off);
+long long ho_mgf_write(uint64_t n, const uint64_t* offsets, const double* mz, const double* inten,
+                       const double* precursor, const uint8_t* charge, const char* id_blob,
+                       const uint64_t* id_off, const char* pep_blob, const uint64_t* pep_off, char* out,
+                       uint64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

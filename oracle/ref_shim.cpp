@@ -36,6 +36,7 @@
 #include "homs/encoder.hpp"
 #include "homs/errors.hpp"
 #include "homs/fdr.hpp"
+#include "homs/mgf.hpp"
 #include "homs/pipeline.hpp"
 #include "homs/preprocess.hpp"
 #include "homs/search.hpp"
@@ -54,6 +55,8 @@ long long guarded(Fn&& fn) {
     g_error = std::string("ConfigError: ") + e.what();
   } catch (const homs::InvariantError& e) {
     g_error = std::string("InvariantError: ") + e.what();
+  } catch (const homs::ParseError& e) {
+    g_error = std::string("ParseError: ") + e.what();
   } catch (const homs::CacheFormatError& e) {
     g_error = std::string("CacheFormatError: ") + e.what();
   } catch (const homs::StaleCacheError& e) {
@@ -578,6 +581,80 @@ long long hr_cache_read(const unsigned char* image, std::uint64_t n_bytes, const
       pep_off[entries.size()] = po;
     }
     return static_cast<long long>(entries.size());
+  });
+}
+
+// ---- MGF text (src/mgf.cpp:93-181 parse_mgf, :183-208 write_mgf) -------------------------------
+
+void* hr_mgf_parse(const char* text, std::uint64_t n_bytes, const char* decoy_prefix) {
+  std::vector<homs::RawSpectrum>* out = nullptr;
+  const long long rc = guarded([&]() -> long long {
+    std::istringstream in(std::string(text, n_bytes));
+    out = new std::vector<homs::RawSpectrum>(homs::parse_mgf(in, decoy_prefix ? decoy_prefix : ""));
+    return 0;
+  });
+  return rc < 0 ? nullptr : out;
+}
+void hr_mgf_free(void* h) { delete static_cast<std::vector<homs::RawSpectrum>*>(h); }
+
+// sizes[0] = spectra, [1] = peaks, [2] = id bytes, [3] = peptide bytes
+void hr_mgf_sizes(const void* h, std::uint64_t* sizes) {
+  const auto& v = *static_cast<const std::vector<homs::RawSpectrum>*>(h);
+  sizes[0] = v.size();
+  sizes[1] = sizes[2] = sizes[3] = 0;
+  for (const auto& s : v) {
+    sizes[1] += s.peaks.size();
+    sizes[2] += s.meta.id.size();
+    sizes[3] += s.meta.peptide.size();
+  }
+}
+
+void hr_mgf_export(const void* h, std::uint64_t* offsets, double* mz, double* inten, double* precursor,
+                   std::uint8_t* charge, std::uint8_t* is_decoy, char* id_blob, std::uint64_t* id_off,
+                   char* pep_blob, std::uint64_t* pep_off) {
+  const auto& v = *static_cast<const std::vector<homs::RawSpectrum>*>(h);
+  std::uint64_t p = 0, c = 0, q = 0;
+  for (std::size_t i = 0; i < v.size(); ++i) {
+    offsets[i] = p;
+    id_off[i] = c;
+    pep_off[i] = q;
+    for (const auto& pk : v[i].peaks) {
+      mz[p] = pk.mz;
+      inten[p] = pk.intensity;
+      ++p;
+    }
+    std::memcpy(id_blob + c, v[i].meta.id.data(), v[i].meta.id.size());
+    c += v[i].meta.id.size();
+    std::memcpy(pep_blob + q, v[i].meta.peptide.data(), v[i].meta.peptide.size());
+    q += v[i].meta.peptide.size();
+    precursor[i] = v[i].meta.precursor_mz;
+    charge[i] = v[i].meta.charge;
+    is_decoy[i] = v[i].meta.is_decoy;
+  }
+  offsets[v.size()] = p;
+  id_off[v.size()] = c;
+  pep_off[v.size()] = q;
+}
+
+// write_mgf of the given spectra; returns the text size (copies it when it fits in cap)
+long long hr_mgf_write(std::uint64_t n, const std::uint64_t* offsets, const double* mz, const double* inten,
+                       const double* precursor, const std::uint8_t* charge, const char* id_blob,
+                       const std::uint64_t* id_off, const char* pep_blob, const std::uint64_t* pep_off,
+                       char* out, std::uint64_t cap) {
+  return guarded([&]() -> long long {
+    std::vector<homs::RawSpectrum> v(n);
+    for (std::uint64_t i = 0; i < n; ++i) {
+      v[i].meta.id.assign(id_blob + id_off[i], id_off[i + 1] - id_off[i]);
+      if (pep_blob) v[i].meta.peptide.assign(pep_blob + pep_off[i], pep_off[i + 1] - pep_off[i]);
+      v[i].meta.precursor_mz = precursor[i];
+      v[i].meta.charge = charge[i];
+      for (std::uint64_t j = offsets[i]; j < offsets[i + 1]; ++j) v[i].peaks.push_back({mz[j], inten[j]});
+    }
+    std::ostringstream os;
+    homs::write_mgf(os, v);
+    const std::string text = os.str();
+    if (out && text.size() <= cap) std::memcpy(out, text.data(), text.size());
+    return static_cast<long long>(text.size());
   });
 }
 

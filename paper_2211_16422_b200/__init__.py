@@ -7,13 +7,13 @@ it without the built library raises ImportError: there is no CPU fallback.
 from . import capi  # noqa: F401  (raises if the CUDA library is missing)
 from .host import (  # noqa: F401
     CacheCorruptError, CacheFormatError, Codebook, ConfigError, Context, CudaError, EncodeOutcome,
-    EncoderConfig, HomsError, InvariantError, Match, PreprocessConfig, StaleCacheError, Tolerance,
+    EncoderConfig, HomsError, InvariantError, Match, ParseError, PreprocessConfig, StaleCacheError, Tolerance,
     cache_parse, compute_fdr_curve, dimension, id_ranks, make_codebook, quantize_intensity, words_for,
 )
 
 __all__ = [
     "CacheCorruptError", "CacheFormatError", "Codebook", "ConfigError", "Context", "CudaError",
-    "EncodeOutcome", "EncoderConfig", "HomsError", "InvariantError", "Match", "PreprocessConfig",
+    "EncodeOutcome", "EncoderConfig", "HomsError", "InvariantError", "Match", "ParseError", "PreprocessConfig",
     "StaleCacheError", "Tolerance", "cache_parse", "compute_fdr_curve", "dimension", "id_ranks",
     "make_codebook", "quantize_intensity", "words_for",
 ]

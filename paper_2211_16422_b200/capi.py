@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("HOMS_B200_LIB") or os.path.join(PKG_DIR, "libhoms_b20
 HEADER_PATH = os.path.join(REPO_ROOT, "include", "homs_b200.h")
 
 OK, ERR_CONFIG, ERR_INVARIANT, ERR_CUDA, ERR_ARGUMENT, ERR_STATE = range(6)
-ERR_CACHE_FORMAT, ERR_CACHE_STALE, ERR_CACHE_CORRUPT = 6, 7, 8
+ERR_CACHE_FORMAT, ERR_CACHE_STALE, ERR_CACHE_CORRUPT, ERR_PARSE = 6, 7, 8, 9
 TOL_PPM, TOL_DALTON = 0, 1
 NO_HIT = 0xFFFFFFFF
 MAX_TOPK = 64
@@ -36,6 +36,12 @@ class EncoderConfigPod(C.Structure):
 class CacheLayoutPod(C.Structure):
     _fields_ = [("count", C.c_uint64), ("hv_offset", C.c_uint64), ("hv_bytes", C.c_uint64),
                 ("stored_digest", C.c_uint64), ("id_bytes", C.c_uint64), ("peptide_bytes", C.c_uint64)]
+
+
+class MgfInfoPod(C.Structure):
+    _fields_ = [("n_lines", C.c_uint64), ("n_spectra", C.c_uint64), ("n_peaks", C.c_uint64),
+                ("n_hard_numbers", C.c_uint64), ("error_line", C.c_uint64), ("error_code", C.c_uint32),
+                ("reserved", C.c_uint32)]
 
 
 class TolerancePod(C.Structure):
@@ -131,6 +137,11 @@ queries_from_spectra = _decl("homs_b200_queries_from_spectra", _I,
 search_resident = _decl("homs_b200_search_resident", _I, [_VP, _P(TolerancePod), _U32, _VP, _VP, _VP, _VP])
 cascade_resident = _decl("homs_b200_cascade_resident", _I,
                          [_VP, _P(TolerancePod), _P(TolerancePod), _F64, _VP, _VP, _VP, _VP, _VP, _VP, _P(_U64)])
+
+mgf_parse = _decl("homs_b200_mgf_parse", _I, [_VP, _VP, _U64, _P(MgfInfoPod)])
+mgf_fetch = _decl("homs_b200_mgf_fetch", _I, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP])
+mgf_device_csr = _decl("homs_b200_mgf_device_csr", _I,
+                       [_VP, _P(_U64), _P(_U64), _P(_VP), _P(_VP), _P(_VP), _P(_VP), _P(_VP)])
 
 fnv1a64_dev = _decl("homs_b200_fnv1a64_dev", _I, [_VP, _VP, _U64, _P(_U64)])
 fnv1a64 = _decl("homs_b200_fnv1a64", _I, [_VP, _VP, _U64, _P(_U64)])

@@ -79,6 +79,15 @@ struct Queries {
   DevBuf d_words, d_mz, d_charge;  // words: padded stride of the query dim
 };
 
+struct MgfState {  // CSR result of the last homs_b200_mgf_parse, resident in the context's scratch
+  bool ready = false;
+  uint64_t n_spectra = 0, n_peaks = 0;
+  const uint64_t* d_offsets = nullptr;
+  const double *d_mz = nullptr, *d_int = nullptr, *d_pepmass = nullptr;
+  const uint8_t* d_charge = nullptr;
+  const uint32_t *d_title_off = nullptr, *d_title_len = nullptr, *d_seq_off = nullptr, *d_seq_len = nullptr;
+};
+
 struct Codebook {
   bool ready = false;
   uint32_t dim = 0, n_bins = 0, levels = 0, W = 0, S = 0;
@@ -98,8 +107,9 @@ struct homs_b200_ctx {
   hb::Codebook cb;
   hb::Library lib;
   hb::Queries q;
+  hb::MgfState mgf;
   // grow-only scratch, keyed by purpose
-  enum { kScratchSlots = 40 };
+  enum { kScratchSlots = 48 };
   hb::DevBuf scratch[kScratchSlots];
   int engine = HOMS_B200_ENGINE_AUTO;  // homs_b200_ctx_set_engine
   void* pinned = nullptr;  // small pinned staging block
@@ -176,7 +186,8 @@ enum Scratch {
   kScrQFirst, kScrQLast, kScrKeys, kScrKeysAlt, kScrVals, kScrValsAlt, kScrCub, kScrPlan,
   kScrPartial, kScrRecords, kScrSubset, kScrDecode, kScrMisc, kScrMisc2, kScrRecords2, kScrHas,
   kScrTcQx, kScrTcPlan, kScrTcPartial, kScrTcTiles, kScrTcBest, kScrFnv, kScrCacheBlock,
-  kScrPipeIn0, kScrPipeIn1, kScrPipeOut0, kScrPipeOut1, kScrFusedRows, kScrFusedOk
+  kScrPipeIn0, kScrPipeIn1, kScrPipeOut0, kScrPipeOut1, kScrFusedRows, kScrFusedOk,
+  kScrMgfText, kScrMgfTiles, kScrMgfLines, kScrMgfBlocks, kScrMgfPeaks, kScrMgfHard
 };
 
 // Tensor-core engine (search_tc.cu).  expand: packed rows -> +-1 int8 swizzled image.

@@ -38,6 +38,17 @@ class CudaError(HomsError):
     pass
 
 
+class ParseError(HomsError):
+    """homs::ParseError (errors.hpp:22-32): str(e) == "line N: message"; .line is N."""
+
+    @property
+    def line(self) -> int:
+        try:
+            return int(str(self).split(":", 1)[0].split()[1])
+        except Exception:
+            return 0
+
+
 class CacheFormatError(HomsError):
     """homs::CacheFormatError (errors.hpp:33-36)."""
 
@@ -53,7 +64,7 @@ class CacheCorruptError(HomsError):
 _ERRORS = {capi.ERR_CONFIG: ConfigError, capi.ERR_INVARIANT: InvariantError,
            capi.ERR_CUDA: CudaError, capi.ERR_ARGUMENT: HomsError, capi.ERR_STATE: HomsError,
            capi.ERR_CACHE_FORMAT: CacheFormatError, capi.ERR_CACHE_STALE: StaleCacheError,
-           capi.ERR_CACHE_CORRUPT: CacheCorruptError}
+           capi.ERR_CACHE_CORRUPT: CacheCorruptError, capi.ERR_PARSE: ParseError}
 
 
 def _check(rc: int, ctx=None) -> None:
@@ -507,6 +518,45 @@ class Context:
         m = cnt.value
         return dict(query=query[:m].copy(), ordinal=ordinal[:m].copy(), stage=stage[:m].copy(),
                     raw_score=score[:m].copy(), q_value=qv[:m].copy())
+
+    # -- MGF text -> CSR -------------------------------------------------------
+    def parse_mgf(self, text: bytes, decoy_prefix: str = "DECOY_", fetch: bool = True) -> dict:
+        """parse_mgf (mgf.cpp:93-181) on the device.  Returns the spectra as CSR arrays plus ids /
+        peptides / decoy flags built the way finalize_block does (mgf.cpp:66-76).  With
+        fetch=False only the counts come back and the CSR stays resident (see mgf_device_csr)."""
+        buf = np.frombuffer(text, np.uint8)
+        info = capi.MgfInfoPod()
+        _check(capi.mgf_parse(self._h, _ptr(buf) if len(buf) else 0, len(buf), C.byref(info)), self._h)
+        n, npk = int(info.n_spectra), int(info.n_peaks)
+        out = dict(n_spectra=n, n_peaks=npk, n_lines=int(info.n_lines), n_hard_numbers=int(info.n_hard_numbers))
+        if not fetch:
+            return out
+        offsets = np.zeros(n + 1, np.uint64)
+        mz, inten = np.zeros(npk, np.float64), np.zeros(npk, np.float64)
+        prec, charge = np.zeros(n, np.float64), np.zeros(n, np.uint8)
+        toff, tlen, soff, slen = (np.zeros(n, np.uint32) for _ in range(4))
+        _check(capi.mgf_fetch(self._h, _ptr(offsets), _ptr(mz), _ptr(inten), _ptr(prec), _ptr(charge), _ptr(toff),
+                              _ptr(tlen), _ptr(soff), _ptr(slen)), self._h)
+        ids, peps = [], []
+        pre = decoy_prefix.encode()
+        decoy = np.zeros(n, np.uint8)
+        for i in range(n):
+            ident = text[int(toff[i]):int(toff[i]) + int(tlen[i])] if tlen[i] else b"spectrum_%d" % (i + 1)
+            pep = text[int(soff[i]):int(soff[i]) + int(slen[i])]
+            ids.append(ident)
+            peps.append(pep)
+            decoy[i] = bool(pre) and (ident.startswith(pre) or pep.startswith(pre))
+        out.update(offsets=offsets, mz=mz, intensity=inten, precursor_mz=prec, charge=charge, is_decoy=decoy,
+                   ids=ids, peptides=peps)
+        return out
+
+    def mgf_device_csr(self) -> dict:
+        """Device pointers of the resident CSR of the last parse_mgf (valid until the next one)."""
+        n, npk = C.c_uint64(), C.c_uint64()
+        p = [C.c_void_p() for _ in range(5)]
+        _check(capi.mgf_device_csr(self._h, C.byref(n), C.byref(npk), *[C.byref(x) for x in p]), self._h)
+        return dict(n_spectra=n.value, n_peaks=npk.value, d_offsets=p[0].value or 0, d_mz=p[1].value or 0,
+                    d_intensity=p[2].value or 0, d_precursor_mz=p[3].value or 0, d_charge=p[4].value or 0)
 
     # -- fused raw-spectra paths (SURVEY.md 8f-4) ---------------------------------------------
     def build_index_from_spectra(self, offsets, mz, intensity, preprocess: PreprocessConfig, precursor_mz,
