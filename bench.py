@@ -579,6 +579,150 @@ def run_encode(args) -> None:
     ctx.close()
 
 
+def synth_mgf_text(n_spectra: int, peaks: int, seed: int = 6):
+    """An MGF image of the synthetic library shape, formatted with vectorised digit arithmetic:
+    'BEGIN IONS / TITLE / PEPMASS / CHARGE / <peaks> / END IONS' blocks, peak lines 'dddd.dd000 d.dddddd'."""
+    from paper_2211_16422_b200 import workload as wl
+    lib = wl.synth_library(n_spectra // 2, peaks, 1.0, seed)
+    n = len(lib["precursor_mz"])
+    mz_c = np.rint(lib["mz"] * 100).astype(np.int64)                  # 0.01 Th grid
+    it_u = np.minimum(np.rint(lib["intensity"] * 1e6).astype(np.int64), 999999)
+    line = np.empty((n * peaks, 20), np.uint8)
+    for col, div in ((0, 100000), (1, 10000), (2, 1000), (3, 100)):
+        line[:, col] = 48 + (mz_c // div) % 10
+    line[:, 4] = ord(".")
+    line[:, 5] = 48 + (mz_c // 10) % 10
+    line[:, 6] = 48 + mz_c % 10
+    line[:, 7:10] = 48
+    line[:, 10] = ord(" ")
+    line[:, 11] = ord("0")
+    line[:, 12] = ord(".")
+    for k in range(6):
+        line[:, 13 + k] = 48 + (it_u // 10 ** (5 - k)) % 10
+    line[:, 19] = 10
+    heads = [("BEGIN IONS\nTITLE=%s\nPEPMASS=%.5f\nCHARGE=%d+\n" % (lib["ids"][i], lib["precursor_mz"][i],
+                                                                  lib["charge"][i])).encode() for i in range(n)]
+    tail = b"END IONS\n\n"
+    body = line.reshape(n, peaks * 20)
+    parts = []
+    for i in range(n):
+        parts.append(heads[i])
+        parts.append(body[i].tobytes())
+        parts.append(tail)
+    # what a correctly rounding parser must produce for this text: exact integers / exact powers of ten
+    expect = dict(mz=mz_c / 100.0, intensity=it_u / 1e6,
+                  precursor_mz=np.rint(lib["precursor_mz"] * 1e5) / 1e5, charge=lib["charge"])
+    return b"".join(parts), expect
+
+
+def run_mgf(args) -> None:
+    """MGF text -> CSR spectra resident in HBM (parse_mgf, mgf.cpp:93-181)."""
+    import torch
+
+    import paper_2211_16422_b200 as hb
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    n_spectra, peaks = args.mgf_spectra, 50
+    t = time.time()
+    text, lib = synth_mgf_text(n_spectra, peaks)
+    nbytes = len(text)
+    log(f"[bench/mgf] {n_spectra} spectra x {peaks} peaks = {nbytes / 1e6:.0f} MB of MGF text in {time.time() - t:.1f}s")
+    ctx = hb.Context(local_rank)
+    ctx.set_stream(stream.cuda_stream)
+    h_text = torch.frombuffer(bytearray(text), dtype=torch.uint8).pin_memory()
+    d_text = h_text.to(dev)
+    for _ in range(args.warmup):
+        info = ctx.parse_mgf_dev(d_text.data_ptr(), nbytes)
+    torch.cuda.synchronize(dev)
+    launches0 = ctx.launch_count()
+    sampler = ClockSampler(local_rank)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        info = ctx.parse_mgf_dev(d_text.data_ptr(), nbytes)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    ms_step = e0.elapsed_time(e1) / args.steps
+    launches = (ctx.launch_count() - launches0) // args.steps
+    n, npk = info["n_spectra"], info["n_peaks"]
+    assert n == n_spectra and npk == n_spectra * peaks
+    value = n / (ms_step * 1e-3)
+
+    # end to end: pinned host text in, the whole CSR + metadata back in pinned host arrays
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory().numpy()
+    out = dict(offsets=pin(n + 1, torch.int64).view(np.uint64), mz=pin(npk, torch.float64),
+               intensity=pin(npk, torch.float64), precursor_mz=pin(n, torch.float64), charge=pin(n, torch.uint8),
+               title_off=pin(n, torch.int32).view(np.uint32), title_len=pin(n, torch.int32).view(np.uint32),
+               seq_off=pin(n, torch.int32).view(np.uint32), seq_len=pin(n, torch.int32).view(np.uint32))
+    h_np = h_text.numpy()
+    times = []
+    for i in range(2 + args.steps):
+        t0 = time.perf_counter()
+        ctx.parse_mgf(h_np, fetch=False)
+        ctx.mgf_fetch(n, npk, out)
+        if i >= 2:
+            times.append(time.perf_counter() - t0)
+    e2e_value = n / (sum(times) / len(times))
+    d2h = sum(v.nbytes for v in out.values())
+    assert np.array_equal(out["mz"], lib["mz"]) and np.array_equal(out["intensity"], lib["intensity"])
+    assert np.array_equal(out["precursor_mz"], lib["precursor_mz"]) and np.array_equal(out["charge"], lib["charge"])
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import binding as ob
+        kind = "ref" if ob.available("ref") else "port"
+        oracle = ob.Oracle(kind)
+        block = nbytes // n  # every block has the same size except for the header digits: cut at a block end
+        probe_end = text.find(b"END IONS\n\n", 2000 * block) + 10
+        t0 = time.perf_counter()
+        oracle.mgf_parse(text[:probe_end])
+        per_byte = (time.perf_counter() - t0) / probe_end
+        end = text.find(b"END IONS\n\n", int(min(nbytes - 20, max(probe_end, 12.0 / per_byte)))) + 10
+        t0 = time.perf_counter()
+        r = oracle.mgf_parse(text[:end])
+        sec = time.perf_counter() - t0
+        m = len(r["precursor_mz"])
+        parity = bool(np.array_equal(r["mz"], out["mz"][:len(r["mz"])]) and
+                      np.array_equal(r["intensity"], out["intensity"][:len(r["mz"])]) and
+                      np.array_equal(r["precursor_mz"], out["precursor_mz"][:m]) and
+                      np.array_equal(r["charge"], out["charge"][:m]) and np.array_equal(r["offsets"], out["offsets"][:m + 1]))
+        cpu = {"value": m / sec, "unit": "spectra/s", "cores": 1, "kind": "reference" if kind == "ref" else "port",
+               "sample": f"parse_mgf over the first {m} spectra ({end / 1e6:.0f} MB); the reference parser is single-threaded",
+               "mb_per_s": end / sec / 1e6, "parity_with_gpu_on_sample": "bit-exact" if parity else "MISMATCH"}
+        if not parity:
+            raise AssertionError("GPU CSR differs from the reference on the CPU-baseline sample")
+
+    peak, peak_src = measured_peak_hbm()
+    # algorithmic bytes: the text once in, the CSR (16 B per peak, 8 + 8 + 1 + 16 B per spectrum) out
+    bytes_alg = nbytes + 16 * npk + 33 * n + 8
+    achieved = bytes_alg / (ms_step * 1e-3) / 1e9
+    line = {
+        "metric": "MGF spectra/sec parsed to CSR in HBM (50 peaks per spectrum, device-timed)", "value": value,
+        "unit": "spectra/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8 text -> f64 (from_chars-exact)", "data": "synthetic",
+        "config": {"workload": f"mgf: {n} spectra x {peaks} peaks, {nbytes / 1e6:.0f} MB of text per step",
+                   "l2_policy": f"inputs larger than L2 ({nbytes / 1e6:.0f} MB of text)",
+                   "parallelism": "replicas (files split at END IONS, no collective)"},
+        "e2e": {"value": e2e_value, "unit": "spectra/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_src, "kernel": "whole parse (11 passes over the line table)",
+                     "text_gb_per_s": nbytes / (ms_step * 1e-3) / 1e9, "algorithmic_bytes_per_step": bytes_alg,
+                     "note": "text read once + CSR written once over the device time of the whole parse; the passes "
+                             "are byte-granular scans and per-line parsing, far from the HBM line by nature"},
+        "cpu_baseline": cpu, "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    ctx.close()
+
+
 def cpu_baseline(lib, qry, dim, lib_words, hq, dev_score, dev_ord):
     from oracle import binding as ob
     kind = "ref" if ob.available("ref") else "port"
@@ -631,6 +775,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--encode-spectra", type=int, default=1_000_000,
                     help="--workload encode: spectra per step")
+    ap.add_argument("--mgf-spectra", type=int, default=400_000, help="--workload mgf: spectra in the text image")
     ap.add_argument("--engine", default="auto", choices=["auto", "popc", "tensor", "tensor_fp4"],
                     help="top-1 search engine (auto = tensor cores, e2m1 operands)")
     ap.add_argument("--dim", type=int, default=0, help="override the hypervector dimension (config 5 sweep)")
@@ -643,6 +788,8 @@ def main():
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.workload == "encode" and args.impl == "ours":
         run_encode(args)
+    elif args.workload == "mgf" and args.impl == "ours":
+        run_mgf(args)
     elif args.impl == "reference":
         run_reference(args)
     else:

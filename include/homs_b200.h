@@ -356,6 +356,8 @@ typedef struct {
   uint32_t error_code, reserved;
 } homs_b200_mgf_info;
 int homs_b200_mgf_parse(homs_b200_ctx* ctx, const void* image, uint64_t n_bytes, homs_b200_mgf_info* info);
+/* Same, image already in device memory. */
+int homs_b200_mgf_parse_dev(homs_b200_ctx* ctx, const void* d_image, uint64_t n_bytes, homs_b200_mgf_info* info);
 int homs_b200_mgf_fetch(homs_b200_ctx* ctx, uint64_t* offsets, double* mz, double* intensity,
                         double* precursor_mz, uint8_t* charge, uint32_t* title_off, uint32_t* title_len,
                         uint32_t* seq_off, uint32_t* seq_len);

@@ -139,6 +139,7 @@ cascade_resident = _decl("homs_b200_cascade_resident", _I,
                          [_VP, _P(TolerancePod), _P(TolerancePod), _F64, _VP, _VP, _VP, _VP, _VP, _VP, _P(_U64)])
 
 mgf_parse = _decl("homs_b200_mgf_parse", _I, [_VP, _VP, _U64, _P(MgfInfoPod)])
+mgf_parse_dev = _decl("homs_b200_mgf_parse_dev", _I, [_VP, _VP, _U64, _P(MgfInfoPod)])
 mgf_fetch = _decl("homs_b200_mgf_fetch", _I, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP])
 mgf_device_csr = _decl("homs_b200_mgf_device_csr", _I,
                        [_VP, _P(_U64), _P(_U64), _P(_VP), _P(_VP), _P(_VP), _P(_VP), _P(_VP)])

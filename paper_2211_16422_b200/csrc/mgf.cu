@@ -724,9 +724,10 @@ using namespace hb;
 
 extern "C" {
 
-int homs_b200_mgf_parse(homs_b200_ctx* ctx, const void* image, uint64_t n_bytes, homs_b200_mgf_info* info) {
-  if (!ctx || !info) return HOMS_B200_ERR_ARGUMENT;
-  Lock lock(ctx);
+}  // extern "C"
+
+static int mgf_parse_locked(homs_b200_ctx* ctx, const void* image, bool on_device, uint64_t n_bytes,
+                            homs_b200_mgf_info* info) {
   MgfState& st = ctx->mgf;
   st = MgfState{};
   *info = homs_b200_mgf_info{};
@@ -739,8 +740,12 @@ int homs_b200_mgf_parse(homs_b200_ctx* ctx, const void* image, uint64_t n_bytes,
   DevBuf& b_text = ctx->scratch[kScrMgfText];
   HB_TRY(ensure(ctx, b_text, n + 64));
   auto* d_text = b_text.as<uint8_t>();
-  if (n) HB_CUDA(ctx, cudaMemcpyAsync(d_text, image, n, cudaMemcpyHostToDevice, s));
+  if (n)
+    HB_CUDA(ctx, cudaMemcpyAsync(d_text, image, n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
   HB_CUDA(ctx, cudaMemsetAsync(d_text + n, 0, 64, s));
+  uint8_t last = '\n';
+  if (n && on_device) HB_CUDA(ctx, cudaMemcpyAsync(&last, d_text + n - 1, 1, cudaMemcpyDeviceToHost, s));
+  else if (n) last = static_cast<const uint8_t*>(image)[n - 1];
 
   // M1
   const uint32_t tiles = static_cast<uint32_t>((n + kM1Threads * kM1Bytes - 1) / (kM1Threads * kM1Bytes));
@@ -760,7 +765,7 @@ int homs_b200_mgf_parse(homs_b200_ctx* ctx, const void* image, uint64_t n_bytes,
     HB_CUDA(ctx, cudaMemcpyAsync(&n_newlines, d_tile_base + tiles, 4, cudaMemcpyDeviceToHost, s));
     HB_CUDA(ctx, cudaStreamSynchronize(s));
   }
-  const uint8_t last = n ? static_cast<const uint8_t*>(image)[n - 1] : '\n';
+  if (!tiles) HB_CUDA(ctx, cudaStreamSynchronize(s));
   const uint64_t n_lines64 = uint64_t(n_newlines) + (n > 0 && last != '\n' ? 1 : 0);  // std::getline
   HB_REQUIRE(ctx, n_lines64 < 0x7FFFFFF0ull, HOMS_B200_ERR_ARGUMENT, "mgf_parse: too many lines");
   const uint32_t n_lines = static_cast<uint32_t>(n_lines64);
@@ -940,6 +945,20 @@ int homs_b200_mgf_parse(homs_b200_ctx* ctx, const void* image, uint64_t n_bytes,
   st.d_seq_off = d_soff;
   st.d_seq_len = d_slen;
   return HOMS_B200_OK;
+}
+
+extern "C" {
+
+int homs_b200_mgf_parse(homs_b200_ctx* ctx, const void* image, uint64_t n_bytes, homs_b200_mgf_info* info) {
+  if (!ctx || !info) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  return mgf_parse_locked(ctx, image, false, n_bytes, info);
+}
+
+int homs_b200_mgf_parse_dev(homs_b200_ctx* ctx, const void* d_image, uint64_t n_bytes, homs_b200_mgf_info* info) {
+  if (!ctx || !info) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  return mgf_parse_locked(ctx, d_image, true, n_bytes, info);
 }
 
 int homs_b200_mgf_fetch(homs_b200_ctx* ctx, uint64_t* offsets, double* mz, double* intensity,

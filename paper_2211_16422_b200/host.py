@@ -550,6 +550,24 @@ class Context:
                    ids=ids, peptides=peps)
         return out
 
+    def parse_mgf_dev(self, d_image: int, n_bytes: int) -> dict:
+        """parse_mgf of an image already in device memory; the CSR stays resident."""
+        info = capi.MgfInfoPod()
+        _check(capi.mgf_parse_dev(self._h, d_image, n_bytes, C.byref(info)), self._h)
+        return dict(n_spectra=int(info.n_spectra), n_peaks=int(info.n_peaks), n_lines=int(info.n_lines),
+                    n_hard_numbers=int(info.n_hard_numbers))
+
+    def mgf_fetch(self, n: int, n_peaks: int, out=None) -> dict:
+        """Copies the resident CSR of the last parse to the host (`out`: dict of preallocated arrays)."""
+        o = out or dict(offsets=np.zeros(n + 1, np.uint64), mz=np.zeros(n_peaks, np.float64),
+                        intensity=np.zeros(n_peaks, np.float64), precursor_mz=np.zeros(n, np.float64),
+                        charge=np.zeros(n, np.uint8), title_off=np.zeros(n, np.uint32),
+                        title_len=np.zeros(n, np.uint32), seq_off=np.zeros(n, np.uint32),
+                        seq_len=np.zeros(n, np.uint32))
+        _check(capi.mgf_fetch(self._h, *[_ptr(o[k]) for k in ("offsets", "mz", "intensity", "precursor_mz", "charge",
+                                                            "title_off", "title_len", "seq_off", "seq_len")]), self._h)
+        return o
+
     def mgf_device_csr(self) -> dict:
         """Device pointers of the resident CSR of the last parse_mgf (valid until the next one)."""
         n, npk = C.c_uint64(), C.c_uint64()

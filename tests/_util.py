@@ -66,3 +66,23 @@ TOLS = {"ppm150": ("ppm", 150.0), "da30": ("da", 30.0), "da500": ("da", 500.0), 
 def product_tol(t):
     import paper_2211_16422_b200 as hb
     return hb.Tolerance("ppm" if t[0] == "ppm" else "dalton", t[1])
+
+
+def mgf_cases():
+    """[(text bytes, expected dict | error string)] generated from the reference (make_golden.py)."""
+    with open(os.path.join(GOLDEN, "mgf_cases.json")) as f:
+        raw = json.load(f)
+    out = []
+    for c in raw:
+        text = bytes.fromhex(c["text"])
+        if not c["ok"]:
+            out.append((text, c["error"]))
+            continue
+        out.append((text, dict(offsets=np.array(c["offsets"], np.uint64),
+                               mz=np.array(c["mz"], np.uint64).view(np.float64),
+                               intensity=np.array(c["intensity"], np.uint64).view(np.float64),
+                               precursor_mz=np.array(c["precursor_mz"], np.uint64).view(np.float64),
+                               charge=np.array(c["charge"], np.uint8), is_decoy=np.array(c["is_decoy"], np.uint8),
+                               ids=[bytes.fromhex(x) for x in c["ids"]],
+                               peptides=[bytes.fromhex(x) for x in c["peptides"]])))
+    return out

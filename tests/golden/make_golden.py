@@ -13,6 +13,8 @@ Outputs (tests/golden/):
   encode_cases.npz    spectra -> (ok, hypervector words, bins, levels) for several configs
   search_cases.npz    small libraries with clones / mirror pairs -> windows, top-1, cascade
   cache_small.homs    a cache file written by the reference's write_cache (+ cache_small.npz: its entries)
+  mgf_cases.json      MGF texts (hex) -> the reference's parse_mgf result (doubles as u64 bit patterns) or
+                      its ParseError text: test_mgf.cpp's cases, number-grammar corner cases, random mutations
 """
 from __future__ import annotations
 
@@ -271,8 +273,55 @@ def cache_case(ref: Oracle):
     return dict(bytes=len(image), fnv_of_file=f"{fnv1a64_words(np.frombuffer(image + bytes(-len(image) % 8), np.uint64)):016x}")
 
 
+def mgf_cases(ref: Oracle):
+    from oracle.binding import OracleError
+    sys.path.insert(0, os.path.dirname(HERE))
+    import _mgf_cases as M
+    texts = [b"BEGIN IONS\nTITLE=run1.scan42\nPEPMASS=500.25\nCHARGE=2+\n100.0 5.0\n200.5 7.25\nEND IONS\n",
+             b"BEGIN IONS\nPEPMASS=500\nCHARGE=+3\n100 1\nEND IONS\n", b"BEGIN IONS\nPEPMASS=500\n100 1\nEND IONS\n",
+             b"BEGIN IONS\nTITLE=x\nSEQ=DECOY_PEPTIDE\nPEPMASS=500\n100 1\nEND IONS\n",
+             b"BEGIN IONS\nPEPMASS=500\n100.0 5.0\n100.0 3.0\n99.5 1.0\nEND IONS\n", b"", b"\n\n  \n# comment\n",
+             b"BEGIN IONS\nPEPMASS=500.25 12345.6\n100 1\nEND IONS\n", b"BEGIN IONS\nPEPMASS=500\n100.25 7.5 1\nEND IONS\n",
+             b"BEGIN IONS\nPEPMASS=500\n100 1\nEND IONS\nBEGIN IONS\nPEPMASS=600\n100 1\nEND IONS\n",
+             b"MASS=Monoisotopic\nBEGIN IONS\nPEPMASS=500\n100 1\nEND IONS\n", b"BEGIN IONS\nTITLE=x\n100 1\nEND IONS\n",
+             b"BEGIN IONS\nPEPMASS=500\n100 abc\nEND IONS\n", b"BEGIN IONS\nPEPMASS=500\n100\nEND IONS\n",
+             b"BEGIN IONS\nPEPMASS=0\n100 1\nEND IONS\n", b"BEGIN IONS\nPEPMASS=500\nCHARGE=two\n100 1\nEND IONS\n",
+             b"BEGIN IONS\nPEPMASS=500\n-5 1\nEND IONS\n", b"BEGIN IONS\nPEPMASS=500\n100 -1\nEND IONS\n", b"100 1\n",
+             b"BEGIN IONS\nPEPMASS=500\nBEGIN IONS\nEND IONS\n", b"BEGIN IONS\nPEPMASS=500\n100 1\n", b"END IONS\n"]
+    for t in M.TOKS:
+        texts.append(b"BEGIN IONS\nPEPMASS=" + t + b"\n" + t + b" 1\n5 " + t + b"\nEND IONS\n")
+        texts.append(b"BEGIN IONS\nPEPMASS=7\n5 " + t + b"\nEND IONS\n")
+        texts.append(b"BEGIN IONS\nPEPMASS=7\n" + t + b" 1\nEND IONS\n")
+    base = M.base_text(ref)
+    rng = np.random.default_rng(2024)
+    texts += [M.mutate(rng, base) for _ in range(120)]
+    cases, n_ok = [], 0
+    for t in texts:
+        try:
+            r = ref.mgf_parse(t)
+            n_ok += 1
+            cases.append(dict(text=t.hex(), ok=True, offsets=r["offsets"].tolist(),
+                              mz=r["mz"].view(np.uint64).tolist(), intensity=r["intensity"].view(np.uint64).tolist(),
+                              precursor_mz=r["precursor_mz"].view(np.uint64).tolist(), charge=r["charge"].tolist(),
+                              is_decoy=r["is_decoy"].tolist(), ids=[i.hex() for i in r["ids"]],
+                              peptides=[p.hex() for p in r["peptides"]]))
+        except OracleError as e:
+            cases.append(dict(text=t.hex(), ok=False, error=str(e)))
+    with open(os.path.join(HERE, "mgf_cases.json"), "w") as f:
+        json.dump(cases, f)
+    return dict(cases=len(cases), parsed=n_ok, errors=len(cases) - n_ok)
+
+
 def main():
     ref = Oracle("ref")
+    if "--mgf-only" in sys.argv:  # adds the MGF fixture without regenerating the others
+        with open(os.path.join(HERE, "fingerprints.json")) as f:
+            fp = json.load(f)
+        fp["mgf_cases"] = mgf_cases(ref)
+        with open(os.path.join(HERE, "fingerprints.json"), "w") as f:
+            json.dump(fp, f, indent=1, sort_keys=True)
+        print(fp["mgf_cases"])
+        return
     if "--cache-only" in sys.argv:  # adds the cache fixture without regenerating the others
         with open(os.path.join(HERE, "fingerprints.json")) as f:
             fp = json.load(f)
@@ -283,6 +332,7 @@ def main():
         return
     fp = fingerprints(ref)
     fp["cache_small"] = cache_case(ref)
+    fp["mgf_cases"] = mgf_cases(ref)
     fp["encode_cases_ok"] = encode_cases(ref)
     fp["search_cases_hits"] = search_cases(ref)
     with open(os.path.join(HERE, "fingerprints.json"), "w") as f:

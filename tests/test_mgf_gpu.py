@@ -149,3 +149,16 @@ def test_write_then_parse_fixpoint_and_resident_encode(hb, ctx, best_oracle):
                          okd.data_ptr())
     ctx.synchronize()
     assert np.array_equal(out.cpu().numpy().view(np.uint64), want) and np.array_equal(okd.cpu().numpy(), ok)
+
+
+def test_golden_mgf_cases(hb, ctx):
+    """The committed fixture generated from the compiled reference (tests/golden/make_golden.py)."""
+    from tests import _util as U
+    for text, want in U.mgf_cases():
+        if isinstance(want, str):
+            with pytest.raises(hb.ParseError) as e:
+                ctx.parse_mgf(text)
+            assert "ParseError: " + str(e.value) == want, text[:200]
+        else:
+            got = ctx.parse_mgf(text)
+            assert M.same(want, {k: got[k] for k in want}), text[:200]

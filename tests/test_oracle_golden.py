@@ -268,3 +268,31 @@ def test_port_equals_reference_random(port, ref):
         wp, okp = port.encode_spectra(cbp, cfg, off, mz, it)
         wr, okr = ref.encode_spectra(cbr, cfg, off, mz, it, threads=3, batch=4)
         assert np.array_equal(okp, okr) and np.array_equal(wp, wr)
+
+
+def test_golden_mgf_cases(oracle):
+    """parse_mgf (mgf.cpp:93-181): the reference's own test cases (test_mgf.cpp), number-grammar corner
+    cases and random mutations, expected results generated from the compiled reference."""
+    from tests import _mgf_cases as M
+    cases = U.mgf_cases()
+    assert len(cases) == U.fingerprints()["mgf_cases"]["cases"]
+    n_ok = 0
+    for text, want in cases:
+        if isinstance(want, str):
+            with pytest.raises(OracleError) as e:
+                oracle.mgf_parse(text)
+            assert str(e.value) == want, text[:200]
+        else:
+            n_ok += 1
+            assert M.same(want, oracle.mgf_parse(text)), text[:200]
+    assert n_ok == U.fingerprints()["mgf_cases"]["parsed"]
+
+
+def test_mgf_write_matches_reference_format(port):
+    """write_mgf (mgf.cpp:183-208): "%.5f" precursor, "%.5f %.6f" peaks, CHARGE only when known."""
+    text = port.mgf_write([0, 2, 2], [100.123456, 200.5], [1.5, 0.1234567], [500.123456, 600.0], [2, 0],
+                          ["a", "b"], [b"PEP", b""])
+    assert text == (b"BEGIN IONS\nTITLE=a\nPEPMASS=500.12346\nCHARGE=2+\nSEQ=PEP\n100.12346 1.500000\n"
+                    b"200.50000 0.123457\nEND IONS\n\nBEGIN IONS\nTITLE=b\nPEPMASS=600.00000\nEND IONS\n\n")
+    r = port.mgf_parse(text)
+    assert r["ids"] == [b"a", b"b"] and list(r["charge"]) == [2, 0] and list(r["offsets"]) == [0, 2, 2]
