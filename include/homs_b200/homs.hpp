@@ -9,6 +9,11 @@
 //   search_one       include/homs/search.hpp:99-100      src/search.cpp:105-169
 //   search_batch     include/homs/search.hpp:104-107     src/search.cpp:171-183
 //   cascade_search   include/homs/search.hpp:114-117     src/search.cpp:219-248
+//   parse_mgf        include/homs/mgf.hpp:20             src/mgf.cpp:93-181
+//
+// plus one composition the reference spells as two calls with host vectors in between:
+//
+//   encode_and_index == build_index(encode_spectra(spectra, ...).encoded)   (hypervectors never leave HBM)
 //
 // The facade is header-only and generic over the data types: instantiate it with a traits struct
 // that names the caller's own types.  With the reference's headers that is
@@ -28,6 +33,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <istream>
+#include <iterator>
 #include <memory>
 #include <mutex>
 #include <optional>
@@ -47,6 +54,14 @@ namespace types {
 struct Error : std::runtime_error { using std::runtime_error::runtime_error; };
 struct ConfigError : Error { using Error::Error; };
 struct InvariantError : Error { using Error::Error; };
+struct ParseError : Error {  // errors.hpp:22-32
+  ParseError(std::size_t line, const std::string& message)
+      : Error("line " + std::to_string(line) + ": " + message), line_(line) {}
+  std::size_t line() const noexcept { return line_; }
+
+ private:
+  std::size_t line_;
+};
 
 struct Peak { double mz = 0.0, intensity = 0.0; };
 struct SpectrumMeta {
@@ -116,6 +131,7 @@ struct DefaultApi {
   using Error = types::Error;
   using ConfigError = types::ConfigError;
   using InvariantError = types::InvariantError;
+  using ParseError = types::ParseError;
   using SpectrumMeta = types::SpectrumMeta;
   using RawSpectrum = types::RawSpectrum;
   using Hypervector = types::Hypervector;
@@ -248,6 +264,9 @@ class LibraryIndex {
  private:
   template <class A>
   friend LibraryIndex<A> build_index(std::span<const typename A::EncodedSpectrum>, int);
+  template <class A>
+  friend LibraryIndex<A> encode_and_index(std::span<const typename A::RawSpectrum>, const typename A::Codebook&,
+                                          const typename A::PreprocessConfig&, std::size_t*, int);
   std::uint32_t dim_ = 0;
   std::vector<typename Api::SpectrumMeta> metas_;
   std::vector<std::uint8_t> decoy_;
@@ -453,6 +472,107 @@ std::vector<typename Api::Ssm> cascade_search(std::span<const typename Api::Enco
     out.push_back(std::move(s));
   }
   return out;
+}
+
+// ---- encode_and_index: build_index(encode_spectra(...).encoded) without the host round trip -------
+// (pipeline.cpp:60-85 + search.cpp:17-60).  Library ordinals -- and index.meta(ordinal) -- count the
+// processable spectra only, exactly as if the reference's two calls had been made.
+template <class Api = DefaultApi>
+LibraryIndex<Api> encode_and_index(std::span<const typename Api::RawSpectrum> spectra,
+                                   const typename Api::Codebook& codebook,
+                                   const typename Api::PreprocessConfig& preprocess,
+                                   std::size_t* unprocessable = nullptr, int device = 0) {
+  if (spectra.empty()) throw typename Api::InvariantError("build_index: library is empty");  // search.cpp:18
+  LibraryIndex<Api> index;
+  index.dim_ = codebook.config.dim;
+  index.ctx_ = detail::make_ctx<Api>(device);
+  {
+    detail::Encoder<Api> enc;  // uploads the codebook into the index's own context
+    enc.ctx = std::move(index.ctx_);
+    enc.ensure_codebook(codebook);
+    index.ctx_ = std::move(enc.ctx);
+  }
+  const std::size_t n = spectra.size();
+  std::vector<std::uint64_t> offsets(n + 1, 0);
+  for (std::size_t i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + spectra[i].peaks.size();
+  std::vector<double> mz(offsets[n]), intensity(offsets[n]), prec(n);
+  std::vector<std::uint8_t> charge(n), ok(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    std::size_t o = offsets[i];
+    for (const auto& p : spectra[i].peaks) {
+      mz[o] = p.mz;
+      intensity[o] = p.intensity;
+      ++o;
+    }
+    prec[i] = spectra[i].meta.precursor_mz;
+    charge[i] = spectra[i].meta.charge;
+  }
+  std::vector<std::uint32_t> order(n), rank(n);  // id_rank over the raw list (search.cpp:43)
+  for (std::size_t i = 0; i < n; ++i) order[i] = static_cast<std::uint32_t>(i);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](std::uint32_t a, std::uint32_t b) { return spectra[a].meta.id < spectra[b].meta.id; });
+  for (std::size_t p = 0; p < n; ++p) rank[order[p]] = static_cast<std::uint32_t>(p);
+  const auto cfg = detail::pod(preprocess);
+  std::uint64_t n_encoded = 0;
+  detail::check<Api>(homs_b200_library_build_from_spectra(index.ctx_.get(), &cfg, n, offsets.data(), mz.data(),
+                                                          intensity.data(), prec.data(), charge.data(), rank.data(),
+                                                          0, 1, ok.data(), &n_encoded),
+                     index.ctx_.get());
+  index.metas_.reserve(n_encoded);
+  index.decoy_.reserve(n_encoded);
+  for (std::size_t i = 0; i < n; ++i)
+    if (ok[i]) {
+      index.metas_.push_back(spectra[i].meta);
+      index.decoy_.push_back(spectra[i].meta.is_decoy ? 1 : 0);
+    }
+  if (unprocessable) *unprocessable = n - n_encoded;
+  return index;
+}
+
+// ---- parse_mgf (mgf.cpp:93-181) -------------------------------------------------------------------
+// Same spectra, same doubles, same first ParseError (line and message) as the reference's sequential
+// parser; the text is parsed on the device.  Api::ParseError(line, message) when the traits name one.
+template <class Api = DefaultApi>
+std::vector<typename Api::RawSpectrum> parse_mgf(std::istream& in, const std::string& decoy_prefix, int device = 0) {
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  auto& enc = detail::Encoder<Api>::on(device);
+  std::lock_guard<std::mutex> g(enc.mu);
+  homs_b200_mgf_info info{};
+  const int rc = homs_b200_mgf_parse(enc.ctx.get(), text.data(), text.size(), &info);
+  if (rc == HOMS_B200_ERR_PARSE) {
+    std::string msg = homs_b200_last_error(enc.ctx.get());
+    const auto colon = msg.find(": ");
+    if (colon != std::string::npos) msg = msg.substr(colon + 2);
+    if constexpr (requires { typename Api::ParseError; })
+      throw typename Api::ParseError(static_cast<std::size_t>(info.error_line), msg);
+    else
+      throw typename Api::Error("line " + std::to_string(info.error_line) + ": " + msg);
+  }
+  detail::check<Api>(rc, enc.ctx.get());
+  const std::size_t n = info.n_spectra;
+  std::vector<std::uint64_t> offsets(n + 1);
+  std::vector<double> mz(info.n_peaks), intensity(info.n_peaks), prec(n);
+  std::vector<std::uint8_t> charge(n);
+  std::vector<std::uint32_t> toff(n), tlen(n), soff(n), slen(n);
+  detail::check<Api>(homs_b200_mgf_fetch(enc.ctx.get(), offsets.data(), mz.data(), intensity.data(), prec.data(),
+                                         charge.data(), toff.data(), tlen.data(), soff.data(), slen.data()),
+                     enc.ctx.get());
+  std::vector<typename Api::RawSpectrum> spectra(n);
+  for (std::size_t i = 0; i < n; ++i) {  // finalize_block, mgf.cpp:66-76
+    auto& s = spectra[i];
+    s.meta.id = tlen[i] ? text.substr(toff[i], tlen[i]) : "spectrum_" + std::to_string(i + 1);
+    s.meta.precursor_mz = prec[i];
+    s.meta.charge = charge[i];
+    s.meta.peptide = text.substr(soff[i], slen[i]);
+    s.meta.is_decoy = !decoy_prefix.empty() && (s.meta.id.compare(0, decoy_prefix.size(), decoy_prefix) == 0 ||
+                                                s.meta.peptide.compare(0, decoy_prefix.size(), decoy_prefix) == 0);
+    s.peaks.resize(offsets[i + 1] - offsets[i]);
+    for (std::size_t k = 0; k < s.peaks.size(); ++k) {
+      s.peaks[k].mz = mz[offsets[i] + k];
+      s.peaks[k].intensity = intensity[offsets[i] + k];
+    }
+  }
+  return spectra;
 }
 
 }  // namespace homs_b200

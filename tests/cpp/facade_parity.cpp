@@ -7,11 +7,13 @@
 // and the binary travels to the GPU box.  Needs a CUDA device to run.
 #include <cstdio>
 #include <cstring>
+#include <sstream>
 #include <string>
 
 #include "homs/codebook.hpp"
 #include "homs/encoder.hpp"
 #include "homs/errors.hpp"
+#include "homs/mgf.hpp"
 #include "homs/pipeline.hpp"
 #include "homs/preprocess.hpp"
 #include "homs/search.hpp"
@@ -24,6 +26,7 @@ struct HomsApi {
   using Error = homs::Error;
   using ConfigError = homs::ConfigError;
   using InvariantError = homs::InvariantError;
+  using ParseError = homs::ParseError;
   using SpectrumMeta = homs::SpectrumMeta;
   using RawSpectrum = homs::RawSpectrum;
   using Hypervector = homs::Hypervector;
@@ -121,6 +124,46 @@ int main() {
     }
     report(ok, "cascade_search (20 ppm, 500 Da, 1% FDR): identical accepted list = " + std::to_string(want.size()) +
                    " (" + std::to_string(n_narrow) + " narrow)");
+  }
+  {  // encode_and_index == build_index(encode_spectra(...).encoded): same answers, no host round trip
+    std::size_t dropped = 0;
+    const auto fused_ix = gpu::encode_and_index<HomsApi>(synth.library, cb, pre, &dropped);
+    bool ok = dropped == ref_lib.unprocessable && fused_ix.size() == ref_ix.size();
+    const Tolerance wide{Tolerance::Kind::dalton, 500.0};
+    const auto want = homs::search_batch(ref_q.encoded, ref_ix, wide, homs::SearchOptions{8, 64});
+    const auto got = gpu::search_batch<HomsApi>(gpu_q.encoded, fused_ix, wide);
+    for (std::size_t i = 0; ok && i < want.size(); ++i)
+      ok = want[i].has_value() == got[i].has_value() && (!want[i] || same_ssm(*want[i], *got[i]));
+    report(ok, "encode_and_index: identical search results, unprocessable = " + std::to_string(dropped));
+  }
+  {  // parse_mgf: write_mgf of the synthetic library (plus dirt) parsed by both
+    std::ostringstream text;
+    homs::write_mgf(text, std::span<const homs::RawSpectrum>(synth.library.data(), 300));
+    std::string mgf = "# comment\nSEARCH=MIS\n\n" + text.str() +
+                      "BEGIN IONS\nPEPMASS=1e2 7\nCHARGE=+3\nSEQ=DECOY_X\n300.5 1\n200.25\t2e0\r\n300.5 3\nEND IONS";
+    std::istringstream a(mgf), b(mgf);
+    const auto want = homs::parse_mgf(a, "DECOY_");
+    const auto got = gpu::parse_mgf<HomsApi>(b, "DECOY_");
+    bool ok = want.size() == got.size();
+    for (std::size_t i = 0; ok && i < want.size(); ++i)
+      ok = want[i].meta.id == got[i].meta.id && want[i].meta.peptide == got[i].meta.peptide &&
+           want[i].meta.charge == got[i].meta.charge && want[i].meta.is_decoy == got[i].meta.is_decoy &&
+           want[i].meta.precursor_mz == got[i].meta.precursor_mz && want[i].peaks == got[i].peaks;
+    report(ok, "parse_mgf: identical RawSpectrum list, " + std::to_string(want.size()) + " spectra");
+    for (const char* bad : {"BEGIN IONS\nTITLE=x\n100 1\nEND IONS\n", "BEGIN IONS\nPEPMASS=500\n100 abc\nEND IONS\n",
+                            "BEGIN IONS\nPEPMASS=500\n100 1\n", "END IONS\n"}) {
+      std::string ref_what, gpu_what;
+      std::size_t ref_line = 0, gpu_line = 0;
+      try {
+        std::istringstream in(bad);
+        homs::parse_mgf(in, "DECOY_");
+      } catch (const homs::ParseError& e) { ref_what = e.what(); ref_line = e.line(); }
+      try {
+        std::istringstream in(bad);
+        gpu::parse_mgf<HomsApi>(in, "DECOY_");
+      } catch (const homs::ParseError& e) { gpu_what = e.what(); gpu_line = e.line(); }
+      report(!ref_what.empty() && ref_what == gpu_what && ref_line == gpu_line, "parse_mgf error: " + gpu_what);
+    }
   }
   // error behaviour
   {
