@@ -361,7 +361,7 @@ def run_ours(args) -> None:
     # DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` captures of
     # this exact command (dram__bytes_read.sum + dram__bytes_write.sum); only valid for the default
     # single-GPU workload, null otherwise
-    ncu_traffic = {"tensor_fp4": (29.553690e9 + 0.107591e9, "profiles/r01_search_kernel_tensor_fp4_ncu.csv"),
+    ncu_traffic = {"tensor_fp4": (28.382962e9 + 0.116947e9, "profiles/r01_search_kernel_tensor_fp4_ncu_v2.csv"),
                    "tensor": (260.988723e9 + 0.019967e9, "profiles/r01_search_kernel_tensor_ncu.csv (before the "
                                                          "short-strip planner)"),
                    "popc": (301.799285e9 + 0.036848e9, "profiles/r01_search_kernel_popc_ncu.csv")}
