@@ -192,9 +192,10 @@ enum Scratch {
 
 // Tensor-core engine (search_tc.cu).  expand: packed rows -> +-1 int8 swizzled image.
 int tc_expand_library(homs_b200_ctx* ctx);
-// top-1 of n sorted slots (keys/vals as produced by bounds + radix sort) -> out[slot * k_stride]
+// top-k (k <= tc_max_topk()) of n sorted slots (keys/vals as produced by bounds + radix sort) -> out[slot * k_stride + j]
 int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
-                     const uint32_t* d_vals, Cand* d_out, uint32_t k_stride);
+                     const uint32_t* d_vals, Cand* d_out, uint32_t k, uint32_t k_stride);
+uint32_t tc_max_topk();
 bool tc_available(const homs_b200_ctx* ctx);
 int tc_peak_probe(homs_b200_ctx* ctx, int fp4, double seconds, double* out_ops_per_s, double* out_ms);
 

@@ -215,7 +215,7 @@ encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stri
   // level rows: shared memory when they fit (LDS with a 32-bit address), else global through L1
   uint4* s_lvl = reinterpret_cast<uint4*>(smem_raw);
   if constexpr (kLvlSmem) {
-    for (uint32_t i = threadIdx.x; i < n_level_rows * row_u4; i += blockDim.x) s_lvl[i] = lvl_global[i];
+    for (uint32_t i = threadIdx.x; i < (n_level_rows + 1) * row_u4; i += blockDim.x) s_lvl[i] = lvl_global[i];
     __syncthreads();
   }
   const int lane = threadIdx.x & 31;
@@ -251,27 +251,36 @@ encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stri
       // The (bin, level) list is staged through registers 32 entries at a time (lane j holds entry
       // c0 + j: one coalesced load per warp, the next block prefetched) and broadcast by shuffle,
       // so the position-row gathers depend on no other memory access.  Votes are summed by a
-      // Harley-Seal tree: c[0..3] are carry-save accumulators of weight 1, 2, 4, 8 (and, being
-      // single bits per position, ARE planes 0..3 of the count); every 16 inputs emit one carry
-      // of weight 16 into the half-adder chain c[4..NP).  15 CSAs + NP-4 half adders per 16 inputs.
+      // Harley-Seal tree: c[0..4] are carry-save accumulators of weight 1, 2, 4, 8, 16 (and, being
+      // single bits per position, ARE planes 0..4 of the count); every 32 inputs emit one carry
+      // of weight 32 into the half-adder chain c[5..NP).  31 CSAs + NP-5 half adders per 32 inputs.
       // Groups of 8 run in a real loop: 8 gathers in flight per lane, bounded registers.
+      // Entries past the end of the list read position row 0 against the extra level row
+      // (~position[0], see homs_b200_codebook_upload): XNOR = 0 everywhere, i.e. no vote and no
+      // per-entry mask.  All addressing is a byte offset prepared by the staging lane, so a gather
+      // costs one wide multiply-add and a level fetch one add next to the logic ops that bound the
+      // kernel (ncu: ALU pipe 85 % before this change).
       const uint32_t uu = active ? u : row_u4 - 1;  // idle lanes gather a valid slab and store nothing
-      const uint4* pos_u = pos + uu;
-      uint32_t nxt_bin = 0, nxt_lev = 0;
+      const unsigned char* pos_b = reinterpret_cast<const unsigned char*>(pos + uu);
+      const unsigned char* lvl_b = reinterpret_cast<const unsigned char*>((kLvlSmem ? s_lvl : lvl_global) + uu);
+      const uint32_t row_bytes = row_u4 * 16;
+      const uint32_t null_lev = n_level_rows * row_bytes;  // the extra row
+      uint32_t nxt_bin = 0, nxt_lev = null_lev;
       if (lane < nb) {
         nxt_bin = sv_bins[start + lane];
-        nxt_lev = sv_levels[start + lane];
+        nxt_lev = sv_levels[start + lane] * row_bytes;
       }
       for (uint32_t c0 = 0; c0 < nb; c0 += 32) {
         const uint32_t my_bin = nxt_bin, my_lev = nxt_lev;
-        nxt_bin = nxt_lev = 0;  // entries beyond the list read row 0 and are masked to zero votes
+        nxt_bin = 0;
+        nxt_lev = null_lev;
         if (c0 + 32 + lane < nb) {
           nxt_bin = sv_bins[start + c0 + 32 + lane];
-          nxt_lev = sv_levels[start + c0 + 32 + lane];
+          nxt_lev = sv_levels[start + c0 + 32 + lane] * row_bytes;
         }
         const uint32_t cn = min(32u, nb - c0);
         const uint32_t n_groups = 2 * ((cn + 15) / 16);  // groups of 8, an even number of them
-        U4 pend{{0, 0, 0, 0}};
+        U4 pend8{{0, 0, 0, 0}}, pend16{{0, 0, 0, 0}};
 #pragma unroll 1
         for (uint32_t g = 0; g < n_groups; ++g) {
           U4 x[8];
@@ -280,18 +289,18 @@ encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stri
           for (int j = 0; j < 8; ++j) {  // 8 position-row gathers in flight
             const uint32_t k = 8 * g + j;
             const uint32_t bin = __shfl_sync(0xffffffffu, my_bin, k);
-            lev[j] = __shfl_sync(0xffffffffu, my_lev, k) * row_u4;
-            x[j] = ld_global_u4(pos_u + size_t(bin) * row_u4);
+            lev[j] = __shfl_sync(0xffffffffu, my_lev, k);
+            x[j] = ld_global_u4(reinterpret_cast<const uint4*>(pos_b + uint64_t(bin) * row_bytes));
           }
           asm volatile("" ::: "memory");  // level rows (shared memory) are fetched only as the gathers land
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const uint32_t m = 8 * g + j < cn ? 0xffffffffu : 0u;
-            const uint4 lw4 = kLvlSmem ? s_lvl[lev[j] + uu] : __ldg(lvl_global + lev[j] + uu);
-            x[j].v[0] = ~(x[j].v[0] ^ lw4.x) & m;  // encoder.cpp:41 agree = ~(pos ^ lvl)
-            x[j].v[1] = ~(x[j].v[1] ^ lw4.y) & m;
-            x[j].v[2] = ~(x[j].v[2] ^ lw4.z) & m;
-            x[j].v[3] = ~(x[j].v[3] ^ lw4.w) & m;
+            const uint4* lp = reinterpret_cast<const uint4*>(lvl_b + lev[j]);
+            const uint4 lw4 = kLvlSmem ? *lp : __ldg(lp);
+            x[j].v[0] = ~(x[j].v[0] ^ lw4.x);  // encoder.cpp:41 agree = ~(pos ^ lvl)
+            x[j].v[1] = ~(x[j].v[1] ^ lw4.y);
+            x[j].v[2] = ~(x[j].v[2] ^ lw4.z);
+            x[j].v[3] = ~(x[j].v[3] ^ lw4.w);
           }
           // 8 inputs -> c[0..2] updated, one carry e of weight 8
           U4 ta, tb, fa, fb, e;
@@ -303,17 +312,23 @@ encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stri
           HB_CSA(c[1], fb, c[1], ta, tb);
           HB_CSA(c[2], e, c[2], fa, fb);
           if ((g & 1u) == 0) {
-            pend = e;
-          } else {  // the carries of an even/odd pair meet in c[3] and ripple into the upper planes
+            pend8 = e;
+          } else {  // the weight-8 carries of an even/odd pair meet in c[3] ...
             U4 carry;
-            HB_CSA(c[3], carry, c[3], pend, e);
+            HB_CSA(c[3], carry, c[3], pend8, e);
+            if ((g & 2u) == 0 && g + 1 < n_groups) {
+              pend16 = carry;
+            } else {  // ... the weight-16 carries of two pairs in c[4], and the rest ripples up
+              if ((g & 2u) == 0) pend16 = U4{{0, 0, 0, 0}};  // a lone pair (at most 16 entries left)
+              HB_CSA(c[4], carry, c[4], pend16, carry);
 #pragma unroll
-            for (int b = 4; b < NP; ++b) {
+              for (int b = 5; b < NP; ++b) {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const uint32_t a = c[b].v[i];
-                c[b].v[i] = a ^ carry.v[i];
-                carry.v[i] = a & carry.v[i];
+                for (int i = 0; i < 4; ++i) {
+                  const uint32_t a = c[b].v[i];
+                  c[b].v[i] = a ^ carry.v[i];
+                  carry.v[i] = a & carry.v[i];
+                }
               }
             }
           }
@@ -439,7 +454,7 @@ static int launch_encode(homs_b200_ctx* ctx, uint64_t n, const uint64_t* d_sv_of
   if (n == 0) return HOMS_B200_OK;
   const Codebook& cb = ctx->cb;
   const uint32_t row_u4 = cb.S / 2;
-  const size_t lvl_bytes = size_t(cb.levels + 1) * cb.S * 8;
+  const size_t lvl_bytes = size_t(cb.levels + 2) * cb.S * 8;  // level rows + the no-vote row
   const int lvl_in_smem = lvl_bytes <= 96 * 1024;
   const size_t smem = lvl_in_smem ? lvl_bytes : 0;
   const int warps = HB_ENC_WARPS;
@@ -619,9 +634,15 @@ int homs_b200_codebook_upload(homs_b200_ctx* ctx, uint32_t dim, uint32_t n_bins,
   cb.W = words_for(dim);
   cb.S = stride_for(dim);
   HB_TRY(ensure(ctx, cb.d_pos, size_t(n_bins) * cb.S * 8));
-  HB_TRY(ensure(ctx, cb.d_lvl, size_t(levels + 1) * cb.S * 8));
+  // one row more than the reference's table: ~position[0] (all ones in the padding), the level an
+  // entry past the end of a spectrum's list is given so that it XNORs to zero votes (encode_kernel)
+  HB_TRY(ensure(ctx, cb.d_lvl, size_t(levels + 2) * cb.S * 8));
   HB_TRY(upload_rows(ctx, cb.d_pos.as<uint64_t>(), pos, n_bins, cb.W, cb.S));
   HB_TRY(upload_rows(ctx, cb.d_lvl.as<uint64_t>(), lvl, levels + 1, cb.W, cb.S));
+  std::vector<uint64_t> no_vote(cb.S, ~0ull);
+  for (uint32_t w = 0; w < cb.W; ++w) no_vote[w] = ~pos[w];
+  HB_CUDA(ctx, cudaMemcpyAsync(cb.d_lvl.as<uint64_t>() + size_t(levels + 1) * cb.S, no_vote.data(), size_t(cb.S) * 8,
+                               cudaMemcpyHostToDevice, ctx->stream));
   HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   cb.ready = true;
   return HOMS_B200_OK;

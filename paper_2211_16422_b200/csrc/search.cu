@@ -581,8 +581,8 @@ static int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint6
   const uint64_t* keys = ctx->scratch[kScrKeysAlt].as<uint64_t>();
   const uint32_t* vals = ctx->scratch[kScrValsAlt].as<uint32_t>();
 
-  if (k == 1 && ctx->engine != HOMS_B200_ENGINE_POPC && tc_available(ctx))
-    return tc_search_sorted(ctx, d_subset, n, keys, vals, d_out, 1);
+  if (k <= tc_max_topk() && ctx->engine != HOMS_B200_ENGINE_POPC && tc_available(ctx))
+    return tc_search_sorted(ctx, d_subset, n, keys, vals, d_out, k, k);
 
   const uint32_t n_blocks = static_cast<uint32_t>((n + qb - 1) / qb);
   const int grid = ctx->sm_count * 2;

@@ -68,6 +68,7 @@ struct TcMode {
   static constexpr uint32_t SfCol = 480;                  // fp4: scale-factor columns [480, 512)
 };
 constexpr uint32_t kTcGroupTiles = 12;  // query tiles per L2 group
+constexpr int kTcMaxK = 16;             // top-k depth the drain keeps per query; larger k -> POPC engine
 constexpr uint64_t kTcBatch = 64 * 1024;  // sorted slots per planning batch
 
 struct TcItem {
@@ -94,8 +95,10 @@ struct TcParams {
   const double* lib_mz;
   const uint32_t* lib_rank;
   uint64_t n;  // sorted positions in this batch
-  Cand* partial;  // [n_items][128]
-  int* gbest;     // [q_rows] best dot found so far per sorted position (a lower bound; see the drain)
+  Cand* partial;  // [n_items][128][k]
+  int* gbest;     // [q_rows][k] best dot seen per residue class (row % k) of a sorted position (see the drain)
+  uint32_t k;     // candidates kept per query (1 .. kTcMaxK)
+  uint32_t pad2;
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
@@ -359,8 +362,69 @@ struct TcAcc<true> {
   static __device__ __forceinline__ T from_int(int v) { return static_cast<float>(v); }
 };
 
-template <bool kFp4>
+// The KM best candidates of one query seen by one work item, ascending in the reference key
+// (distance asc == dot desc, |mass diff| asc, id_rank asc), held in REGISTERS: every access is
+// fully unrolled, so an insert is ~6 KM ALU operations and no memory traffic (a local-memory
+// list cost several dependent L2 round trips per insert with the L1 carved down to its minimum).
+// Only (dot, row) are kept; the rest of the key is fetched when two dots tie and when the list is
+// written out.  Unused entries hold kTcNoDot / kNone.  The caller needs the best k <= KM only.
+constexpr int kTcNoDot = -(1 << 30);  // below every real dot (|dot| <= dim <= 65536), exact in fp32
+template <int KM>
+struct TcTopK {
+  int dot[KM];
+  uint32_t row[KM];
+};
+
+// candidate row a before row b among equal dots: |mass diff|, then id, then ordinal (search.cpp:137-145)
+__device__ __forceinline__ bool tc_row_before(const double* __restrict__ lib_mz, const uint32_t* __restrict__ lib_rank,
+                                              double qmz, uint32_t a, uint32_t b) {
+  const uint64_t ada = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - lib_mz[a])));
+  const uint64_t adb = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - lib_mz[b])));
+  return ada != adb ? ada < adb : lib_rank[a] < lib_rank[b];
+}
+
+template <int KM>
+__device__ __forceinline__ void tc_topk_insert(TcTopK<KM>& l, const double* __restrict__ lib_mz,
+                                               const uint32_t* __restrict__ lib_rank, double qmz, int dot,
+                                               uint32_t row) {
+  uint32_t ahead = 0;  // entries that stay in front of the new one (a prefix: the list is sorted)
+#pragma unroll
+  for (int i = 0; i < KM; ++i) {
+    bool a = l.dot[i] > dot;
+    if (l.dot[i] == dot) a = tc_row_before(lib_mz, lib_rank, qmz, l.row[i], row);  // rare
+    ahead += a ? 1u : 0u;
+  }
+#pragma unroll
+  for (int i = KM - 1; i >= 0; --i) {
+    if (uint32_t(i) > ahead) {
+      if (i > 0) {
+        l.dot[i] = l.dot[i - 1];
+        l.row[i] = l.row[i - 1];
+      }
+    } else if (uint32_t(i) == ahead) {
+      l.dot[i] = dot;
+      l.row[i] = row;
+    }
+  }
+}
+
+// dot of the k-th entry (k >= 1), kTcNoDot while the list holds fewer than k candidates
+template <int KM>
+__device__ __forceinline__ int tc_topk_kth(const TcTopK<KM>& l, uint32_t k) {
+  int d = l.dot[0];
+#pragma unroll
+  for (int i = 1; i < KM; ++i) {
+    int t = l.dot[i];
+    asm("" : "+r"(t));  // keeps this a chain of selects: a dynamic index would move the list to local memory
+    d = uint32_t(i) == k - 1 ? t : d;
+  }
+  return d;
+}
+
+// KM = 1: plain top-1 drain; KM > 1: the drain keeps the best KM >= p.k candidates per query
+template <bool kFp4, int KM>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams p) {
+  constexpr bool kTopK = KM > 1;
   using Mode = TcMode<kFp4>;
   using Acc = TcAcc<kFp4>;
   using AccT = typename Acc::T;
@@ -502,13 +566,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         }
         const uint32_t slot = p.vals[pos];
         qmz = p.q_mz[p.subset ? p.subset[slot] : slot];
-        floor_i = __ldcg(p.gbest + pos);
+        if constexpr (kTopK) {  // k dots of distinct candidates: the smallest bounds the final k-th best
+          floor_i = INT_MAX;
+          for (uint32_t j = 0; j < p.k; ++j) floor_i = min(floor_i, __ldcg(p.gbest + pos * p.k + j));
+        } else {
+          floor_i = __ldcg(p.gbest + pos);
+        }
       }
       AccT bar = Acc::from_int(floor_i);
       AccT best_dot = Acc::lowest();
       uint32_t best_row = kNone, best_rk = 0;
       uint64_t best_ad = 0;
       bool have_key = false;
+      TcTopK<KM> topk;  // kTopK only
+#pragma unroll
+      for (int i = 0; i < KM; ++i) {
+        topk.dot[i] = kTcNoDot;
+        topk.row[i] = kNone;
+      }
 
       for (uint32_t nt = 0; nt < n_nt; ++nt) {
         const uint32_t row0 = it.row_begin + nt * kN;
@@ -535,6 +610,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
             return;
           }
           if (cm < bar) return;
+          if constexpr (kTopK) {
+            // every valid column at or above the bar is a candidate for the k best; the bar rises
+            // to the list's k-th dot as soon as the list is full (ties with it must still be looked at)
+            uint32_t hits = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) hits |= (Acc::get(v[j]) >= bar ? 1u : 0u) << j;
+            const int lo = max(c0 - cb, 0), hi = min(c1 - cb, 32);  // 0 <= lo < hi <= 32 here
+            hits &= (hi >= 32 ? 0xffffffffu : (1u << hi) - 1u) & ~((1u << lo) - 1u);
+            while (hits) {
+              const int jj = __ffs(hits) - 1;
+              hits &= hits - 1;
+              AccT vj = Acc::lowest();
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j == jj) vj = Acc::get(v[j]);
+              if (vj < bar) continue;  // the bar rose since the mask was taken
+              tc_topk_insert<KM>(topk, p.lib_mz, p.lib_rank, qmz, Acc::to_int(vj), row0 + cb + jj);
+              bar = max(bar, Acc::from_int(tc_topk_kth<KM>(topk, p.k)));
+            }
+            return;
+          }
           uint32_t hits = 0;  // the columns that hold the chunk maximum
 #pragma unroll
           for (int j = 0; j < 32; ++j) hits |= (Acc::get(v[j]) == cm ? 1u : 0u) << j;
@@ -565,7 +661,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           if (best_row != kNone) bar = best_dot;
         };
 
-                int va[32], vb[32];
+        int va[32], vb[32];
         tc_ld32_issue(taddr, va);
         tc_ld_wait(va);
 #pragma unroll 1
@@ -583,6 +679,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty_bar(acc));
         acc ^= 1u;
+      }
+
+      if constexpr (kTopK) {
+        const uint32_t k = p.k;
+        Cand* dst = p.partial + (uint64_t(item) * kTcM + qrow) * k;
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          if (uint32_t(j) < k) {
+            Cand out{kNone, kNone, ~0ull};
+            const uint32_t r = topk.row[j];
+            if (r != kNone) {
+              out.d = static_cast<uint32_t>(static_cast<int>(p.dim) - topk.dot[j]) >> 1;  // dot = dim - 2 * distance
+              out.rk = p.lib_rank[r];
+              out.ad = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - p.lib_mz[r])));
+              // Publish: slot (row % k) of the query holds the best dot seen among the rows of that
+              // residue class.  Classes are disjoint, so the k slots are dots of k distinct real
+              // candidates and min(slots) can never exceed the final k-th best dot, under any
+              // interleaving of the (fire-and-forget) atomicMax of concurrent items.
+              if (topk.dot[j] > floor_i) atomicMax(p.gbest + pos * k + r % k, topk.dot[j]);
+            }
+            dst[j] = out;
+          }
+        }
+        continue;
       }
 
       Cand out{kNone, kNone, ~0ull};
@@ -627,6 +747,42 @@ __global__ void tc_reduce_kernel(uint64_t n, const uint32_t* __restrict__ vals,
   out[uint64_t(vals[pos]) * k_stride] = best;
 }
 
+// top-k: per sorted position the k best of the (sorted) lists its query tile's items left
+__global__ void tc_reduce_topk_kernel(uint64_t n, const uint32_t* __restrict__ vals,
+                                      const uint32_t* __restrict__ tile_item_start,
+                                      const uint32_t* __restrict__ tile_items, const Cand* __restrict__ partial,
+                                      Cand* __restrict__ out, uint32_t k, uint32_t k_stride) {
+  const uint64_t pos = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (pos >= n) return;
+  const uint32_t t = static_cast<uint32_t>(pos / kTcM), r = static_cast<uint32_t>(pos % kTcM);
+  Cand best[kTcMaxK];
+  uint32_t count = 0;
+  for (uint32_t i = tile_item_start[t]; i < tile_item_start[t + 1]; ++i) {
+    const Cand* src = partial + (uint64_t(tile_items[i]) * kTcM + r) * k;
+    for (uint32_t j = 0; j < k; ++j) {
+      const Cand c = src[j];
+      if (c.d == kNone) break;  // lists are sorted, empty entries last
+      uint32_t m = count;
+      if (m == k) {
+        const Cand& w = best[k - 1];
+        if (!(c.d != w.d ? c.d < w.d : key_less(c.ad, c.rk, w.ad, w.rk))) break;  // nor can the rest of this list
+        --m;
+      }
+      uint32_t q = m;
+      while (q > 0) {
+        const Cand& b = best[q - 1];
+        if (b.d != c.d ? b.d < c.d : key_less(b.ad, b.rk, c.ad, c.rk)) break;
+        best[q] = b;
+        --q;
+      }
+      best[q] = c;
+      count = m + 1;
+    }
+  }
+  Cand* dst = out + uint64_t(vals[pos]) * k_stride;
+  for (uint32_t j = 0; j < k; ++j) dst[j] = j < count ? best[j] : Cand{kNone, kNone, ~0ull};
+}
+
 // ---- host side --------------------------------------------------------------------------------
 
 bool tc_available(const homs_b200_ctx* ctx) { return ctx->lib.d_x.p != nullptr && ctx->lib.x_rows > 0; }
@@ -658,14 +814,14 @@ int tc_expand_library(homs_b200_ctx* ctx) {
                               lib.dim, lib.n_kc, lib.d_x.as<uint8_t>());
 }
 
-template <bool kFp4>
+template <bool kFp4, int KM>
 static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
-                                 const uint32_t* d_vals, Cand* d_out, uint32_t k_stride) {
+                                 const uint32_t* d_vals, Cand* d_out, uint32_t k, uint32_t k_stride) {
   using Mode = TcMode<kFp4>;
   constexpr uint32_t kN = Mode::N;
   const Library& lib = ctx->lib;
   const Queries& q = ctx->q;
-  HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<kFp4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<kFp4, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(Mode::SmemBytes)));
   const uint32_t q_stride = stride_for(q.dim);
   for (uint64_t b0 = 0; b0 < n; b0 += kTcBatch) {
@@ -756,10 +912,10 @@ static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, u
     auto* d_start = reinterpret_cast<uint32_t*>(d_items + plan_cap_items);
     auto* d_list = d_start + n_tiles + 1;
     HB_CUDA(ctx, cudaMemcpyAsync(d_items, h_items, plan_bytes, cudaMemcpyHostToDevice, ctx->stream));
-    HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], std::max<size_t>(1, n_items) * kTcM * sizeof(Cand)));
-    HB_TRY(ensure(ctx, ctx->scratch[kScrTcBest], q_rows * sizeof(int)));
+    HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], std::max<size_t>(1, n_items) * kTcM * k * sizeof(Cand)));
+    HB_TRY(ensure(ctx, ctx->scratch[kScrTcBest], q_rows * k * sizeof(int)));
     // every byte 0x80: a dot no candidate can be below
-    HB_CUDA(ctx, cudaMemsetAsync(ctx->scratch[kScrTcBest].p, 0x80, q_rows * sizeof(int), ctx->stream));
+    HB_CUDA(ctx, cudaMemsetAsync(ctx->scratch[kScrTcBest].p, 0x80, q_rows * k * sizeof(int), ctx->stream));
 
     // 4. search + reduce
     if (n_items > 0) {
@@ -782,15 +938,21 @@ static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, u
       tp.n = nb;
       tp.partial = ctx->scratch[kScrTcPartial].as<Cand>();
       tp.gbest = ctx->scratch[kScrTcBest].as<int>();
+      tp.k = k;
+      tp.pad2 = 0;
       const int grid = static_cast<int>(std::min<uint32_t>(n_items, static_cast<uint32_t>(ctx->sm_count)));
       {
         KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
-        tc_search_kernel<kFp4><<<grid, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
+        tc_search_kernel<kFp4, KM><<<grid, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
       }
       HB_LAUNCHED(ctx);
     }
-    tc_reduce_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, ctx->stream>>>(
-        nb, d_vals + b0, d_start, d_list, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k_stride);
+    if constexpr (KM > 1)
+      tc_reduce_topk_kernel<<<static_cast<unsigned>((nb + 127) / 128), 128, 0, ctx->stream>>>(
+          nb, d_vals + b0, d_start, d_list, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k, k_stride);
+    else
+      tc_reduce_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, ctx->stream>>>(
+          nb, d_vals + b0, d_start, d_list, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k_stride);
     HB_LAUNCHED(ctx);
     // the pinned plan block is reused by the next batch
     if (b0 + kTcBatch < n) HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -798,10 +960,20 @@ static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, u
   return HOMS_B200_OK;
 }
 
+uint32_t tc_max_topk() { return kTcMaxK; }
+
 int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
-                     const uint32_t* d_vals, Cand* d_out, uint32_t k_stride) {
-  return ctx->lib.x_fp4 ? tc_search_sorted_mode<true>(ctx, d_subset, n, d_keys, d_vals, d_out, k_stride)
-                        : tc_search_sorted_mode<false>(ctx, d_subset, n, d_keys, d_vals, d_out, k_stride);
+                     const uint32_t* d_vals, Cand* d_out, uint32_t k, uint32_t k_stride) {
+  HB_REQUIRE(ctx, k >= 1 && k <= uint32_t(kTcMaxK), HOMS_B200_ERR_ARGUMENT, "tensor engine: k above its top-k depth");
+  const bool f = ctx->lib.x_fp4;
+  if (k == 1)
+    return f ? tc_search_sorted_mode<true, 1>(ctx, d_subset, n, d_keys, d_vals, d_out, 1, k_stride)
+             : tc_search_sorted_mode<false, 1>(ctx, d_subset, n, d_keys, d_vals, d_out, 1, k_stride);
+  if (k <= 4)
+    return f ? tc_search_sorted_mode<true, 4>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride)
+             : tc_search_sorted_mode<false, 4>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride);
+  return f ? tc_search_sorted_mode<true, kTcMaxK>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride)
+           : tc_search_sorted_mode<false, kTcMaxK>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride);
 }
 
 // ---- tensor-pipe ceiling probe ----------------------------------------------------------------

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(params=["tensor_fp4", "tensor", "popc"])
 def ctx(hb, request):
-    """Every search test runs on all top-1 engines: tcgen05 mxf4 (e2m1), tcgen05 int8, XOR+POPC."""
+    """Every search test runs on all engines: tcgen05 mxf4 (e2m1), tcgen05 int8, XOR+POPC."""
     c = hb.Context(0)
     c.set_engine(request.param)
     c.engine_name = request.param
@@ -167,6 +167,32 @@ def test_topk_vs_port(hb, ctx, port):
         assert np.array_equal(m.raw_score, score), (tol, k)
 
 
+def test_topk_many_work_items_vs_port(hb, ctx, port):
+    """Top-k where every query tile is cut into many work items (20k rows: ~12 strips of at most 8
+    row tiles per query tile), so that the tensor engines' per-item k-lists, the published k-th-best
+    floor and the list merge are all exercised; heavy score ties (rows duplicated four times, few
+    distinct m/z values and ids).  k = 16 is the tensor engines' depth, k = 17 falls to XOR+POPC."""
+    rng = np.random.default_rng(29)
+    dim, n, nq = 256, 20000, 300
+    base = U.random_hvs(rng, n // 4, dim)
+    words = np.concatenate([base, base, base, base])
+    mz = np.round(rng.uniform(500.0, 520.0, n), 1)
+    charge = np.full(n, 2, np.uint8)
+    ids = [f"id{rng.integers(0, 50)}" for _ in range(n)]
+    qw = base[rng.integers(0, n // 4, nq)] ^ (U.random_hvs(rng, nq, dim) & U.random_hvs(rng, nq, dim)
+                                               & U.random_hvs(rng, nq, dim))
+    qmz = np.round(rng.uniform(495.0, 525.0, nq), 1)
+    qch = np.full(nq, 2, np.uint8)
+    ctx.build_index(dim, words, mz, charge, ids=ids)
+    oix = port.build_index(dim, words, mz, charge, None, ids)
+    for tol, k in ((("da", 500.0), 2), (("da", 500.0), 16), (("da", 3.0), 7), (("da", 500.0), 17)):
+        m = ctx.search_batch(qw, qmz, qch, U.product_tol(tol), k=k)
+        score, ordinal = oix.search_topk(qw, qmz, qch, tol, k)
+        assert np.array_equal(m.ordinal, ordinal), (tol, k)
+        assert np.array_equal(m.raw_score, score), (tol, k)
+    oix.close()
+
+
 def test_sharded_search_merges_to_single(hb):
     """Multi-GPU path on one device: G contexts each hold slice g of every bucket; per-shard
     candidates -> concatenate (what the all-gather yields) -> merge == unsharded result."""
@@ -183,7 +209,7 @@ def test_sharded_search_merges_to_single(hb):
     qch = rng.integers(2, 5, nq).astype(np.uint8)
     with hb.Context(0) as single:
         single.build_index(dim, words, mz, charge, ids=ids)
-        # k = 3 runs on the POPC engine, k = 1 on the tensor engine
+        # k = 3 keeps per-item k-lists in the tensor engine's drain, k = 1 is the plain top-1 path
         for tol, k in ((hb.Tolerance("dalton", 500.0), 3), (hb.Tolerance("ppm", 30.0), 3),
                        (hb.Tolerance("dalton", 500.0), 1), (hb.Tolerance("ppm", 30.0), 1)):
             want = single.search_batch(qw, qmz, qch, tol, k=k)
