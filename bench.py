@@ -368,7 +368,7 @@ def run_ours(args) -> None:
     eng_key = "tensor_fp4" if args.engine == "auto" else args.engine
     traffic, traffic_src = (ncu_traffic[eng_key] if (args.workload == "iprg2012" and world == 1 and k == 1)
                             else (None, None))
-    tensor = args.engine != "popc" and k == 1
+    tensor = args.engine != "popc" and k <= 16  # the tensor engines keep up to 16 candidates per query
     hbm_view = {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_per_launch,
                 "note": "SURVEY 8(d) algorithmic bytes (every candidate row read once per query) over the "
@@ -572,9 +572,17 @@ def run_encode(args) -> None:
                      "algorithmic_bytes_per_launch": bytes_per_spectrum * spectra_per_launch,
                      "note": "SURVEY 8(d) bytes: 16*P + 8 + D/8 compulsory + P*D/8 codebook-row gather per "
                              "spectrum; the gather (98 % of the bytes) is served by L2 (28.65 MB codebook), "
-                             "so this is an L2-gather + LOP3 bound kernel measured against the HBM line"},
+                             "so this is an L2-throughput bound kernel measured against the HBM line",
+                     "l2_view": {"achieved": peaks * (dim // 8) * spectra_per_launch / (kernel_ms * 1e-3) / 1e9
+                                 if kernel_ms > 0 else 0.0,
+                                 "peak": 6300.0 * (clocks or {}).get("sm_mhz", 1965.0) * 1e6 / 1e9, "unit": "GB/s",
+                                 "peak_source": "L2 slice throughput cap ~6300 B/clk (B300_MICROARCH.md, LTS "
+                                                "throughput cap) x the SM clock sampled during the run",
+                                 "note": "codebook-row gather bytes only"}},
         "cpu_baseline": cpu, "clocks": clocks,
     }
+    lv = line["roofline"]["l2_view"]
+    lv["frac"] = lv["achieved"] / lv["peak"] if lv["peak"] else None
     print(json.dumps(line), flush=True)
     ctx.close()
 
