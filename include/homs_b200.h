@@ -104,10 +104,11 @@ uint64_t homs_b200_ctx_launch_count(const homs_b200_ctx* ctx);
  * kernels is bracketed by CUDA events on the context's stream.  kernel_time() synchronises, returns
  * the summed duration and launch count since the last call, and resets the counters. */
 enum { HOMS_B200_KERNEL_SEARCH = 0, HOMS_B200_KERNEL_ENCODE = 1, HOMS_B200_KERNEL_PREPROCESS = 2 };
-/* Search engine for top-1 searches: POPC (XOR + POPC on the integer pipes) or a tcgen05 tensor-core
- * contraction of the +-1 expanded hypervectors (similarity = (dim + dot) / 2, exact): TENSOR with
- * int8 operands, TENSOR_FP4 with e2m1 operands and unit block scales (twice the rate, half the
- * bytes).  AUTO = TENSOR_FP4.  All engines are bit-exact; k > 1 always runs on the POPC engine.
+/* Search engine: POPC (XOR + POPC on the integer pipes) or a tcgen05 tensor-core contraction of the
+ * +-1 expanded hypervectors (similarity = (dim + dot) / 2, exact): TENSOR with int8 operands,
+ * TENSOR_FP4 with e2m1 operands and unit block scales (twice the rate, half the bytes).
+ * AUTO = TENSOR_FP4.  All engines are bit-exact.  The tensor engines keep up to 16 candidates per
+ * query (k <= 16); larger k (up to HOMS_B200_MAX_TOPK) runs on the POPC engine.
  * Set it BEFORE library_upload: the tensor image of the library (8x / 4x the packed size) is built
  * there for the selected engine, and POPC skips it. */
 enum {
