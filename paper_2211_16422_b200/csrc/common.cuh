@@ -114,9 +114,6 @@ struct homs_b200_ctx {
   int engine = HOMS_B200_ENGINE_AUTO;  // homs_b200_ctx_set_engine
   void* pinned = nullptr;  // small pinned staging block
   size_t pinned_cap = 0;
-  void* pinned_plan = nullptr;  // pinned block of the tensor engine's host planner
-  size_t pinned_plan_cap = 0;
-  cudaEvent_t plan_event = nullptr;  // host planner waits on this instead of the whole stream
   // chunked host <-> device pipeline of the encoder (encode.cu:encode_pipeline): copy-in and
   // copy-out streams beside the compute stream, per-slot events, created on first use
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
@@ -177,7 +174,6 @@ struct KernelTimer {
 
 int ensure(homs_b200_ctx* ctx, DevBuf& b, size_t bytes);
 int ensure_pinned(homs_b200_ctx* ctx, size_t bytes);
-int ensure_pinned_plan(homs_b200_ctx* ctx, size_t bytes);
 void release(DevBuf& b);
 
 // scratch slot names

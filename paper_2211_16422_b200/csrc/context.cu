@@ -55,19 +55,6 @@ int ensure_pinned(homs_b200_ctx* ctx, size_t bytes) {
   return HOMS_B200_OK;
 }
 
-int ensure_pinned_plan(homs_b200_ctx* ctx, size_t bytes) {
-  if (ctx->pinned_plan_cap >= bytes) return HOMS_B200_OK;
-  if (ctx->pinned_plan) {
-    HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    cudaFreeHost(ctx->pinned_plan);
-    ctx->pinned_plan = nullptr;
-    ctx->pinned_plan_cap = 0;
-  }
-  const size_t want = std::max<size_t>(bytes * 2, 1 << 20);
-  HB_CUDA(ctx, cudaMallocHost(&ctx->pinned_plan, want));
-  ctx->pinned_plan_cap = want;
-  return HOMS_B200_OK;
-}
 
 int upload_rows(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* h_src, uint64_t n, uint32_t W,
                 uint32_t S) {
@@ -159,8 +146,6 @@ void homs_b200_ctx_destroy(homs_b200_ctx* ctx) {
                     &ctx->q.d_words, &ctx->q.d_mz, &ctx->q.d_charge})
     release(*b);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
-  if (ctx->pinned_plan) cudaFreeHost(ctx->pinned_plan);
-  if (ctx->plan_event) cudaEventDestroy(ctx->plan_event);
   for (int i = 0; i < 2; ++i)
     for (cudaEvent_t e : {ctx->pipe_in_ready[i], ctx->pipe_done[i], ctx->pipe_out_free[i]})
       if (e) cudaEventDestroy(e);

@@ -1,4 +1,4 @@
-// Tensor-core engine of the windowed Hamming top-1 search (sm_100a: tcgen05 + TMEM + bulk copies).
+// Tensor-core engine of the windowed Hamming top-k search (k <= 16) (sm_100a: tcgen05 + TMEM + bulk copies).
 //
 // Reference semantics are those of search.cu (search.cpp:93-169): per query the candidate row with
 // the largest Hamming similarity inside its precursor window, ties broken by (|q - r|, id, ordinal).
@@ -27,8 +27,9 @@
 //   thread keeps the running best of its query with the exact 3-level key and masks columns
 //   outside the query's own window.  The drain (256 columns) costs ~2 % of the 64-stage K loop
 //   at D = 8192 and overlaps with the next tile's MMAs.
-// * work items (query tile x strip of row tiles) are planned on the host from 8 bytes per query
-//   tile and ordered so that CTAs running at the same time share both query and row tiles in L2.
+// * work items (query tile x strip of row tiles) are planned on the device (tc_plan_*_kernel) and
+//   ordered so that CTAs running at the same time share both query and row tiles in L2; the whole
+//   search is stream-ordered, without a host round trip.
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -86,8 +87,7 @@ struct TcParams {
   uint32_t n_kc;
   uint32_t dim;
   const TcItem* items;
-  uint32_t n_items;
-  uint32_t pad;
+  const uint32_t* n_items;  // device: number of work items (written by the planner)
   const uint64_t* keys;  // sorted (local first row << 32 | local last row), batch base applied
   const uint32_t* vals;  // sorted slot ids
   const uint32_t* subset;
@@ -336,6 +336,180 @@ __global__ void tc_tile_ranges_kernel(uint64_t n, const uint64_t* __restrict__ k
   if (lane == 0) ranges[tile] = (lo == kNone || hi <= lo) ? make_uint2(0, 0) : make_uint2(lo, hi);
 }
 
+// ---- device planner ---------------------------------------------------------------------------
+// Work items = (query tile, strip of row tiles).  Strips sit at absolute multiples of `strip` row
+// tiles so that different query tiles fetch identical blocks; items are ordered (query-tile group,
+// strip, tile) and kept short (<= max_strip row tiles, about items_per_sm items per SM) so that the
+// CTAs running at the same time stay in step and share both operands in L2 (ncu: DRAM 261 GB ->
+// 30 GB per launch on config 2).  Planning on the device keeps the whole search stream-ordered:
+// no host round trip between the window bounds and the search kernel.
+
+struct TcPlanHead {
+  uint32_t n_items, strip, n_pairs, n_groups;
+};
+struct TcPlanCfg {
+  uint32_t n_tiles, group_tiles, max_strip, tiles_total;
+  uint64_t target_items;  // items the planner aims for (SM count x items per SM)
+  uint32_t item_cap;      // capacity of the item / partial arrays
+  uint32_t pad;
+};
+// plan block layout (uint32 units after the head): see tc_plan_layout()
+struct TcPlanPtrs {
+  TcPlanHead* head;
+  TcItem* items;
+  uint32_t *tile_start, *tile_items, *tlo, *thi, *grp_item_base, *grp_pair_base, *grp_lo_strip;
+};
+static __host__ __device__ inline size_t tc_plan_bytes(uint32_t n_tiles, uint32_t item_cap) {
+  return 64 + size_t(item_cap) * (sizeof(TcItem) + 4) + (size_t(n_tiles) * 6 + 8) * 4;
+}
+static __host__ __device__ inline TcPlanPtrs tc_plan_layout(void* base, uint32_t n_tiles, uint32_t item_cap) {
+  TcPlanPtrs q;
+  auto* b = static_cast<unsigned char*>(base);
+  q.head = reinterpret_cast<TcPlanHead*>(b);
+  q.items = reinterpret_cast<TcItem*>(b + 64);
+  q.tile_items = reinterpret_cast<uint32_t*>(q.items + item_cap);
+  q.tile_start = q.tile_items + item_cap;   // n_tiles + 1
+  q.tlo = q.tile_start + n_tiles + 1;       // n_tiles
+  q.thi = q.tlo + n_tiles;                  // n_tiles
+  q.grp_item_base = q.thi + n_tiles;        // <= n_tiles + 1
+  q.grp_pair_base = q.grp_item_base + n_tiles + 1;
+  q.grp_lo_strip = q.grp_pair_base + n_tiles + 1;  // <= n_tiles
+  return q;
+}
+
+constexpr int kTcPlanThreads = 512;  // >= query tiles per planning batch (kTcBatch / kTcM)
+
+template <uint32_t kN>
+__global__ void __launch_bounds__(kTcPlanThreads) tc_plan_head_kernel(TcPlanCfg c, const uint2* __restrict__ ranges,
+                                                                      void* plan) {
+  const TcPlanPtrs q = tc_plan_layout(plan, c.n_tiles, c.item_cap);
+  __shared__ uint32_t s_scan[kTcPlanThreads];
+  __shared__ unsigned long long s_work;
+  __shared__ uint32_t s_strip;
+  const uint32_t t = threadIdx.x;
+  uint32_t lo = 0, hi = 0;
+  if (t < c.n_tiles) {
+    const uint2 r = ranges[t];
+    lo = r.x / kN;
+    hi = r.y > r.x ? (r.y + kN - 1) / kN : lo;
+    q.tlo[t] = lo;
+    q.thi[t] = hi;
+  }
+  if (t == 0) s_work = 0;
+  __syncthreads();
+  if (hi > lo) atomicAdd(&s_work, static_cast<unsigned long long>(hi - lo));
+  __syncthreads();
+  if (t == 0) {
+    const uint64_t work = s_work;
+    uint64_t strip = (work + c.target_items - 1) / c.target_items;
+    strip = strip < 1 ? 1 : (strip > c.max_strip ? c.max_strip : strip);
+    // never more items than the arrays hold: items <= work / strip + 2 * n_tiles
+    const uint64_t slack = 2ull * c.n_tiles + 16;
+    const uint64_t fit = c.item_cap > slack ? (work + (c.item_cap - slack) - 1) / (c.item_cap - slack)
+                                            : uint64_t(c.tiles_total) + 1;
+    if (fit > strip) strip = fit;
+    s_strip = static_cast<uint32_t>(strip < 0xffffffffull ? strip : 0xffffffffull);
+  }
+  __syncthreads();
+  const uint32_t strip = s_strip;
+  const uint32_t ns = hi > lo ? (hi + strip - 1) / strip - lo / strip : 0;  // strips this tile overlaps
+  // exclusive scan of ns over the tiles (Hillis-Steele in shared memory; 512 entries)
+  s_scan[t] = ns;
+  __syncthreads();
+  for (uint32_t o = 1; o < kTcPlanThreads; o <<= 1) {
+    const uint32_t v = t >= o ? s_scan[t - o] : 0;
+    __syncthreads();
+    s_scan[t] += v;
+    __syncthreads();
+  }
+  if (t < c.n_tiles) q.tile_start[t] = s_scan[t] - ns;
+  if (t == c.n_tiles - 1) q.tile_start[c.n_tiles] = s_scan[t];
+  // groups of consecutive query tiles
+  const uint32_t n_groups = (c.n_tiles + c.group_tiles - 1) / c.group_tiles;
+  __syncthreads();
+  uint32_t g_items = 0, g_pairs = 0, g_lo_strip = 0;
+  if (t < n_groups) {
+    const uint32_t t0 = t * c.group_tiles, t1 = min(c.n_tiles, t0 + c.group_tiles);
+    uint32_t glo = 0xffffffffu, ghi = 0;
+    for (uint32_t j = t0; j < t1; ++j) {
+      const uint32_t a = q.tlo[j], b = q.thi[j];
+      if (b > a) {
+        glo = min(glo, a);
+        ghi = max(ghi, b);
+        g_items += (b + strip - 1) / strip - a / strip;
+      }
+    }
+    if (glo != 0xffffffffu) {
+      g_lo_strip = glo / strip;
+      g_pairs = (ghi + strip - 1) / strip - g_lo_strip;
+    }
+    q.grp_lo_strip[t] = g_lo_strip;
+  }
+  // exclusive scans over the groups (reuse the scan buffer twice)
+  s_scan[t] = g_items;
+  __syncthreads();
+  for (uint32_t o = 1; o < kTcPlanThreads; o <<= 1) {
+    const uint32_t v = t >= o ? s_scan[t - o] : 0;
+    __syncthreads();
+    s_scan[t] += v;
+    __syncthreads();
+  }
+  if (t < n_groups) q.grp_item_base[t] = s_scan[t] - g_items;
+  const uint32_t total_items = s_scan[kTcPlanThreads - 1];
+  __syncthreads();
+  s_scan[t] = g_pairs;
+  __syncthreads();
+  for (uint32_t o = 1; o < kTcPlanThreads; o <<= 1) {
+    const uint32_t v = t >= o ? s_scan[t - o] : 0;
+    __syncthreads();
+    s_scan[t] += v;
+    __syncthreads();
+  }
+  if (t < n_groups) q.grp_pair_base[t] = s_scan[t] - g_pairs;
+  if (t == 0) {
+    q.grp_item_base[n_groups] = total_items;
+    q.grp_pair_base[n_groups] = s_scan[kTcPlanThreads - 1];
+    q.head->n_items = total_items;
+    q.head->strip = strip;
+    q.head->n_pairs = s_scan[kTcPlanThreads - 1];
+    q.head->n_groups = n_groups;
+  }
+}
+
+// one thread per (group, strip) pair: its items, in tile order, and the per-tile item lists
+template <uint32_t kN>
+__global__ void tc_plan_items_kernel(TcPlanCfg c, void* plan) {
+  const TcPlanPtrs q = tc_plan_layout(plan, c.n_tiles, c.item_cap);
+  const uint32_t n_pairs = q.head->n_pairs, n_groups = q.head->n_groups, strip = q.head->strip;
+  for (uint32_t pr = blockIdx.x * blockDim.x + threadIdx.x; pr < n_pairs; pr += gridDim.x * blockDim.x) {
+    uint32_t g = 0, gh = n_groups;  // last group whose pair base is <= pr
+    while (gh - g > 1) {
+      const uint32_t mid = (g + gh) >> 1;
+      if (q.grp_pair_base[mid] <= pr) g = mid;
+      else gh = mid;
+    }
+    const uint32_t sidx = q.grp_lo_strip[g] + (pr - q.grp_pair_base[g]);
+    const uint32_t t0 = g * c.group_tiles, t1 = min(c.n_tiles, t0 + c.group_tiles);
+    // items of this group that come before strip sidx: per tile, its strips below sidx
+    uint32_t idx = q.grp_item_base[g];
+    for (uint32_t j = t0; j < t1; ++j) {
+      const uint32_t a = q.tlo[j], b = q.thi[j];
+      if (b <= a) continue;
+      const uint32_t first = a / strip, cnt = (b + strip - 1) / strip - first;
+      idx += sidx > first ? min(sidx - first, cnt) : 0;
+    }
+    const uint64_t s_lo = uint64_t(sidx) * strip, s_hi = s_lo + strip;
+    for (uint32_t j = t0; j < t1; ++j) {
+      const uint32_t tl = q.tlo[j], th = q.thi[j];
+      const uint64_t a = max(uint64_t(tl), s_lo), b = min(uint64_t(th), s_hi);
+      if (b <= a) continue;
+      q.items[idx] = TcItem{j, static_cast<uint32_t>(a) * kN, static_cast<uint32_t>(b) * kN, 0};
+      q.tile_items[q.tile_start[j] + (sidx - tl / strip)] = idx;
+      ++idx;
+    }
+  }
+}
+
 // ---- the search kernel ----------------------------------------------------------------------
 
 __device__ __forceinline__ bool key_less(uint64_t ad1, uint32_t rk1, uint64_t ad2, uint32_t rk2) {
@@ -477,12 +651,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   }
 
   const uint32_t n_kc = p.n_kc;
+  const uint32_t n_items = __ldg(p.n_items);
 
   if (warp == 0) {
     // ===== producer: two bulk copies per stage =====
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
         const TcItem it = p.items[item];
         const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
         const uint8_t* a_src = p.q_x + uint64_t(it.tile) * kTcM * kTcKB;
@@ -506,7 +681,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     // ===== MMA issuer: one thread =====
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;  // aphase: one parity bit per accumulator
-      for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
         const TcItem it = p.items[item];
         const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
         for (uint32_t nt = 0; nt < n_nt; ++nt) {
@@ -551,7 +726,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     const int qrow = quarter * 32 + lane;
     constexpr int kChunks = (kN + 31) / 32;
     uint32_t acc = 0, tphase = 0;
-    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+    for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const TcItem it = p.items[item];
       const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
       const uint64_t pos = uint64_t(it.tile) * kTcM + qrow;
@@ -829,133 +1004,82 @@ static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, u
     const uint32_t n_tiles = static_cast<uint32_t>((nb + kTcM - 1) / kTcM);
     const uint64_t q_rows = uint64_t(n_tiles) * kTcM;
 
-    // 1. union window of every query tile -> host (the event lets the host plan while the
-    //    query expansion of step 2 is still running)
+    // 1. union window of every query tile
     HB_TRY(ensure(ctx, ctx->scratch[kScrTcTiles], size_t(n_tiles) * sizeof(uint2)));
     auto* d_ranges = ctx->scratch[kScrTcTiles].as<uint2>();
     tc_tile_ranges_kernel<<<(n_tiles * 32 + 255) / 256, 256, 0, ctx->stream>>>(nb, d_keys + b0, n_tiles, d_ranges);
     HB_LAUNCHED(ctx);
-    HB_TRY(ensure_pinned_plan(ctx, size_t(n_tiles) * sizeof(uint2)));
-    HB_CUDA(ctx, cudaMemcpyAsync(ctx->pinned_plan, d_ranges, size_t(n_tiles) * sizeof(uint2), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
-    if (!ctx->plan_event) HB_CUDA(ctx, cudaEventCreateWithFlags(&ctx->plan_event, cudaEventDisableTiming));
-    HB_CUDA(ctx, cudaEventRecord(ctx->plan_event, ctx->stream));
-    // 2. expand the batch's queries in sorted order
+
+    // 2. plan on the device (see the planner above).  Capacity of the item arrays from what the
+    //    host knows: every tile's window is at most the whole local library.
+    TcPlanCfg pc;
+    pc.n_tiles = n_tiles;
+    pc.group_tiles = kTcGroupTiles;
+    pc.max_strip = 8;
+    uint32_t items_per_sm = 400;  // env: development knobs
+    if (const char* e = getenv("HOMS_B200_TC_GROUP")) pc.group_tiles = std::max(1, atoi(e));
+    if (const char* e = getenv("HOMS_B200_TC_ITEMS_PER_SM")) items_per_sm = std::max(1, atoi(e));
+    if (const char* e = getenv("HOMS_B200_TC_MAX_STRIP")) pc.max_strip = std::max(1, atoi(e));
+    pc.tiles_total = static_cast<uint32_t>((lib.n_local + kN - 1) / kN + 1);
+    pc.target_items = uint64_t(ctx->sm_count) * items_per_sm;
+    const uint64_t slack = 2ull * n_tiles + 16;
+    const uint64_t by_shape =
+        std::max<uint64_t>(pc.target_items, (uint64_t(n_tiles) * pc.tiles_total + pc.max_strip - 1) / pc.max_strip) + slack;
+    const uint64_t by_memory = std::max<uint64_t>((4ull << 30) / (size_t(kTcM) * k * sizeof(Cand)), slack + 4ull * ctx->sm_count);
+    pc.item_cap = static_cast<uint32_t>(std::min<uint64_t>(std::min(by_shape, by_memory), 0x7fffffffull));
+    pc.pad = 0;
+    HB_TRY(ensure(ctx, ctx->scratch[kScrTcPlan], tc_plan_bytes(n_tiles, pc.item_cap)));
+    void* d_plan = ctx->scratch[kScrTcPlan].p;
+    const TcPlanPtrs pp = tc_plan_layout(d_plan, n_tiles, pc.item_cap);
+    static_assert(kTcBatch / kTcM <= kTcPlanThreads, "one planner thread per query tile");
+    tc_plan_head_kernel<kN><<<1, kTcPlanThreads, 0, ctx->stream>>>(pc, d_ranges, d_plan);
+    HB_LAUNCHED(ctx);
+    tc_plan_items_kernel<kN><<<ctx->sm_count, 256, 0, ctx->stream>>>(pc, d_plan);
+    HB_LAUNCHED(ctx);
+
+    // 3. expand the batch's queries in sorted order
     HB_TRY(ensure(ctx, ctx->scratch[kScrTcQx], size_t(lib.n_kc) * q_rows * kTcKB));
     HB_TRY(expand_launch<kFp4>(ctx, q_rows, nb, d_vals, d_subset, b0, q.d_words.as<uint64_t>(), q_stride, q.dim,
                                lib.n_kc, ctx->scratch[kScrTcQx].as<uint8_t>()));
-    HB_CUDA(ctx, cudaEventSynchronize(ctx->plan_event));
-
-    // 3. plan: strips of row tiles at absolute multiples of `strip` tiles; items ordered
-    //    (query-tile group, strip, tile) so that concurrently running CTAs share operands in L2.
-    //    Short strips (<= 8 row tiles, about 400 items per SM on config 2) keep co-running CTAs in
-    //    step, which is what makes the L2 sharing work (ncu: DRAM 261 GB -> 30 GB per launch).
-    uint32_t group_tiles = kTcGroupTiles, items_per_sm = 400, max_strip = 8;  // env: development knobs
-    if (const char* e = getenv("HOMS_B200_TC_GROUP")) group_tiles = std::max(1, atoi(e));
-    if (const char* e = getenv("HOMS_B200_TC_ITEMS_PER_SM")) items_per_sm = std::max(1, atoi(e));
-    if (const char* e = getenv("HOMS_B200_TC_MAX_STRIP")) max_strip = std::max(1, atoi(e));
-    std::vector<uint32_t> t_lo(n_tiles), t_hi(n_tiles);  // in row tiles of kN rows
-    uint64_t work = 0;
-    {
-      const auto* h_ranges = static_cast<const uint2*>(ctx->pinned_plan);
-      for (uint32_t t = 0; t < n_tiles; ++t) {
-        t_lo[t] = h_ranges[t].x / kN;
-        t_hi[t] = h_ranges[t].y > h_ranges[t].x ? (h_ranges[t].y + kN - 1) / kN : t_lo[t];
-        work += t_hi[t] - t_lo[t];
-      }
-    }
-    const uint64_t target = uint64_t(ctx->sm_count) * items_per_sm;
-    const uint32_t strip = static_cast<uint32_t>(
-        std::min<uint64_t>(max_strip, std::max<uint64_t>(1, (work + target - 1) / target)));
-    std::vector<TcItem> items;
-    items.reserve(work / strip + 2 * size_t(n_tiles) + 16);
-    std::vector<uint32_t> tile_count(n_tiles + 1, 0);
-    for (uint32_t g0 = 0; g0 < n_tiles; g0 += group_tiles) {
-      const uint32_t g1 = std::min(n_tiles, g0 + group_tiles);
-      uint32_t lo = ~0u, hi = 0;
-      for (uint32_t t = g0; t < g1; ++t)
-        if (t_hi[t] > t_lo[t]) {
-          lo = std::min(lo, t_lo[t]);
-          hi = std::max(hi, t_hi[t]);
-        }
-      if (lo == ~0u) continue;
-      for (uint32_t s = lo / strip; s * uint64_t(strip) < hi; ++s)
-        for (uint32_t t = g0; t < g1; ++t) {
-          const uint32_t a = std::max<uint32_t>(t_lo[t], s * strip);
-          const uint32_t b = std::min<uint64_t>(t_hi[t], (uint64_t(s) + 1) * strip);
-          if (b <= a) continue;
-          ++tile_count[t];
-          items.push_back(TcItem{t, a * kN, b * kN, 0});
-        }
-    }
-    const uint32_t n_items = static_cast<uint32_t>(items.size());
-    const size_t plan_cap_items = n_items;
-    // pinned layout: items | per-tile CSR start | per-tile item list
-    const size_t pinned_bytes = plan_cap_items * (sizeof(TcItem) + 4) + (size_t(n_tiles) + 1) * 4 + 64;
-    HB_TRY(ensure_pinned_plan(ctx, pinned_bytes));
-    auto* h_items = static_cast<TcItem*>(ctx->pinned_plan);
-    auto* h_start = reinterpret_cast<uint32_t*>(h_items + plan_cap_items);
-    auto* h_list = h_start + n_tiles + 1;
-    if (n_items) std::memcpy(h_items, items.data(), size_t(n_items) * sizeof(TcItem));
-    uint32_t cursor = 0;
-    for (uint32_t t = 0; t < n_tiles; ++t) {
-      h_start[t] = cursor;
-      cursor += tile_count[t];
-      tile_count[t] = h_start[t];  // becomes the fill cursor of tile t
-    }
-    h_start[n_tiles] = cursor;
-    for (uint32_t i = 0; i < n_items; ++i) h_list[tile_count[items[i].tile]++] = i;
-
-    const size_t plan_bytes = plan_cap_items * (sizeof(TcItem) + 4) + (size_t(n_tiles) + 1) * 4;
-    HB_TRY(ensure(ctx, ctx->scratch[kScrTcPlan], plan_bytes));
-    auto* d_items = ctx->scratch[kScrTcPlan].as<TcItem>();
-    auto* d_start = reinterpret_cast<uint32_t*>(d_items + plan_cap_items);
-    auto* d_list = d_start + n_tiles + 1;
-    HB_CUDA(ctx, cudaMemcpyAsync(d_items, h_items, plan_bytes, cudaMemcpyHostToDevice, ctx->stream));
-    HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], std::max<size_t>(1, n_items) * kTcM * k * sizeof(Cand)));
+    HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], size_t(pc.item_cap) * kTcM * k * sizeof(Cand)));
     HB_TRY(ensure(ctx, ctx->scratch[kScrTcBest], q_rows * k * sizeof(int)));
     // every byte 0x80: a dot no candidate can be below
     HB_CUDA(ctx, cudaMemsetAsync(ctx->scratch[kScrTcBest].p, 0x80, q_rows * k * sizeof(int), ctx->stream));
 
     // 4. search + reduce
-    if (n_items > 0) {
-      TcParams tp;
-      tp.lib_x = lib.d_x.as<uint8_t>();
-      tp.q_x = ctx->scratch[kScrTcQx].as<uint8_t>();
-      tp.lib_rows = lib.x_rows;
-      tp.q_rows = q_rows;
-      tp.n_kc = lib.n_kc;
-      tp.dim = lib.dim;
-      tp.items = d_items;
-      tp.n_items = n_items;
-      tp.pad = 0;
-      tp.keys = d_keys + b0;
-      tp.vals = d_vals + b0;
-      tp.subset = d_subset;
-      tp.q_mz = q.d_mz.as<double>();
-      tp.lib_mz = lib.d_mz_local.as<double>();
-      tp.lib_rank = lib.d_id_rank_local.as<uint32_t>();
-      tp.n = nb;
-      tp.partial = ctx->scratch[kScrTcPartial].as<Cand>();
-      tp.gbest = ctx->scratch[kScrTcBest].as<int>();
-      tp.k = k;
-      tp.pad2 = 0;
-      const int grid = static_cast<int>(std::min<uint32_t>(n_items, static_cast<uint32_t>(ctx->sm_count)));
-      {
-        KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
-        tc_search_kernel<kFp4, KM><<<grid, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
-      }
-      HB_LAUNCHED(ctx);
+    TcParams tp;
+    tp.lib_x = lib.d_x.as<uint8_t>();
+    tp.q_x = ctx->scratch[kScrTcQx].as<uint8_t>();
+    tp.lib_rows = lib.x_rows;
+    tp.q_rows = q_rows;
+    tp.n_kc = lib.n_kc;
+    tp.dim = lib.dim;
+    tp.items = pp.items;
+    tp.n_items = &pp.head->n_items;
+    tp.keys = d_keys + b0;
+    tp.vals = d_vals + b0;
+    tp.subset = d_subset;
+    tp.q_mz = q.d_mz.as<double>();
+    tp.lib_mz = lib.d_mz_local.as<double>();
+    tp.lib_rank = lib.d_id_rank_local.as<uint32_t>();
+    tp.n = nb;
+    tp.partial = ctx->scratch[kScrTcPartial].as<Cand>();
+    tp.gbest = ctx->scratch[kScrTcBest].as<int>();
+    tp.k = k;
+    tp.pad2 = 0;
+    {
+      KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
+      tc_search_kernel<kFp4, KM><<<ctx->sm_count, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
     }
+    HB_LAUNCHED(ctx);
     if constexpr (KM > 1)
       tc_reduce_topk_kernel<<<static_cast<unsigned>((nb + 127) / 128), 128, 0, ctx->stream>>>(
-          nb, d_vals + b0, d_start, d_list, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k, k_stride);
+          nb, d_vals + b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k, k_stride);
     else
       tc_reduce_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, ctx->stream>>>(
-          nb, d_vals + b0, d_start, d_list, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k_stride);
+          nb, d_vals + b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k_stride);
     HB_LAUNCHED(ctx);
-    // the pinned plan block is reused by the next batch
-    if (b0 + kTcBatch < n) HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    // the next batch reuses the plan / operand / partial blocks: stream order keeps that safe
   }
   return HOMS_B200_OK;
 }
