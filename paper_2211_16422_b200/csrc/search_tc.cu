@@ -906,17 +906,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   }
 }
 
-// per sorted position: minimum over the items of its query tile
-__global__ void tc_reduce_kernel(uint64_t n, const uint32_t* __restrict__ vals,
-                                 const uint32_t* __restrict__ tile_item_start,
-                                 const uint32_t* __restrict__ tile_items, const Cand* __restrict__ partial,
-                                 Cand* __restrict__ out, uint32_t k_stride) {
-  const uint64_t pos = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (pos >= n) return;
-  const uint32_t t = static_cast<uint32_t>(pos / kTcM), r = static_cast<uint32_t>(pos % kTcM);
+// per sorted position: minimum over the items of its query tile.  One CTA per query tile,
+// 128 positions x 8 item slices (a tile has a few hundred items), then a shared-memory fold.
+constexpr int kTcReduceSlices = 8;
+__global__ void __launch_bounds__(kTcM * kTcReduceSlices)
+tc_reduce_kernel(uint64_t n, const uint32_t* __restrict__ vals, const uint32_t* __restrict__ tile_item_start,
+                 const uint32_t* __restrict__ tile_items, const Cand* __restrict__ partial,
+                 Cand* __restrict__ out, uint32_t k_stride) {
+  __shared__ Cand s_best[kTcReduceSlices][kTcM];
+  const uint32_t t = blockIdx.x, r = threadIdx.x, slice = threadIdx.y;
   Cand best{kNone, kNone, ~0ull};
-  for (uint32_t i = tile_item_start[t]; i < tile_item_start[t + 1]; ++i) {
+  for (uint32_t i = tile_item_start[t] + slice; i < tile_item_start[t + 1]; i += kTcReduceSlices) {
     const Cand c = partial[uint64_t(tile_items[i]) * kTcM + r];
+    if (c.d != best.d ? c.d < best.d : key_less(c.ad, c.rk, best.ad, best.rk)) best = c;
+  }
+  s_best[slice][r] = best;
+  __syncthreads();
+  const uint64_t pos = uint64_t(t) * kTcM + r;
+  if (slice != 0 || pos >= n) return;
+  for (int sl = 1; sl < kTcReduceSlices; ++sl) {
+    const Cand c = s_best[sl][r];
     if (c.d != best.d ? c.d < best.d : key_less(c.ad, c.rk, best.ad, best.rk)) best = c;
   }
   out[uint64_t(vals[pos]) * k_stride] = best;
@@ -1076,7 +1085,7 @@ static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, u
       tc_reduce_topk_kernel<<<static_cast<unsigned>((nb + 127) / 128), 128, 0, ctx->stream>>>(
           nb, d_vals + b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k, k_stride);
     else
-      tc_reduce_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, ctx->stream>>>(
+      tc_reduce_kernel<<<n_tiles, dim3(kTcM, kTcReduceSlices), 0, ctx->stream>>>(
           nb, d_vals + b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k_stride);
     HB_LAUNCHED(ctx);
     // the next batch reuses the plan / operand / partial blocks: stream order keeps that safe
