@@ -157,7 +157,12 @@ int homs_b200_codebook_upload(homs_b200_ctx* ctx, uint32_t dim, uint32_t n_bins,
 /* encode_spectra, src/pipeline.cpp:60-85: refine_peaks -> vectorize -> encode per spectrum.
  * out_ok[i] = 1 and row i of out_words holds the hypervector when spectrum i is processable,
  * else out_ok[i] = 0 and the row is zero (the reference drops such spectra; the C++ facade
- * compacts).  HOMS_B200_ERR_INVARIANT when homs_b200_dimension(cfg) != uploaded n_bins. */
+ * compacts).  HOMS_B200_ERR_INVARIANT when homs_b200_dimension(cfg) != uploaded n_bins, and --
+ * as quantize_intensity throws out of the reference's encode_spectra (src/encoder.cpp:12-14) --
+ * when a kept peak's normalised intensity is outside [0, 1] (an infinite intensity: inf / inf).
+ * The _dev form cannot fail late: it marks such a spectrum with
+ * d_out_ok[i] = HOMS_B200_OK_FLAG_INVARIANT and a zero row, for the caller to act on. */
+#define HOMS_B200_OK_FLAG_INVARIANT 2
 int homs_b200_encode_batch(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint64_t n,
                            const uint64_t* offsets, const double* mz, const double* intensity,
                            uint64_t* out_words, uint8_t* out_ok);

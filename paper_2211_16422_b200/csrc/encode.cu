@@ -26,6 +26,10 @@ namespace hb {
 // K1: refine_peaks + vectorize + quantize_intensity
 // ------------------------------------------------------------------------------------------
 
+// out_count marker of a spectrum on which the reference would throw InvariantError (a normalised
+// intensity outside [0, 1]); encode_kernel turns it into ok flag HOMS_B200_OK_FLAG_INVARIANT
+constexpr uint32_t kInvalidCount = 0xFFFFFFFFu;
+
 struct PreParams {
   double min_mz, max_mz, bin_size, intensity_floor;
   uint32_t max_peaks, min_peaks, scaling, dims, levels;
@@ -166,9 +170,14 @@ preprocess_kernel(PreParams p, uint64_t n, const uint64_t* __restrict__ offsets,
     double top = 0.0;
     for (uint32_t k = lane; k < nb; k += 32) top = fmax(top, o_val[k]);
     top = warp_max(top);
-    for (uint32_t k = lane; k < nb; k += 32)
-      out_levels[spec * MP + k] = quantize_level(o_val[k] / top, p.levels);
-    if (lane == 0) out_count[spec] = nb;
+    bool bad = false;  // encoder.cpp:12-14: quantize_intensity throws outside [0, 1] (inf / inf = NaN)
+    for (uint32_t k = lane; k < nb; k += 32) {
+      const double v = o_val[k] / top;
+      bad |= !(v >= 0.0 && v <= 1.0);
+      out_levels[spec * MP + k] = quantize_level(v, p.levels);
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) out_count[spec] = bad ? kInvalidCount : nb;
     __syncwarp();
   }
 }
@@ -234,9 +243,9 @@ encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stri
       nb = sv_count[spec];
     }
     uint64_t* out_row = out_words + spec * W;
-    if (nb == 0) {  // unprocessable: zero row (pipeline.cpp:68 `continue`)
+    if (nb == 0 || nb == kInvalidCount) {  // unprocessable: zero row (pipeline.cpp:68 `continue`)
       for (uint32_t w = lane; w < W; w += 32) out_row[w] = 0;
-      if (lane == 0 && out_ok) out_ok[spec] = 0;
+      if (lane == 0 && out_ok) out_ok[spec] = nb == 0 ? 0 : HOMS_B200_OK_FLAG_INVARIANT;
       continue;
     }
     const uint32_t thresh = nb / 2 + 1;  // 2*votes > n  <=>  votes >= floor(n/2)+1  (encoder.cpp:52)
@@ -610,6 +619,10 @@ int encode_pipeline(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, 
   HB_CUDA(ctx, cudaStreamSynchronize(in));
   HB_CUDA(ctx, cudaStreamSynchronize(cs));
   HB_CUDA(ctx, cudaStreamSynchronize(out));
+  if (h_ok)  // the reference's encode_spectra lets quantize_intensity's exception escape (pipeline.cpp:67-72)
+    for (uint64_t i = 0; i < n; ++i)
+      HB_REQUIRE(ctx, h_ok[i] != HOMS_B200_OK_FLAG_INVARIANT, HOMS_B200_ERR_INVARIANT,
+                 "quantize_intensity: intensity outside [0, 1]");
   return HOMS_B200_OK;
 }
 
@@ -708,6 +721,9 @@ int homs_b200_preprocess_batch(homs_b200_ctx* ctx, const homs_b200_preprocess_co
   HB_CUDA(ctx, cudaMemcpyAsync(out_levels, d_lev, sv, cudaMemcpyDeviceToHost, ctx->stream));
   HB_CUDA(ctx, cudaMemcpyAsync(out_count, d_cnt, size_t(n) * 4, cudaMemcpyDeviceToHost, ctx->stream));
   HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  for (uint64_t i = 0; i < n; ++i)
+    HB_REQUIRE(ctx, out_count[i] != kInvalidCount, HOMS_B200_ERR_INVARIANT,
+               "quantize_intensity: intensity outside [0, 1]");
   return HOMS_B200_OK;
 }
 

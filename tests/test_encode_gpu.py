@@ -87,6 +87,49 @@ def test_encode_errors(hb, ctx):
     assert words.shape[0] == 0
 
 
+def test_non_finite_peaks(hb, ctx, best_oracle):
+    """NaN m/z or intensity never passes the range / positivity filter (preprocess.cpp:45-49) and is
+    dropped silently; an INFINITE kept intensity normalises to inf / inf = NaN, on which
+    quantize_intensity throws out of the reference's encode_spectra (encoder.cpp:12-14,
+    pipeline.cpp:67-72) -- the product reports the same InvariantError."""
+    from oracle.binding import OracleError
+    pre, opre = hb.PreprocessConfig(), PreCfg()
+    dim = 1024
+    cb = _upload(hb, ctx, dim, dim // 2, 16, 1, hb.dimension(pre))
+    ocb = best_oracle.codebook_from_words(dim, 16, cb.position, cb.level)
+    rng = np.random.default_rng(3)
+    base_mz = np.sort(rng.choice(np.arange(20000, 120000), 16, replace=False)) * 0.01
+    base_it = rng.uniform(0.1, 1.0, 16)
+    with_nan = (base_mz.copy(), base_it.copy())
+    with_nan[0][3] = np.nan
+    with_nan[1][7] = np.nan
+    off, mz, it = U.csr([(base_mz, base_it), with_nan, (base_mz[:11], base_it[:11])])
+    words, ok = ctx.encode_batch(off, mz, it, pre)
+    ow, ook = best_oracle.encode_spectra(ocb, opre, off, mz, it)
+    assert ok.all() and np.array_equal(ok, ook) and np.array_equal(words, ow)
+
+    # min_peaks (10) infinite peaks survive their own floor; each normalises to inf / inf
+    with_inf = (base_mz.copy(), base_it.copy())
+    with_inf[1][2:14] = np.inf
+    off, mz, it = U.csr([(base_mz, base_it), with_inf])
+    with pytest.raises(OracleError, match="outside"):
+        best_oracle.encode_spectra(ocb, opre, off, mz, it)
+    with pytest.raises(hb.InvariantError, match="quantize_intensity"):
+        ctx.encode_batch(off, mz, it, pre)
+    with pytest.raises(hb.InvariantError, match="quantize_intensity"):
+        ctx.preprocess_batch(off, mz, it, pre, 16)
+    with pytest.raises(hb.InvariantError, match="quantize_intensity"):
+        ctx.build_index_from_spectra(off, mz, it, pre, np.array([500.0, 600.0]), np.array([2, 2], np.uint8))
+    # a single infinite peak is the base peak: every finite peak falls below 1 % of it and is
+    # dropped, the infinite one is kept alone -> below min_peaks, unprocessable, no error
+    lone = base_it.copy()
+    lone[4] = np.inf
+    words, ok = ctx.encode_batch(*U.csr([(base_mz, lone)]), pre)
+    ow, ook = best_oracle.encode_spectra(ocb, opre, *U.csr([(base_mz, lone)]))
+    assert np.array_equal(ok, ook) and not ok.any()
+    best_oracle.free_codebook(ocb)
+
+
 def test_encode_vectors_random_vs_oracle(hb, ctx, best_oracle):  # test_encoder.cpp:132-139, wider
     rng = np.random.default_rng(21)
     for dim, n_bins, levels, max_n in ((128, 40, 16, 12), (64, 9, 2, 9), (1088, 300, 31, 300),
