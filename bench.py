@@ -355,7 +355,10 @@ def run_ours(args) -> None:
     # ---- roofline of the dominant kernel ---------------------------------------------------
     peak, peak_src = measured_peak_hbm()
     # per launch: this rank's share of the algorithmic bytes (1/world of the rows of every window)
-    bytes_per_launch = bytes_alg / world
+    # (a step of more than 64 Ki queries is several launches, one per planning batch of the tensor
+    # engine, or k launches on the XOR+POPC engine: the step's work is spread over them)
+    launches_per_step = max(1.0, search_launches / max(1, args.steps))
+    bytes_per_launch = bytes_alg / world / launches_per_step
     achieved = bytes_per_launch / (search_ms / max(1, search_launches) * 1e-3) / 1e9 if search_ms > 0 else 0.0
     kernel_ms = search_ms / max(1, search_launches)
     # DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` captures of
@@ -377,7 +380,7 @@ def run_ours(args) -> None:
         # int8 contraction: 2 ops per (pair, dimension); K is padded to a multiple of 128
         fp4 = args.engine in ("auto", "tensor_fp4")
         kpad = (dim + 255) // 256 * 256 if fp4 else (dim + 127) // 128 * 128
-        ops = 2.0 * (n_pairs / world) * kpad
+        ops = 2.0 * (n_pairs / world / launches_per_step) * kpad
         tpeak, tsrc = measured_peak_tensor_i8()
         if fp4:  # 4-bit operands: twice the 8-bit rate (9 vs 4.5 PFLOP/s nominal)
             tpeak, tsrc = 2.0 * tpeak, tsrc.replace("2 x", "4 x")
@@ -392,7 +395,8 @@ def run_ours(args) -> None:
                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": tsrc, "peak_probe": probe, "kernel": "tc_search_kernel",
                     "kernel_ms_per_launch": kernel_ms,
                     "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
-                    "algorithmic_ops_per_launch": ops, "pairs_per_launch": n_pairs / world,
+                    "algorithmic_ops_per_launch": ops, "pairs_per_launch": n_pairs / world / launches_per_step,
+                    "launches_per_step": launches_per_step,
                     "note": ("e2m1 tensor ops (tcgen05 kind::mxf4, unit block scales)" if fp4 else
                              "int8 tensor ops (tcgen05 kind::i8)") + " counted over the candidate pairs of "
                             "the windows only; masked columns of edge tiles are not counted",
@@ -402,8 +406,8 @@ def run_ours(args) -> None:
                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                     "peak_source": peak_src, "kernel": "search_kernel", "kernel_ms_per_launch": kernel_ms,
                     "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
-                    "algorithmic_bytes_per_launch": bytes_per_launch, "pairs_per_launch": n_pairs / world,
-                    "note": hbm_view["note"]}
+                    "algorithmic_bytes_per_launch": bytes_per_launch, "pairs_per_launch": n_pairs / world / launches_per_step,
+                    "launches_per_step": launches_per_step, "note": hbm_view["note"]}
 
     # ---- CPU baseline: the compiled reference on this box's cores, bounded sample ----------
     cpu = None

@@ -104,5 +104,6 @@ WORKLOADS = {
     "config1": (5_000, 1_000, 2048, 50, 1),       # reference CPU test workload
     "iprg2012": (600_000, 16_000, 8192, 50, 2),   # 16k queries x 1.2M library, D = 8192
     "hek293": (2_150_000, 65_536, 8192, 50, 3),   # 4.3M library; query prefix of the 1M set
+    "hek293_full": (2_150_000, 1_000_000, 8192, 50, 3),  # BASELINE config 3 at full size (seconds per step)
     "tiny": (2_000, 256, 2048, 50, 9),            # CI-sized
 }
