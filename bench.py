@@ -364,21 +364,22 @@ def run_ours(args) -> None:
     # DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` captures of
     # this exact command (dram__bytes_read.sum + dram__bytes_write.sum); only valid for the default
     # single-GPU workload, null otherwise
-    ncu_traffic = {"tensor_fp4": (28.382962e9 + 0.116947e9, "profiles/r01_search_kernel_tensor_fp4_ncu_v2.csv"),
+    ncu_traffic = {"tensor_fp4": (29.069353e9 + 0.115425e9, "profiles/r01_search_kernel_tensor_fp4_ncu_v3.csv"),
                    "tensor": (260.988723e9 + 0.019967e9, "profiles/r01_search_kernel_tensor_ncu.csv (before the "
                                                          "short-strip planner)"),
                    "popc": (301.799285e9 + 0.036848e9, "profiles/r01_search_kernel_popc_ncu.csv")}
-    eng_key = "tensor_fp4" if args.engine == "auto" else args.engine
-    traffic, traffic_src = (ncu_traffic[eng_key] if (args.workload == "iprg2012" and world == 1 and k == 1)
-                            else (None, None))
-    tensor = args.engine != "popc" and k <= 16  # the tensor engines keep up to 16 candidates per query
+    ran_on = ctx.last_engine()  # AUTO resolves per call (tensor_fp4, or direct for narrow top-1 windows)
+    traffic, traffic_src = (ncu_traffic[ran_on] if (args.workload == "iprg2012" and world == 1 and k == 1
+                                                    and TOL == ("da", 500.0) and not DIM_OVERRIDE
+                                                    and ran_on in ncu_traffic) else (None, None))
+    tensor = ran_on in ("tensor", "tensor_fp4")
     hbm_view = {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_per_launch,
                 "note": "SURVEY 8(d) algorithmic bytes (every candidate row read once per query) over the "
                         "kernel time; > peak is legitimate because queries share library tiles on chip"}
     if tensor:
         # int8 contraction: 2 ops per (pair, dimension); K is padded to a multiple of 128
-        fp4 = args.engine in ("auto", "tensor_fp4")
+        fp4 = ran_on == "tensor_fp4"
         kpad = (dim + 255) // 256 * 256 if fp4 else (dim + 127) // 128 * 128
         ops = 2.0 * (n_pairs / world / launches_per_step) * kpad
         tpeak, tsrc = measured_peak_tensor_i8()
@@ -404,7 +405,8 @@ def run_ours(args) -> None:
     else:
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                    "peak_source": peak_src, "kernel": "search_kernel", "kernel_ms_per_launch": kernel_ms,
+                    "peak_source": peak_src, "kernel": "direct_search_kernel" if ran_on == "direct" else "search_kernel",
+                    "kernel_ms_per_launch": kernel_ms,
                     "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
                     "algorithmic_bytes_per_launch": bytes_per_launch, "pairs_per_launch": n_pairs / world / launches_per_step,
                     "launches_per_step": launches_per_step, "note": hbm_view["note"]}
@@ -422,10 +424,11 @@ def run_ours(args) -> None:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": (("e2m1 (+-1 expansion of the packed u64 bits, unit block scales), f32 accumulate (exact)" if args.engine in ("auto", "tensor_fp4") else "s8 (+-1 expansion of the packed u64 bits), s32 accumulate") if tensor else "u64"), "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": (("e2m1 (+-1 expansion of the packed u64 bits, unit block scales), f32 accumulate (exact)" if ran_on == "tensor_fp4" else "s8 (+-1 expansion of the packed u64 bits), s32 accumulate") if tensor else "u64"), "data": "synthetic",
             "config": {"workload": workload_name(args.workload, dim, n_lib, nq), "tolerance": "%s %g" % ("dalton" if TOL[0] == "da" else "ppm", TOL[1]),
                        "k": k, "candidate_pairs_per_step": n_pairs,
-                       "engine": ("tensor (tcgen05 mxf4 e2m1)" if args.engine in ("auto", "tensor_fp4") else "tensor (tcgen05 int8)") if tensor else "popc",
+                       "engine": {"tensor_fp4": "tensor (tcgen05 mxf4 e2m1)", "tensor": "tensor (tcgen05 int8)", "popc": "popc",
+                                  "direct": "direct (warp per query, XOR+POPC)"}.get(ran_on, ran_on),
                        "l2_policy": "inputs larger than L2 (library hypervectors "
                                     f"{n_lib * W * 8 / 1e9:.2f} GB >> 126 MB)",
                        "parallelism": f"library sharded by m/z slices x{world}, queries replicated, "
@@ -788,7 +791,7 @@ def main():
     ap.add_argument("--encode-spectra", type=int, default=1_000_000,
                     help="--workload encode: spectra per step")
     ap.add_argument("--mgf-spectra", type=int, default=400_000, help="--workload mgf: spectra in the text image")
-    ap.add_argument("--engine", default="auto", choices=["auto", "popc", "tensor", "tensor_fp4"],
+    ap.add_argument("--engine", default="auto", choices=["auto", "popc", "tensor", "tensor_fp4", "direct"],
                     help="top-1 search engine (auto = tensor cores, e2m1 operands)")
     ap.add_argument("--dim", type=int, default=0, help="override the hypervector dimension (config 5 sweep)")
     ap.add_argument("--tol", default="da:500", help="tolerance KIND:VALUE, KIND in {da, ppm} (config 5 sweep)")

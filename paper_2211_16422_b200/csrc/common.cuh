@@ -112,6 +112,7 @@ struct homs_b200_ctx {
   enum { kScratchSlots = 48 };
   hb::DevBuf scratch[kScratchSlots];
   int engine = HOMS_B200_ENGINE_AUTO;  // homs_b200_ctx_set_engine
+  int last_engine = HOMS_B200_ENGINE_AUTO;  // engine the last search call ran on (never AUTO after a search)
   void* pinned = nullptr;  // small pinned staging block
   size_t pinned_cap = 0;
   // chunked host <-> device pipeline of the encoder (encode.cu:encode_pipeline): copy-in and

@@ -170,7 +170,7 @@ int homs_b200_ctx_set_stream(homs_b200_ctx* ctx, void* cuda_stream) {
 int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
-  HB_REQUIRE(ctx, engine >= HOMS_B200_ENGINE_AUTO && engine <= HOMS_B200_ENGINE_TENSOR_FP4,
+  HB_REQUIRE(ctx, engine >= HOMS_B200_ENGINE_AUTO && engine <= HOMS_B200_ENGINE_DIRECT,
              HOMS_B200_ERR_ARGUMENT, "set_engine: unknown engine");
   const bool tensor = engine == HOMS_B200_ENGINE_TENSOR || engine == HOMS_B200_ENGINE_TENSOR_FP4;
   HB_REQUIRE(ctx, !tensor || !ctx->lib.ready ||
@@ -180,6 +180,8 @@ int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine) {
   ctx->engine = engine;
   return HOMS_B200_OK;
 }
+
+int homs_b200_ctx_last_engine(const homs_b200_ctx* ctx) { return ctx ? ctx->last_engine : -1; }
 
 int homs_b200_ctx_synchronize(homs_b200_ctx* ctx) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;

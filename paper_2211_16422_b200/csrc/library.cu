@@ -175,7 +175,7 @@ static int build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h
       if (rc != HOMS_B200_OK) return set_error(ctx, rc, "build_index: host->device row upload failed");
     }
   }
-  if (ctx->engine != HOMS_B200_ENGINE_POPC && local) {
+  if (ctx->engine != HOMS_B200_ENGINE_POPC && ctx->engine != HOMS_B200_ENGINE_DIRECT && local) {
     HB_TRY(tc_expand_library(ctx));
   } else {
     release(lib.d_x);

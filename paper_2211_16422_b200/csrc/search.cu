@@ -497,6 +497,128 @@ __global__ void decode_kernel(uint64_t total, const Cand* __restrict__ rec, uint
 // host side
 // ------------------------------------------------------------------------------------------
 
+// ------------------------------------------------------------------------------------------
+// K4c: direct engine -- one warp per query, for windows of a few dozen rows
+// ------------------------------------------------------------------------------------------
+// The tensor engine's cost has a floor of one pass over the library image per call (every query
+// tile's union window, summed over the tiles, covers the library once: 0.7 ms on config 2 however
+// narrow the tolerance).  A 20 ppm window holds ~25 rows: reading exactly those rows (neighbouring
+// sorted queries share them in L2) is an order of magnitude less traffic.  Top-1 only.
+
+__global__ void __launch_bounds__(256)
+direct_search_kernel(uint64_t n, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                     const uint32_t* __restrict__ subset, const uint4* __restrict__ q_words,
+                     const double* __restrict__ q_mz, const uint4* __restrict__ lib_words,
+                     const double* __restrict__ lib_mz, const uint32_t* __restrict__ lib_rank, uint32_t row_u4,
+                     Cand* __restrict__ out, uint32_t k_stride) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t pos = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (pos >= n) return;
+  const uint64_t key = keys[pos];
+  const uint32_t slot = vals[pos];
+  const uint32_t qi = subset ? subset[slot] : slot;
+  uint32_t lf = 0, ll = 0;
+  if (key != ~0ull) {
+    lf = static_cast<uint32_t>(key >> 32);
+    ll = static_cast<uint32_t>(key);
+  }
+  const double qmz = q_mz[qi];
+  const uint4* q = q_words + size_t(qi) * row_u4;
+  uint32_t best_d = kNone, best_rk = kNone, best_row = kNone;
+  uint64_t best_ad = ~0ull;
+  bool have_key = false;
+
+  auto consider = [&](uint32_t row, uint32_t d) {  // warp-uniform
+    if (d < best_d) {
+      best_d = d;
+      best_row = row;
+      have_key = false;
+    } else if (d == best_d) {  // tie on score: |mass diff|, then id, then ordinal (search.cpp:137-145)
+      if (!have_key) {
+        best_ad = abs_diff_bits(qmz, lib_mz[best_row]);
+        best_rk = lib_rank[best_row];
+        have_key = true;
+      }
+      const uint64_t ad = abs_diff_bits(qmz, lib_mz[row]);
+      const uint32_t rk = lib_rank[row];
+      if (cand_less(d, ad, rk, d, best_ad, best_rk)) {
+        best_row = row;
+        best_ad = ad;
+        best_rk = rk;
+      }
+    }
+  };
+
+  uint32_t r = lf;
+  for (; r + 4 <= ll; r += 4) {  // four rows in flight per lane
+    uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    const uint4* b = lib_words + size_t(r) * row_u4;
+    for (uint32_t u = lane; u < row_u4; u += 32) {
+      const uint4 a = q[u];
+      const uint4 x0 = __ldg(b + u), x1 = __ldg(b + row_u4 + u), x2 = __ldg(b + 2 * size_t(row_u4) + u),
+                  x3 = __ldg(b + 3 * size_t(row_u4) + u);
+      c0 += __popc(a.x ^ x0.x) + __popc(a.y ^ x0.y) + __popc(a.z ^ x0.z) + __popc(a.w ^ x0.w);
+      c1 += __popc(a.x ^ x1.x) + __popc(a.y ^ x1.y) + __popc(a.z ^ x1.z) + __popc(a.w ^ x1.w);
+      c2 += __popc(a.x ^ x2.x) + __popc(a.y ^ x2.y) + __popc(a.z ^ x2.z) + __popc(a.w ^ x2.w);
+      c3 += __popc(a.x ^ x3.x) + __popc(a.y ^ x3.y) + __popc(a.z ^ x3.z) + __popc(a.w ^ x3.w);
+    }
+    consider(r, __reduce_add_sync(0xffffffffu, c0));
+    consider(r + 1, __reduce_add_sync(0xffffffffu, c1));
+    consider(r + 2, __reduce_add_sync(0xffffffffu, c2));
+    consider(r + 3, __reduce_add_sync(0xffffffffu, c3));
+  }
+  for (; r < ll; ++r) {
+    uint32_t c0 = 0;
+    const uint4* b = lib_words + size_t(r) * row_u4;
+    for (uint32_t u = lane; u < row_u4; u += 32) {
+      const uint4 a = q[u];
+      const uint4 x0 = __ldg(b + u);
+      c0 += __popc(a.x ^ x0.x) + __popc(a.y ^ x0.y) + __popc(a.z ^ x0.z) + __popc(a.w ^ x0.w);
+    }
+    consider(r, __reduce_add_sync(0xffffffffu, c0));
+  }
+  if (lane == 0) {
+    Cand c{kNone, kNone, ~0ull};
+    if (best_row != kNone) {
+      if (!have_key) {
+        best_ad = abs_diff_bits(qmz, lib_mz[best_row]);
+        best_rk = lib_rank[best_row];
+      }
+      c = Cand{best_d, best_rk, best_ad};
+    }
+    out[uint64_t(slot) * k_stride] = c;
+  }
+}
+
+// Expected candidate rows per query for this tolerance, from the library's own m/z distribution
+// (queries are assumed to be distributed like the library): 16 probe points per bucket.
+static double expected_window_rows(const Library& lib, const homs_b200_tolerance* tol) {
+  double acc = 0.0;
+  for (const BucketDev& b : lib.buckets) {
+    if (b.size == 0) continue;
+    const double* m = lib.h_mz.data() + b.begin;
+    double rows = 0.0;
+    for (int j = 0; j < 16; ++j) {
+      const double c = m[b.size * (2 * j + 1) / 32];
+      const double w = tol->kind == HOMS_B200_TOL_PPM ? tol->value * c * 1e-6 : tol->value;
+      rows += static_cast<double>(std::upper_bound(m, m + b.size, c + w) - std::lower_bound(m, m + b.size, c - w));
+    }
+    acc += rows / 16.0 * static_cast<double>(b.size);
+  }
+  return lib.n ? acc / static_cast<double>(lib.n) : 0.0;
+}
+
+// AUTO: the direct engine when the rows it would read are far fewer bytes than the tensor engine's
+// floor of one pass over the library image per planning batch (measured crossover, profiles/)
+static bool direct_is_cheaper(const homs_b200_ctx* ctx, uint64_t n, const homs_b200_tolerance* tol) {
+  const Library& lib = ctx->lib;
+  const double share = lib.n ? static_cast<double>(lib.n_local) / static_cast<double>(lib.n) : 1.0;
+  const double direct_bytes = expected_window_rows(lib, tol) * share * static_cast<double>(n) * lib.S * 8.0;
+  const double batches = static_cast<double>((n + 65535) / 65536);
+  const double tensor_bytes = static_cast<double>(lib.n_kc) * static_cast<double>(lib.x_rows) * 128.0 * batches;
+  return direct_bytes * 2.0 < tensor_bytes;
+}
+
 static int pick_qb(uint32_t row_bytes) {
   if (row_bytes <= 2048) return 16;
   if (row_bytes <= 4096) return 8;
@@ -581,8 +703,25 @@ static int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint6
   const uint64_t* keys = ctx->scratch[kScrKeysAlt].as<uint64_t>();
   const uint32_t* vals = ctx->scratch[kScrValsAlt].as<uint32_t>();
 
-  if (k <= tc_max_topk() && ctx->engine != HOMS_B200_ENGINE_POPC && tc_available(ctx))
+  const bool tensor_ok = ctx->engine != HOMS_B200_ENGINE_POPC && ctx->engine != HOMS_B200_ENGINE_DIRECT && tc_available(ctx);
+  if (k == 1 && (ctx->engine == HOMS_B200_ENGINE_DIRECT ||
+                 (ctx->engine == HOMS_B200_ENGINE_AUTO && tensor_ok && direct_is_cheaper(ctx, n, tol)))) {
+    const uint64_t threads = n * 32;
+    {
+      KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
+      direct_search_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, ctx->stream>>>(
+          n, keys, vals, d_subset, q.d_words.as<uint4>(), q.d_mz.as<double>(), lib.d_words.as<uint4>(),
+          lib.d_mz_local.as<double>(), lib.d_id_rank_local.as<uint32_t>(), lib.S / 2, d_out, 1);
+    }
+    HB_LAUNCHED(ctx);
+    ctx->last_engine = HOMS_B200_ENGINE_DIRECT;
+    return HOMS_B200_OK;
+  }
+  if (k <= tc_max_topk() && tensor_ok) {
+    ctx->last_engine = lib.x_fp4 ? HOMS_B200_ENGINE_TENSOR_FP4 : HOMS_B200_ENGINE_TENSOR;
     return tc_search_sorted(ctx, d_subset, n, keys, vals, d_out, k, k);
+  }
+  ctx->last_engine = HOMS_B200_ENGINE_POPC;
 
   const uint32_t n_blocks = static_cast<uint32_t>((n + qb - 1) / qb);
   const int grid = ctx->sm_count * 2;

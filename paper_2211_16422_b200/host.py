@@ -275,11 +275,17 @@ class Context:
         _check(capi.ctx_set_stream(self._h, cuda_stream or 0), self._h)
 
     def set_engine(self, engine: str | int) -> None:
-        """Top-1 search engine: "auto" (tensor when available), "popc" or "tensor".  Choose it
-        before build_index: "popc" skips the tensor image of the library."""
+        """Search engine: "auto" (tensor_fp4, or direct for narrow top-1 calls), "popc", "tensor",
+        "tensor_fp4" or "direct".  Choose it before build_index: "popc" and "direct" skip the tensor
+        image of the library."""
         code = {"auto": capi.ENGINE_AUTO, "popc": capi.ENGINE_POPC, "tensor": capi.ENGINE_TENSOR,
-                "tensor_fp4": capi.ENGINE_TENSOR_FP4}.get(engine, engine)
+                "tensor_fp4": capi.ENGINE_TENSOR_FP4, "direct": capi.ENGINE_DIRECT}.get(engine, engine)
         _check(capi.ctx_set_engine(self._h, int(code)), self._h)
+
+    def last_engine(self) -> str:
+        """Engine the last search call ran on: "popc", "tensor", "tensor_fp4" or "direct"."""
+        return {capi.ENGINE_POPC: "popc", capi.ENGINE_TENSOR: "tensor", capi.ENGINE_TENSOR_FP4: "tensor_fp4",
+                capi.ENGINE_DIRECT: "direct"}.get(int(capi.ctx_last_engine(self._h)), "auto")
 
     def synchronize(self) -> None:
         _check(capi.ctx_synchronize(self._h), self._h)

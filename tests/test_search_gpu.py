@@ -9,9 +9,10 @@ from tests import _util as U
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["tensor_fp4", "tensor", "popc"])
+@pytest.fixture(params=["tensor_fp4", "tensor", "popc", "direct", "auto"])
 def ctx(hb, request):
-    """Every search test runs on all engines: tcgen05 mxf4 (e2m1), tcgen05 int8, XOR+POPC."""
+    """Every search test runs on all engines: tcgen05 mxf4 (e2m1), tcgen05 int8, XOR+POPC, the
+    warp-per-query direct engine, and AUTO (which picks direct or tensor_fp4 per call)."""
     c = hb.Context(0)
     c.set_engine(request.param)
     c.engine_name = request.param
@@ -271,14 +272,14 @@ def test_many_queries_span_planning_batches(hb, best_oracle):
     qmz = np.round(rng.uniform(380.0, 1220.0, nq), 2)
     qch = rng.integers(1, 4, nq).astype(np.uint8)
     got = {}
-    for eng in ("tensor", "tensor_fp4", "popc"):
+    for eng in ("tensor", "tensor_fp4", "popc", "direct"):
         with hb.Context(0) as c:
             c.set_engine(eng)
             c.build_index(dim, words, mz, charge, ids=ids)
             got[eng] = c.search_batch(qw, qmz, qch, hb.Tolerance("dalton", 3.0))
             none = c.search_batch(qw[:300], qmz[:300], np.zeros(300, np.uint8), hb.Tolerance("dalton", 3.0))
             assert not none.has_hit.any()
-    for eng in ("tensor", "tensor_fp4"):
+    for eng in ("tensor", "tensor_fp4", "direct"):
         assert np.array_equal(got[eng].ordinal, got["popc"].ordinal), eng
         assert np.array_equal(got[eng].raw_score, got["popc"].raw_score), eng
     oix = best_oracle.build_index(dim, words, mz, charge, None, ids)
