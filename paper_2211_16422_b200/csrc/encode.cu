@@ -292,34 +292,37 @@ encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stri
         U4 pend8{{0, 0, 0, 0}}, pend16{{0, 0, 0, 0}};
 #pragma unroll 1
         for (uint32_t g = 0; g < n_groups; ++g) {
-          U4 x[8];
-          uint32_t lev[8];
+          U4 e{{0, 0, 0, 0}};
+          if (8 * g < cn) {  // a group wholly past the end of the list only completes the carry pairing
+            U4 x[8];
+            uint32_t lev[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {  // 8 position-row gathers in flight
-            const uint32_t k = 8 * g + j;
-            const uint32_t bin = __shfl_sync(0xffffffffu, my_bin, k);
-            lev[j] = __shfl_sync(0xffffffffu, my_lev, k);
-            x[j] = ld_global_u4(reinterpret_cast<const uint4*>(pos_b + uint64_t(bin) * row_bytes));
-          }
-          asm volatile("" ::: "memory");  // level rows (shared memory) are fetched only as the gathers land
+            for (int j = 0; j < 8; ++j) {  // 8 position-row gathers in flight
+              const uint32_t k = 8 * g + j;
+              const uint32_t bin = __shfl_sync(0xffffffffu, my_bin, k);
+              lev[j] = __shfl_sync(0xffffffffu, my_lev, k);
+              x[j] = ld_global_u4(reinterpret_cast<const uint4*>(pos_b + uint64_t(bin) * row_bytes));
+            }
+            asm volatile("" ::: "memory");  // level rows (shared memory) are fetched only as the gathers land
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint4* lp = reinterpret_cast<const uint4*>(lvl_b + lev[j]);
-            const uint4 lw4 = kLvlSmem ? *lp : __ldg(lp);
-            x[j].v[0] = ~(x[j].v[0] ^ lw4.x);  // encoder.cpp:41 agree = ~(pos ^ lvl)
-            x[j].v[1] = ~(x[j].v[1] ^ lw4.y);
-            x[j].v[2] = ~(x[j].v[2] ^ lw4.z);
-            x[j].v[3] = ~(x[j].v[3] ^ lw4.w);
+            for (int j = 0; j < 8; ++j) {
+              const uint4* lp = reinterpret_cast<const uint4*>(lvl_b + lev[j]);
+              const uint4 lw4 = kLvlSmem ? *lp : __ldg(lp);
+              x[j].v[0] = ~(x[j].v[0] ^ lw4.x);  // encoder.cpp:41 agree = ~(pos ^ lvl)
+              x[j].v[1] = ~(x[j].v[1] ^ lw4.y);
+              x[j].v[2] = ~(x[j].v[2] ^ lw4.z);
+              x[j].v[3] = ~(x[j].v[3] ^ lw4.w);
+            }
+            // 8 inputs -> c[0..2] updated, one carry e of weight 8
+            U4 ta, tb, fa, fb;
+            HB_CSA(c[0], ta, c[0], x[0], x[1]);
+            HB_CSA(c[0], tb, c[0], x[2], x[3]);
+            HB_CSA(c[1], fa, c[1], ta, tb);
+            HB_CSA(c[0], ta, c[0], x[4], x[5]);
+            HB_CSA(c[0], tb, c[0], x[6], x[7]);
+            HB_CSA(c[1], fb, c[1], ta, tb);
+            HB_CSA(c[2], e, c[2], fa, fb);
           }
-          // 8 inputs -> c[0..2] updated, one carry e of weight 8
-          U4 ta, tb, fa, fb, e;
-          HB_CSA(c[0], ta, c[0], x[0], x[1]);
-          HB_CSA(c[0], tb, c[0], x[2], x[3]);
-          HB_CSA(c[1], fa, c[1], ta, tb);
-          HB_CSA(c[0], ta, c[0], x[4], x[5]);
-          HB_CSA(c[0], tb, c[0], x[6], x[7]);
-          HB_CSA(c[1], fb, c[1], ta, tb);
-          HB_CSA(c[2], e, c[2], fa, fb);
           if ((g & 1u) == 0) {
             pend8 = e;
           } else {  // the weight-8 carries of an even/odd pair meet in c[3] ...
