@@ -199,6 +199,12 @@ def run_ours(args) -> None:
     # HOMS_BENCH_BACKEND=gloo: development smoke of the world > 1 path on a box with fewer GPUs than
     # ranks (ranks share devices, the gather is staged through the host); the product path is NCCL
     backend = os.environ.get("HOMS_BENCH_BACKEND", "nccl")
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    if backend == "nccl" and world > 1 and torch.cuda.device_count() < local_world:
+        # NCCL cannot put two ranks on one GPU: fall back to the smoke path and say so in the line
+        log(f"[bench] {local_world} ranks on {torch.cuda.device_count()} GPU(s): ranks share devices, candidates "
+            "gathered through the host (gloo) -- a functional check, not a scaling measurement")
+        backend = "gloo"
     if backend != "nccl":
         local_rank = local_rank % torch.cuda.device_count()
     if world > 1:
@@ -431,8 +437,11 @@ def run_ours(args) -> None:
                                   "direct": "direct (warp per query, XOR+POPC)"}.get(ran_on, ran_on),
                        "l2_policy": "inputs larger than L2 (library hypervectors "
                                     f"{n_lib * W * 8 / 1e9:.2f} GB >> 126 MB)",
-                       "parallelism": f"library sharded by m/z slices x{world}, queries replicated, "
-                                      "all-gather + merge of 16-byte candidates" if world > 1 else "single GPU"},
+                       "parallelism": (f"library sharded by m/z slices x{world}, queries replicated, "
+                                       "all-gather + merge of 16-byte candidates"
+                                       + ("" if backend == "nccl" else " [ranks SHARE GPUs, gather through the host "
+                                          "(gloo): functional check, not a scaling measurement]"))
+                                      if world > 1 else "single GPU"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
             "result_digest": result_digest,
