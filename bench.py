@@ -330,6 +330,8 @@ def run_ours(args) -> None:
     import hashlib
     result_digest = hashlib.sha256(dev_ord.tobytes() + dev_score.tobytes()).hexdigest()[:16]  # same at every N
 
+    ran_on = ctx.last_engine()  # AUTO resolves per call (tensor_fp4, or direct for narrow top-1 windows)
+
     # ---- end to end through the public host-buffer call ----------------------------------
     h_words = torch.empty((nq, W), dtype=torch.int64).pin_memory()
     h_words.copy_(q_words.cpu())
@@ -358,6 +360,25 @@ def run_ours(args) -> None:
     if world == 1:
         assert np.array_equal(e2e_result.ordinal, dev_ord) and np.array_equal(e2e_result.raw_score, dev_score)
 
+    # ---- cascade_search (search.cpp:219-248): the reference's `homs search` call ------------
+    # narrow 20 ppm stage on all queries (direct engine), target-decoy FDR on the host, open stage on the
+    # rest (tensor engine), FDR again; from host buffers, like the e2e leg.  Reported next to the headline.
+    cascade = None
+    if world == 1 and k == 1 and TOL == ("da", 500.0):
+        narrow_tol = hb.Tolerance("ppm", 20.0)
+        times, got = [], None
+        for i in range(1 + max(1, min(args.steps, 3))):
+            sync_all()
+            t0 = time.perf_counter()
+            got = ctx.cascade_search(hq, qry["precursor_mz"], qry["charge"], narrow_tol, tol, 0.01)
+            if i >= 1:
+                times.append(time.perf_counter() - t0)
+        sec = sum(times) / len(times)
+        cascade = {"ms_per_call": sec * 1e3, "queries_per_s": nq / sec, "narrow": "ppm 20", "wide": "dalton 500",
+                   "fdr_q": 0.01, "accepted": int(len(got["query"])),
+                   "accepted_narrow": int((got["stage"] == 0).sum()), "accepted_wide": int((got["stage"] == 1).sum()),
+                   "note": "host buffers in, accepted SSMs out; includes both FDR passes on the host"}
+
     # ---- roofline of the dominant kernel ---------------------------------------------------
     peak, peak_src = measured_peak_hbm()
     # per launch: this rank's share of the algorithmic bytes (1/world of the rows of every window)
@@ -374,7 +395,6 @@ def run_ours(args) -> None:
                    "tensor": (260.988723e9 + 0.019967e9, "profiles/r01_search_kernel_tensor_ncu.csv (before the "
                                                          "short-strip planner)"),
                    "popc": (301.799285e9 + 0.036848e9, "profiles/r01_search_kernel_popc_ncu.csv")}
-    ran_on = ctx.last_engine()  # AUTO resolves per call (tensor_fp4, or direct for narrow top-1 windows)
     traffic, traffic_src = (ncu_traffic[ran_on] if (args.workload == "iprg2012" and world == 1 and k == 1
                                                     and TOL == ("da", 500.0) and not DIM_OVERRIDE
                                                     and ran_on in ncu_traffic) else (None, None))
@@ -421,7 +441,8 @@ def run_ours(args) -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(lib, qry, dim, lib_words, hq, dev_score[:, 0], dev_ord[:, 0])
+            cpu = cpu_baseline(lib, qry, dim, lib_words, hq, dev_score[:, 0], dev_ord[:, 0],
+                               ctx if cascade is not None else None, hb)
         except Exception as exc:  # the baseline is a report, never a reason to lose the bench line
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
                    "sample": f"failed: {exc!r}"}
@@ -444,7 +465,7 @@ def run_ours(args) -> None:
                                       if world > 1 else "single GPU"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
-            "result_digest": result_digest,
+            "result_digest": result_digest, "cascade": cascade,
             "encode": {"spectra_per_s": n_lib / ((pre_ms + enc_ms) * 1e-3), "preprocess_ms": pre_ms,
                        "encode_ms": enc_ms, "spectra": n_lib, "peaks": lib["peaks"]},
         }
@@ -747,7 +768,7 @@ def run_mgf(args) -> None:
     ctx.close()
 
 
-def cpu_baseline(lib, qry, dim, lib_words, hq, dev_score, dev_ord):
+def cpu_baseline(lib, qry, dim, lib_words, hq, dev_score, dev_ord, ctx=None, hb=None):
     from oracle import binding as ob
     kind = "ref" if ob.available("ref") else "port"
     oracle = ob.Oracle(kind)
@@ -773,6 +794,21 @@ def cpu_baseline(lib, qry, dim, lib_words, hq, dev_score, dev_ord):
            "sample": f"search_batch over the first {sample} queries against the full library, {cores} threads, "
                      "as-shipped flags (-O3, no -march)",
            "parity_with_gpu_on_sample": "bit-exact" if parity else "MISMATCH"}
+    if ctx is not None and TOL == ("da", 500.0):
+        # cascade_search on the same prefix: identical accepted list (ids, stage, score, q-value bits)
+        t0 = time.perf_counter()
+        want = ix.cascade_search(hq[:sample], qry["precursor_mz"][:sample], qry["charge"][:sample], ("ppm", 20.0),
+                                 ("da", 500.0), 0.01, threads=cores, batch=8)
+        sec_c = time.perf_counter() - t0
+        got = ctx.cascade_search(hq[:sample], qry["precursor_mz"][:sample], qry["charge"][:sample],
+                                 hb.Tolerance("ppm", 20.0), hb.Tolerance("dalton", 500.0), 0.01)
+        same = all(np.array_equal(got[key], want[key]) for key in ("query", "ordinal", "stage", "raw_score")) and \
+            np.array_equal(got["q_value"].view(np.uint64), want["q_value"].view(np.uint64))
+        out["cascade"] = {"value": sample / sec_c, "unit": UNIT, "accepted": int(len(want["query"])),
+                          "accepted_narrow": int((want["stage"] == 0).sum()),
+                          "parity_with_gpu_on_sample": "identical accepted list" if same else "MISMATCH"}
+        if not same:
+            raise AssertionError("GPU cascade differs from the reference on the CPU-baseline sample")
     if ob.available("ref_v3"):
         o3 = ob.Oracle("ref_v3")
         ix3 = o3.build_index(dim, lw, lib["precursor_mz"], lib["charge"], lib["is_decoy"], lib["ids"])
