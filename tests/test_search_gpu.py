@@ -194,6 +194,37 @@ def test_topk_many_work_items_vs_port(hb, ctx, port):
     oix.close()
 
 
+def test_search_fuzz_vs_port(hb, ctx, port):
+    """Randomised differential test against the full-sort oracle: random sizes, dimensions (also
+    not multiples of 64), k, tolerance kinds and widths (empty windows included), charges with
+    missing buckets and charge 0, few distinct hypervectors / m/z values / ids so that every level
+    of the tie-break key decides somewhere."""
+    rng = np.random.default_rng(20221116)
+    for case in range(24):
+        dim = int(rng.choice([64, 100, 256, 500, 1024, 2048]))
+        n = int(rng.integers(1, 2500))
+        nq = int(rng.integers(1, 300))
+        k = int(rng.choice([1, 1, 2, 3, 5, 16, 17, 20]))
+        distinct = max(1, int(n * rng.choice([0.02, 0.3, 1.0])))
+        pool = U.random_hvs(rng, distinct, dim)
+        words = pool[rng.integers(0, distinct, n)]
+        mz = np.round(rng.uniform(300.0, 300.0 + rng.choice([0.5, 20.0, 900.0]), n), int(rng.choice([0, 1, 3])))
+        charge = rng.choice([1, 2, 3, 4], n, p=[0.05, 0.5, 0.4, 0.05]).astype(np.uint8)
+        ids = [f"p{rng.integers(0, max(1, n // int(rng.choice([1, 7, 400]))))}" for _ in range(n)]
+        flip = U.random_hvs(rng, nq, dim) & U.random_hvs(rng, nq, dim) & U.random_hvs(rng, nq, dim)
+        qw = pool[rng.integers(0, distinct, nq)] ^ (flip if case % 2 else 0)
+        qmz = mz[rng.integers(0, n, nq)] + rng.choice([0.0, 0.0, 0.001, 0.5, -3.0, 450.0], nq)
+        qch = rng.choice([0, 1, 2, 3, 5], nq, p=[0.05, 0.05, 0.5, 0.35, 0.05]).astype(np.uint8)
+        tol = [("da", 500.0), ("da", 0.0005), ("da", 2.0), ("ppm", 10.0), ("ppm", 5000.0), ("da", 40.0)][case % 6]
+        ctx.build_index(dim, words, mz, charge, ids=ids)
+        oix = port.build_index(dim, words, mz, charge, None, ids)
+        m = ctx.search_batch(qw, qmz, qch, U.product_tol(tol), k=k)
+        score, ordinal = oix.search_topk(qw, qmz, qch, tol, k)
+        oix.close()
+        assert np.array_equal(m.ordinal, ordinal), (case, dim, n, nq, k, tol)
+        assert np.array_equal(m.raw_score, score), (case, dim, n, nq, k, tol)
+
+
 def test_sharded_search_merges_to_single(hb):
     """Multi-GPU path on one device: G contexts each hold slice g of every bucket; per-shard
     candidates -> concatenate (what the all-gather yields) -> merge == unsharded result."""
