@@ -130,6 +130,45 @@ def test_non_finite_peaks(hb, ctx, best_oracle):
     best_oracle.free_codebook(ocb)
 
 
+def test_encode_fuzz_vs_oracle(hb, ctx, best_oracle):
+    """Randomised differential test of refine_peaks -> vectorize -> quantize -> encode against the
+    compiled reference: random preprocess configs (bin size, range, floor, max / min peaks, sqrt
+    scaling), level counts and dimensions; spectra with out-of-range and non-positive peaks, m/z
+    values on bin boundaries, tied intensities (top-N rule), bin collisions and too few peaks."""
+    rng = np.random.default_rng(8192)
+    seen_ok = seen_bad = 0
+    for case in range(12):
+        bin_size = float(rng.choice([0.05, 0.1, 1.0005, 0.01]))
+        lo = float(rng.choice([101.0, 50.0, 200.5]))
+        hi = lo + float(rng.choice([300.0, 1399.0]))
+        max_peaks = int(rng.choice([8, 50, 150, 300]))
+        min_peaks = int(rng.choice([1, 5, 10]))
+        floor = float(rng.choice([0.0, 0.01, 0.2]))
+        scaling = int(case % 2)
+        levels = int(rng.choice([1, 16, 31]))
+        dim = int(rng.choice([64, 1000, 2048, 4096]))
+        pre = hb.PreprocessConfig(lo, hi, bin_size, max_peaks, min_peaks, floor, scaling)
+        opre = PreCfg(lo, hi, bin_size, max_peaks, min_peaks, floor, scaling)
+        cb = _upload(hb, ctx, dim, dim // 2, levels, case + 1, hb.dimension(pre))
+        ocb = best_oracle.codebook_from_words(dim, levels, cb.position, cb.level)
+        spectra = []
+        for _ in range(150):
+            p = int(rng.choice([0, 1, 3, 9, 10, 11, 40, 200, 700]))
+            grid = rng.choice([bin_size, bin_size / 2, 0.013])
+            m = np.sort(np.unique(np.round(rng.uniform(lo - 20.0, hi + 20.0, p) / grid) * grid))
+            v = np.round(rng.uniform(-0.1, 1.0, len(m)), int(rng.choice([1, 2, 6])))
+            spectra.append((m, v))
+        off, mz, it = U.csr(spectra)
+        words, ok = ctx.encode_batch(off, mz, it, pre)
+        ow, ook = best_oracle.encode_spectra(ocb, opre, off, mz, it)
+        best_oracle.free_codebook(ocb)
+        seen_ok += int(ok.sum())
+        seen_bad += int(len(ok) - ok.sum())
+        assert np.array_equal(ok, ook), (case, pre)
+        assert np.array_equal(words, ow), (case, pre)
+    assert seen_ok > 500 and seen_bad > 500  # both outcomes are exercised
+
+
 def test_encode_vectors_random_vs_oracle(hb, ctx, best_oracle):  # test_encoder.cpp:132-139, wider
     rng = np.random.default_rng(21)
     for dim, n_bins, levels, max_n in ((128, 40, 16, 12), (64, 9, 2, 9), (1088, 300, 31, 300),
