@@ -107,7 +107,7 @@ enum { HOMS_B200_KERNEL_SEARCH = 0, HOMS_B200_KERNEL_ENCODE = 1, HOMS_B200_KERNE
 /* Search engine: POPC (XOR + POPC on the integer pipes) or a tcgen05 tensor-core contraction of the
  * +-1 expanded hypervectors (similarity = (dim + dot) / 2, exact): TENSOR with int8 operands,
  * TENSOR_FP4 with e2m1 operands and unit block scales (twice the rate, half the bytes).
- * AUTO = TENSOR_FP4, or DIRECT for top-1 calls with narrow windows.  All engines are bit-exact.  The tensor engines keep up to 16 candidates per
+ * AUTO = TENSOR_FP4, or DIRECT for calls with narrow windows.  All engines are bit-exact.  The tensor engines keep up to 16 candidates per
  * query (k <= 16); larger k (up to HOMS_B200_MAX_TOPK) runs on the POPC engine.
  * Set it BEFORE library_upload: the tensor image of the library (8x / 4x the packed size) is built
  * there for the selected engine, and POPC skips it. */
@@ -116,11 +116,11 @@ enum {
   HOMS_B200_ENGINE_POPC = 1,
   HOMS_B200_ENGINE_TENSOR = 2,     /* int8 operands, int32 accumulate (kind::i8) */
   HOMS_B200_ENGINE_TENSOR_FP4 = 3, /* e2m1 operands with unit block scales, fp32 accumulate (kind::mxf4) */
-  HOMS_B200_ENGINE_DIRECT = 4      /* one warp per query over exactly its window rows (XOR + POPC): the
-                                      engine for windows of a few dozen rows (ppm tolerances), top-1.
-                                      AUTO picks it per call when the rows it would read are far fewer
-                                      bytes than one pass over the tensor image; forcing it keeps only
-                                      the packed rows, k > 1 then runs on the POPC engine */
+  HOMS_B200_ENGINE_DIRECT = 4      /* one warp per query over exactly its window rows (XOR + POPC, warp-level
+                                      top-k, k <= 16): the engine for windows of a few dozen rows (ppm
+                                      tolerances).  AUTO picks it per call when the rows it would read are
+                                      far fewer bytes than one pass over the tensor image; forcing it keeps
+                                      only the packed rows, k > 16 then runs on the POPC engine */
 };
 int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine);
 /* The engine the last search call of this context ran on (one of the non-AUTO codes; reporting aid). */

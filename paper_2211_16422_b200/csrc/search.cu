@@ -31,6 +31,7 @@
 #include <numeric>
 
 #include "common.cuh"
+#include "topk.cuh"
 
 namespace hb {
 
@@ -503,14 +504,17 @@ __global__ void decode_kernel(uint64_t total, const Cand* __restrict__ rec, uint
 // The tensor engine's cost has a floor of one pass over the library image per call (every query
 // tile's union window, summed over the tiles, covers the library once: 0.7 ms on config 2 however
 // narrow the tolerance).  A 20 ppm window holds ~25 rows: reading exactly those rows (neighbouring
-// sorted queries share them in L2) is an order of magnitude less traffic.  Top-1 only.
+// sorted queries share them in L2) is an order of magnitude less traffic.  k <= 16.
 
+// KM = 1: running best; KM > 1: the k <= KM best in a register list every lane holds identically
+// (the comparisons are warp-uniform) -- the warp-level top-k with the reference's tie-break.
+template <int KM>
 __global__ void __launch_bounds__(256)
 direct_search_kernel(uint64_t n, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                      const uint32_t* __restrict__ subset, const uint4* __restrict__ q_words,
                      const double* __restrict__ q_mz, const uint4* __restrict__ lib_words,
                      const double* __restrict__ lib_mz, const uint32_t* __restrict__ lib_rank, uint32_t row_u4,
-                     Cand* __restrict__ out, uint32_t k_stride) {
+                     Cand* __restrict__ out, uint32_t k, uint32_t k_stride) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t pos = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (pos >= n) return;
@@ -527,8 +531,22 @@ direct_search_kernel(uint64_t n, const uint64_t* __restrict__ keys, const uint32
   uint32_t best_d = kNone, best_rk = kNone, best_row = kNone;
   uint64_t best_ad = ~0ull;
   bool have_key = false;
+  TcTopK<KM> topk;  // KM > 1 only; "dot" = -distance
+  int kth = kTcNoDot;
+#pragma unroll
+  for (int i = 0; i < KM; ++i) {
+    topk.dot[i] = kTcNoDot;
+    topk.row[i] = kNone;
+  }
 
   auto consider = [&](uint32_t row, uint32_t d) {  // warp-uniform
+    if constexpr (KM > 1) {
+      const int dot = -static_cast<int>(d);
+      if (dot < kth) return;  // below the k-th best so far (ties with it are looked at)
+      tc_topk_insert<KM>(topk, lib_mz, lib_rank, qmz, dot, row);
+      kth = tc_topk_kth<KM>(topk, k);
+      return;
+    }
     if (d < best_d) {
       best_d = d;
       best_row = row;
@@ -577,17 +595,30 @@ direct_search_kernel(uint64_t n, const uint64_t* __restrict__ keys, const uint32
     }
     consider(r, __reduce_add_sync(0xffffffffu, c0));
   }
-  if (lane == 0) {
-    Cand c{kNone, kNone, ~0ull};
-    if (best_row != kNone) {
-      if (!have_key) {
-        best_ad = abs_diff_bits(qmz, lib_mz[best_row]);
-        best_rk = lib_rank[best_row];
+  if (lane != 0) return;
+  Cand* dst = out + uint64_t(slot) * k_stride;
+  if constexpr (KM > 1) {
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+      if (uint32_t(j) < k) {
+        Cand c{kNone, kNone, ~0ull};
+        const uint32_t row = topk.row[j];
+        if (row != kNone)
+          c = Cand{static_cast<uint32_t>(-topk.dot[j]), lib_rank[row], abs_diff_bits(qmz, lib_mz[row])};
+        dst[j] = c;
       }
-      c = Cand{best_d, best_rk, best_ad};
     }
-    out[uint64_t(slot) * k_stride] = c;
+    return;
   }
+  Cand c{kNone, kNone, ~0ull};
+  if (best_row != kNone) {
+    if (!have_key) {
+      best_ad = abs_diff_bits(qmz, lib_mz[best_row]);
+      best_rk = lib_rank[best_row];
+    }
+    c = Cand{best_d, best_rk, best_ad};
+  }
+  dst[0] = c;
 }
 
 // Expected candidate rows per query for this tolerance, from the library's own m/z distribution
@@ -704,15 +735,20 @@ static int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint6
   const uint32_t* vals = ctx->scratch[kScrValsAlt].as<uint32_t>();
 
   const bool tensor_ok = ctx->engine != HOMS_B200_ENGINE_POPC && ctx->engine != HOMS_B200_ENGINE_DIRECT && tc_available(ctx);
-  if (k == 1 && (ctx->engine == HOMS_B200_ENGINE_DIRECT ||
-                 (ctx->engine == HOMS_B200_ENGINE_AUTO && tensor_ok && direct_is_cheaper(ctx, n, tol)))) {
-    const uint64_t threads = n * 32;
+  if (k <= tc_max_topk() && (ctx->engine == HOMS_B200_ENGINE_DIRECT ||
+                             (ctx->engine == HOMS_B200_ENGINE_AUTO && tensor_ok && direct_is_cheaper(ctx, n, tol)))) {
+    const unsigned blocks = static_cast<unsigned>((n * 32 + 255) / 256);
+#define HB_DIRECT_LAUNCH(KM)                                                                                  \
+  direct_search_kernel<KM><<<blocks, 256, 0, ctx->stream>>>(                                                  \
+      n, keys, vals, d_subset, q.d_words.as<uint4>(), q.d_mz.as<double>(), lib.d_words.as<uint4>(),           \
+      lib.d_mz_local.as<double>(), lib.d_id_rank_local.as<uint32_t>(), lib.S / 2, d_out, k, k)
     {
       KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
-      direct_search_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, ctx->stream>>>(
-          n, keys, vals, d_subset, q.d_words.as<uint4>(), q.d_mz.as<double>(), lib.d_words.as<uint4>(),
-          lib.d_mz_local.as<double>(), lib.d_id_rank_local.as<uint32_t>(), lib.S / 2, d_out, 1);
+      if (k == 1) HB_DIRECT_LAUNCH(1);
+      else if (k <= 4) HB_DIRECT_LAUNCH(4);
+      else HB_DIRECT_LAUNCH(16);
     }
+#undef HB_DIRECT_LAUNCH
     HB_LAUNCHED(ctx);
     ctx->last_engine = HOMS_B200_ENGINE_DIRECT;
     return HOMS_B200_OK;
