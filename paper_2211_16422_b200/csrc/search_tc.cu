@@ -89,6 +89,7 @@ struct TcParams {
   uint32_t dim;
   const TcItem* items;
   const uint32_t* n_items;  // device: number of work items (written by the planner)
+  uint32_t* counter;        // device: next work item to hand out (zeroed by the planner)
   const uint64_t* keys;  // sorted (local first row << 32 | local last row), batch base applied
   const uint32_t* vals;  // sorted slot ids
   const uint32_t* subset;
@@ -347,6 +348,7 @@ __global__ void tc_tile_ranges_kernel(uint64_t n, const uint64_t* __restrict__ k
 
 struct TcPlanHead {
   uint32_t n_items, strip, n_pairs, n_groups;
+  uint32_t counter;  // work-item queue of tc_search_kernel
 };
 struct TcPlanCfg {
   uint32_t n_tiles, group_tiles, max_strip, tiles_total;
@@ -471,6 +473,7 @@ __global__ void __launch_bounds__(kTcPlanThreads) tc_plan_head_kernel(TcPlanCfg 
     q.grp_item_base[n_groups] = total_items;
     q.grp_pair_base[n_groups] = s_scan[kTcPlanThreads - 1];
     q.head->n_items = total_items;
+    q.head->counter = 0;
     q.head->strip = strip;
     q.head->n_pairs = s_scan[kTcPlanThreads - 1];
     q.head->n_groups = n_groups;
@@ -555,6 +558,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kStages + 2 + a); };
   volatile uint32_t* tmem_slot =
       reinterpret_cast<volatile uint32_t*>(gen_base + kStages * Mode::StageBytes + 8 * (2 * kStages + 4));
+  // Work items are handed out dynamically, in plan order, through one device-wide counter: however
+  // long a CTA's drain takes, the CTAs running at any moment work on ~gridDim consecutive items, which
+  // is what keeps their operand tiles shared in L2 (with a static round-robin a delayed CTA stays
+  // behind for good and drifts out of its neighbours' tiles: top-5 read 108 GB from DRAM per launch
+  // instead of 29).  The producer draws the ids and passes them to the MMA thread and the drain warps
+  // through a small FIFO in shared memory (ifull / iempty barriers per slot).
+  constexpr int kItemQ = 4;
+  const uint32_t ibar_off = 8u * (2 * kStages + 4) + 8u;
+  auto ifull_bar = [&](int s) { return bar0 + ibar_off + 8u * s; };
+  auto iempty_bar = [&](int s) { return bar0 + ibar_off + 8u * (kItemQ + s); };
+  volatile uint32_t* s_item = reinterpret_cast<volatile uint32_t*>(gen_base + kStages * Mode::StageBytes + ibar_off +
+                                                                   8 * 2 * kItemQ);
+  static_assert(8 * (2 * Mode::Stages + 4) + 8 + 8 * 2 * kItemQ + 4 * kItemQ <= kTcBarBytes, "barrier block too small");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -562,6 +578,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
+    }
+    for (int s = 0; s < kItemQ; ++s) {
+      mbar_init(ifull_bar(s), 1);
+      mbar_init(iempty_bar(s), 5);  // the MMA thread and one lane per drain warp
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
@@ -595,9 +615,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   if (warp == 0) {
     // ===== producer: two bulk copies per stage =====
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      uint32_t stage = 0, phase = 0, qslot = 0, qphase = 0;
+      uint32_t next = atomicAdd(p.counter, 1u);
+      for (;;) {
+        const uint32_t item = next;
+        mbar_wait(iempty_bar(qslot), qphase ^ 1u);
+        s_item[qslot] = item < n_items ? item : kNone;
+        mbar_arrive(ifull_bar(qslot));
+        if (++qslot == kItemQ) {
+          qslot = 0;
+          qphase ^= 1u;
+        }
+        if (item >= n_items) break;
         const TcItem it = p.items[item];
+        next = atomicAdd(p.counter, 1u);  // the next id arrives while this item streams
         const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
         const uint8_t* a_src = p.q_x + uint64_t(it.tile) * kTcM * kTcKB;
         for (uint32_t nt = 0; nt < n_nt; ++nt) {
@@ -620,7 +651,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     // ===== MMA issuer: one thread =====
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;  // aphase: one parity bit per accumulator
-      for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      uint32_t qslot = 0, qphase = 0;
+      for (;;) {
+        mbar_wait(ifull_bar(qslot), qphase);
+        const uint32_t item = s_item[qslot];
+        mbar_arrive(iempty_bar(qslot));
+        if (++qslot == kItemQ) {
+          qslot = 0;
+          qphase ^= 1u;
+        }
+        if (item == kNone) break;
         const TcItem it = p.items[item];
         const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
         for (uint32_t nt = 0; nt < n_nt; ++nt) {
@@ -664,8 +704,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     const int quarter = warp & 3;  // a warp may only touch TMEM lanes [32 * (warp % 4), +32)
     const int qrow = quarter * 32 + lane;
     constexpr int kChunks = (kN + 31) / 32;
-    uint32_t acc = 0, tphase = 0;
-    for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    uint32_t acc = 0, tphase = 0, qslot = 0, qphase = 0;
+    for (;;) {
+      mbar_wait(ifull_bar(qslot), qphase);
+      const uint32_t item = s_item[qslot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(iempty_bar(qslot));
+      if (++qslot == kItemQ) {
+        qslot = 0;
+        qphase ^= 1u;
+      }
+      if (item == kNone) break;
       const TcItem it = p.items[item];
       const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
       const uint64_t pos = uint64_t(it.tile) * kTcM + qrow;
@@ -1004,6 +1053,7 @@ static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, u
     tp.dim = lib.dim;
     tp.items = pp.items;
     tp.n_items = &pp.head->n_items;
+    tp.counter = &pp.head->counter;
     tp.keys = d_keys + b0;
     tp.vals = d_vals + b0;
     tp.subset = d_subset;
