@@ -391,7 +391,7 @@ def run_ours(args) -> None:
     # DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` captures of
     # this exact command (dram__bytes_read.sum + dram__bytes_write.sum); only valid for the default
     # single-GPU workload, null otherwise
-    ncu_traffic = {"tensor_fp4": (29.069353e9 + 0.115425e9, "profiles/r01_search_kernel_tensor_fp4_ncu_v3.csv"),
+    ncu_traffic = {"tensor_fp4": (28.268047e9 + 0.117659e9, "profiles/r01_search_kernel_tensor_fp4_ncu_v4.csv"),
                    "tensor": (260.988723e9 + 0.019967e9, "profiles/r01_search_kernel_tensor_ncu.csv (before the "
                                                          "short-strip planner)"),
                    "popc": (301.799285e9 + 0.036848e9, "profiles/r01_search_kernel_popc_ncu.csv")}
