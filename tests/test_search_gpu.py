@@ -308,11 +308,16 @@ def test_many_queries_span_planning_batches(hb, best_oracle):
             c.set_engine(eng)
             c.build_index(dim, words, mz, charge, ids=ids)
             got[eng] = c.search_batch(qw, qmz, qch, hb.Tolerance("dalton", 3.0))
+            got[eng + "/k3"] = c.search_batch(qw, qmz, qch, hb.Tolerance("dalton", 3.0), k=3)
             none = c.search_batch(qw[:300], qmz[:300], np.zeros(300, np.uint8), hb.Tolerance("dalton", 3.0))
             assert not none.has_hit.any()
     for eng in ("tensor", "tensor_fp4", "direct"):
         assert np.array_equal(got[eng].ordinal, got["popc"].ordinal), eng
         assert np.array_equal(got[eng].raw_score, got["popc"].raw_score), eng
+        # top-3 across planning batches: per-item lists, class-slot floors and the list merge
+        assert np.array_equal(got[eng + "/k3"].ordinal, got["popc/k3"].ordinal), eng
+        assert np.array_equal(got[eng + "/k3"].raw_score, got["popc/k3"].raw_score), eng
+        assert np.array_equal(got[eng + "/k3"].ordinal[:, 0], got["popc"].ordinal[:, 0]), eng
     oix = best_oracle.build_index(dim, words, mz, charge, None, ids)
     sample = rng.integers(0, nq, 2000)
     has, score, ordinal, _ = oix.search_batch(qw[sample], qmz[sample], qch[sample], ("da", 3.0), threads=8)
