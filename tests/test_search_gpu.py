@@ -326,6 +326,50 @@ def test_many_queries_span_planning_batches(hb, best_oracle):
     oix.close()
 
 
+def test_concurrent_callers(hb):
+    """The reference's calls are synchronous and re-entrant.  Here: threads that
+    share ONE context are serialised by its mutex, threads with their OWN contexts run on their own
+    streams; either way every call returns the serial answer."""
+    import threading
+    rng = np.random.default_rng(53)
+    dim, n, nq = 1024, 30000, 2000
+    words = U.random_hvs(rng, n, dim)
+    words[25000:] = words[:5000]
+    mz = np.round(rng.uniform(400.0, 1200.0, n), 2)
+    charge = rng.integers(2, 4, n).astype(np.uint8)
+    qw = words[rng.integers(0, n, nq)] ^ (U.random_hvs(rng, nq, dim) & U.random_hvs(rng, nq, dim))
+    qmz = np.round(rng.uniform(380.0, 1220.0, nq), 2)
+    qch = rng.integers(2, 4, nq).astype(np.uint8)
+    tols = [hb.Tolerance("dalton", 500.0), hb.Tolerance("ppm", 30.0), hb.Tolerance("dalton", 5.0)]
+    shared = hb.Context(0)
+    shared.build_index(dim, words, mz, charge)
+    want = [shared.search_batch(qw, qmz, qch, t, k=2) for t in tols]
+    own = [hb.Context(0) for _ in range(3)]
+    for c in own:
+        c.build_index(dim, words, mz, charge)
+    errors = []
+
+    def worker(c, i):
+        try:
+            for rep in range(6):
+                j = (i + rep) % len(tols)
+                got = c.search_batch(qw, qmz, qch, tols[j], k=2)
+                if not (np.array_equal(got.ordinal, want[j].ordinal) and np.array_equal(got.raw_score, want[j].raw_score)):
+                    errors.append((i, rep, j))
+        except Exception as exc:  # surfaced below: an exception in a thread would otherwise be lost
+            errors.append((i, repr(exc)))
+
+    threads = [threading.Thread(target=worker, args=(shared, i)) for i in range(3)]
+    threads += [threading.Thread(target=worker, args=(c, i)) for i, c in enumerate(own)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for c in own + [shared]:
+        c.close()
+    assert not errors, errors
+
+
 def test_engine_selection_errors(hb):
     with hb.Context(0) as c:
         with pytest.raises(hb.HomsError):
