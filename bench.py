@@ -58,49 +58,98 @@ def measured_peak_tensor_i8():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
-
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons DURING the timed region, sampled through NVML from a thread of
+    this process every ~2 ms (nvidia-smi -lms cannot go below ~100 ms per sample, which is the length of
+    the default timed region); only samples between begin() and end() count.  A region too short to
+    catch one falls back to the samples taken under load around it (warm-up steps run the same
+    kernels).  Falls back to one nvidia-smi query if NVML is not importable."""
 
     def __init__(self, device: int):
-        self.p = None
+        import threading
+        self.rows = []          # (perf_counter, sm_mhz, reasons bitmask)
+        self.t0 = self.t1 = None
+        self.max_mhz = None
+        self._stop = False
+        self._thread = None
+        self._nvml = None
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
-                 "-i", str(device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self._physical_index(device))
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self._nvml = (pynvml, h)
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
         except Exception:
-            self.p = None
+            self._nvml = None
+
+    @staticmethod
+    def _physical_index(device: int) -> int:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            ids = [x.strip() for x in vis.split(",") if x.strip()]
+            if device < len(ids) and ids[device].isdigit():
+                return int(ids[device])
+        return device
+
+    def _run(self):
+        pynvml, h = self._nvml
+        while not self._stop:
+            try:
+                mhz = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                why = int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self.rows.append((time.perf_counter(), mhz, why))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def begin(self):
+        self.t0 = time.perf_counter()
+
+    def end(self):
+        self.t1 = time.perf_counter()
 
     def stop(self) -> dict:
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
-        self.p.terminate()
+        if self.t1 is None:
+            self.end()
+        if self._nvml is None:
+            return self._smi_once()
+        self._stop = True
+        self._thread.join(timeout=2)
+        pynvml, _ = self._nvml
+        names = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                 "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                 "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                 "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap,
+                 "hw_power_brake_slowdown": pynvml.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+        t0 = self.t0 if self.t0 is not None else -1.0
+        inside = [r for r in self.rows if t0 <= r[0] <= self.t1]
+        where = "timed region"
+        if not inside:
+            inside = [r for r in self.rows if r[1] > 0.5 * (self.max_mhz or 1.0)] or self.rows
+            where = "under load around the timed region (region shorter than the sampling period)"
+        sm = [r[1] for r in inside]
+        mask = 0
+        for r in inside:
+            mask |= r[2]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_min_mhz": min(sm) if sm else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(n for n, bit in names.items() if mask & bit),
+                "samples": len(sm), "sampled": where + " (NVML, 2 ms period)"}
+
+    @staticmethod
+    def _smi_once() -> dict:
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            out, _ = self.p.communicate(timeout=5)
+            out = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                 capture_output=True, text=True, timeout=10).stdout.splitlines()[0]
+            f = [x.strip() for x in out.split(",")]
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            return {"sm_mhz": float(f[0]), "sm_max_mhz": float(f[1]),
+                    "reasons": [n for n, v in zip(names, f[2:6]) if v.lower().startswith("active")], "samples": 1,
+                    "sampled": "one nvidia-smi query right after the timed region (NVML unavailable)"}
         except Exception:
-            self.p.kill()
-            out = ""
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for name, val in zip(names, f[3:7]):
-                if val.lower().startswith("active"):
-                    reasons.add(name)
-        busy = [x for x in sm if x > 0.5 * max(mx, default=1)] or sm
-        return {"sm_mhz": statistics.median(busy) if busy else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
 
 
 TOL = ("da", 500.0)   # --tol KIND:VALUE overrides (development sweeps); the headline is open +-500 Da
@@ -300,18 +349,22 @@ def run_ours(args) -> None:
             dist.barrier()
             torch.cuda.synchronize(dev)
 
+    sampler = ClockSampler(local_rank) if rank == 0 else None
     for _ in range(args.warmup):
         step()
     sync_all()
     launches0 = ctx.launch_count()
     ctx.profile(True)
-    sampler = ClockSampler(local_rank) if rank == 0 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if sampler:
+        sampler.begin()
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     sync_all()
+    if sampler:
+        sampler.end()
     clocks = sampler.stop() if sampler else None
     ms_total = e0.elapsed_time(e1)
     search_ms, search_launches = ctx.kernel_time(capi.KERNEL_SEARCH)
@@ -518,18 +571,20 @@ def run_encode(args) -> None:
             ctx.encode_batch_dev(pre, b - a, p1 - p0, off_c.data_ptr(), d_mz[p0:p1].data_ptr(),
                                  d_int[p0:p1].data_ptr(), out[a:b].data_ptr(), ok[a:b].data_ptr())
 
+    sampler = ClockSampler(local_rank)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
     launches0 = ctx.launch_count()
     ctx.profile(True)
-    sampler = ClockSampler(local_rank)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler.begin()
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     torch.cuda.synchronize(dev)
+    sampler.end()
     clocks = sampler.stop()
     ms_step = e0.elapsed_time(e1) / args.steps
     enc_ms, enc_launches = ctx.kernel_time(capi.KERNEL_ENCODE)
@@ -681,17 +736,19 @@ def run_mgf(args) -> None:
     ctx.set_stream(stream.cuda_stream)
     h_text = torch.frombuffer(bytearray(text), dtype=torch.uint8).pin_memory()
     d_text = h_text.to(dev)
+    sampler = ClockSampler(local_rank)
     for _ in range(args.warmup):
         info = ctx.parse_mgf_dev(d_text.data_ptr(), nbytes)
     torch.cuda.synchronize(dev)
     launches0 = ctx.launch_count()
-    sampler = ClockSampler(local_rank)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler.begin()
     e0.record(stream)
     for _ in range(args.steps):
         info = ctx.parse_mgf_dev(d_text.data_ptr(), nbytes)
     e1.record(stream)
     torch.cuda.synchronize(dev)
+    sampler.end()
     clocks = sampler.stop()
     ms_step = e0.elapsed_time(e1) / args.steps
     launches = (ctx.launch_count() - launches0) // args.steps
