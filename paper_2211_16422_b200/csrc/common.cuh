@@ -184,7 +184,7 @@ enum Scratch {
   kScrPartial, kScrRecords, kScrSubset, kScrDecode, kScrMisc, kScrMisc2, kScrRecords2, kScrHas,
   kScrTcQx, kScrTcPlan, kScrTcPartial, kScrTcTiles, kScrTcBest, kScrFnv, kScrCacheBlock,
   kScrPipeIn0, kScrPipeIn1, kScrPipeOut0, kScrPipeOut1, kScrFusedRows, kScrFusedOk,
-  kScrMgfText, kScrMgfTiles, kScrMgfLines, kScrMgfBlocks, kScrMgfPeaks, kScrMgfHard
+  kScrMgfText, kScrMgfTiles, kScrMgfLines, kScrMgfBlocks, kScrMgfPeaks, kScrMgfHard, kScrIndexSort
 };
 
 // Tensor-core engine (search_tc.cu).  expand: packed rows -> +-1 int8 swizzled image.

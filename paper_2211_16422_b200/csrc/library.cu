@@ -9,6 +9,8 @@
 // Sharding: shard g of G keeps rows [size*g/G, size*(g+1)/G) of EVERY bucket
 // (contiguous m/z slices); precursor m/z, id_rank and the rank->ordinal table are replicated so
 // that window bounds are computed in full-bucket coordinates on every rank.
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <cstring>
 #include <numeric>
@@ -27,6 +29,94 @@ __global__ void gather_rows_kernel(uint64_t n_rows, const uint32_t* __restrict__
   const uint64_t* s = src + uint64_t(src_index[row]) * W;
   uint64_t* d = dst + row * S;
   for (uint32_t w = lane; w < S; w += 32) d[w] = w < W ? s[w] : 0;
+}
+
+// ---- (charge, precursor m/z, id, ordinal) order on the device (search.cpp:37-46) ---------------
+// Three stable LSD radix sorts of the entry indices, least significant key first: id_rank (when ids
+// are given; otherwise the initial order already is the ordinal order), the m/z bits mapped to an
+// order-preserving u64, the charge.  1.2 M entries sort in well under a millisecond; the host's
+// comparison sort took 0.2-0.3 s.
+
+// IEEE double -> u64 with the same order (negative values flipped; -0.0 joins +0.0 as the reference's
+// `mz[a] != mz[b]` sees them equal)
+__global__ void index_mz_keys_kernel(uint64_t n, const double* __restrict__ mz, const uint32_t* __restrict__ idx,
+                                     uint64_t* __restrict__ keys) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t b = static_cast<uint64_t>(__double_as_longlong(mz[idx[i]]));
+  if (b == 0x8000000000000000ull) b = 0;
+  keys[i] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__global__ void index_charge_keys_kernel(uint64_t n, const uint8_t* __restrict__ charge,
+                                         const uint32_t* __restrict__ idx, uint8_t* __restrict__ keys) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = charge[idx[i]];
+}
+__global__ void index_iota_kernel(uint64_t n, uint32_t* __restrict__ idx) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) idx[i] = static_cast<uint32_t>(i);
+}
+
+static int device_sort_order(homs_b200_ctx* ctx, uint64_t n, const double* mz, const uint8_t* charge,
+                             const uint32_t* id_rank, uint32_t* h_order) {
+  const int ni = static_cast<int>(n);
+  size_t t1 = 0, t2 = 0, t3 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                  static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), ni, 0, 32,
+                                  ctx->stream);
+  cub::DeviceRadixSort::SortPairs(nullptr, t2, static_cast<const uint64_t*>(nullptr), static_cast<uint64_t*>(nullptr),
+                                  static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), ni, 0, 64,
+                                  ctx->stream);
+  cub::DeviceRadixSort::SortPairs(nullptr, t3, static_cast<const uint8_t*>(nullptr), static_cast<uint8_t*>(nullptr),
+                                  static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), ni, 0, 8,
+                                  ctx->stream);
+  const size_t temp = (std::max({t1, t2, t3}) + 255) / 256 * 256;
+  const size_t a8 = (n * 8 + 255) / 256 * 256, a4 = (n * 4 + 255) / 256 * 256, a1 = (n + 255) / 256 * 256;
+  // layout: mz | key64 a | key64 b | idx a | idx b | rank a | rank b | charge | key8 a | key8 b | cub temp
+  HB_TRY(ensure(ctx, ctx->scratch[kScrIndexSort], 3 * a8 + 4 * a4 + 3 * a1 + temp));
+  auto* base = ctx->scratch[kScrIndexSort].as<unsigned char>();
+  auto* d_mz = reinterpret_cast<double*>(base);
+  auto* k64a = reinterpret_cast<uint64_t*>(base + a8);
+  auto* k64b = reinterpret_cast<uint64_t*>(base + 2 * a8);
+  auto* idx_a = reinterpret_cast<uint32_t*>(base + 3 * a8);
+  auto* idx_b = idx_a + a4 / 4;
+  auto* rank_a = idx_b + a4 / 4;
+  auto* rank_b = rank_a + a4 / 4;
+  auto* d_charge = base + 3 * a8 + 4 * a4;
+  auto* k8a = d_charge + a1;
+  auto* k8b = k8a + a1;
+  void* d_temp = k8b + a1;
+  cudaStream_t st = ctx->stream;
+  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+  HB_CUDA(ctx, cudaMemcpyAsync(d_mz, mz, n * 8, cudaMemcpyHostToDevice, st));
+  HB_CUDA(ctx, cudaMemcpyAsync(d_charge, charge, n, cudaMemcpyHostToDevice, st));
+  index_iota_kernel<<<blocks, 256, 0, st>>>(n, idx_a);
+  HB_LAUNCHED(ctx);
+  uint32_t* cur = idx_a;
+  uint32_t* alt = idx_b;
+  if (id_rank) {
+    HB_CUDA(ctx, cudaMemcpyAsync(rank_a, id_rank, n * 4, cudaMemcpyHostToDevice, st));
+    size_t t = temp;
+    HB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(d_temp, t, rank_a, rank_b, cur, alt, ni, 0, 32, st));
+    std::swap(cur, alt);
+  }
+  index_mz_keys_kernel<<<blocks, 256, 0, st>>>(n, d_mz, cur, k64a);
+  HB_LAUNCHED(ctx);
+  {
+    size_t t = temp;
+    HB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(d_temp, t, k64a, k64b, cur, alt, ni, 0, 64, st));
+    std::swap(cur, alt);
+  }
+  index_charge_keys_kernel<<<blocks, 256, 0, st>>>(n, d_charge, cur, k8a);
+  HB_LAUNCHED(ctx);
+  {
+    size_t t = temp;
+    HB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(d_temp, t, k8a, k8b, cur, alt, ni, 0, 8, st));
+    std::swap(cur, alt);
+  }
+  HB_CUDA(ctx, cudaMemcpyAsync(h_order, cur, n * 4, cudaMemcpyDeviceToHost, st));
+  HB_CUDA(ctx, cudaStreamSynchronize(st));
+  return HOMS_B200_OK;
 }
 
 static int build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h_words,
@@ -51,13 +141,7 @@ static int build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h
 
   // (charge, mz, id, ordinal) order; id comparison through id_rank (search.cpp:37-46, :30-33)
   std::vector<uint32_t> order(n);
-  std::iota(order.begin(), order.end(), 0u);
-  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-    if (charge[a] != charge[b]) return charge[a] < charge[b];
-    if (mz[a] != mz[b]) return mz[a] < mz[b];
-    if (id_rank && id_rank[a] != id_rank[b]) return id_rank[a] < id_rank[b];
-    return a < b;
-  });
+  HB_TRY(device_sort_order(ctx, n, mz, charge, id_rank, order.data()));
 
   lib.h_mz.resize(n);
   lib.h_ordinal = order;
