@@ -17,19 +17,21 @@
 //   [k-chunk][row][128 bytes] with the 16-byte units of every row XOR-swizzled by (row & 7): a
 //   tile of R consecutive rows of one k-chunk is then ONE contiguous R*128-byte block that is
 //   already in the SWIZZLE_128B K-major layout tcgen05.mma wants, so a stage of the pipeline is
-//   two cp.async.bulk copies (no tensor map needed) completing on an mbarrier.
+//   two cp.async.bulk copies (no tensor map needed) completing on an mbarrier.  Two operand
+//   encodings (TcMode): int8 (kind::i8, 128 dimensions per 128-byte row, N = 256, 4 stages) and
+//   e2m1 (kind::mxf4 with unit block scales, 256 dimensions per row, N = 224, 5 stages; default).
 // * queries are sorted by window start (search.cu) and cut into tiles of 128 = the 128 TMEM lanes;
-//   the library rows a tile needs (union of its windows) are cut into 256-row MMA tiles aligned
-//   to absolute multiples of 256, so that different query tiles fetch identical blocks (L2 hits).
-// * one CTA = 6 warps: warp 0 issues the bulk copies (4-stage ring, 48 KB per stage), one thread
-//   of warp 1 issues the MMAs (4 x K=32 per stage) into one of two 128x256 int32 accumulators
-//   in TMEM, warps 2-5 drain the other accumulator: lane = query, column = library row; every
-//   thread keeps the running best of its query with the exact 3-level key and masks columns
-//   outside the query's own window.  The drain (256 columns) costs ~2 % of the 64-stage K loop
-//   at D = 8192 and overlaps with the next tile's MMAs.
-// * work items (query tile x strip of row tiles) are planned on the device (tc_plan_*_kernel) and
-//   ordered so that CTAs running at the same time share both query and row tiles in L2; the whole
-//   search is stream-ordered, without a host round trip.
+//   the library rows a tile needs (union of its windows) are cut into N-row MMA tiles aligned to
+//   absolute multiples of N, so that different query tiles fetch identical blocks (L2 hits).
+// * one CTA per SM, 6 warps: warp 0 draws work items and issues the bulk copies, one thread of
+//   warp 1 issues the MMAs (4 per stage) into one of two 128 x N accumulators in TMEM, warps 2-5
+//   drain the other accumulator: lane = query, column = library row; every thread keeps the
+//   running best (or the k <= 16 best, in registers) of its query with the exact 3-level key and
+//   masks columns outside the query's own window.  The drain overlaps with the next tile's MMAs.
+// * work items (query tile x strip of row tiles) are planned on the device (tc_plan_*_kernel),
+//   ordered (group of query tiles, strip, tile) and handed out dynamically in that order, so that
+//   the CTAs running at any moment share both query and row tiles in L2; the whole search is
+//   stream-ordered, without a host round trip.
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
