@@ -746,6 +746,7 @@ static int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint6
       KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
       if (k == 1) HB_DIRECT_LAUNCH(1);
       else if (k <= 4) HB_DIRECT_LAUNCH(4);
+      else if (k <= 8) HB_DIRECT_LAUNCH(8);
       else HB_DIRECT_LAUNCH(16);
     }
 #undef HB_DIRECT_LAUNCH

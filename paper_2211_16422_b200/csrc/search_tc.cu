@@ -1071,6 +1071,9 @@ int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, c
   if (k <= 4)
     return f ? tc_search_sorted_mode<true, 4>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride)
              : tc_search_sorted_mode<false, 4>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride);
+  if (k <= 8)
+    return f ? tc_search_sorted_mode<true, 8>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride)
+             : tc_search_sorted_mode<false, 8>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride);
   return f ? tc_search_sorted_mode<true, kTcMaxK>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride)
            : tc_search_sorted_mode<false, kTcMaxK>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride);
 }
