@@ -1001,6 +1001,8 @@ static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, u
         std::max<uint64_t>(pc.target_items, (uint64_t(n_tiles) * pc.tiles_total + pc.max_strip - 1) / pc.max_strip) + slack;
     const uint64_t by_memory = std::max<uint64_t>((4ull << 30) / (size_t(kTcM) * k * sizeof(Cand)), slack + 4ull * ctx->sm_count);
     pc.item_cap = static_cast<uint32_t>(std::min<uint64_t>(std::min(by_shape, by_memory), 0x7fffffffull));
+    if (const char* e = getenv("HOMS_B200_TC_ITEM_CAP"))  // development / test knob: force the capacity-bound plan
+      pc.item_cap = static_cast<uint32_t>(std::min<uint64_t>(pc.item_cap, std::max<uint64_t>(slack + 1, atoi(e))));
     pc.pad = 0;
     HB_TRY(ensure(ctx, ctx->scratch[kScrTcPlan], tc_plan_bytes(n_tiles, pc.item_cap)));
     void* d_plan = ctx->scratch[kScrTcPlan].p;

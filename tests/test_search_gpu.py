@@ -326,6 +326,35 @@ def test_many_queries_span_planning_batches(hb, best_oracle):
     oix.close()
 
 
+def test_planner_under_a_tight_item_capacity(hb, monkeypatch):
+    """The device planner must never emit more work items than the item / partial arrays hold: with
+    the capacity forced far below what the shape asks for (the path a huge top-16 search takes when
+    4 GB of partials is the limit) the strips get longer and the answers stay the same -- also when
+    the capacity is down at the planner's slack (2 items per query tile + 16) and every query tile
+    becomes a single item."""
+    rng = np.random.default_rng(61)
+    dim, n, nq = 256, 40000, 3000
+    words = U.random_hvs(rng, n, dim)
+    words[30000:] = words[:10000]
+    mz = np.round(rng.uniform(400.0, 1200.0, n), 2)
+    charge = rng.integers(2, 4, n).astype(np.uint8)
+    qw = words[rng.integers(0, n, nq)]
+    qmz = np.round(rng.uniform(380.0, 1220.0, nq), 2)
+    qch = rng.integers(2, 4, nq).astype(np.uint8)
+    tol = hb.Tolerance("dalton", 500.0)
+    with hb.Context(0) as c:
+        c.set_engine("tensor_fp4")
+        c.build_index(dim, words, mz, charge)
+        want = {k: c.search_batch(qw, qmz, qch, tol, k=k) for k in (1, 3)}
+        for cap in ("400", "120", "10"):
+            monkeypatch.setenv("HOMS_B200_TC_ITEM_CAP", cap)
+            for k in (1, 3):
+                got = c.search_batch(qw, qmz, qch, tol, k=k)
+                assert np.array_equal(got.ordinal, want[k].ordinal), (cap, k)
+                assert np.array_equal(got.raw_score, want[k].raw_score), (cap, k)
+        monkeypatch.delenv("HOMS_B200_TC_ITEM_CAP")
+
+
 def test_concurrent_callers(hb):
     """The reference's calls are synchronous and re-entrant.  Here: threads that
     share ONE context are serialised by its mutex, threads with their OWN contexts run on their own
