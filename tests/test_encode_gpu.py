@@ -169,6 +169,26 @@ def test_encode_fuzz_vs_oracle(hb, ctx, best_oracle):
     assert seen_ok > 500 and seen_bad > 500  # both outcomes are exercised
 
 
+def test_level_rows_beyond_shared_memory(hb, ctx, best_oracle):
+    """32 level rows of 4 KiB (D = 32768, Q = 30) exceed the 96 KB the encode kernel stages in shared
+    memory: the level slabs (and the no-vote row) then come from global memory through L1."""
+    rng = np.random.default_rng(12)
+    dim, levels = 32768, 30
+    pre, opre = hb.PreprocessConfig(max_peaks=40, min_peaks=3), PreCfg(max_peaks=40, min_peaks=3)
+    cb = _upload(hb, ctx, dim, dim // 2, levels, 3, hb.dimension(pre))
+    ocb = best_oracle.codebook_from_words(dim, levels, cb.position, cb.level)
+    spectra = []
+    for p in (0, 2, 3, 17, 33, 40, 41, 90):
+        idx = np.sort(rng.choice(np.arange(11000, 140000), p, replace=False))
+        spectra.append((idx * 0.01, np.round(rng.uniform(0.0, 1.0, p), 3)))
+    off, mz, it = U.csr(spectra)
+    words, ok = ctx.encode_batch(off, mz, it, pre)
+    ow, ook = best_oracle.encode_spectra(ocb, opre, off, mz, it)
+    best_oracle.free_codebook(ocb)
+    assert np.array_equal(ok, ook) and ok.sum() >= 5
+    assert np.array_equal(words, ow)
+
+
 def test_encode_vectors_random_vs_oracle(hb, ctx, best_oracle):  # test_encoder.cpp:132-139, wider
     rng = np.random.default_rng(21)
     for dim, n_bins, levels, max_n in ((128, 40, 16, 12), (64, 9, 2, 9), (1088, 300, 31, 300),
