@@ -229,13 +229,13 @@ def test_encode_ragged_and_large_spectra(hb, ctx, best_oracle):
     """Ragged inputs: empty spectra, thousands of raw peaks (top-N path), max_peaks > 255
     (16 counter planes), dimension sweep."""
     rng = np.random.default_rng(5)
-    for dim, max_peaks in ((1024, 50), (2048, 150), (8192, 50), (16384, 400), (192, 20)):
+    for dim, max_peaks in ((1024, 50), (2048, 150), (8192, 50), (16384, 400), (192, 20), (512, 3000)):
         pre = hb.PreprocessConfig(max_peaks=max_peaks, min_peaks=5)
         opre = PreCfg(max_peaks=max_peaks, min_peaks=5)
         cb = _upload(hb, ctx, dim, dim // 2, 16, 1, hb.dimension(pre))
         ocb = best_oracle.codebook_from_words(dim, 16, cb.position, cb.level)
         spectra = [(np.zeros(0), np.zeros(0))]
-        for p in (1, 4, 5, 49, 50, 51, 333, 2500):
+        for p in (1, 4, 5, 49, 50, 51, 333, 2500, 4000):
             idx = np.sort(rng.choice(np.arange(9000, 160000), p, replace=False))
             inten = np.round(rng.uniform(0, 1, p), 2)  # heavy ties
             spectra.append((idx * 0.01, inten))

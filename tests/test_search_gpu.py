@@ -121,7 +121,7 @@ def test_config1_search_and_cascade(hb, ctx, best_oracle):
     assert f"{fnv1a64_words(c['q_value'].view(np.uint64)):016x}" == fp["cascade_qvalue_fnv"]
 
 
-@pytest.mark.parametrize("dim", [64, 1024, 2048, 4096, 8192, 16384, 32768])
+@pytest.mark.parametrize("dim", [64, 1024, 2048, 4096, 8192, 16384, 32768, 65536])
 def test_random_library_vs_oracle(hb, ctx, best_oracle, dim):
     """Dimension sweep (BASELINE config 5 shapes, small n): random hypervectors, both tolerance
     kinds, clones for ties; top-1 vs the oracle's search_batch."""
