@@ -121,6 +121,61 @@ def test_config1_search_and_cascade(hb, ctx, best_oracle):
     assert f"{fnv1a64_words(c['q_value'].view(np.uint64)):016x}" == fp["cascade_qvalue_fnv"]
 
 
+def test_cascade_behaviours(hb, ctx, best_oracle):
+    """The reference's cascade tests (test_search.cpp:329-421) on every engine: exact matches are
+    accepted in the narrow stage with score D and q = 0; a +79.97 precursor shift strands the query
+    in the wide stage; stages whose top hits are all decoys accept nothing; every query is accepted
+    at most once, never on a decoy -- and the accepted list equals the oracle's each time."""
+    rng = np.random.default_rng(14)
+    dim = 1024
+    narrow, wide = hb.Tolerance("ppm", 20.0), hb.Tolerance("dalton", 500.0)
+
+    def refs(n, decoy_fraction):
+        words = U.random_hvs(rng, n, dim)
+        mz = rng.uniform(400.0, 1200.0, n)
+        charge = rng.integers(2, 4, n).astype(np.uint8)
+        decoy = (rng.uniform(0, 1, n) < decoy_fraction).astype(np.uint8)
+        return words, mz, charge, decoy, [f"ref_{i}" for i in range(n)]
+
+    def both(lib, qw, qmz, qch, fdr_q):
+        words, mz, charge, decoy, ids = lib
+        ctx.build_index(dim, words, mz, charge, ids=ids, is_decoy=decoy)
+        oix = best_oracle.build_index(dim, words, mz, charge, decoy, ids)
+        got = ctx.cascade_search(qw, qmz, qch, narrow, wide, fdr_q)
+        want = oix.cascade_search(qw, qmz, qch, ("ppm", 20.0), ("da", 500.0), fdr_q)
+        oix.close()
+        for key in ("query", "ordinal", "stage", "raw_score"):
+            assert np.array_equal(got[key], want[key]), key
+        assert np.array_equal(got["q_value"].view(np.uint64), want["q_value"].view(np.uint64))
+        return got
+
+    lib = refs(30, 0.0)                                   # :329-346
+    got = both(lib, lib[0][[3, 9]], lib[1][[3, 9]], lib[2][[3, 9]], 0.01)
+    assert list(got["query"]) == [0, 1] and list(got["ordinal"]) == [3, 9]
+    assert (got["stage"] == 0).all() and (got["raw_score"] == dim).all() and (got["q_value"] == 0.0).all()
+
+    lib = refs(30, 0.0)                                   # :348-375
+    got = both(lib, lib[0][[5]], lib[1][[5]] + 79.97, lib[2][[5]], 0.01)
+    assert list(got["ordinal"]) == [5] and list(got["stage"]) == [1] and list(got["raw_score"]) == [dim]
+
+    lib = refs(20, 1.0)                                   # :377-385 decoys only
+    got = both(lib, lib[0][[0, 7, 13]], lib[1][[0, 7, 13]], lib[2][[0, 7, 13]], 0.01)
+    assert len(got["query"]) == 0
+
+    lib = refs(200, 0.5)                                  # :387-421
+    pick = rng.integers(0, 200, 120)
+    qw, qmz, qch = lib[0][pick].copy(), lib[1][pick].copy(), lib[2][pick].copy()
+    qmz[1::3] += 40.0
+    noise = np.arange(2, 120, 3)
+    qw[noise] = U.random_hvs(rng, len(noise), dim)
+    qmz[noise] = rng.uniform(450.0, 1150.0, len(noise))
+    qch[noise] = 2
+    got = both(lib, qw, qmz, qch, 0.05)
+    assert len(set(got["query"])) == len(got["query"]) <= 120
+    assert not lib[3][got["ordinal"]].any()
+    assert set(got["stage"]) <= {0, 1}
+
+
 @pytest.mark.parametrize("dim", [64, 1024, 2048, 4096, 8192, 16384, 32768, 65536])
 def test_random_library_vs_oracle(hb, ctx, best_oracle, dim):
     """Dimension sweep (BASELINE config 5 shapes, small n): random hypervectors, both tolerance
