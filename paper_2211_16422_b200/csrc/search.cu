@@ -719,24 +719,33 @@ static int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint6
   HB_TRY(run_bounds(ctx, n, d_subset, q.d_mz.as<double>(), q.d_charge.as<uint8_t>(), tol, d_first,
                     d_last, d_has));
 
-  // sort slots by window start (upper 32 key bits)
-  HB_TRY(ensure(ctx, ctx->scratch[kScrKeysAlt], n * 8));
-  HB_TRY(ensure(ctx, ctx->scratch[kScrValsAlt], n * 4));
-  size_t cub_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, static_cast<const uint64_t*>(nullptr),
-                                  static_cast<uint64_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
-                                  static_cast<uint32_t*>(nullptr), static_cast<int>(n), 32, 64, ctx->stream);
-  HB_TRY(ensure(ctx, ctx->scratch[kScrCub], cub_bytes));
-  HB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(
-                   ctx->scratch[kScrCub].p, cub_bytes, ctx->scratch[kScrKeys].as<uint64_t>(),
-                   ctx->scratch[kScrKeysAlt].as<uint64_t>(), ctx->scratch[kScrVals].as<uint32_t>(),
-                   ctx->scratch[kScrValsAlt].as<uint32_t>(), static_cast<int>(n), 32, 64, ctx->stream));
-  const uint64_t* keys = ctx->scratch[kScrKeysAlt].as<uint64_t>();
-  const uint32_t* vals = ctx->scratch[kScrValsAlt].as<uint32_t>();
-
   const bool tensor_ok = ctx->engine != HOMS_B200_ENGINE_POPC && ctx->engine != HOMS_B200_ENGINE_DIRECT && tc_available(ctx);
-  if (k <= tc_max_topk() && (ctx->engine == HOMS_B200_ENGINE_DIRECT ||
-                             (ctx->engine == HOMS_B200_ENGINE_AUTO && tensor_ok && direct_is_cheaper(ctx, n, tol)))) {
+  const bool use_direct =
+      k <= tc_max_topk() && (ctx->engine == HOMS_B200_ENGINE_DIRECT ||
+                             (ctx->engine == HOMS_B200_ENGINE_AUTO && tensor_ok && direct_is_cheaper(ctx, n, tol)));
+  // Sort the slots by window start (upper 32 key bits): neighbours then share library rows on chip.
+  // The direct engine skips it when the windows are so sparse that neighbours would share nothing
+  // anyway (expected rows read < rows resident: every row comes from HBM once either way).
+  const bool sparse = use_direct && expected_window_rows(lib, tol) * static_cast<double>(n) < static_cast<double>(lib.n);
+  const uint64_t* keys = ctx->scratch[kScrKeys].as<uint64_t>();
+  const uint32_t* vals = ctx->scratch[kScrVals].as<uint32_t>();
+  if (!sparse) {
+    HB_TRY(ensure(ctx, ctx->scratch[kScrKeysAlt], n * 8));
+    HB_TRY(ensure(ctx, ctx->scratch[kScrValsAlt], n * 4));
+    size_t cub_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, static_cast<const uint64_t*>(nullptr),
+                                    static_cast<uint64_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                    static_cast<uint32_t*>(nullptr), static_cast<int>(n), 32, 64, ctx->stream);
+    HB_TRY(ensure(ctx, ctx->scratch[kScrCub], cub_bytes));
+    HB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(
+                     ctx->scratch[kScrCub].p, cub_bytes, ctx->scratch[kScrKeys].as<uint64_t>(),
+                     ctx->scratch[kScrKeysAlt].as<uint64_t>(), ctx->scratch[kScrVals].as<uint32_t>(),
+                     ctx->scratch[kScrValsAlt].as<uint32_t>(), static_cast<int>(n), 32, 64, ctx->stream));
+    keys = ctx->scratch[kScrKeysAlt].as<uint64_t>();
+    vals = ctx->scratch[kScrValsAlt].as<uint32_t>();
+  }
+
+  if (use_direct) {
     const unsigned blocks = static_cast<unsigned>((n * 32 + 255) / 256);
 #define HB_DIRECT_LAUNCH(KM)                                                                                  \
   direct_search_kernel<KM><<<blocks, 256, 0, ctx->stream>>>(                                                  \
