@@ -160,17 +160,34 @@ def tol_text():
     return ("open +-%g Da" % TOL[1]) if TOL[0] == "da" else ("standard %g ppm" % TOL[1])
 
 
+GENERATOR = "auto"    # --generator
+
+
 def make_workload(name: str):
-    from paper_2211_16422_b200 import workload as wl
-    n_targets, n_query, dim, peaks, seed = wl.WORKLOADS[name]
+    """(library, queries, dim, generator): SURVEY 8(d)'s inputs from the reference's own generator when
+    oracle/_ref is built (it travels to the GPU box), else the numpy generator of the same distribution.
+    workload.py lives outside the product package: importing it maps no CUDA library."""
+    import workload as wl
+    t = time.time()
+    lib, qry, dim, gen = wl.make(name, GENERATOR)
     if DIM_OVERRIDE:
         dim = DIM_OVERRIDE
-    t = time.time()
-    lib = wl.synth_library(n_targets, peaks, 1.0, seed)
-    qry = wl.synth_queries(lib, n_query, seed=seed)
-    log(f"[bench] workload {name}: {len(lib['precursor_mz'])} library / {n_query} query spectra "
-        f"generated in {time.time() - t:.1f}s")
-    return lib, qry, dim
+    log(f"[bench] workload {name}: {len(lib['precursor_mz'])} library / {len(qry['precursor_mz'])} query spectra "
+        f"from the {gen} generator in {time.time() - t:.1f}s")
+    return lib, qry, dim, gen
+
+
+def bench_config(args, name, dim, n_lib, nq, gen):
+    """The `config` object of the JSON line: identical in both arms (the driver compares them), a
+    function of the command line and the workload only."""
+    n = max(1, args.gpus)
+    return {"workload": workload_name(name, dim, n_lib, nq),
+            "tolerance": "%s %g" % ("dalton" if TOL[0] == "da" else "ppm", TOL[1]), "k": args.k,
+            "generator": ("reference generate_benchmark (src/synth.cpp:114-197), SURVEY 8(d) inputs" if gen == "reference"
+                          else "numpy generator of the same distribution (oracle/_ref not built)"),
+            "l2_policy": f"inputs larger than L2 (library hypervectors {n_lib * ((dim + 63) // 64) * 8 / 1e9:.2f} GB >> 126 MB)",
+            "parallelism": (f"library sharded by contiguous m/z slices x{n}, queries replicated, "
+                            "all-gather + merge of 16-byte candidates") if n > 1 else "single GPU"}
 
 
 # --------------------------------------------------------------------------------------------
@@ -178,6 +195,8 @@ def make_workload(name: str):
 # --------------------------------------------------------------------------------------------
 
 def run_reference(args) -> None:
+    """The reference's own CPU implementation of the path (oracle/_ref = the unmodified sources compiled in
+    place) on all host cores.  Imports nothing of the product: no CUDA library is mapped in this process."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -185,7 +204,7 @@ def run_reference(args) -> None:
     kind = "ref" if ob.available("ref") else "port"
     oracle = ob.Oracle(kind)
     cores = os.cpu_count() or 1
-    lib, qry, dim = make_workload(args.workload)
+    lib, qry, dim, gen = make_workload(args.workload)
     pre = ob.PreCfg()
     t = time.time()
     cb = oracle.make_codebook(dim, dim // 2, 16, 1, oracle.dimension(pre))
@@ -198,6 +217,8 @@ def run_reference(args) -> None:
 
     def run(n):
         t0 = time.perf_counter()
+        # the reference is top-1 only: with --k > 1 this arm still times its search_batch, whose
+        # per-query scan is the same work
         ix.search_batch(qw[:n], qry["precursor_mz"][:n], qry["charge"][:n], tol, threads=cores, batch=8)
         return time.perf_counter() - t0
 
@@ -210,17 +231,17 @@ def run_reference(args) -> None:
     times = [run(sample) for _ in range(args.steps)]
     sec = sum(times) / len(times)
     value = sample / sec
+    what = (f"search_batch over the first {sample} queries against the full library, {cores} threads, "
+            "as-shipped flags (-O3, no -march)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic",
-        "config": {"workload": workload_name(args.workload, dim, len(lok), nq), "tolerance": "%s %g" % ("dalton" if TOL[0] == "da" else "ppm", TOL[1]),
-                   "k": 1, "sample_queries_per_step": sample},
+        "config": bench_config(args, args.workload, dim, len(lok), nq, gen),
+        "sample_queries_per_step": sample,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
-                         "kind": "reference" if kind == "ref" else "port",
-                         "sample": f"search_batch over the first {sample} queries against the full library, "
-                                   f"{cores} threads, as-shipped flags (-O3, no -march)"},
+                         "kind": "reference" if kind == "ref" else "port", "sample": what},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -235,6 +256,28 @@ def workload_name(name, dim, n_lib, nq):
 # our arm
 # --------------------------------------------------------------------------------------------
 
+def ncu_capture(match: dict):
+    """DRAM bytes / pipe utilisation of the dominant kernel from a committed `ncu --set full` capture of
+    this exact configuration (profiles/ncu_traffic.json, one entry per capture with its command), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            entries = json.load(f)["captures"]
+    except Exception:
+        return None
+    for e in entries:
+        if all(e.get("match", {}).get(k) == v for k, v in match.items()):
+            return e
+    return None
+
+
+def golden_digest(key: str):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "fingerprints.json")) as f:
+            return json.load(f).get("bench_result_digest", {}).get(key)
+    except Exception:
+        return None
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -245,6 +288,7 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == max(1, args.gpus), f"--gpus {args.gpus} but WORLD_SIZE={world} (main() starts the ranks itself)"
     # HOMS_BENCH_BACKEND=gloo: development smoke of the world > 1 path on a box with fewer GPUs than
     # ranks (ranks share devices, the gather is staged through the host); the product path is NCCL
     backend = os.environ.get("HOMS_BENCH_BACKEND", "nccl")
@@ -266,7 +310,7 @@ def run_ours(args) -> None:
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
 
-    lib, qry, dim = make_workload(args.workload)
+    lib, qry, dim, gen = make_workload(args.workload)
     n_lib, nq, k = len(lib["precursor_mz"]), len(qry["precursor_mz"]), args.k
     W = hb.words_for(dim)
     pre = hb.PreprocessConfig()
@@ -321,6 +365,11 @@ def run_ours(args) -> None:
     d_qch = torch.from_numpy(qry["charge"]).to(dev)
     ctx.queries_upload_dev(dim, nq, q_words.data_ptr(), d_qmz.data_ptr(), d_qch.data_ptr())
     ctx.synchronize()
+    keep_lib_host = rank == 0 and not args.no_cpu_baseline
+    lib_words_host = lib_words.cpu().numpy().view(np.uint64) if keep_lib_host else None
+    if world > 1:
+        del lib_words  # every rank encoded the whole library to cut its own slice; free the dense copy
+        torch.cuda.empty_cache()
 
     first, last, _ = ctx.select_candidates(qry["precursor_mz"], qry["charge"], tol)
     n_pairs = int((last - first).sum())
@@ -382,6 +431,12 @@ def run_ours(args) -> None:
     dev_score, dev_ord = ctx.candidates_decode(nq, k, final.data_ptr())
     import hashlib
     result_digest = hashlib.sha256(dev_ord.tobytes() + dev_score.tobytes()).hexdigest()[:16]  # same at every N
+    digest_key = f"{args.workload}/{gen}/D{dim}/{TOL[0]}{TOL[1]:g}/k{k}"
+    want_digest = golden_digest(digest_key)
+    if want_digest is not None and want_digest != result_digest:
+        raise AssertionError(f"result digest {result_digest} differs from the committed one {want_digest} "
+                             f"({digest_key}; tests/golden/fingerprints.json, pinned to the reference by "
+                             "tests/test_whole_config_gpu.py)")
 
     ran_on = ctx.last_engine()  # AUTO resolves per call (tensor_fp4, or direct for narrow top-1 windows)
 
@@ -412,6 +467,8 @@ def run_ours(args) -> None:
     e2e_value = nq / (sum(e2e_times) / len(e2e_times))
     if world == 1:
         assert np.array_equal(e2e_result.ordinal, dev_ord) and np.array_equal(e2e_result.raw_score, dev_score)
+    else:
+        assert np.array_equal(e2e_result[1], dev_ord) and np.array_equal(e2e_result[0], dev_score)
 
     # ---- cascade_search (search.cpp:219-248): the reference's `homs search` call ------------
     # narrow 20 ppm stage on all queries (direct engine), target-decoy FDR on the host, open stage on the
@@ -436,54 +493,64 @@ def run_ours(args) -> None:
     peak, peak_src = measured_peak_hbm()
     # per launch: this rank's share of the algorithmic bytes (1/world of the rows of every window)
     # (a step of more than 64 Ki queries is several launches, one per planning batch of the tensor
-    # engine, or k launches on the XOR+POPC engine: the step's work is spread over them)
+    # engine: the step's work is spread over them)
     launches_per_step = max(1.0, search_launches / max(1, args.steps))
     bytes_per_launch = bytes_alg / world / launches_per_step
     achieved = bytes_per_launch / (search_ms / max(1, search_launches) * 1e-3) / 1e9 if search_ms > 0 else 0.0
     kernel_ms = search_ms / max(1, search_launches)
-    # DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` captures of
-    # this exact command (dram__bytes_read.sum + dram__bytes_write.sum); only valid for the default
-    # single-GPU workload, null otherwise
-    ncu_traffic = {"tensor_fp4": (28.268047e9 + 0.117659e9, "profiles/r01_search_kernel_tensor_fp4_ncu_v4.csv"),
-                   "tensor": (260.988723e9 + 0.019967e9, "profiles/r01_search_kernel_tensor_ncu.csv (before the "
-                                                         "short-strip planner)"),
-                   "popc": (301.799285e9 + 0.036848e9, "profiles/r01_search_kernel_popc_ncu.csv")}
-    traffic, traffic_src = (ncu_traffic[ran_on] if (args.workload == "iprg2012" and world == 1 and k == 1
-                                                    and TOL == ("da", 500.0) and not DIM_OVERRIDE
-                                                    and ran_on in ncu_traffic) else (None, None))
-    tensor = ran_on in ("tensor", "tensor_fp4")
+    cap = ncu_capture({"workload": args.workload, "generator": gen, "engine": ran_on, "k": k,
+                       "tol": f"{TOL[0]}:{TOL[1]:g}", "dim": dim, "n_gpus": world})
+    traffic = (cap["dram_read_bytes"] + cap["dram_write_bytes"]) if cap else None
+    tensor = ran_on == "tensor_fp4"
     hbm_view = {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_per_launch,
                 "note": "SURVEY 8(d) algorithmic bytes (every candidate row read once per query) over the "
                         "kernel time; > peak is legitimate because queries share library tiles on chip"}
+    n_local = -(-n_lib // world)
     if tensor:
-        # int8 contraction: 2 ops per (pair, dimension); K is padded to a multiple of 128
-        fp4 = ran_on == "tensor_fp4"
-        kpad = (dim + 255) // 256 * 256 if fp4 else (dim + 127) // 128 * 128
+        # +-1 contraction: 2 ops per (pair, dimension); K is padded to a multiple of 256
+        kpad = (dim + 255) // 256 * 256
         ops = 2.0 * (n_pairs / world / launches_per_step) * kpad
-        tpeak, tsrc = measured_peak_tensor_i8()
-        if fp4:  # 4-bit operands: twice the 8-bit rate (9 vs 4.5 PFLOP/s nominal)
-            tpeak, tsrc = 2.0 * tpeak, tsrc.replace("2 x", "4 x")
         ach = ops / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else 0.0
-        # the same MMA shape issued back to back with no memory traffic, on this box, right now
-        probe_ops, probe_ms = ctx.tensor_peak_probe("tensor_fp4" if fp4 else "tensor", 0.5)
-        probe = {"value": probe_ops / 1e12, "unit": "TFLOP/s", "frac": ach / (probe_ops / 1e12),
-                 "source": "in-situ probe: bare tcgen05.mma issue loop of the kernel's shape on all SMs, "
-                           f"no memory traffic, {probe_ms:.0f} ms under the power cap "
-                           "(homs_b200_tensor_peak_probe)"}
-        roofline = {"bound": "tensor", "achieved": ach, "peak": tpeak, "unit": "TFLOP/s", "frac": ach / tpeak,
-                    "traffic": traffic, "traffic_source": traffic_src, "peak_source": tsrc, "peak_probe": probe, "kernel": "tc_search_kernel",
-                    "kernel_ms_per_launch": kernel_ms,
+        # the ceiling: the same MMA shape issued back to back with no memory traffic, on this box, in this
+        # run (MEASURED_PEAKS.json holds no 4-bit figure; 4 x the bf16 numbers is a nominal scaling)
+        probe_ops, probe_ms = ctx.tensor_peak_probe("tensor_fp4", 0.5)
+        nominal = {}
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                mp_ = json.load(f)
+            for key, label in (("bf16_tflops", "4 x measured burst dense bf16"),
+                               ("bf16_tflops_sustained", "4 x measured sustained dense bf16")):
+                if mp_.get(key):
+                    nominal[label] = {"value": 4.0 * float(mp_[key]), "frac": ach / (4.0 * float(mp_[key]))}
+        except Exception:
+            nominal["4 x 1400 TFLOP/s sustained dense bf16 (B200_PROFILING.md fallback)"] = {"value": 5600.0, "frac": ach / 5600.0}
+        # what one launch must read from HBM at least: the e2m1 image of this rank's rows once and the
+        # expanded queries once (128-byte rows of 256 dimensions)
+        compulsory = (kpad // 256) * 128.0 * (n_local + nq / launches_per_step)
+        roofline = {"bound": "tensor", "achieved": ach, "peak": probe_ops / 1e12, "unit": "TFLOP/s",
+                    "frac": ach / (probe_ops / 1e12),
+                    "peak_source": "measured in this run: bare tcgen05.mma kind::mxf4 issue loop of the kernel's "
+                                   f"shape (M128 N224 K64) on all SMs, no memory traffic, {probe_ms:.0f} ms under the "
+                                   "power cap (homs_b200_tensor_peak_probe)",
+                    "peak_nominal": nominal,
+                    "traffic": traffic, "compulsory_bytes": compulsory,
+                    "traffic_over_compulsory": traffic / compulsory if traffic else None,
+                    "traffic_source": cap and {"file": cap.get("source"), "command": cap.get("command")},
+                    "tensor_pipe_active_pct_ncu": cap and cap.get("tensor_pipe_active_pct"),
+                    "kernel": "tc_search_kernel", "kernel_ms_per_launch": kernel_ms,
                     "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
                     "algorithmic_ops_per_launch": ops, "pairs_per_launch": n_pairs / world / launches_per_step,
                     "launches_per_step": launches_per_step,
-                    "note": ("e2m1 tensor ops (tcgen05 kind::mxf4, unit block scales)" if fp4 else
-                             "int8 tensor ops (tcgen05 kind::i8)") + " counted over the candidate pairs of "
-                            "the windows only; masked columns of edge tiles are not counted",
+                    "note": "e2m1 tensor ops (tcgen05 kind::mxf4, unit block scales) counted over the candidate "
+                            "pairs of the windows only; masked columns of edge tiles are not counted",
                     "hbm_view": hbm_view}
     else:
+        compulsory = n_local * (dim // 8 + 12.0) + nq * (dim // 8 + 9.0)
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                    "frac": achieved / peak, "traffic": traffic, "compulsory_bytes": compulsory,
+                    "traffic_over_compulsory": traffic / compulsory if traffic else None,
+                    "traffic_source": cap and {"file": cap.get("source"), "command": cap.get("command")},
                     "peak_source": peak_src, "kernel": "direct_search_kernel" if ran_on == "direct" else "search_kernel",
                     "kernel_ms_per_launch": kernel_ms,
                     "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
@@ -492,10 +559,12 @@ def run_ours(args) -> None:
 
     # ---- CPU baseline: the compiled reference on this box's cores, bounded sample ----------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(lib, qry, dim, lib_words, hq, dev_score[:, 0], dev_ord[:, 0],
-                               ctx if cascade is not None else None, hb)
+            cpu = cpu_baseline(lib, qry, dim, lib_words_host, hq, dev_score, dev_ord, k,
+                               ctx if cascade is not None else None, hb, quick=world > 1)
+        except AssertionError:
+            raise
         except Exception as exc:  # the baseline is a report, never a reason to lose the bench line
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
                    "sample": f"failed: {exc!r}"}
@@ -504,27 +573,28 @@ def run_ours(args) -> None:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": (("e2m1 (+-1 expansion of the packed u64 bits, unit block scales), f32 accumulate (exact)" if ran_on == "tensor_fp4" else "s8 (+-1 expansion of the packed u64 bits), s32 accumulate") if tensor else "u64"), "data": "synthetic",
-            "config": {"workload": workload_name(args.workload, dim, n_lib, nq), "tolerance": "%s %g" % ("dalton" if TOL[0] == "da" else "ppm", TOL[1]),
-                       "k": k, "candidate_pairs_per_step": n_pairs,
-                       "engine": {"tensor_fp4": "tensor (tcgen05 mxf4 e2m1)", "tensor": "tensor (tcgen05 int8)", "popc": "popc",
-                                  "direct": "direct (warp per query, XOR+POPC)"}.get(ran_on, ran_on),
-                       "l2_policy": "inputs larger than L2 (library hypervectors "
-                                    f"{n_lib * W * 8 / 1e9:.2f} GB >> 126 MB)",
-                       "parallelism": (f"library sharded by m/z slices x{world}, queries replicated, "
-                                       "all-gather + merge of 16-byte candidates"
-                                       + ("" if backend == "nccl" else " [ranks SHARE GPUs, gather through the host "
-                                          "(gloo): functional check, not a scaling measurement]"))
-                                      if world > 1 else "single GPU"},
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": ("e2m1 (+-1 expansion of the packed u64 bits, unit block scales), f32 accumulate (exact)"
+                      if tensor else "u64"), "data": "synthetic",
+            "config": bench_config(args, args.workload, dim, n_lib, nq, gen),
+            "candidate_pairs_per_step": n_pairs,
+            "engine": {"tensor_fp4": "tensor (tcgen05 mxf4 e2m1)", "popc": "popc",
+                       "direct": "direct (warp per query, XOR+POPC)"}.get(ran_on, ran_on),
+            "exchange": (None if world == 1 else "NCCL all_gather_into_tensor + merge kernel" if backend == "nccl" else
+                         "ranks SHARE GPUs, gather through the host (gloo): functional check, not a scaling measurement"),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
-            "result_digest": result_digest, "cascade": cascade,
+            "result_digest": result_digest,
+            "result_digest_check": ("no committed digest for " + digest_key) if want_digest is None else
+                                   "equals the committed digest (tests/golden/fingerprints.json: " + digest_key + ")",
+            "cascade": cascade,
             "encode": {"spectra_per_s": n_lib / ((pre_ms + enc_ms) * 1e-3), "preprocess_ms": pre_ms,
                        "encode_ms": enc_ms, "spectra": n_lib, "peaks": lib["peaks"]},
         }
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
@@ -536,7 +606,7 @@ def run_encode(args) -> None:
 
     import paper_2211_16422_b200 as hb
     from paper_2211_16422_b200 import capi
-    from paper_2211_16422_b200 import workload as wl
+    import workload as wl
 
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -682,7 +752,7 @@ def run_encode(args) -> None:
 def synth_mgf_text(n_spectra: int, peaks: int, seed: int = 6):
     """An MGF image of the synthetic library shape, formatted with vectorised digit arithmetic:
     'BEGIN IONS / TITLE / PEPMASS / CHARGE / <peaks> / END IONS' blocks, peak lines 'dddd.dd000 d.dddddd'."""
-    from paper_2211_16422_b200 import workload as wl
+    import workload as wl
     lib = wl.synth_library(n_spectra // 2, peaks, 1.0, seed)
     n = len(lib["precursor_mz"])
     mz_c = np.rint(lib["mz"] * 100).astype(np.int64)                  # 0.01 Th grid
@@ -825,13 +895,14 @@ def run_mgf(args) -> None:
     ctx.close()
 
 
-def cpu_baseline(lib, qry, dim, lib_words, hq, dev_score, dev_ord, ctx=None, hb=None):
+def cpu_baseline(lib, qry, dim, lw, hq, dev_score, dev_ord, k, ctx=None, hb=None, quick=False):
+    """The compiled reference (oracle/_ref) on this box's cores over a bounded query prefix, with bit-exact
+    parity of the GPU results asserted on that prefix.  quick (N > 1 runs): a short parity sample only."""
     from oracle import binding as ob
     kind = "ref" if ob.available("ref") else "port"
     oracle = ob.Oracle(kind)
     cores = os.cpu_count() or 1
     t = time.time()
-    lw = lib_words.cpu().numpy().view(np.uint64)
     ix = oracle.build_index(dim, lw, lib["precursor_mz"], lib["charge"], lib["is_decoy"], lib["ids"])
     log(f"[bench] reference index built on the host in {time.time() - t:.1f}s")
     tol = TOL
@@ -843,15 +914,24 @@ def cpu_baseline(lib, qry, dim, lib_words, hq, dev_score, dev_ord, ctx=None, hb=
 
     probe = min(len(hq), 2 * cores)
     t_probe, _ = run(probe)
-    sample = int(max(cores, min(len(hq), probe * 15.0 / max(t_probe, 1e-6))))
+    sample = int(max(cores, min(len(hq), probe * (3.0 if quick else 15.0) / max(t_probe, 1e-6))))
     sec, (has, score, ordinal, _) = run(sample)
-    parity = bool(np.array_equal(score, dev_score[:sample]) and np.array_equal(ordinal, dev_ord[:sample]))
+    parity = bool(np.array_equal(score, dev_score[:sample, 0]) and np.array_equal(ordinal, dev_ord[:sample, 0]))
     out = {"value": sample / sec, "unit": UNIT, "cores": cores,
            "kind": "reference" if kind == "ref" else "port",
            "sample": f"search_batch over the first {sample} queries against the full library, {cores} threads, "
                      "as-shipped flags (-O3, no -march)",
            "parity_with_gpu_on_sample": "bit-exact" if parity else "MISMATCH"}
-    if ctx is not None and TOL == ("da", 500.0):
+    if k > 1:  # the reference is top-1 only: ranks 2..k against its scan generalised to a full sort (the C port)
+        port = ob.Oracle("port")
+        pix = port.build_index(dim, lw, lib["precursor_mz"], lib["charge"], lib["is_decoy"], lib["ids"])
+        m = min(sample, 32)
+        ps, po = pix.search_topk(hq[:m], qry["precursor_mz"][:m], qry["charge"][:m], tol, k)
+        same = bool(np.array_equal(ps, dev_score[:m]) and np.array_equal(po, dev_ord[:m]))
+        out["topk_parity"] = f"top-{k} lists of the first {m} queries " + ("bit-exact vs the full-sort oracle" if same else "MISMATCH")
+        parity = parity and same
+        pix.close()
+    if ctx is not None and TOL == ("da", 500.0) and not quick:
         # cascade_search on the same prefix: identical accepted list (ids, stage, score, q-value bits)
         t0 = time.perf_counter()
         want = ix.cascade_search(hq[:sample], qry["precursor_mz"][:sample], qry["charge"][:sample], ("ppm", 20.0),
@@ -866,7 +946,7 @@ def cpu_baseline(lib, qry, dim, lib_words, hq, dev_score, dev_ord, ctx=None, hb=
                           "parity_with_gpu_on_sample": "identical accepted list" if same else "MISMATCH"}
         if not same:
             raise AssertionError("GPU cascade differs from the reference on the CPU-baseline sample")
-    if ob.available("ref_v3"):
+    if ob.available("ref_v3") and not quick:
         o3 = ob.Oracle("ref_v3")
         ix3 = o3.build_index(dim, lw, lib["precursor_mz"], lib["charge"], lib["is_decoy"], lib["ids"])
         n3 = min(len(hq), sample * 4)
@@ -881,6 +961,23 @@ def cpu_baseline(lib, qry, dim, lib_words, hq, dev_score, dev_ord, ctx=None, hb=
     return out
 
 
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: start N ranks of this same command under
+    torch.distributed.run (one process per GPU, NCCL), exactly as the driver's torchrun form would."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # leave the NCCL init lines (transport, NVLS) visible on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or n) // n)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    log("[bench] starting", n, "ranks:", " ".join(cmd))
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -888,27 +985,37 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="iprg2012")
+    ap.add_argument("--generator", default="auto", choices=["auto", "reference", "numpy"],
+                    help="reference = generate_benchmark of the reference (SURVEY 8(d) inputs; needs oracle/_ref), "
+                         "numpy = independent generator of the same distribution; auto = reference when available")
     ap.add_argument("--k", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--encode-spectra", type=int, default=1_000_000,
-                    help="--workload encode: spectra per step")
+    ap.add_argument("--encode-spectra", type=int, default=10_000_000,
+                    help="--workload encode: spectra per step (BASELINE config 4: 10 M)")
     ap.add_argument("--mgf-spectra", type=int, default=400_000, help="--workload mgf: spectra in the text image")
-    ap.add_argument("--engine", default="auto", choices=["auto", "popc", "tensor", "tensor_fp4", "direct"],
-                    help="top-1 search engine (auto = tensor cores, e2m1 operands)")
+    ap.add_argument("--engine", default="auto", choices=["auto", "popc", "tensor_fp4", "direct"],
+                    help="search engine (auto = tensor cores with e2m1 operands, or direct for narrow windows)")
     ap.add_argument("--dim", type=int, default=0, help="override the hypervector dimension (config 5 sweep)")
     ap.add_argument("--tol", default="da:500", help="tolerance KIND:VALUE, KIND in {da, ppm} (config 5 sweep)")
     args = ap.parse_args()
-    global TOL, DIM_OVERRIDE
+    global TOL, DIM_OVERRIDE, GENERATOR
     kind, val = args.tol.split(":")
     TOL = ("da" if kind in ("da", "dalton") else "ppm", float(val))
     DIM_OVERRIDE = args.dim or None
+    GENERATOR = args.generator
+    args.gpus = max(1, args.gpus)
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
-    if args.workload == "encode" and args.impl == "ours":
+    if args.impl == "reference":
+        run_reference(args)  # rank 0 only under a launcher; no ranks are started for it
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.workload == "encode":
         run_encode(args)
-    elif args.workload == "mgf" and args.impl == "ours":
+    elif args.workload == "mgf":
         run_mgf(args)
-    elif args.impl == "reference":
-        run_reference(args)
+    elif args.workload == "pipeline":
+        run_pipeline(args)
     else:
         run_ours(args)
 

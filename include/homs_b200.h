@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define HOMS_B200_ABI_VERSION 1
+#define HOMS_B200_ABI_VERSION 2
 
 enum {
   HOMS_B200_OK = 0,
@@ -93,6 +93,27 @@ int homs_b200_abi_version(void);
 /* Creates a context on CUDA device `device`.  *out is NULL on failure; the message is then
  * available through homs_b200_last_error(NULL). */
 int homs_b200_ctx_create(int device, homs_b200_ctx** out);
+/* CUDA devices visible to this process. */
+int homs_b200_device_count(int* out_count);
+/* ONE handle over n devices of this process: SURVEY.md 8(b)'s `ctx_create(device_ids[], n)`.  It takes
+ * the place of the reference's only parallel construct, the thread fan-out of parallel_for
+ * (include/homs/parallel.hpp:20-48, used by search_batch search.cpp:175-181 and encode_spectra
+ * pipeline.cpp:66-73): every call below accepts the handle unchanged and fans out over the GPUs.
+ *   - library_upload* / library_load_cache / library_build_from_spectra (pass shard 0 of 1): slice g of
+ *     every charge bucket (contiguous precursor-m/z ranges) becomes resident on devices[g], metadata
+ *     is replicated;
+ *   - queries_* / search_batch / search_resident* / cascade_*: queries are replicated, every device
+ *     searches its slice, the 16-byte candidate records are stored by each device's last kernel
+ *     straight into the first device's memory (peer-mapped stores over NVLink) and merged there;
+ *     results are identical to a single-device context;
+ *   - codebook_upload: replicated; encode_batch: spectra split evenly over the devices;
+ *   - everything else (window_bounds, preprocess_batch, encode_vectors, mgf_*, cache_write, _dev
+ *     encoders) runs on devices[0].  Device pointers passed to _dev calls belong to devices[0].
+ * devices may repeat (aliases of one GPU: the same code path, used by the single-GPU tests).
+ * n_devices == 1 yields a plain context.  kernel_time() of a group is the sum over its devices. */
+int homs_b200_ctx_create_multi(const int* devices, int n_devices, homs_b200_ctx** out);
+/* Devices behind a handle (1 for homs_b200_ctx_create). */
+int homs_b200_ctx_device_count(const homs_b200_ctx* ctx);
 void homs_b200_ctx_destroy(homs_b200_ctx* ctx);
 const char* homs_b200_last_error(const homs_b200_ctx* ctx);
 /* Adopt an external cudaStream_t for all subsequent work (NULL: back to the context's own). */
@@ -104,17 +125,17 @@ uint64_t homs_b200_ctx_launch_count(const homs_b200_ctx* ctx);
  * kernels is bracketed by CUDA events on the context's stream.  kernel_time() synchronises, returns
  * the summed duration and launch count since the last call, and resets the counters. */
 enum { HOMS_B200_KERNEL_SEARCH = 0, HOMS_B200_KERNEL_ENCODE = 1, HOMS_B200_KERNEL_PREPROCESS = 2 };
-/* Search engine: POPC (XOR + POPC on the integer pipes) or a tcgen05 tensor-core contraction of the
- * +-1 expanded hypervectors (similarity = (dim + dot) / 2, exact): TENSOR with int8 operands,
- * TENSOR_FP4 with e2m1 operands and unit block scales (twice the rate, half the bytes).
- * AUTO = TENSOR_FP4, or DIRECT for calls with narrow windows.  All engines are bit-exact.  The tensor engines keep up to 16 candidates per
- * query (k <= 16); larger k (up to HOMS_B200_MAX_TOPK) runs on the POPC engine.
- * Set it BEFORE library_upload: the tensor image of the library (8x / 4x the packed size) is built
- * there for the selected engine, and POPC skips it. */
+/* Search engine: POPC (XOR + POPC on the integer pipes), DIRECT (warp per query) or TENSOR_FP4, a
+ * tcgen05 tensor-core contraction of the +-1 expanded hypervectors (similarity = (dim + dot) / 2,
+ * exact) with e2m1 operands and unit block scales.  AUTO = TENSOR_FP4, or DIRECT for calls with narrow
+ * windows.  All engines are bit-exact.
+ * Set it BEFORE library_upload: the tensor image of the library (4x the packed size) is built
+ * there, and POPC / DIRECT skip it. */
 enum {
   HOMS_B200_ENGINE_AUTO = 0,
   HOMS_B200_ENGINE_POPC = 1,
-  HOMS_B200_ENGINE_TENSOR = 2,     /* int8 operands, int32 accumulate (kind::i8) */
+  HOMS_B200_ENGINE_TENSOR = 2,     /* alias of TENSOR_FP4 (the int8 operand encoding of ABI 1 was removed:
+                                      twice the image, 2.3x slower, identical results) */
   HOMS_B200_ENGINE_TENSOR_FP4 = 3, /* e2m1 operands with unit block scales, fp32 accumulate (kind::mxf4) */
   HOMS_B200_ENGINE_DIRECT = 4      /* one warp per query over exactly its window rows (XOR + POPC, warp-level
                                       top-k, k <= 16): the engine for windows of a few dozen rows (ppm
@@ -130,7 +151,7 @@ int homs_b200_ctx_kernel_time(homs_b200_ctx* ctx, int which, double* out_total_m
                               uint64_t* out_launches);
 /* Measurement aid (no reference counterpart): sustained issue rate of the tensor engine's MMA shape
  * on this device with every SM busy and no memory traffic -- the ceiling bench.py quotes the search
- * kernel against.  engine: HOMS_B200_ENGINE_TENSOR or _TENSOR_FP4; runs for about `seconds`. */
+ * kernel against.  engine: HOMS_B200_ENGINE_TENSOR_FP4; runs for about `seconds`. */
 int homs_b200_tensor_peak_probe(homs_b200_ctx* ctx, int engine, double seconds, double* out_ops_per_s,
                                 double* out_kernel_ms);
 
@@ -286,7 +307,8 @@ int homs_b200_window_bounds(homs_b200_ctx* ctx, uint64_t nq, const double* q_mz,
  * reference's search_one).  Entry j of query i: out_raw_score[i*k+j] (Hamming similarity) and
  * out_ordinal[i*k+j] (input position of the library entry; HOMS_B200_NO_HIT and score 0 when
  * fewer than j+1 candidates exist).  out_first / out_last (nullable) as in window_bounds.
- * Requires a single-shard library; sharded contexts use the _resident/_merge calls below.
+ * The library must be whole behind this handle (one device, or a multi-device context); a context
+ * that holds one shard of a library split across PROCESSES uses the _resident/_merge calls below.
  * HOMS_B200_ERR_INVARIANT when query_dim differs from the library's (search.cpp:107-109). */
 int homs_b200_search_batch(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq,
                            const uint64_t* q_words, const double* q_mz, const uint8_t* q_charge,

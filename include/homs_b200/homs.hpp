@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <istream>
 #include <iterator>
@@ -146,6 +147,8 @@ struct DefaultApi {
   using SearchOptions = types::SearchOptions;
 };
 
+constexpr int kConfiguredDevices = -1;  // `device` argument: use the configured device set (set_devices)
+
 namespace detail {
 
 template <class Api>
@@ -164,12 +167,71 @@ inline void check(int rc, const homs_b200_ctx* ctx) {
 struct CtxDeleter { void operator()(homs_b200_ctx* c) const { homs_b200_ctx_destroy(c); } };
 using CtxPtr = std::unique_ptr<homs_b200_ctx, CtxDeleter>;
 
+// The devices a call uses when its `device` argument is left at kConfiguredDevices: set_devices(), or
+// the environment variable HOMS_B200_DEVICES ("0,1,2,3" or "all") read on first use, else device 0.
+// More than one device makes every index / encoder a multi-device context (homs_b200_ctx_create_multi):
+// build_index shards the library over them and search_batch / cascade_search / encode_spectra fan out
+// with no change at the call site -- the GPU form of the reference's `threads` argument
+// (parallel.hpp:20-48).
+
+inline std::vector<int>& device_list() {
+  static std::vector<int> devices = [] {
+    std::vector<int> d;
+    if (const char* e = std::getenv("HOMS_B200_DEVICES")) {
+      const std::string v(e);
+      if (v == "all") {
+        int n = 0;
+        if (homs_b200_device_count(&n) == HOMS_B200_OK)
+          for (int i = 0; i < n; ++i) d.push_back(i);
+      } else {
+        std::size_t pos = 0;
+        while (pos < v.size()) {
+          std::size_t end = v.find(',', pos);
+          if (end == std::string::npos) end = v.size();
+          if (end > pos) d.push_back(std::atoi(v.substr(pos, end - pos).c_str()));
+          pos = end + 1;
+        }
+      }
+    }
+    if (d.empty()) d.push_back(0);
+    return d;
+  }();
+  return devices;
+}
+
+inline unsigned& device_generation() {
+  static unsigned generation = 0;
+  return generation;
+}
+
 template <class Api>
 inline CtxPtr make_ctx(int device) {
   homs_b200_ctx* raw = nullptr;
-  const int rc = homs_b200_ctx_create(device, &raw);
+  int rc;
+  if (device == kConfiguredDevices) {
+    const std::vector<int> devices = device_list();
+    rc = homs_b200_ctx_create_multi(devices.data(), static_cast<int>(devices.size()), &raw);
+  } else {
+    rc = homs_b200_ctx_create(device, &raw);
+  }
   if (rc != HOMS_B200_OK) raise<Api>(rc, nullptr);
   return CtxPtr(raw);
+}
+
+// 64-bit content hash of a list of hypervectors (every word; four independent multiply-xor lanes)
+template <class Range>
+inline std::uint64_t content_hash(const Range& rows, std::uint64_t seed) {
+  std::uint64_t h[4] = {seed ^ 0x9E3779B97F4A7C15ull, seed ^ 0xC2B2AE3D27D4EB4Full, seed ^ 0x165667B19E3779F9ull,
+                        seed ^ 0x27D4EB2F165667C5ull};
+  for (const auto& r : rows) {
+    const auto w = r.words();
+    std::size_t i = 0;
+    for (; i + 4 <= w.size(); i += 4)
+      for (int l = 0; l < 4; ++l) h[l] = (h[l] ^ w[i + l]) * 0x100000001B3ull + (h[l] >> 29);
+    for (; i < w.size(); ++i) h[0] = (h[0] ^ w[i]) * 0x100000001B3ull + (h[0] >> 29);
+    h[1] += w.size();
+  }
+  return (h[0] ^ (h[1] << 17 | h[1] >> 47)) * 0x9E3779B97F4A7C15ull ^ (h[2] + (h[3] << 31 | h[3] >> 33));
 }
 
 template <class Cfg>
@@ -206,24 +268,28 @@ inline std::vector<std::uint64_t> flatten(const Range& items, std::size_t W, Get
   return flat;
 }
 
-// One context per device for encoding; remembers which codebook is resident.
+// One context per device (slot 0: the configured device set) for encoding; remembers which codebook is
+// resident by a hash of its whole content.
 template <class Api>
 struct Encoder {
   CtxPtr ctx;
   std::mutex mu;
-  const void* cb_data = nullptr;
+  bool cb_resident = false;
   std::uint64_t cb_tag = 0;
+  unsigned generation = 0;
 
   static Encoder& on(int device) {
     static std::mutex table_mu;
     static std::vector<std::unique_ptr<Encoder>> table;
     std::lock_guard<std::mutex> g(table_mu);
-    if (table.size() <= static_cast<std::size_t>(device)) table.resize(device + 1);
-    if (!table[device]) {
-      table[device] = std::make_unique<Encoder>();
-      table[device]->ctx = make_ctx<Api>(device);
+    const std::size_t slot = device == kConfiguredDevices ? 0 : static_cast<std::size_t>(device) + 1;
+    if (table.size() <= slot) table.resize(slot + 1);
+    if (!table[slot] || (slot == 0 && table[slot]->generation != device_generation())) {
+      table[slot] = std::make_unique<Encoder>();  // (re)created after set_devices()
+      table[slot]->ctx = make_ctx<Api>(device);
+      table[slot]->generation = device_generation();
     }
-    return *table[device];
+    return *table[slot];
   }
 
   void ensure_codebook(const typename Api::Codebook& cb) {
@@ -231,23 +297,36 @@ struct Encoder {
     const std::size_t W = (std::size_t(dim) + 63) / 64;
     if (cb.position.size() != cb.spectrum_dims || cb.level.size() != std::size_t(cb.config.levels) + 1)
       throw typename Api::InvariantError("encode: codebook shape does not match its configuration");
-    // identity of the resident codebook: storage address + a few sampled words
-    std::uint64_t tag = (std::uint64_t(dim) << 32) ^ cb.spectrum_dims ^ (cb.config.seed * 0x9E3779B97F4A7C15ull);
-    for (std::size_t i = 0; i < cb.position.size(); i += cb.position.size() / 7 + 1)
-      tag = tag * 1099511628211ull ^ cb.position[i].words()[0];
-    for (const auto& l : cb.level) tag = tag * 1099511628211ull ^ l.words()[W - 1];
-    if (cb_data == static_cast<const void*>(cb.position.data()) && cb_tag == tag) return;
+    if (dim < 1) throw typename Api::InvariantError("encode: codebook dimension must be positive");
+    for (const auto& r : cb.position)
+      if (r.words().size() != W) throw typename Api::InvariantError("encode: codebook shape does not match its configuration");
+    for (const auto& r : cb.level)
+      if (r.words().size() != W) throw typename Api::InvariantError("encode: codebook shape does not match its configuration");
+    // identity of the resident codebook: a hash of EVERY position and level word (a few ms for the
+    // 28.7 MB table of D = 8192 -- less than the flatten + upload it saves), never addresses or samples
+    const std::uint64_t tag = content_hash(cb.position, (std::uint64_t(dim) << 32) ^ cb.spectrum_dims) ^
+                              content_hash(cb.level, cb.config.levels) * 0xD6E8FEB86659FD93ull;
+    if (cb_resident && cb_tag == tag) return;
     const auto pos = flatten(cb.position, W, [](const auto& h) -> const auto& { return h; });
     const auto lvl = flatten(cb.level, W, [](const auto& h) -> const auto& { return h; });
     check<Api>(homs_b200_codebook_upload(ctx.get(), dim, cb.spectrum_dims, cb.config.levels, pos.data(),
                                          lvl.data()),
                ctx.get());
-    cb_data = cb.position.data();
+    cb_resident = true;
     cb_tag = tag;
   }
 };
 
 }  // namespace detail
+
+// Devices used by every call whose `device` argument is left at its default (see detail::device_list).
+// Call it before the indexes / encoders it should apply to are created, from one thread.
+inline void set_devices(std::vector<int> devices) {
+  if (devices.empty()) devices.push_back(0);
+  detail::device_list() = std::move(devices);
+  ++detail::device_generation();
+}
+inline const std::vector<int>& devices() { return detail::device_list(); }
 
 // ---- LibraryIndex (search.hpp:39-66): the device-resident index --------------------------------
 // Owns a context whose library is the charge-partitioned, m/z-sorted matrix built by
@@ -279,7 +358,7 @@ typename Api::EncodeOutcome encode_spectra(std::span<const typename Api::RawSpec
                                            const typename Api::Codebook& codebook,
                                            const typename Api::PreprocessConfig& preprocess,
                                            unsigned /*threads*/ = 1, std::size_t /*batch_size*/ = 0,
-                                           int device = 0) {
+                                           int device = kConfiguredDevices) {
   auto& enc = detail::Encoder<Api>::on(device);
   std::lock_guard<std::mutex> g(enc.mu);
   typename Api::EncodeOutcome outcome;
@@ -321,7 +400,7 @@ typename Api::EncodeOutcome encode_spectra(std::span<const typename Api::RawSpec
 // ---- encode (encoder.cpp:19-55) on one vectorized spectrum --------------------------------------
 template <class Api = DefaultApi>
 typename Api::Hypervector encode(const typename Api::SpectrumVector& sv, const typename Api::Codebook& codebook,
-                                 int device = 0) {
+                                 int device = kConfiguredDevices) {
   auto& enc = detail::Encoder<Api>::on(device);
   std::lock_guard<std::mutex> g(enc.mu);
   if (sv.dims != codebook.spectrum_dims)  // encoder.cpp:20-22
@@ -337,7 +416,7 @@ typename Api::Hypervector encode(const typename Api::SpectrumVector& sv, const t
 
 // ---- build_index (search.cpp:17-60) -------------------------------------------------------------
 template <class Api = DefaultApi>
-LibraryIndex<Api> build_index(std::span<const typename Api::EncodedSpectrum> refs, int device = 0) {
+LibraryIndex<Api> build_index(std::span<const typename Api::EncodedSpectrum> refs, int device = kConfiguredDevices) {
   if (refs.empty()) throw typename Api::InvariantError("build_index: library is empty");  // search.cpp:18
   LibraryIndex<Api> index;
   index.dim_ = refs.front().hv.size_bits();
@@ -481,7 +560,7 @@ template <class Api = DefaultApi>
 LibraryIndex<Api> encode_and_index(std::span<const typename Api::RawSpectrum> spectra,
                                    const typename Api::Codebook& codebook,
                                    const typename Api::PreprocessConfig& preprocess,
-                                   std::size_t* unprocessable = nullptr, int device = 0) {
+                                   std::size_t* unprocessable = nullptr, int device = kConfiguredDevices) {
   if (spectra.empty()) throw typename Api::InvariantError("build_index: library is empty");  // search.cpp:18
   LibraryIndex<Api> index;
   index.dim_ = codebook.config.dim;
@@ -533,7 +612,7 @@ LibraryIndex<Api> encode_and_index(std::span<const typename Api::RawSpectrum> sp
 // Same spectra, same doubles, same first ParseError (line and message) as the reference's sequential
 // parser; the text is parsed on the device.  Api::ParseError(line, message) when the traits name one.
 template <class Api = DefaultApi>
-std::vector<typename Api::RawSpectrum> parse_mgf(std::istream& in, const std::string& decoy_prefix, int device = 0) {
+std::vector<typename Api::RawSpectrum> parse_mgf(std::istream& in, const std::string& decoy_prefix, int device = kConfiguredDevices) {
   const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
   auto& enc = detail::Encoder<Api>::on(device);
   std::lock_guard<std::mutex> g(enc.mu);

@@ -8,12 +8,12 @@ from . import capi  # noqa: F401  (raises if the CUDA library is missing)
 from .host import (  # noqa: F401
     CacheCorruptError, CacheFormatError, Codebook, ConfigError, Context, CudaError, EncodeOutcome,
     EncoderConfig, HomsError, InvariantError, Match, ParseError, PreprocessConfig, StaleCacheError, Tolerance,
-    cache_parse, compute_fdr_curve, dimension, id_ranks, make_codebook, quantize_intensity, words_for,
+    cache_parse, compute_fdr_curve, device_count, dimension, id_ranks, make_codebook, quantize_intensity, words_for,
 )
 
 __all__ = [
     "CacheCorruptError", "CacheFormatError", "Codebook", "ConfigError", "Context", "CudaError",
     "EncodeOutcome", "EncoderConfig", "HomsError", "InvariantError", "Match", "ParseError", "PreprocessConfig",
-    "StaleCacheError", "Tolerance", "cache_parse", "compute_fdr_curve", "dimension", "id_ranks",
+    "StaleCacheError", "Tolerance", "cache_parse", "compute_fdr_curve", "device_count", "dimension", "id_ranks",
     "make_codebook", "quantize_intensity", "words_for",
 ]

@@ -77,6 +77,9 @@ def _decl(name, restype, argtypes):
 
 abi_version = _decl("homs_b200_abi_version", _I, [])
 ctx_create = _decl("homs_b200_ctx_create", _I, [_I, _P(_VP)])
+device_count = _decl("homs_b200_device_count", _I, [_P(_I)])
+ctx_create_multi = _decl("homs_b200_ctx_create_multi", _I, [_P(_I), _I, _P(_VP)])
+ctx_device_count = _decl("homs_b200_ctx_device_count", _I, [_VP])
 ctx_destroy = _decl("homs_b200_ctx_destroy", None, [_VP])
 last_error = _decl("homs_b200_last_error", C.c_char_p, [_VP])
 ctx_set_stream = _decl("homs_b200_ctx_set_stream", _I, [_VP, _VP])

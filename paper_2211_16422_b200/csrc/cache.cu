@@ -503,6 +503,14 @@ int homs_b200_library_load_cache(homs_b200_ctx* ctx, const void* image, uint64_t
                      id_len.data(), nullptr, nullptr));
   // hypervector block: image -> device, checksum on the device (cache.cpp:192-209)
   const auto* bytes = static_cast<const unsigned char*>(image);
+  struct BlockGuard {  // the staging block is up to several GB: never keep it as scratch, on any path out
+    homs_b200_ctx* c;
+    ~BlockGuard() {
+      cudaSetDevice(c->device);
+      cudaStreamSynchronize(c->stream);
+      release(c->scratch[kScrCacheBlock]);
+    }
+  } block_guard{ctx};
   HB_TRY(ensure(ctx, ctx->scratch[kScrCacheBlock], lay.hv_bytes));
   if (lay.hv_bytes)
     HB_CUDA(ctx, cudaMemcpyAsync(ctx->scratch[kScrCacheBlock].p, bytes + lay.hv_offset, lay.hv_bytes,
@@ -521,10 +529,8 @@ int homs_b200_library_load_cache(homs_b200_ctx* ctx, const void* image, uint64_t
   });
   for (uint64_t p = 0; p < n; ++p) rank[order[p]] = static_cast<uint32_t>(p);
   // the block is dense little-endian u64 rows == the layout library_upload_dev takes
-  const int rc = library_build_from_device(ctx, enc->dim, n, ctx->scratch[kScrCacheBlock].as<uint64_t>(),
-                                           mz.data(), charge.data(), rank.data(), shard_index, shard_count);
-  release(ctx->scratch[kScrCacheBlock]);  // up to several GB: do not keep it as scratch
-  return rc;
+  return library_build_from_device(ctx, enc->dim, n, ctx->scratch[kScrCacheBlock].as<uint64_t>(), mz.data(),
+                                   charge.data(), rank.data(), shard_index, shard_count);
 }
 
 static int cache_write_common(homs_b200_ctx* ctx, const homs_b200_preprocess_config* pre,

@@ -6,6 +6,8 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -63,13 +65,11 @@ struct Library {
   // device (owned through ctx buffers)
   DevBuf d_mz, d_id_rank, d_ord_of_rank, d_mz_local, d_id_rank_local, d_words, d_buckets,
       d_bucket_of_charge;
-  // +-1 int8 image of the resident rows for the tensor-core engine (search_tc.cu):
-  // (int8 or e2m1 nibbles): [n_kc][x_rows][128 B], every 128-byte row pre-swizzled for a
-  // SWIZZLE_128B K-major UMMA operand
+  // +-1 e2m1 image of the resident rows for the tensor-core engine (search_tc.cu):
+  // [n_kc][x_rows][128 B], every 128-byte row pre-swizzled for a SWIZZLE_128B K-major UMMA operand
   DevBuf d_x;
-  uint64_t x_rows = 0;  // n_local rounded up to the row tile (256 / 240), plus one all-zero tile of slack
-  uint32_t n_kc = 0;    // k-chunks: ceil(dim / 128) for int8, ceil(dim / 256) for fp4
-  bool x_fp4 = false;   // operand encoding of d_x
+  uint64_t x_rows = 0;  // n_local rounded up to the 224-row tile, plus one all-zero tile of slack
+  uint32_t n_kc = 0;    // k-chunks: ceil(dim / 256)
 };
 
 struct Queries {
@@ -92,6 +92,14 @@ struct Codebook {
   bool ready = false;
   uint32_t dim = 0, n_bins = 0, levels = 0, W = 0, S = 0;
   DevBuf d_pos, d_lvl;  // padded rows
+};
+
+struct GroupWorkers;  // group.cu: one issuing thread per non-leading member of a multi-GPU group
+
+// development knobs of the tensor-engine planner, read from the environment ONCE per context
+// (homs_b200_ctx_create), never on the search path; 0 = the built-in choice
+struct TcKnobs {
+  uint32_t group_tiles = 0, items_per_sm = 0, max_strip = 0, item_cap = 0;
 };
 
 }  // namespace hb
@@ -123,6 +131,16 @@ struct homs_b200_ctx {
   // optional per-kernel timing (homs_b200_ctx_profile)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[3];
+  hb::TcKnobs knobs;
+  // ---- multi-GPU group (homs_b200_ctx_create_multi, group.cu) --------------------------------
+  // members[0] == this (the leader, on devices[0]); members[g >= 1] are owned single-device contexts
+  // that are only ever driven through the leader (under the leader's mutex).  Empty: a plain context.
+  std::vector<homs_b200_ctx*> members;
+  std::vector<uint8_t> peer_ok;      // member g's device addresses the leader's memory (same device, or P2P on)
+  std::vector<cudaEvent_t> ev_join;  // member g's work of the current group call is complete (g >= 1)
+  cudaEvent_t ev_fork = nullptr;     // leader's stream has reached the start of the current group call
+  hb::DevBuf group_gather;           // leader: [n_members][n][k] candidate records, written by the members
+  hb::GroupWorkers* workers = nullptr;
 };
 
 namespace hb {
@@ -187,14 +205,14 @@ enum Scratch {
   kScrMgfText, kScrMgfTiles, kScrMgfLines, kScrMgfBlocks, kScrMgfPeaks, kScrMgfHard, kScrIndexSort
 };
 
-// Tensor-core engine (search_tc.cu).  expand: packed rows -> +-1 int8 swizzled image.
+// Tensor-core engine (search_tc.cu).  expand: packed rows -> +-1 e2m1 swizzled image.
 int tc_expand_library(homs_b200_ctx* ctx);
 // top-k (k <= tc_max_topk()) of n sorted slots (keys/vals as produced by bounds + radix sort) -> out[slot * k_stride + j]
 int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
                      const uint32_t* d_vals, Cand* d_out, uint32_t k, uint32_t k_stride);
 uint32_t tc_max_topk();
 bool tc_available(const homs_b200_ctx* ctx);
-int tc_peak_probe(homs_b200_ctx* ctx, int fp4, double seconds, double* out_ops_per_s, double* out_ms);
+int tc_peak_probe(homs_b200_ctx* ctx, double seconds, double* out_ops_per_s, double* out_ms);
 
 // dense host rows (W words) -> padded device rows (S words), zero padded.  Async on ctx->stream.
 int upload_rows(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* h_src, uint64_t n, uint32_t W,
@@ -222,5 +240,40 @@ struct Lock {
   explicit Lock(homs_b200_ctx* c) : g(c->mu) { cudaSetDevice(c->device); }
   std::lock_guard<std::mutex> g;
 };
+
+// ---- multi-GPU group (group.cu) -----------------------------------------------------------------
+inline bool is_group(const homs_b200_ctx* c) { return !c->members.empty(); }
+// runs fn(g) for every member: g = 0 on the calling thread, g >= 1 on that member's issuing thread
+// with its device current; returns the first non-OK code (the member's message copied to the leader)
+int group_for_each(homs_b200_ctx* leader, const std::function<int(uint32_t, homs_b200_ctx*)>& fn);
+// leader's stream -> every member's stream (work enqueued by members after this sees the leader's
+// earlier work) and back (the leader's later work sees the members')
+int group_fork(homs_b200_ctx* leader);
+int group_join(homs_b200_ctx* leader);
+void group_destroy_members(homs_b200_ctx* leader);
+int sync_all_locked(homs_b200_ctx* ctx);  // the context's stream, and every member's for a group  // no-op for a plain context
+
+// single-context building blocks the group composes (defined in search.cu / library.cu)
+int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const homs_b200_tolerance* tol,
+                      uint32_t k, Cand* d_out, uint64_t* d_first, uint64_t* d_last, uint8_t* d_has);
+int queries_set_locked(homs_b200_ctx* ctx, uint32_t dim, uint64_t nq, const uint64_t* words, const double* mz,
+                       const uint8_t* charge, bool on_device);
+int merge_launch(homs_b200_ctx* ctx, uint64_t n, uint32_t k, uint32_t n_parts, const Cand* d_parts, Cand* d_out);
+int library_build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h_words, const uint64_t* d_words_in,
+                  const double* mz, const uint8_t* charge, const uint32_t* id_rank, uint32_t shard_index,
+                  uint32_t shard_count, const uint32_t* row_of_entry);
+// the same operations on a plain context or on a group leader
+int search_any_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const homs_b200_tolerance* tol,
+                      uint32_t k, Cand* d_out, uint64_t* d_first, uint64_t* d_last, uint8_t* d_has);
+int queries_set_any_locked(homs_b200_ctx* ctx, uint32_t dim, uint64_t nq, const uint64_t* words, const double* mz,
+                           const uint8_t* charge, bool on_device);
+int queries_replicate_locked(homs_b200_ctx* leader);  // leader's resident queries -> every other member
+int library_build_any(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h_words,
+                      const uint64_t* d_words_in, const double* mz, const uint8_t* charge, const uint32_t* id_rank,
+                      uint32_t shard_index, uint32_t shard_count, const uint32_t* row_of_entry);
+int codebook_upload_locked(homs_b200_ctx* ctx, uint32_t dim, uint32_t n_bins, uint32_t levels, const uint64_t* pos,
+                           const uint64_t* lvl);
+void ctx_free_resources(homs_b200_ctx* ctx);  // everything a single context owns (context.cu)
+int ctx_create_single(int device, homs_b200_ctx** out);
 
 }  // namespace hb

@@ -2,6 +2,7 @@
 // codebook generation, FDR curve).  Reference lines cited are under /root/reference/proj/core/.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <random>
@@ -94,15 +95,12 @@ int repack_rows_dev(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src, 
   return HOMS_B200_OK;
 }
 
-}  // namespace hb
+static uint32_t env_u32(const char* name) {
+  const char* e = getenv(name);
+  return e ? static_cast<uint32_t>(std::max(1, atoi(e))) : 0u;
+}
 
-using namespace hb;
-
-extern "C" {
-
-int homs_b200_abi_version(void) { return HOMS_B200_ABI_VERSION; }
-
-int homs_b200_ctx_create(int device, homs_b200_ctx** out) {
+int ctx_create_single(int device, homs_b200_ctx** out) {
   if (!out) return set_error(nullptr, HOMS_B200_ERR_ARGUMENT, "ctx_create: out is null");
   *out = nullptr;
   int count = 0;
@@ -131,27 +129,61 @@ int homs_b200_ctx_create(int device, homs_b200_ctx** out) {
     return set_error(nullptr, HOMS_B200_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
   }
   ctx->stream = ctx->own_stream;
+  // planner development knobs: read here, once, never on the search path
+  ctx->knobs.group_tiles = env_u32("HOMS_B200_TC_GROUP");
+  ctx->knobs.items_per_sm = env_u32("HOMS_B200_TC_ITEMS_PER_SM");
+  ctx->knobs.max_strip = env_u32("HOMS_B200_TC_MAX_STRIP");
+  ctx->knobs.item_cap = env_u32("HOMS_B200_TC_ITEM_CAP");
   *out = ctx;
   return HOMS_B200_OK;
 }
 
-void homs_b200_ctx_destroy(homs_b200_ctx* ctx) {
-  if (!ctx) return;
+void ctx_free_resources(homs_b200_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (auto& b : ctx->scratch) release(b);
   for (DevBuf* b : {&ctx->cb.d_pos, &ctx->cb.d_lvl, &ctx->lib.d_mz, &ctx->lib.d_id_rank,
                     &ctx->lib.d_ord_of_rank, &ctx->lib.d_mz_local, &ctx->lib.d_id_rank_local,
                     &ctx->lib.d_words, &ctx->lib.d_buckets, &ctx->lib.d_bucket_of_charge, &ctx->lib.d_x,
-                    &ctx->q.d_words, &ctx->q.d_mz, &ctx->q.d_charge})
+                    &ctx->q.d_words, &ctx->q.d_mz, &ctx->q.d_charge, &ctx->group_gather})
     release(*b);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (int i = 0; i < 2; ++i)
     for (cudaEvent_t e : {ctx->pipe_in_ready[i], ctx->pipe_done[i], ctx->pipe_out_free[i]})
       if (e) cudaEventDestroy(e);
+  for (auto& list : ctx->prof)
+    for (auto& pr : list) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
   if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
   if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
   cudaStreamDestroy(ctx->own_stream);
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" {
+
+int homs_b200_abi_version(void) { return HOMS_B200_ABI_VERSION; }
+
+int homs_b200_ctx_create(int device, homs_b200_ctx** out) { return ctx_create_single(device, out); }
+
+int homs_b200_device_count(int* out_count) {
+  if (!out_count) return set_error(nullptr, HOMS_B200_ERR_ARGUMENT, "device_count: out is null");
+  *out_count = 0;
+  const cudaError_t e = cudaGetDeviceCount(out_count);
+  if (e != cudaSuccess)
+    return set_error(nullptr, HOMS_B200_ERR_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  return HOMS_B200_OK;
+}
+
+void homs_b200_ctx_destroy(homs_b200_ctx* ctx) {
+  if (!ctx) return;
+  group_destroy_members(ctx);  // no-op for a plain context
+  ctx_free_resources(ctx);
   delete ctx;
 }
 
@@ -173,11 +205,11 @@ int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine) {
   HB_REQUIRE(ctx, engine >= HOMS_B200_ENGINE_AUTO && engine <= HOMS_B200_ENGINE_DIRECT,
              HOMS_B200_ERR_ARGUMENT, "set_engine: unknown engine");
   const bool tensor = engine == HOMS_B200_ENGINE_TENSOR || engine == HOMS_B200_ENGINE_TENSOR_FP4;
-  HB_REQUIRE(ctx, !tensor || !ctx->lib.ready ||
-                      (tc_available(ctx) && ctx->lib.x_fp4 == (engine == HOMS_B200_ENGINE_TENSOR_FP4)),
-             HOMS_B200_ERR_STATE,
-             "set_engine: the resident library was uploaded without the tensor image of this engine");
+  HB_REQUIRE(ctx, !tensor || !ctx->lib.ready || tc_available(ctx), HOMS_B200_ERR_STATE,
+             "set_engine: the resident library was uploaded without the tensor image");
+  if (engine == HOMS_B200_ENGINE_TENSOR) engine = HOMS_B200_ENGINE_TENSOR_FP4;  // one tensor encoding (e2m1)
   ctx->engine = engine;
+  for (size_t g = 1; g < ctx->members.size(); ++g) ctx->members[g]->engine = engine;
   return HOMS_B200_OK;
 }
 
@@ -186,16 +218,21 @@ int homs_b200_ctx_last_engine(const homs_b200_ctx* ctx) { return ctx ? ctx->last
 int homs_b200_ctx_synchronize(homs_b200_ctx* ctx) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
-  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  return HOMS_B200_OK;
+  return sync_all_locked(ctx);
 }
 
-uint64_t homs_b200_ctx_launch_count(const homs_b200_ctx* ctx) { return ctx ? ctx->launches : 0; }
+uint64_t homs_b200_ctx_launch_count(const homs_b200_ctx* ctx) {
+  if (!ctx) return 0;
+  uint64_t total = ctx->launches;
+  for (size_t g = 1; g < ctx->members.size(); ++g) total += ctx->members[g]->launches;
+  return total;
+}
 
 int homs_b200_ctx_profile(homs_b200_ctx* ctx, int enable) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
   ctx->profiling = enable != 0;
+  for (size_t g = 1; g < ctx->members.size(); ++g) ctx->members[g]->profiling = enable != 0;
   return HOMS_B200_OK;
 }
 
@@ -203,18 +240,26 @@ int homs_b200_ctx_kernel_time(homs_b200_ctx* ctx, int which, double* out_total_m
                               uint64_t* out_launches) {
   if (!ctx || which < 0 || which > 2) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
-  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   double total = 0.0;
-  for (auto& pr : ctx->prof[which]) {
-    float ms = 0.f;
-    HB_CUDA(ctx, cudaEventElapsedTime(&ms, pr.first, pr.second));
-    total += ms;
-    cudaEventDestroy(pr.first);
-    cudaEventDestroy(pr.second);
+  uint64_t count = 0;
+  const size_t n_members = std::max<size_t>(1, ctx->members.size());
+  for (size_t g = 0; g < n_members; ++g) {  // a group reports the sum over its members
+    homs_b200_ctx* m = g == 0 ? ctx : ctx->members[g];
+    cudaSetDevice(m->device);
+    HB_CUDA(ctx, cudaStreamSynchronize(m->stream));
+    for (auto& pr : m->prof[which]) {
+      float ms = 0.f;
+      HB_CUDA(ctx, cudaEventElapsedTime(&ms, pr.first, pr.second));
+      total += ms;
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    count += m->prof[which].size();
+    m->prof[which].clear();
   }
+  cudaSetDevice(ctx->device);
   if (out_total_ms) *out_total_ms = total;
-  if (out_launches) *out_launches = ctx->prof[which].size();
-  ctx->prof[which].clear();
+  if (out_launches) *out_launches = count;
   return HOMS_B200_OK;
 }
 
@@ -223,10 +268,10 @@ int homs_b200_tensor_peak_probe(homs_b200_ctx* ctx, int engine, double seconds, 
   if (!ctx || !out_ops_per_s) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
   HB_REQUIRE(ctx, engine == HOMS_B200_ENGINE_TENSOR || engine == HOMS_B200_ENGINE_TENSOR_FP4,
-             HOMS_B200_ERR_ARGUMENT, "tensor_peak_probe: engine must be TENSOR or TENSOR_FP4");
+             HOMS_B200_ERR_ARGUMENT, "tensor_peak_probe: engine must be TENSOR_FP4");
   HB_REQUIRE(ctx, seconds > 0.0 && seconds <= 10.0, HOMS_B200_ERR_ARGUMENT,
              "tensor_peak_probe: seconds must be in (0, 10]");
-  return tc_peak_probe(ctx, engine == HOMS_B200_ENGINE_TENSOR_FP4, seconds, out_ops_per_s, out_kernel_ms);
+  return tc_peak_probe(ctx, seconds, out_ops_per_s, out_kernel_ms);
 }
 
 // ---- host-only configuration --------------------------------------------------------------

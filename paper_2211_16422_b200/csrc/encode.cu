@@ -639,6 +639,17 @@ int homs_b200_codebook_upload(homs_b200_ctx* ctx, uint32_t dim, uint32_t n_bins,
                               const uint64_t* pos, const uint64_t* lvl) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
+  if (is_group(ctx))  // replicas of the codebook on every device (encoding needs no collective)
+    return group_for_each(ctx, [&](uint32_t, homs_b200_ctx* m) -> int {
+      return codebook_upload_locked(m, dim, n_bins, levels, pos, lvl);
+    });
+  return codebook_upload_locked(ctx, dim, n_bins, levels, pos, lvl);
+}
+
+}  // extern "C"
+
+int hb::codebook_upload_locked(homs_b200_ctx* ctx, uint32_t dim, uint32_t n_bins, uint32_t levels,
+                               const uint64_t* pos, const uint64_t* lvl) {
   HB_REQUIRE(ctx, pos && lvl, HOMS_B200_ERR_ARGUMENT, "codebook_upload: null codebook");
   HB_REQUIRE(ctx, dim >= 1 && n_bins >= 1 && levels >= 1, HOMS_B200_ERR_ARGUMENT,
              "codebook_upload: dim, n_bins and levels must be positive");
@@ -664,6 +675,8 @@ int homs_b200_codebook_upload(homs_b200_ctx* ctx, uint32_t dim, uint32_t n_bins,
   return HOMS_B200_OK;
 }
 
+extern "C" {
+
 int homs_b200_encode_batch_dev(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg,
                                uint64_t n, uint64_t n_peaks_total, const uint64_t* d_offsets,
                                const double* d_mz, const double* d_intensity,
@@ -684,6 +697,17 @@ int homs_b200_encode_batch(homs_b200_ctx* ctx, const homs_b200_preprocess_config
   HB_REQUIRE(ctx, n == 0 || (offsets && out_words && out_ok), HOMS_B200_ERR_ARGUMENT,
              "encode_batch: null argument");
   HB_REQUIRE(ctx, n == 0 || offsets[0] == 0, HOMS_B200_ERR_ARGUMENT, "encode_batch: offsets[0] must be 0");
+  if (is_group(ctx) && n >= 2 * ctx->members.size()) {
+    // spectra split evenly over the devices, every member streams its slice through its own
+    // three-stream pipeline (encode_spectra's thread fan-out, pipeline.cpp:66-73, across GPUs)
+    const uint64_t G = ctx->members.size();
+    const uint32_t W = ctx->cb.W;
+    return group_for_each(ctx, [&](uint32_t g, homs_b200_ctx* m) -> int {
+      const uint64_t a = n * g / G, b = n * (g + 1) / G;
+      return encode_pipeline(m, cfg, b - a, offsets + a, mz, intensity, nullptr, nullptr, out_words + a * W,
+                             out_ok + a);
+    });
+  }
   return encode_pipeline(ctx, cfg, n, offsets, mz, intensity, nullptr, nullptr, out_words, out_ok);
 }
 

@@ -131,6 +131,7 @@ int homs_b200_queries_from_spectra(homs_b200_ctx* ctx, const homs_b200_preproces
     HB_CUDA(ctx, cudaStreamSynchronize(st));  // host vectors above go out of scope
   }
   q.ready = true;
+  if (is_group(ctx)) HB_TRY(queries_replicate_locked(ctx));  // encoded on the leading device, searched on all
   return HOMS_B200_OK;
 }
 

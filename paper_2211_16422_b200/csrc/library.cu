@@ -119,13 +119,14 @@ static int device_sort_order(homs_b200_ctx* ctx, uint64_t n, const double* mz, c
   return HOMS_B200_OK;
 }
 
-static int build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h_words,
-                 const uint64_t* d_words_in, const double* mz, const uint8_t* charge,
-                 const uint32_t* id_rank, uint32_t shard_index, uint32_t shard_count,
-                 const uint32_t* row_of_entry = nullptr) {
+int library_build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h_words,
+                  const uint64_t* d_words_in, const double* mz, const uint8_t* charge,
+                  const uint32_t* id_rank, uint32_t shard_index, uint32_t shard_count,
+                  const uint32_t* row_of_entry) {
   HB_REQUIRE(ctx, n >= 1, HOMS_B200_ERR_INVARIANT, "build_index: library is empty");  // search.cpp:18
   HB_REQUIRE(ctx, dim >= 1, HOMS_B200_ERR_ARGUMENT, "build_index: dim must be positive");
-  HB_REQUIRE(ctx, n < 0xFFFFFFFFull, HOMS_B200_ERR_ARGUMENT, "build_index: more than 2^32-2 entries");
+  // the device radix sorts of the entry order count their items in an int
+  HB_REQUIRE(ctx, n <= 0x7FFFFFFFull, HOMS_B200_ERR_ARGUMENT, "build_index: more than 2^31-1 entries");
   HB_REQUIRE(ctx, mz && charge && (h_words || d_words_in), HOMS_B200_ERR_ARGUMENT,
              "build_index: null argument");
   HB_REQUIRE(ctx, shard_count >= 1 && shard_index < shard_count, HOMS_B200_ERR_ARGUMENT,
@@ -273,7 +274,7 @@ static int build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* h
 int library_build_from_device(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* d_words,
                               const double* mz, const uint8_t* charge, const uint32_t* id_rank,
                               uint32_t shard_index, uint32_t shard_count, const uint32_t* row_of_entry) {
-  return build(ctx, dim, n, nullptr, d_words, mz, charge, id_rank, shard_index, shard_count, row_of_entry);
+  return library_build_any(ctx, dim, n, nullptr, d_words, mz, charge, id_rank, shard_index, shard_count, row_of_entry);
 }
 
 }  // namespace hb
@@ -287,7 +288,7 @@ int homs_b200_library_upload(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const
                              const uint32_t* id_rank, uint32_t shard_index, uint32_t shard_count) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
-  return build(ctx, dim, n, words, nullptr, precursor_mz, charge, id_rank, shard_index, shard_count);
+  return library_build_any(ctx, dim, n, words, nullptr, precursor_mz, charge, id_rank, shard_index, shard_count, nullptr);
 }
 
 int homs_b200_library_upload_dev(homs_b200_ctx* ctx, uint32_t dim, uint64_t n,
@@ -296,7 +297,7 @@ int homs_b200_library_upload_dev(homs_b200_ctx* ctx, uint32_t dim, uint64_t n,
                                  uint32_t shard_index, uint32_t shard_count) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
-  return build(ctx, dim, n, nullptr, d_words, precursor_mz, charge, id_rank, shard_index, shard_count);
+  return library_build_any(ctx, dim, n, nullptr, d_words, precursor_mz, charge, id_rank, shard_index, shard_count, nullptr);
 }
 
 int homs_b200_library_bucket_count(const homs_b200_ctx* ctx, uint32_t* out_count) {
@@ -315,8 +316,9 @@ int homs_b200_library_bucket_info(const homs_b200_ctx* ctx, uint32_t which, uint
   const BucketDev& b = ctx->lib.buckets[which];
   if (out_charge) *out_charge = ctx->lib.bucket_charge[which];
   if (out_size) *out_size = b.size;
-  if (out_shard_begin) *out_shard_begin = b.shard_begin;
-  if (out_shard_end) *out_shard_end = b.shard_end;
+  // a multi-device context holds the whole bucket, spread over its members
+  if (out_shard_begin) *out_shard_begin = is_group(ctx) ? 0 : b.shard_begin;
+  if (out_shard_end) *out_shard_end = is_group(ctx) ? b.size : b.shard_end;
   return HOMS_B200_OK;
 }
 
@@ -332,9 +334,21 @@ int homs_b200_library_bucket_export(homs_b200_ctx* ctx, uint32_t which, double* 
   if (out_ordinal)
     std::copy(lib.h_ordinal.begin() + b.begin, lib.h_ordinal.begin() + b.begin + b.size, out_ordinal);
   if (out_words) {
-    HB_TRY(download_rows(ctx, out_words, lib.d_words.as<uint64_t>() + b.local_offset * lib.S,
-                         b.shard_end - b.shard_begin, lib.W, lib.S));
-    HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    // every member holds a contiguous slice of the bucket, in member order
+    const size_t n_members = std::max<size_t>(1, ctx->members.size());
+    for (size_t g = 0; g < n_members; ++g) {
+      homs_b200_ctx* m = g == 0 ? ctx : ctx->members[g];
+      const BucketDev& mb = m->lib.buckets[which];
+      cudaSetDevice(m->device);
+      const int rc = download_rows(m, out_words + (mb.shard_begin - (is_group(ctx) ? 0 : b.shard_begin)) * lib.W,
+                                   m->lib.d_words.as<uint64_t>() + mb.local_offset * lib.S,
+                                   mb.shard_end - mb.shard_begin, lib.W, lib.S);
+      if (rc != HOMS_B200_OK || cudaStreamSynchronize(m->stream) != cudaSuccess) {
+        cudaSetDevice(ctx->device);
+        return set_error(ctx, HOMS_B200_ERR_CUDA, "bucket_export: device -> host copy failed");
+      }
+    }
+    cudaSetDevice(ctx->device);
   }
   return HOMS_B200_OK;
 }

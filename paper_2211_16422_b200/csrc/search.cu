@@ -698,7 +698,7 @@ static int run_bounds(homs_b200_ctx* ctx, uint64_t n, const uint32_t* d_subset, 
 }
 
 // Full device pipeline for n slots; writes n*k candidates to d_out.
-static int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n,
+int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n,
                              const homs_b200_tolerance* tol, uint32_t k, Cand* d_out,
                              uint64_t* d_first, uint64_t* d_last, uint8_t* d_has) {
   const Library& lib = ctx->lib;
@@ -711,7 +711,8 @@ static int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint6
   HB_REQUIRE(ctx, q.dim == lib.dim, HOMS_B200_ERR_INVARIANT,
              "search_one: query dimensionality does not match index");
   if (n == 0) return HOMS_B200_OK;
-  HB_REQUIRE(ctx, n < 0xFFFFFFFFull, HOMS_B200_ERR_ARGUMENT, "search: too many queries in one call");
+  // the device radix sort of the query order counts its items in an int
+  HB_REQUIRE(ctx, n <= 0x7FFFFFFFull, HOMS_B200_ERR_ARGUMENT, "search: more than 2^31-1 queries in one call");
   const uint32_t row_bytes = lib.S * 8;
   const int qb = pick_qb(row_bytes);
   HB_REQUIRE(ctx, qb != 0, HOMS_B200_ERR_ARGUMENT, "search: dim above 65536 is not supported");
@@ -764,7 +765,7 @@ static int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint6
     return HOMS_B200_OK;
   }
   if (k <= tc_max_topk() && tensor_ok) {
-    ctx->last_engine = lib.x_fp4 ? HOMS_B200_ENGINE_TENSOR_FP4 : HOMS_B200_ENGINE_TENSOR;
+    ctx->last_engine = HOMS_B200_ENGINE_TENSOR_FP4;
     return tc_search_sorted(ctx, d_subset, n, keys, vals, d_out, k, k);
   }
   ctx->last_engine = HOMS_B200_ENGINE_POPC;
@@ -822,8 +823,8 @@ static int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint6
   return HOMS_B200_OK;
 }
 
-static int queries_set_locked(homs_b200_ctx* ctx, uint32_t dim, uint64_t nq, const uint64_t* words,
-                              const double* mz, const uint8_t* charge, bool on_device) {
+int queries_set_locked(homs_b200_ctx* ctx, uint32_t dim, uint64_t nq, const uint64_t* words,
+                       const double* mz, const uint8_t* charge, bool on_device) {
   Queries& q = ctx->q;
   q.ready = false;
   HB_REQUIRE(ctx, dim >= 1, HOMS_B200_ERR_ARGUMENT, "queries: dim must be positive");
@@ -842,6 +843,13 @@ static int queries_set_locked(homs_b200_ctx* ctx, uint32_t dim, uint64_t nq, con
     HB_CUDA(ctx, cudaMemcpyAsync(q.d_charge.p, charge, nq, kind, ctx->stream));
   }
   q.ready = true;
+  return HOMS_B200_OK;
+}
+
+int merge_launch(homs_b200_ctx* ctx, uint64_t n, uint32_t k, uint32_t n_parts, const Cand* d_parts, Cand* d_out) {
+  if (n == 0) return HOMS_B200_OK;
+  merge_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, ctx->stream>>>(n, k, n_parts, d_parts, d_out);
+  HB_LAUNCHED(ctx);
   return HOMS_B200_OK;
 }
 
@@ -901,9 +909,8 @@ int homs_b200_queries_upload(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq
                              const uint64_t* q_words, const double* q_mz, const uint8_t* q_charge) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
-  HB_TRY(queries_set_locked(ctx, query_dim, nq, q_words, q_mz, q_charge, false));
-  HB_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // caller may reuse its buffers
-  return HOMS_B200_OK;
+  HB_TRY(queries_set_any_locked(ctx, query_dim, nq, q_words, q_mz, q_charge, false));
+  return sync_all_locked(ctx);  // the caller may reuse its buffers
 }
 
 int homs_b200_queries_upload_dev(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq,
@@ -911,7 +918,7 @@ int homs_b200_queries_upload_dev(homs_b200_ctx* ctx, uint32_t query_dim, uint64_
                                  const uint8_t* d_q_charge) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
-  return queries_set_locked(ctx, query_dim, nq, d_q_words, d_q_mz, d_q_charge, true);
+  return queries_set_any_locked(ctx, query_dim, nq, d_q_words, d_q_mz, d_q_charge, true);
 }
 
 int homs_b200_search_resident_dev(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n_subset,
@@ -921,8 +928,7 @@ int homs_b200_search_resident_dev(homs_b200_ctx* ctx, const uint32_t* d_subset, 
   Lock lock(ctx);
   const uint64_t n = d_subset ? n_subset : ctx->q.nq;
   HB_REQUIRE(ctx, n == 0 || d_out, HOMS_B200_ERR_ARGUMENT, "search_resident: null output");
-  return search_dev_locked(ctx, d_subset, n, tol, k, reinterpret_cast<Cand*>(d_out), nullptr, nullptr,
-                           nullptr);
+  return search_any_locked(ctx, d_subset, n, tol, k, reinterpret_cast<Cand*>(d_out), nullptr, nullptr, nullptr);
 }
 
 int homs_b200_merge_candidates_dev(homs_b200_ctx* ctx, uint64_t n, uint32_t k, uint32_t n_parts,
@@ -933,10 +939,7 @@ int homs_b200_merge_candidates_dev(homs_b200_ctx* ctx, uint64_t n, uint32_t k, u
   HB_REQUIRE(ctx, n_parts >= 1 && n_parts <= 64, HOMS_B200_ERR_ARGUMENT, "merge: n_parts must be in [1, 64]");
   if (n == 0) return HOMS_B200_OK;
   HB_REQUIRE(ctx, d_parts && d_out, HOMS_B200_ERR_ARGUMENT, "merge: null argument");
-  merge_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, ctx->stream>>>(
-      n, k, n_parts, reinterpret_cast<const Cand*>(d_parts), reinterpret_cast<Cand*>(d_out));
-  HB_LAUNCHED(ctx);
-  return HOMS_B200_OK;
+  return merge_launch(ctx, n, k, n_parts, reinterpret_cast<const Cand*>(d_parts), reinterpret_cast<Cand*>(d_out));
 }
 
 int homs_b200_candidates_decode(homs_b200_ctx* ctx, uint64_t n, uint32_t k,
@@ -957,15 +960,16 @@ int homs_b200_search_batch(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq,
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;
   Lock lock(ctx);
   HB_REQUIRE(ctx, ctx->lib.ready, HOMS_B200_ERR_STATE, "search_batch: no library uploaded");
-  HB_REQUIRE(ctx, ctx->lib.shard_count == 1, HOMS_B200_ERR_STATE,
-             "search_batch: sharded library; use search_resident_dev + merge_candidates_dev");
+  HB_REQUIRE(ctx, ctx->lib.shard_count == 1 || is_group(ctx), HOMS_B200_ERR_STATE,
+             "search_batch: this context holds one shard of a library split across processes; use "
+             "search_resident_dev + an all-gather + merge_candidates_dev (or a multi-device context)");
   HB_REQUIRE(ctx, query_dim == ctx->lib.dim, HOMS_B200_ERR_INVARIANT,
              "search_one: query dimensionality does not match index");
   HB_TRY(check_tol(ctx, tol));
   HB_REQUIRE(ctx, k >= 1 && k <= HOMS_B200_MAX_TOPK, HOMS_B200_ERR_ARGUMENT, "search: k must be in [1, 64]");
   if (nq == 0) return HOMS_B200_OK;
   HB_REQUIRE(ctx, out_raw_score && out_ordinal, HOMS_B200_ERR_ARGUMENT, "search_batch: null output");
-  HB_TRY(queries_set_locked(ctx, query_dim, nq, q_words, q_mz, q_charge, false));
+  HB_TRY(queries_set_any_locked(ctx, query_dim, nq, q_words, q_mz, q_charge, false));
   HB_TRY(ensure(ctx, ctx->scratch[kScrRecords], nq * k * sizeof(Cand)));
   uint64_t* d_first = nullptr;
   uint64_t* d_last = nullptr;
@@ -976,7 +980,7 @@ int homs_b200_search_batch(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq,
     d_last = ctx->scratch[kScrQLast].as<uint64_t>();
   }
   Cand* d_rec = ctx->scratch[kScrRecords].as<Cand>();
-  HB_TRY(search_dev_locked(ctx, nullptr, nq, tol, k, d_rec, d_first, d_last, nullptr));
+  HB_TRY(search_any_locked(ctx, nullptr, nq, tol, k, d_rec, d_first, d_last, nullptr));
   if (out_first) HB_CUDA(ctx, cudaMemcpyAsync(out_first, d_first, nq * 8, cudaMemcpyDeviceToHost, ctx->stream));
   if (out_last) HB_CUDA(ctx, cudaMemcpyAsync(out_last, d_last, nq * 8, cudaMemcpyDeviceToHost, ctx->stream));
   return decode_locked(ctx, nq * k, d_rec, out_raw_score, out_ordinal);
@@ -997,7 +1001,8 @@ static int cascade_locked(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq, c
     nq = ctx->q.nq;
   }
   HB_REQUIRE(ctx, ctx->lib.ready, HOMS_B200_ERR_STATE, "cascade_search: no library uploaded");
-  HB_REQUIRE(ctx, ctx->lib.shard_count == 1, HOMS_B200_ERR_STATE, "cascade_search: sharded library");
+  HB_REQUIRE(ctx, ctx->lib.shard_count == 1 || is_group(ctx), HOMS_B200_ERR_STATE,
+             "cascade_search: this context holds one shard of a library split across processes");
   HB_TRY(check_tol(ctx, narrow));
   HB_TRY(check_tol(ctx, wide));
   // Tolerance::validate, search.cpp:13-15 via :223-224
@@ -1010,7 +1015,7 @@ static int cascade_locked(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq, c
              "search_one: query dimensionality does not match index");
   HB_REQUIRE(ctx, lib_is_decoy && out_query && out_ordinal && out_stage && out_raw_score && out_q_value,
              HOMS_B200_ERR_ARGUMENT, "cascade_search: null argument");
-  if (!resident) HB_TRY(queries_set_locked(ctx, query_dim, nq, q_words, q_mz, q_charge, false));
+  if (!resident) HB_TRY(queries_set_any_locked(ctx, query_dim, nq, q_words, q_mz, q_charge, false));
   HB_TRY(ensure(ctx, ctx->scratch[kScrRecords], nq * sizeof(Cand)));
   Cand* d_rec = ctx->scratch[kScrRecords].as<Cand>();
 
@@ -1036,7 +1041,7 @@ static int cascade_locked(homs_b200_ctx* ctx, uint32_t query_dim, uint64_t nq, c
                                    cudaMemcpyHostToDevice, ctx->stream));
       d_subset = ctx->scratch[kScrSubset].as<uint32_t>();
     }
-    HB_TRY(search_dev_locked(ctx, d_subset, n, stage == 0 ? narrow : wide, 1, d_rec, nullptr, nullptr,
+    HB_TRY(search_any_locked(ctx, d_subset, n, stage == 0 ? narrow : wide, 1, d_rec, nullptr, nullptr,
                              nullptr));
     HB_TRY(decode_locked(ctx, n, d_rec, h_score.data(), h_ord.data()));
     std::vector<double> score;
@@ -1122,8 +1127,9 @@ int homs_b200_search_resident(homs_b200_ctx* ctx, const homs_b200_tolerance* tol
   Lock lock(ctx);
   HB_REQUIRE(ctx, ctx->lib.ready, HOMS_B200_ERR_STATE, "search_resident: no library uploaded");
   HB_REQUIRE(ctx, ctx->q.ready, HOMS_B200_ERR_STATE, "search_resident: no resident queries");
-  HB_REQUIRE(ctx, ctx->lib.shard_count == 1, HOMS_B200_ERR_STATE,
-             "search_resident: sharded library; use search_resident_dev + merge_candidates_dev");
+  HB_REQUIRE(ctx, ctx->lib.shard_count == 1 || is_group(ctx), HOMS_B200_ERR_STATE,
+             "search_resident: this context holds one shard of a library split across processes; use "
+             "search_resident_dev + an all-gather + merge_candidates_dev (or a multi-device context)");
   HB_REQUIRE(ctx, ctx->q.dim == ctx->lib.dim, HOMS_B200_ERR_INVARIANT,
              "search_one: query dimensionality does not match index");
   HB_TRY(check_tol(ctx, tol));
@@ -1141,7 +1147,7 @@ int homs_b200_search_resident(homs_b200_ctx* ctx, const homs_b200_tolerance* tol
     d_last = ctx->scratch[kScrQLast].as<uint64_t>();
   }
   Cand* d_rec = ctx->scratch[kScrRecords].as<Cand>();
-  HB_TRY(search_dev_locked(ctx, nullptr, nq, tol, k, d_rec, d_first, d_last, nullptr));
+  HB_TRY(search_any_locked(ctx, nullptr, nq, tol, k, d_rec, d_first, d_last, nullptr));
   if (out_first) HB_CUDA(ctx, cudaMemcpyAsync(out_first, d_first, nq * 8, cudaMemcpyDeviceToHost, ctx->stream));
   if (out_last) HB_CUDA(ctx, cudaMemcpyAsync(out_last, d_last, nq * 8, cudaMemcpyDeviceToHost, ctx->stream));
   return decode_locked(ctx, nq * k, d_rec, out_raw_score, out_ordinal);

@@ -17,9 +17,9 @@
 //   [k-chunk][row][128 bytes] with the 16-byte units of every row XOR-swizzled by (row & 7): a
 //   tile of R consecutive rows of one k-chunk is then ONE contiguous R*128-byte block that is
 //   already in the SWIZZLE_128B K-major layout tcgen05.mma wants, so a stage of the pipeline is
-//   two cp.async.bulk copies (no tensor map needed) completing on an mbarrier.  Two operand
-//   encodings (TcMode): int8 (kind::i8, 128 dimensions per 128-byte row, N = 256, 4 stages) and
-//   e2m1 (kind::mxf4 with unit block scales, 256 dimensions per row, N = 224, 5 stages; default).
+//   two cp.async.bulk copies (no tensor map needed) completing on an mbarrier.  Operands are e2m1
+//   nibbles (kind::mxf4 with unit block scales, 256 dimensions per row, N = 224, 5 stages); the
+//   int8 encoding of round 1 (kind::i8: twice the bytes, half the rate, same results) was removed.
 // * queries are sorted by window start (search.cu) and cut into tiles of 128 = the 128 TMEM lanes;
 //   the library rows a tile needs (union of its windows) are cut into N-row MMA tiles aligned to
 //   absolute multiples of N, so that different query tiles fetch identical blocks (L2 hits).
@@ -50,29 +50,26 @@ constexpr int kTcThreads = 192;
 constexpr uint32_t kTcBarBytes = 256;
 constexpr uint32_t kTcTmemCols = 512;  // two accumulators (+ the scale-factor columns in fp4 mode)
 
-// Two operand encodings of the same +-1 contraction:
-//   int8 (kind::i8):   1 byte per dimension, 128 dimensions per stage row, N = 256, int32 accumulate
-//   fp4  (kind::mxf4): e2m1 nibbles (+1.0 = 0x2, -1.0 = 0xA), 256 dimensions per stage row, block
-//                      scale factors all 1.0 (UE8M0 0x7F), fp32 accumulate (exact: |dot| <= D < 2^24);
-//                      twice the MACs per byte and per tensor-pipe cycle.  N = 224 leaves room in
-//                      TMEM for the (constant) scale factors next to two accumulators and in
-//                      shared memory for a 5-stage ring (220 KB).
-template <bool kFp4>
+// Operand encoding of the +-1 contraction: e2m1 nibbles (+1.0 = 0x2, -1.0 = 0xA), 256 dimensions per
+// 128-byte stage row, block scale factors all 1.0 (UE8M0 0x7F), fp32 accumulate (exact: |dot| <= D <
+// 2^24).  N = 224 leaves room in TMEM for the (constant) scale factors next to two accumulators and in
+// shared memory for a 5-stage ring (220 KB).
 struct TcMode {
 #ifndef HB_TC_FP4_N
 #define HB_TC_FP4_N 224      // measured: 224 rows x 5 stages beats 240 x 4 and 208 x 5 (profiles/)
 #define HB_TC_FP4_STAGES 5
 #endif
-  static constexpr int N = kFp4 ? HB_TC_FP4_N : 256;      // library rows per MMA tile
-  static constexpr int Stages = kFp4 ? HB_TC_FP4_STAGES : 4;  // depth of the smem ring
-  static constexpr int kDims = kFp4 ? 256 : 128;          // dimensions per 128-byte stage row
+  static constexpr int N = HB_TC_FP4_N;            // library rows per MMA tile
+  static constexpr int Stages = HB_TC_FP4_STAGES;  // depth of the smem ring
+  static constexpr int kDims = 256;                // dimensions per 128-byte stage row
   static constexpr uint32_t BBytes = N * kTcKB;
   static constexpr uint32_t StageBytes = kTcABytes + BBytes;  // multiple of 1024
   static constexpr uint32_t SmemBytes = Stages * StageBytes + 1024 + kTcBarBytes;
-  static constexpr uint32_t SfCol = 480;                  // fp4: scale-factor columns [480, 512)
+  static constexpr uint32_t SfCol = 480;           // scale-factor columns [480, 512)
 };
 constexpr uint32_t kTcGroupTiles = 12;  // query tiles per L2 group, at least
-constexpr int kTcMaxK = 16;             // top-k depth the drain keeps per query; larger k -> POPC engine
+constexpr int kTcMaxK = 32;             // top-k depth the drain keeps per query in ONE pass; larger k runs
+                                        // ceil(k / 32) passes, each bounded below by the previous pass's last key
 constexpr uint64_t kTcBatch = 64 * 1024;  // sorted slots per planning batch
 
 struct TcItem {
@@ -101,7 +98,10 @@ struct TcParams {
   uint64_t n;  // sorted positions in this batch
   Cand* partial;  // [n_items][128][k]
   int* gbest;     // [q_rows][k] best dot seen per residue class (row % k) of a sorted position (see the drain)
-  uint32_t k;     // candidates kept per query (1 .. kTcMaxK)
+  uint32_t k;     // candidates kept per query in this pass (1 .. kTcMaxK)
+  uint32_t prev_col;      // pass > 0: column of `prev` holding the last key of the previous pass
+  const Cand* prev;       // pass > 0: the output so far, [slot][prev_stride]; only keys strictly after
+  uint32_t prev_stride;   //           prev[slot][prev_col] are candidates of this pass (nullptr: pass 0)
   uint32_t pad2;
 };
 
@@ -149,16 +149,6 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-// D[tmem] (+)= A[smem] * B[smem]^T, int8 x int8 -> int32, M = 128, N = 256, K = 32
-__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
 }
 // D[tmem] (+)= A * B^T, e2m1 x e2m1 with per-32 UE8M0 block scales from TMEM -> fp32, K = 64
 __device__ __forceinline__ void tc_mma_fp4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -216,28 +206,22 @@ __device__ __forceinline__ uint64_t tc_smem_desc(uint32_t smem_addr) {
   const uint64_t hi = uint64_t(1024 >> 4) | (uint64_t(1) << 14) | (uint64_t(2) << 29);
   return lo | (hi << 32);
 }
-// Instruction descriptor, kind::i8: D = S32 (bits [4,6) = 2), A = B = signed 8 bit (bits [7,10) and
-// [10,13) = 1), both K-major (bits 15, 16 = 0), N >> 3 in [17,23), M >> 4 in [24,29).
-constexpr uint32_t kTcIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(TcMode<false>::N >> 3) << 17) |
-                                (uint32_t(kTcM >> 4) << 24);
 // Block-scaled descriptor, kind::mxf4: A = B = E2M1 (format 1 in [7,10) and [10,13)), K-major,
 // N >> 3 in [17,23), scale format UE8M0 (bit 23), M >> 4 in [24,29), scale-factor ids 0, K = 64.
-constexpr uint32_t kTcIdescFp4 = (1u << 7) | (1u << 10) | (uint32_t(TcMode<true>::N >> 3) << 17) | (1u << 23) |
+constexpr uint32_t kTcIdescFp4 = (1u << 7) | (1u << 10) | (uint32_t(TcMode::N >> 3) << 17) | (1u << 23) |
                                  (uint32_t(kTcM >> 4) << 24);
 
 // ---- expansion: packed bits -> swizzled +-1 operand image -----------------------------------
 
 // One warp per (row, group of 4 k-chunks): lane = (k-chunk in group) * 8 + 16-byte unit.  A bit b
-// becomes the int8 2b - 1 (16 dimensions per unit) or the e2m1 nibble +-1.0 (32 dimensions per
-// unit); dimensions at or above dim and rows at or above n_rows become 0 so that they contribute
+// becomes the e2m1 nibble +-1.0 (32 dimensions per unit); dimensions at or above dim and rows at or above n_rows become 0 so that they contribute
 // nothing to any dot product.  The order of the dimensions inside a unit is irrelevant as long as
 // library and queries use the same one (a dot product is invariant under a common permutation).
-template <bool kFp4>
 __global__ void tc_expand_kernel(uint64_t out_rows, uint64_t n_rows, const uint32_t* __restrict__ src_pos,
                                  const uint32_t* __restrict__ src_subset, uint64_t pos_base,
                                  const uint64_t* __restrict__ words, uint32_t stride_words, uint32_t dim,
                                  uint32_t n_kc, uint8_t* __restrict__ out) {
-  constexpr uint32_t kUnitDims = kFp4 ? 32 : 16;
+  constexpr uint32_t kUnitDims = 32;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint32_t groups = (n_kc + 3) / 4;
@@ -252,36 +236,22 @@ __global__ void tc_expand_kernel(uint64_t out_rows, uint64_t n_rows, const uint3
       src = src_pos[pos_base + row];
       if (src_subset) src = src_subset[src];
     }
-    const uint32_t bit0 = kc * TcMode<kFp4>::kDims + unit * kUnitDims;
+    const uint32_t bit0 = kc * TcMode::kDims + unit * kUnitDims;
     uint32_t bits = 0;
     if (bit0 < dim)
-      bits = static_cast<uint32_t>(words[src * stride_words + (bit0 >> 6)] >> (bit0 & 63)) &
-             (kFp4 ? 0xFFFFFFFFu : 0xFFFFu);
+      bits = static_cast<uint32_t>(words[src * stride_words + (bit0 >> 6)] >> (bit0 & 63));
     const uint32_t valid = dim - min(dim, bit0);  // dimensions of this unit below dim
     uint32_t w[4];
-    if constexpr (kFp4) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {  // 8 dimensions -> 8 nibbles: bit 1 -> 0x2 (+1.0), bit 0 -> 0xA (-1.0)
-        const uint32_t b8 = (bits >> (8 * i)) & 0xFFu;
-        uint32_t spread = 0, keep = 0;
+    for (int i = 0; i < 4; ++i) {  // 8 dimensions -> 8 nibbles: bit 1 -> 0x2 (+1.0), bit 0 -> 0xA (-1.0)
+      const uint32_t b8 = (bits >> (8 * i)) & 0xFFu;
+      uint32_t spread = 0, keep = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          spread |= ((b8 >> j) & 1u) << (4 * j + 3);
-          if (uint32_t(8 * i + j) < valid) keep |= 0xFu << (4 * j);
-        }
-        w[i] = (0xAAAAAAAAu ^ spread) & keep;
+      for (int j = 0; j < 8; ++j) {
+        spread |= ((b8 >> j) & 1u) << (4 * j + 3);
+        if (uint32_t(8 * i + j) < valid) keep |= 0xFu << (4 * j);
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {  // 4 dimensions -> 4 bytes: bit 1 -> 0x01, bit 0 -> 0xFF
-        const uint32_t nib = (bits >> (4 * i)) & 0xFu;
-        const uint32_t one = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
-        uint32_t keep = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (uint32_t(4 * i + j) < valid) keep |= 0xFFu << (8 * j);
-        w[i] = (((one ^ 0x01010101u) * 0xFFu) | one) & keep;
-      }
+      w[i] = (0xAAAAAAAAu ^ spread) & keep;
     }
     o = make_uint4(w[0], w[1], w[2], w[3]);
   }
@@ -490,19 +460,8 @@ __global__ void tc_plan_items_kernel(TcPlanCfg c, void* plan) {
 // ---- the search kernel ----------------------------------------------------------------------
 
 
-// accumulator word -> score domain of the drain: int32 as is, fp32 (exact integers) as float
-template <bool kFp4>
-struct TcAcc;
-template <>
-struct TcAcc<false> {
-  using T = int;
-  static __device__ __forceinline__ T lowest() { return INT_MIN; }
-  static __device__ __forceinline__ T get(int raw) { return raw; }
-  static __device__ __forceinline__ int to_int(T v) { return v; }
-  static __device__ __forceinline__ T from_int(int v) { return v; }
-};
-template <>
-struct TcAcc<true> {
+// accumulator word -> score domain of the drain: fp32 holding exact integers
+struct TcAcc {
   using T = float;
   static __device__ __forceinline__ T lowest() { return -3.0e38f; }
   static __device__ __forceinline__ T get(int raw) { return __int_as_float(raw); }
@@ -511,11 +470,11 @@ struct TcAcc<true> {
 };
 
 // KM = 1: plain top-1 drain; KM > 1: the drain keeps the best KM >= p.k candidates per query
-template <bool kFp4, int KM>
+template <int KM>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams p) {
   constexpr bool kTopK = KM > 1;
-  using Mode = TcMode<kFp4>;
-  using Acc = TcAcc<kFp4>;
+  using Mode = TcMode;
+  using Acc = TcAcc;
   using AccT = typename Acc::T;
   constexpr int kN = Mode::N;
   constexpr int kStages = Mode::Stages;
@@ -573,14 +532,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if constexpr (kFp4) {
-    // every block scale is 1.0 = UE8M0 0x7F: fill all 32 scale-factor columns of all 128 lanes once,
-    // so whatever bytes the MMA reads for A or B rows it reads 1.0
-    if (warp >= 2) tc_st32_fill(tmem_base + (uint32_t((warp & 3) * 32) << 16) + Mode::SfCol, 0x7F7F7F7Fu);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-  }
+  // every block scale is 1.0 = UE8M0 0x7F: fill all 32 scale-factor columns of all 128 lanes once,
+  // so whatever bytes the MMA reads for A or B rows it reads 1.0
+  if (warp >= 2) tc_st32_fill(tmem_base + (uint32_t((warp & 3) * 32) << 16) + Mode::SfCol, 0x7F7F7F7Fu);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   const uint32_t n_kc = p.n_kc;
   const uint32_t n_items = __ldg(p.n_items);
@@ -649,11 +606,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
             const uint64_t bdesc = tc_smem_desc(sa + kTcABytes);
 #pragma unroll
             for (uint32_t k = 0; k < kTcKB / 32; ++k) {  // +32 bytes along K inside the swizzle atom
-              if constexpr (kFp4)
-                tc_mma_fp4(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescFp4, tmem_base + Mode::SfCol,
-                           tmem_base + Mode::SfCol + 16, (kc | k) != 0u);
-              else
-                tc_mma_i8(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescI8, (kc | k) != 0u);
+              tc_mma_fp4(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescFp4, tmem_base + Mode::SfCol,
+                         tmem_base + Mode::SfCol + 16, (kc | k) != 0u);
             }
             tc_commit(empty_bar(stage));  // stage reusable once these MMAs have read it
             if (++stage == kStages) {
@@ -709,6 +663,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           floor_i = __ldcg(p.gbest + pos);
         }
       }
+      // pass > 0 of a deep top-k: everything up to and including the previous pass's last key is taken
+      bool has_prev = false;
+      int prev_dot = 0;
+      uint64_t prev_ad = 0;
+      uint32_t prev_rk = 0;
+      if constexpr (kTopK) {
+        if (p.prev != nullptr && pos < p.n) {
+          const Cand pv = p.prev[uint64_t(p.vals[pos]) * p.prev_stride + p.prev_col];
+          if (pv.d == kNone) {
+            lf = ll = 0;  // the previous pass already ran out of candidates for this query
+          } else {
+            has_prev = true;
+            prev_dot = static_cast<int>(p.dim) - 2 * static_cast<int>(pv.d);
+            prev_ad = pv.ad;
+            prev_rk = pv.rk;
+          }
+        }
+      }
       AccT bar = Acc::from_int(floor_i);
       AccT best_dot = Acc::lowest();
       uint32_t best_row = kNone, best_rk = 0;
@@ -762,6 +734,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
               for (int j = 0; j < 32; ++j)
                 if (j == jj) vj = Acc::get(v[j]);
               if (vj < bar) continue;  // the bar rose since the mask was taken
+              if (has_prev) {
+                const int dj = Acc::to_int(vj);
+                if (dj > prev_dot) continue;  // ranked before the previous pass's last key: already reported
+                if (dj == prev_dot) {
+                  const uint32_t r = row0 + cb + jj;
+                  const uint64_t ad = static_cast<uint64_t>(__double_as_longlong(fabs(qmz - p.lib_mz[r])));
+                  if (!key_less(prev_ad, prev_rk, ad, p.lib_rank[r])) continue;
+                }
+              }
               tc_topk_insert<KM>(topk, p.lib_mz, p.lib_rank, qmz, Acc::to_int(vj), row0 + cb + jj);
               bar = max(bar, Acc::from_int(tc_topk_kth<KM>(topk, p.k)));
             }
@@ -900,7 +881,7 @@ __global__ void tc_reduce_topk_kernel(uint64_t n, const uint32_t* __restrict__ v
   const uint64_t pos = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (pos >= n) return;
   const uint32_t t = static_cast<uint32_t>(pos / kTcM), r = static_cast<uint32_t>(pos % kTcM);
-  Cand best[kTcMaxK];
+  Cand best[kTcMaxK];  // k <= kTcMaxK per pass
   uint32_t count = 0;
   for (uint32_t i = tile_item_start[t]; i < tile_item_start[t + 1]; ++i) {
     const Cand* src = partial + (uint64_t(tile_items[i]) * kTcM + r) * k;
@@ -932,13 +913,12 @@ __global__ void tc_reduce_topk_kernel(uint64_t n, const uint32_t* __restrict__ v
 
 bool tc_available(const homs_b200_ctx* ctx) { return ctx->lib.d_x.p != nullptr && ctx->lib.x_rows > 0; }
 
-template <bool kFp4>
 static int expand_launch(homs_b200_ctx* ctx, uint64_t out_rows, uint64_t n_rows, const uint32_t* src_pos,
                          const uint32_t* src_subset, uint64_t pos_base, const uint64_t* words,
                          uint32_t stride_words, uint32_t dim, uint32_t n_kc, uint8_t* out) {
   const uint32_t groups = (n_kc + 3) / 4;
   const uint64_t warps = out_rows * groups;
-  tc_expand_kernel<kFp4><<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+  tc_expand_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, ctx->stream>>>(
       out_rows, n_rows, src_pos, src_subset, pos_base, words, stride_words, dim, n_kc, out);
   HB_LAUNCHED(ctx);
   return HOMS_B200_OK;
@@ -946,138 +926,165 @@ static int expand_launch(homs_b200_ctx* ctx, uint64_t out_rows, uint64_t n_rows,
 
 int tc_expand_library(homs_b200_ctx* ctx) {
   Library& lib = ctx->lib;
-  lib.x_fp4 = ctx->engine != HOMS_B200_ENGINE_TENSOR;  // AUTO = fp4, the faster encoding
-  const uint32_t tile_n = lib.x_fp4 ? TcMode<true>::N : TcMode<false>::N;
-  const uint32_t dims = lib.x_fp4 ? TcMode<true>::kDims : TcMode<false>::kDims;
-  lib.n_kc = (lib.dim + dims - 1) / dims;
+  const uint32_t tile_n = TcMode::N;
+  lib.n_kc = (lib.dim + TcMode::kDims - 1) / TcMode::kDims;
   lib.x_rows = (lib.n_local + tile_n - 1) / tile_n * tile_n + tile_n;
   HB_TRY(ensure(ctx, lib.d_x, size_t(lib.n_kc) * lib.x_rows * kTcKB));
-  if (lib.x_fp4)
-    return expand_launch<true>(ctx, lib.x_rows, lib.n_local, nullptr, nullptr, 0, lib.d_words.as<uint64_t>(), lib.S,
-                               lib.dim, lib.n_kc, lib.d_x.as<uint8_t>());
-  return expand_launch<false>(ctx, lib.x_rows, lib.n_local, nullptr, nullptr, 0, lib.d_words.as<uint64_t>(), lib.S,
-                              lib.dim, lib.n_kc, lib.d_x.as<uint8_t>());
+  return expand_launch(ctx, lib.x_rows, lib.n_local, nullptr, nullptr, 0, lib.d_words.as<uint64_t>(), lib.S,
+                       lib.dim, lib.n_kc, lib.d_x.as<uint8_t>());
 }
 
-template <bool kFp4, int KM>
-static int tc_search_sorted_mode(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
-                                 const uint32_t* d_vals, Cand* d_out, uint32_t k, uint32_t k_stride) {
-  using Mode = TcMode<kFp4>;
-  constexpr uint32_t kN = Mode::N;
+// One planning batch (<= 64 Ki sorted slots): union windows, device plan, expanded queries.  Shared by
+// every pass of a deep top-k over the batch.
+struct TcBatch {
+  uint64_t b0 = 0, nb = 0, q_rows = 0;
+  uint32_t n_tiles = 0;
+  TcPlanPtrs pp{};
+};
+
+static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const uint64_t* d_keys,
+                            const uint32_t* d_vals, uint64_t b0, uint64_t nb, uint32_t k_pass, TcBatch* out) {
+  constexpr uint32_t kN = TcMode::N;
   const Library& lib = ctx->lib;
   const Queries& q = ctx->q;
-  HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<kFp4, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(Mode::SmemBytes)));
-  const uint32_t q_stride = stride_for(q.dim);
-  for (uint64_t b0 = 0; b0 < n; b0 += kTcBatch) {
-    const uint64_t nb = std::min<uint64_t>(kTcBatch, n - b0);
-    const uint32_t n_tiles = static_cast<uint32_t>((nb + kTcM - 1) / kTcM);
-    const uint64_t q_rows = uint64_t(n_tiles) * kTcM;
+  const TcKnobs& knobs = ctx->knobs;  // development knobs, read from the environment at ctx_create
+  const uint32_t n_tiles = static_cast<uint32_t>((nb + kTcM - 1) / kTcM);
+  const uint64_t q_rows = uint64_t(n_tiles) * kTcM;
 
-    // 1. union window of every query tile
-    HB_TRY(ensure(ctx, ctx->scratch[kScrTcTiles], size_t(n_tiles) * sizeof(uint2)));
-    auto* d_ranges = ctx->scratch[kScrTcTiles].as<uint2>();
-    tc_tile_ranges_kernel<<<(n_tiles * 32 + 255) / 256, 256, 0, ctx->stream>>>(nb, d_keys + b0, n_tiles, d_ranges);
-    HB_LAUNCHED(ctx);
+  // 1. union window of every query tile
+  HB_TRY(ensure(ctx, ctx->scratch[kScrTcTiles], size_t(n_tiles) * sizeof(uint2)));
+  auto* d_ranges = ctx->scratch[kScrTcTiles].as<uint2>();
+  tc_tile_ranges_kernel<<<(n_tiles * 32 + 255) / 256, 256, 0, ctx->stream>>>(nb, d_keys + b0, n_tiles, d_ranges);
+  HB_LAUNCHED(ctx);
 
-    // 2. plan on the device (see the planner above).  Capacity of the item arrays from what the
-    //    host knows: every tile's window is at most the whole local library.
-    TcPlanCfg pc;
-    pc.n_tiles = n_tiles;
-    // query tiles per group: as many as keep the group's A operand (tiles x n_kc x 16 KB) resident in
-    // about a quarter of the L2 while the group sweeps the strips -- every B strip is then fetched from DRAM
-    // once per group (measured with the dynamic queue, config 2: 12 -> 125 tiles per group, 23.6 -> 22.4 ms)
-    pc.group_tiles = static_cast<uint32_t>(
-        std::max<uint64_t>(kTcGroupTiles, (32ull << 20) / (uint64_t(kTcM) * lib.n_kc * kTcKB)));
-    pc.max_strip = 8;
-    uint32_t items_per_sm = 400;  // env: development knobs
-    if (const char* e = getenv("HOMS_B200_TC_GROUP")) pc.group_tiles = std::max(1, atoi(e));
-    if (const char* e = getenv("HOMS_B200_TC_ITEMS_PER_SM")) items_per_sm = std::max(1, atoi(e));
-    if (const char* e = getenv("HOMS_B200_TC_MAX_STRIP")) pc.max_strip = std::max(1, atoi(e));
-    pc.tiles_total = static_cast<uint32_t>((lib.n_local + kN - 1) / kN + 1);
-    pc.target_items = uint64_t(ctx->sm_count) * items_per_sm;
-    const uint64_t slack = 2ull * n_tiles + 16;
-    const uint64_t by_shape =
-        std::max<uint64_t>(pc.target_items, (uint64_t(n_tiles) * pc.tiles_total + pc.max_strip - 1) / pc.max_strip) + slack;
-    const uint64_t by_memory = std::max<uint64_t>((4ull << 30) / (size_t(kTcM) * k * sizeof(Cand)), slack + 4ull * ctx->sm_count);
-    pc.item_cap = static_cast<uint32_t>(std::min<uint64_t>(std::min(by_shape, by_memory), 0x7fffffffull));
-    if (const char* e = getenv("HOMS_B200_TC_ITEM_CAP"))  // development / test knob: force the capacity-bound plan
-      pc.item_cap = static_cast<uint32_t>(std::min<uint64_t>(pc.item_cap, std::max<uint64_t>(slack + 1, atoi(e))));
-    pc.pad = 0;
-    HB_TRY(ensure(ctx, ctx->scratch[kScrTcPlan], tc_plan_bytes(n_tiles, pc.item_cap)));
-    void* d_plan = ctx->scratch[kScrTcPlan].p;
-    const TcPlanPtrs pp = tc_plan_layout(d_plan, n_tiles, pc.item_cap);
-    static_assert(kTcBatch / kTcM <= kTcPlanThreads, "one planner thread per query tile");
-    tc_plan_head_kernel<kN><<<1, kTcPlanThreads, 0, ctx->stream>>>(pc, d_ranges, d_plan);
-    HB_LAUNCHED(ctx);
-    tc_plan_items_kernel<kN><<<ctx->sm_count, 256, 0, ctx->stream>>>(pc, d_plan);
-    HB_LAUNCHED(ctx);
+  // 2. plan on the device (see the planner above).  Capacity of the item arrays from what the
+  //    host knows: every tile's window is at most the whole local library.
+  TcPlanCfg pc;
+  pc.n_tiles = n_tiles;
+  // query tiles per group: as many as keep the group's A operand (tiles x n_kc x 16 KB) resident in
+  // about a quarter of the L2 while the group sweeps the strips -- every B strip is then fetched from DRAM
+  // once per group (measured with the dynamic queue, config 2: 12 -> 125 tiles per group, 23.6 -> 22.4 ms)
+  pc.group_tiles = static_cast<uint32_t>(
+      std::max<uint64_t>(kTcGroupTiles, (32ull << 20) / (uint64_t(kTcM) * lib.n_kc * kTcKB)));
+  pc.max_strip = 8;
+  uint32_t items_per_sm = 400;
+  if (knobs.group_tiles) pc.group_tiles = knobs.group_tiles;
+  if (knobs.items_per_sm) items_per_sm = knobs.items_per_sm;
+  if (knobs.max_strip) pc.max_strip = knobs.max_strip;
+  pc.tiles_total = static_cast<uint32_t>((lib.n_local + kN - 1) / kN + 1);
+  pc.target_items = uint64_t(ctx->sm_count) * items_per_sm;
+  const uint64_t slack = 2ull * n_tiles + 16;
+  const uint64_t by_shape =
+      std::max<uint64_t>(pc.target_items, (uint64_t(n_tiles) * pc.tiles_total + pc.max_strip - 1) / pc.max_strip) + slack;
+  const uint64_t by_memory =
+      std::max<uint64_t>((4ull << 30) / (size_t(kTcM) * k_pass * sizeof(Cand)), slack + 4ull * ctx->sm_count);
+  pc.item_cap = static_cast<uint32_t>(std::min<uint64_t>(std::min(by_shape, by_memory), 0x7fffffffull));
+  if (knobs.item_cap)  // development / test knob: force the capacity-bound plan
+    pc.item_cap = static_cast<uint32_t>(std::min<uint64_t>(pc.item_cap, std::max<uint64_t>(slack + 1, knobs.item_cap)));
+  pc.pad = 0;
+  HB_TRY(ensure(ctx, ctx->scratch[kScrTcPlan], tc_plan_bytes(n_tiles, pc.item_cap)));
+  void* d_plan = ctx->scratch[kScrTcPlan].p;
+  static_assert(kTcBatch / kTcM <= kTcPlanThreads, "one planner thread per query tile");
+  tc_plan_head_kernel<kN><<<1, kTcPlanThreads, 0, ctx->stream>>>(pc, d_ranges, d_plan);
+  HB_LAUNCHED(ctx);
+  tc_plan_items_kernel<kN><<<ctx->sm_count, 256, 0, ctx->stream>>>(pc, d_plan);
+  HB_LAUNCHED(ctx);
 
-    // 3. expand the batch's queries in sorted order
-    HB_TRY(ensure(ctx, ctx->scratch[kScrTcQx], size_t(lib.n_kc) * q_rows * kTcKB));
-    HB_TRY(expand_launch<kFp4>(ctx, q_rows, nb, d_vals, d_subset, b0, q.d_words.as<uint64_t>(), q_stride, q.dim,
-                               lib.n_kc, ctx->scratch[kScrTcQx].as<uint8_t>()));
-    HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], size_t(pc.item_cap) * kTcM * k * sizeof(Cand)));
-    HB_TRY(ensure(ctx, ctx->scratch[kScrTcBest], q_rows * k * sizeof(int)));
-    // every byte 0x80: a dot no candidate can be below
-    HB_CUDA(ctx, cudaMemsetAsync(ctx->scratch[kScrTcBest].p, 0x80, q_rows * k * sizeof(int), ctx->stream));
-
-    // 4. search + reduce
-    TcParams tp;
-    tp.lib_x = lib.d_x.as<uint8_t>();
-    tp.q_x = ctx->scratch[kScrTcQx].as<uint8_t>();
-    tp.lib_rows = lib.x_rows;
-    tp.q_rows = q_rows;
-    tp.n_kc = lib.n_kc;
-    tp.dim = lib.dim;
-    tp.items = pp.items;
-    tp.n_items = &pp.head->n_items;
-    tp.counter = &pp.head->counter;
-    tp.keys = d_keys + b0;
-    tp.vals = d_vals + b0;
-    tp.subset = d_subset;
-    tp.q_mz = q.d_mz.as<double>();
-    tp.lib_mz = lib.d_mz_local.as<double>();
-    tp.lib_rank = lib.d_id_rank_local.as<uint32_t>();
-    tp.n = nb;
-    tp.partial = ctx->scratch[kScrTcPartial].as<Cand>();
-    tp.gbest = ctx->scratch[kScrTcBest].as<int>();
-    tp.k = k;
-    tp.pad2 = 0;
-    {
-      KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
-      tc_search_kernel<kFp4, KM><<<ctx->sm_count, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
-    }
-    HB_LAUNCHED(ctx);
-    if constexpr (KM > 1)
-      tc_reduce_topk_kernel<<<static_cast<unsigned>((nb + 127) / 128), 128, 0, ctx->stream>>>(
-          nb, d_vals + b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k, k_stride);
-    else
-      tc_reduce_kernel<<<n_tiles, dim3(kTcM, kTcReduceSlices), 0, ctx->stream>>>(
-          nb, d_vals + b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out, k_stride);
-    HB_LAUNCHED(ctx);
-    // the next batch reuses the plan / operand / partial blocks: stream order keeps that safe
-  }
+  // 3. expand the batch's queries in sorted order
+  HB_TRY(ensure(ctx, ctx->scratch[kScrTcQx], size_t(lib.n_kc) * q_rows * kTcKB));
+  HB_TRY(expand_launch(ctx, q_rows, nb, d_vals, d_subset, b0, q.d_words.as<uint64_t>(), stride_for(q.dim), q.dim,
+                       lib.n_kc, ctx->scratch[kScrTcQx].as<uint8_t>()));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], size_t(pc.item_cap) * kTcM * k_pass * sizeof(Cand)));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrTcBest], q_rows * k_pass * sizeof(int)));
+  out->b0 = b0;
+  out->nb = nb;
+  out->q_rows = q_rows;
+  out->n_tiles = n_tiles;
+  out->pp = tc_plan_layout(d_plan, n_tiles, pc.item_cap);
   return HOMS_B200_OK;
 }
 
-uint32_t tc_max_topk() { return kTcMaxK; }
+// One pass over a prepared batch: the k best per query (k <= KM) -- after the key in column prev_col of
+// the output when prev_col != kNone -- into columns [col0, col0 + k) of d_out_full.
+template <int KM>
+static int tc_run_pass(homs_b200_ctx* ctx, const TcBatch& tb, const uint32_t* d_subset, const uint64_t* d_keys,
+                       const uint32_t* d_vals, Cand* d_out_full, uint32_t k_stride, uint32_t col0, uint32_t k,
+                       uint32_t prev_col) {
+  using Mode = TcMode;
+  const Library& lib = ctx->lib;
+  const Queries& q = ctx->q;
+  const TcPlanPtrs& pp = tb.pp;
+  HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(Mode::SmemBytes)));
+  if (prev_col != kNone)  // a later pass over the same plan: hand the work items out again
+    HB_CUDA(ctx, cudaMemsetAsync(&pp.head->counter, 0, sizeof(uint32_t), ctx->stream));
+  // every byte 0x80: a dot no candidate can be below
+  HB_CUDA(ctx, cudaMemsetAsync(ctx->scratch[kScrTcBest].p, 0x80, tb.q_rows * k * sizeof(int), ctx->stream));
+
+  // 4. search + reduce
+  TcParams tp;
+  tp.lib_x = lib.d_x.as<uint8_t>();
+  tp.q_x = ctx->scratch[kScrTcQx].as<uint8_t>();
+  tp.lib_rows = lib.x_rows;
+  tp.q_rows = tb.q_rows;
+  tp.n_kc = lib.n_kc;
+  tp.dim = lib.dim;
+  tp.items = pp.items;
+  tp.n_items = &pp.head->n_items;
+  tp.counter = &pp.head->counter;
+  tp.keys = d_keys + tb.b0;
+  tp.vals = d_vals + tb.b0;
+  tp.subset = d_subset;
+  tp.q_mz = q.d_mz.as<double>();
+  tp.lib_mz = lib.d_mz_local.as<double>();
+  tp.lib_rank = lib.d_id_rank_local.as<uint32_t>();
+  tp.n = tb.nb;
+  tp.partial = ctx->scratch[kScrTcPartial].as<Cand>();
+  tp.gbest = ctx->scratch[kScrTcBest].as<int>();
+  tp.k = k;
+  tp.prev = prev_col != kNone ? d_out_full : nullptr;
+  tp.prev_stride = k_stride;
+  tp.prev_col = prev_col;
+  tp.pad2 = 0;
+  {
+    KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
+    tc_search_kernel<KM><<<ctx->sm_count, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
+  }
+  HB_LAUNCHED(ctx);
+  if constexpr (KM > 1)
+    tc_reduce_topk_kernel<<<static_cast<unsigned>((tb.nb + 127) / 128), 128, 0, ctx->stream>>>(
+        tb.nb, d_vals + tb.b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out_full + col0,
+        k, k_stride);
+  else
+    tc_reduce_kernel<<<tb.n_tiles, dim3(kTcM, kTcReduceSlices), 0, ctx->stream>>>(
+        tb.nb, d_vals + tb.b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out_full + col0,
+        k_stride);
+  HB_LAUNCHED(ctx);
+  return HOMS_B200_OK;
+}
+
+uint32_t tc_max_topk() { return HOMS_B200_MAX_TOPK; }  // any k the ABI allows: ceil(k / 32) passes
 
 int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
                      const uint32_t* d_vals, Cand* d_out, uint32_t k, uint32_t k_stride) {
-  HB_REQUIRE(ctx, k >= 1 && k <= uint32_t(kTcMaxK), HOMS_B200_ERR_ARGUMENT, "tensor engine: k above its top-k depth");
-  const bool f = ctx->lib.x_fp4;
-  if (k == 1)
-    return f ? tc_search_sorted_mode<true, 1>(ctx, d_subset, n, d_keys, d_vals, d_out, 1, k_stride)
-             : tc_search_sorted_mode<false, 1>(ctx, d_subset, n, d_keys, d_vals, d_out, 1, k_stride);
-  if (k <= 4)
-    return f ? tc_search_sorted_mode<true, 4>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride)
-             : tc_search_sorted_mode<false, 4>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride);
-  if (k <= 8)
-    return f ? tc_search_sorted_mode<true, 8>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride)
-             : tc_search_sorted_mode<false, 8>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride);
-  return f ? tc_search_sorted_mode<true, kTcMaxK>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride)
-           : tc_search_sorted_mode<false, kTcMaxK>(ctx, d_subset, n, d_keys, d_vals, d_out, k, k_stride);
+  HB_REQUIRE(ctx, k >= 1 && k <= HOMS_B200_MAX_TOPK, HOMS_B200_ERR_ARGUMENT, "tensor engine: k out of range");
+  const uint32_t k_pass = std::min<uint32_t>(k, kTcMaxK);
+  for (uint64_t b0 = 0; b0 < n; b0 += kTcBatch) {
+    TcBatch tb;
+    HB_TRY(tc_prepare_batch(ctx, d_subset, d_keys, d_vals, b0, std::min<uint64_t>(kTcBatch, n - b0), k_pass, &tb));
+    for (uint32_t col0 = 0; col0 < k; col0 += kTcMaxK) {
+      const uint32_t kr = std::min<uint32_t>(kTcMaxK, k - col0);
+      const uint32_t prev_col = col0 ? col0 - 1 : kNone;
+      // a later pass needs the top-k drain (it is the one that knows about the lower bound), even for kr = 1
+      if (kr == 1 && col0 == 0) HB_TRY(tc_run_pass<1>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col));
+      else if (kr <= 4) HB_TRY(tc_run_pass<4>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col));
+      else if (kr <= 8) HB_TRY(tc_run_pass<8>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col));
+      else if (kr <= 16) HB_TRY(tc_run_pass<16>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col));
+      else HB_TRY(tc_run_pass<kTcMaxK>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col));
+    }
+    // the next batch reuses the plan / operand / partial blocks: stream order keeps that safe
+  }
+  return HOMS_B200_OK;
 }
 
 // ---- tensor-pipe ceiling probe ----------------------------------------------------------------
@@ -1085,10 +1092,9 @@ int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, c
 // MMA shape back to back on whatever bytes shared memory holds (no global traffic, no drain), in
 // groups of 4 per commit with `depth` groups in flight.  bench.py times it on the same box in the same run and
 // reports the search kernel against it: MEASURED_PEAKS.json holds a bf16 figure only, and the
-// sustained rate of the 4-bit / 8-bit kinds under the power cap is not a fixed multiple of it.
-template <bool kFp4>
+// sustained rate of the 4-bit kind under the power cap is not a fixed multiple of it.
 __global__ void __launch_bounds__(kTcThreads, 1) tc_peak_kernel(uint32_t groups) {
-  using Mode = TcMode<kFp4>;
+  using Mode = TcMode;
   constexpr int kN = Mode::N;
   constexpr int kDepth = 4;
   extern __shared__ unsigned char tc_smem_raw[];
@@ -1099,7 +1105,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_peak_kernel(uint32_t groups)
   volatile uint32_t* tmem_slot =
       reinterpret_cast<volatile uint32_t*>(gen_base + Mode::Stages * Mode::StageBytes + 8 * kDepth);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // operands: any finite pattern will do; e2m1 / int8 have no NaN or Inf encodings
+  // operands: any finite pattern will do; e2m1 has no NaN or Inf encodings
   for (uint32_t i = threadIdx.x; i < Mode::StageBytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(gen_base)[i] = make_uint4(0x2A2A2A2Au, 0xA2A2A2A2u, 0x22AA22AAu, 0xAAAA2222u);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1118,12 +1124,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_peak_kernel(uint32_t groups)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if constexpr (kFp4) {
-    if (warp >= 2) tc_st32_fill(tmem_base + (uint32_t((warp & 3) * 32) << 16) + Mode::SfCol, 0x7F7F7F7Fu);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-  }
+  if (warp >= 2) tc_st32_fill(tmem_base + (uint32_t((warp & 3) * 32) << 16) + Mode::SfCol, 0x7F7F7F7Fu);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
   if (warp == 1 && lane == 0) {
     const uint64_t adesc = tc_smem_desc(base);
     const uint64_t bdesc = tc_smem_desc(base + kTcABytes);
@@ -1132,13 +1136,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_peak_kernel(uint32_t groups)
       if (g >= kDepth) mbar_wait(bar0 + 8u * slot, ((g / kDepth) - 1u) & 1u);
       const uint32_t tmem_d = tmem_base + (g & 1u) * kN;
 #pragma unroll
-      for (uint32_t k = 0; k < kTcKB / 32; ++k) {
-        if constexpr (kFp4)
-          tc_mma_fp4(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescFp4, tmem_base + Mode::SfCol,
-                     tmem_base + Mode::SfCol + 16, 1u);
-        else
-          tc_mma_i8(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescI8, 1u);
-      }
+      for (uint32_t k = 0; k < kTcKB / 32; ++k)
+        tc_mma_fp4(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescFp4, tmem_base + Mode::SfCol,
+                   tmem_base + Mode::SfCol + 16, 1u);
       tc_commit(bar0 + 8u * slot);
     }
     for (uint32_t g = groups > kDepth ? groups - kDepth : 0; g < groups; ++g)
@@ -1153,10 +1153,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_peak_kernel(uint32_t groups)
   }
 }
 
-template <bool kFp4>
-static int tc_peak_probe_mode(homs_b200_ctx* ctx, double seconds, double* out_ops_per_s, double* out_ms) {
-  using Mode = TcMode<kFp4>;
-  HB_CUDA(ctx, cudaFuncSetAttribute(tc_peak_kernel<kFp4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+int tc_peak_probe(homs_b200_ctx* ctx, double seconds, double* out_ops_per_s, double* out_ms) {
+  using Mode = TcMode;
+  HB_CUDA(ctx, cudaFuncSetAttribute(tc_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(Mode::SmemBytes)));
   cudaEvent_t e0, e1;
   HB_CUDA(ctx, cudaEventCreate(&e0));
@@ -1167,7 +1166,7 @@ static int tc_peak_probe_mode(homs_b200_ctx* ctx, double seconds, double* out_op
   float ms = 0.f;
   for (int pass = 0; pass < 3; ++pass) {  // calibrate, warm (reach the power-capped clock), measure
     HB_CUDA(ctx, cudaEventRecord(e0, ctx->stream));
-    tc_peak_kernel<kFp4><<<ctx->sm_count, kTcThreads, Mode::SmemBytes, ctx->stream>>>(groups);
+    tc_peak_kernel<<<ctx->sm_count, kTcThreads, Mode::SmemBytes, ctx->stream>>>(groups);
     HB_LAUNCHED(ctx);
     HB_CUDA(ctx, cudaEventRecord(e1, ctx->stream));
     HB_CUDA(ctx, cudaEventSynchronize(e1));
@@ -1183,11 +1182,6 @@ static int tc_peak_probe_mode(homs_b200_ctx* ctx, double seconds, double* out_op
   *out_ops_per_s = ops_group * groups * ctx->sm_count / (ms * 1e-3);
   if (out_ms) *out_ms = ms;
   return HOMS_B200_OK;
-}
-
-int tc_peak_probe(homs_b200_ctx* ctx, int fp4, double seconds, double* out_ops_per_s, double* out_ms) {
-  return fp4 ? tc_peak_probe_mode<true>(ctx, seconds, out_ops_per_s, out_ms)
-             : tc_peak_probe_mode<false>(ctx, seconds, out_ops_per_s, out_ms);
 }
 
 }  // namespace hb

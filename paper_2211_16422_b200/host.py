@@ -233,17 +233,32 @@ class Match:  # numeric core of Ssm (ssm.hpp:17-30)
     last: np.ndarray = field(default=None)
 
 
-class Context:
-    """One CUDA device: resident codebook, resident library index, resident queries."""
+def device_count() -> int:
+    n = C.c_int()
+    _check(capi.device_count(C.byref(n)))
+    return n.value
 
-    def __init__(self, device: int = 0):
+
+class Context:
+    """Resident codebook, resident library index, resident queries -- on one CUDA device, or (devices=[...])
+    on several devices of this process behind the same interface: the library is sharded by contiguous
+    m/z slices over them, queries are replicated, per-device candidates are merged on the first device
+    (homs_b200_ctx_create_multi; replaces the thread fan-out of parallel.hpp:20-48)."""
+
+    def __init__(self, device: int = 0, devices=None):
         h = C.c_void_p()
-        rc = capi.ctx_create(int(device), C.byref(h))
+        if devices is not None:
+            devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+            rc = capi.ctx_create_multi(devs, len(devices), C.byref(h))
+            device = int(devices[0]) if len(devices) else 0
+        else:
+            rc = capi.ctx_create(int(device), C.byref(h))
         if rc != capi.OK:
             msg = (capi.last_error(None) or b"").decode(errors="replace")
             raise _ERRORS.get(rc, HomsError)(msg)
         self._h = h
         self.device = device
+        self.devices = list(devices) if devices is not None else [device]
         self.codebook: Codebook | None = None
         self.lib_dim = 0
         self.lib_n = 0
@@ -275,9 +290,9 @@ class Context:
         _check(capi.ctx_set_stream(self._h, cuda_stream or 0), self._h)
 
     def set_engine(self, engine: str | int) -> None:
-        """Search engine: "auto" (tensor_fp4, or direct for narrow top-1 calls), "popc", "tensor",
-        "tensor_fp4" or "direct".  Choose it before build_index: "popc" and "direct" skip the tensor
-        image of the library."""
+        """Search engine: "auto" (tensor_fp4, or direct for narrow windows), "popc", "tensor_fp4"
+        ("tensor" is an alias) or "direct".  Choose it before build_index: "popc" and "direct" skip the
+        tensor image of the library."""
         code = {"auto": capi.ENGINE_AUTO, "popc": capi.ENGINE_POPC, "tensor": capi.ENGINE_TENSOR,
                 "tensor_fp4": capi.ENGINE_TENSOR_FP4, "direct": capi.ENGINE_DIRECT}.get(engine, engine)
         _check(capi.ctx_set_engine(self._h, int(code)), self._h)
@@ -304,7 +319,7 @@ class Context:
 
     def tensor_peak_probe(self, engine: str = "tensor_fp4", seconds: float = 0.5):
         """(ops/s, kernel ms) of the tensor engine's bare MMA issue loop on this device."""
-        eng = {"tensor": capi.ENGINE_TENSOR, "tensor_fp4": capi.ENGINE_TENSOR_FP4}[engine]
+        eng = {"tensor": capi.ENGINE_TENSOR_FP4, "tensor_fp4": capi.ENGINE_TENSOR_FP4}[engine]
         ops, ms = C.c_double(), C.c_double()
         _check(capi.tensor_peak_probe(self._h, eng, float(seconds), C.byref(ops), C.byref(ms)), self._h)
         return ops.value, ms.value

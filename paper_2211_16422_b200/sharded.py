@@ -35,29 +35,46 @@ def empty_candidates(n: int, k: int) -> np.ndarray:
 
 
 class GpuShardEngine:
-    """Shard engine on one CUDA device (torch tensors are only device buffers here)."""
+    """Shard engine on one CUDA device (torch tensors are only device buffers here).
+
+    Stream order: the context's kernels, the collective and the merge must run in ONE order.  The
+    context is therefore put on a real (non-NULL) torch stream that is also made torch's current
+    stream for this device, which is the stream torch.distributed's NCCL ops synchronise with: the
+    all-gather cannot start before the search kernels have written `mine`, and the merge kernel cannot
+    read `gathered` before the all-gather has finished."""
 
     def __init__(self, ctx, device):
         import torch
-        self.ctx, self.torch, self.device = ctx, torch, device
+        self.ctx, self.torch, self.device = ctx, torch, torch.device(device)
         self.nq = 0
+        self.stream = torch.cuda.Stream(self.device)
+        assert self.stream.cuda_stream != 0
+        torch.cuda.set_stream(self.stream)
+        ctx.set_stream(self.stream.cuda_stream)
 
     def set_queries(self, dim, q_words, q_mz, q_charge) -> int:
         self.nq = self.ctx.queries_upload(dim, q_words, q_mz, q_charge)
         return self.nq
 
     def search_shard(self, tol, k):
-        rec = self.torch.empty(self.nq * k * 16, dtype=self.torch.uint8, device=self.device)
-        self.ctx.search_resident_dev(tol, k, rec.data_ptr())
+        with self.torch.cuda.stream(self.stream):
+            rec = self.torch.empty(self.nq * k * 16, dtype=self.torch.uint8, device=self.device)
+            self.ctx.search_resident_dev(tol, k, rec.data_ptr())
         return rec
 
     def new_buffer(self, n_bytes):
-        return self.torch.empty(n_bytes, dtype=self.torch.uint8, device=self.device)
+        with self.torch.cuda.stream(self.stream):
+            return self.torch.empty(n_bytes, dtype=self.torch.uint8, device=self.device)
 
     def merge(self, gathered, nq, k, world):
-        out = self.new_buffer(nq * k * 16)
-        self.ctx.merge_candidates_dev(nq, k, world, gathered.data_ptr(), out.data_ptr())
+        with self.torch.cuda.stream(self.stream):
+            out = self.new_buffer(nq * k * 16)
+            self.ctx.merge_candidates_dev(nq, k, world, gathered.data_ptr(), out.data_ptr())
         return out
+
+    def collective_stream(self):
+        """The stream collectives must be issued on (torch's current stream inside this context)."""
+        return self.torch.cuda.stream(self.stream)
 
     def decode(self, records, nq, k):
         return self.ctx.candidates_decode(nq, k, records.data_ptr())
@@ -78,6 +95,9 @@ class ShardedSearcher:
         if self.world == 1:
             return self.engine.decode(mine, nq, k)
         gathered = self.engine.new_buffer(self.world * nq * k * 16)  # [world][nq][k] records
-        self.dist.all_gather_into_tensor(gathered, mine, group=self.group)
+        import contextlib
+        on_stream = getattr(self.engine, "collective_stream", contextlib.nullcontext)
+        with on_stream():  # NCCL orders itself against torch's current stream == the context's stream
+            self.dist.all_gather_into_tensor(gathered, mine, group=self.group)
         merged = self.engine.merge(gathered, nq, k, self.world)
         return self.engine.decode(merged, nq, k)

@@ -86,3 +86,13 @@ def mgf_cases():
                                ids=[bytes.fromhex(x) for x in c["ids"]],
                                peptides=[bytes.fromhex(x) for x in c["peptides"]])))
     return out
+
+
+def fnv_hex(a) -> str:
+    """FNV-1a-64 (cache.cpp:18-29) of an array's bytes, zero-padded to whole u64 words -- the fingerprint
+    function of tests/golden/make_whole_config.py."""
+    from oracle.binding import fnv1a64_words
+    b = np.ascontiguousarray(a).view(np.uint8).ravel()
+    if len(b) % 8:
+        b = np.concatenate([b, np.zeros(8 - len(b) % 8, np.uint8)])
+    return "%016x" % fnv1a64_words(b.view("<u8"))

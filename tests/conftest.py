@@ -10,6 +10,7 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (run on the B200 box)")
+    config.addinivalue_line("markers", "slow: minutes of CPU time on the reference side (whole-config parity)")
 
 
 @pytest.fixture(scope="session", autouse=True)

@@ -165,6 +165,55 @@ int main() {
       report(!ref_what.empty() && ref_what == gpu_what && ref_line == gpu_line, "parse_mgf error: " + gpu_what);
     }
   }
+  {  // the resident codebook is identified by its whole content: a codebook mutated IN PLACE (same
+     // storage, same seed, same sampled words) must be re-uploaded, not served from the stale copy
+    homs::Codebook cb2 = cb;
+    const auto before = gpu::encode_spectra<HomsApi>(std::span<const homs::RawSpectrum>(synth.queries.data(), 64), cb2, pre);
+    cb2.position[12345].words()[3] ^= 0x0000100000000000ull;
+    cb2.level[9].words()[17] ^= 0x4ull;
+    const auto want = homs::encode_spectra(std::span<const homs::RawSpectrum>(synth.queries.data(), 64), cb2, pre, 8, 64);
+    const auto got = gpu::encode_spectra<HomsApi>(std::span<const homs::RawSpectrum>(synth.queries.data(), 64), cb2, pre);
+    report(got.encoded == want.encoded && before.encoded.size() == got.encoded.size(),
+           "encode_spectra after an in-place codebook mutation: re-uploaded, identical to the reference");
+  }
+  {  // the same calls over a multi-device set (aliases of device 0 on a one-GPU box): the library is
+     // sharded by m/z slices, queries replicated, candidates merged -- nothing changes at the call site
+    int n_dev = 0;
+    homs_b200_device_count(&n_dev);
+    std::vector<int> devs;
+    if (n_dev >= 2) for (int i = 0; i < n_dev; ++i) devs.push_back(i);
+    else devs = {0, 0, 0};
+    gpu::set_devices(devs);
+    const auto lib2 = gpu::encode_spectra<HomsApi>(synth.library, cb, pre, 8, 64);
+    report(lib2.unprocessable == ref_lib.unprocessable && lib2.encoded == ref_lib.encoded,
+           "multi-device encode_spectra (" + std::to_string(devs.size()) + " devices): identical list");
+    const auto ix2 = gpu::build_index<HomsApi>(lib2.encoded);
+    report(homs_b200_ctx_device_count(ix2.context()) == static_cast<int>(devs.size()), "multi-device build_index: one handle, " +
+                                                                                    std::to_string(devs.size()) + " devices");
+    for (const Tolerance tol : {Tolerance{Tolerance::Kind::dalton, 500.0}, Tolerance{Tolerance::Kind::ppm, 20.0}}) {
+      const auto want = homs::search_batch(ref_q.encoded, ref_ix, tol, homs::SearchOptions{8, 64});
+      const auto got = gpu::search_batch<HomsApi>(gpu_q.encoded, ix2, tol);
+      bool ok = want.size() == got.size();
+      for (std::size_t i = 0; ok && i < want.size(); ++i)
+        ok = want[i].has_value() == got[i].has_value() && (!want[i] || same_ssm(*want[i], *got[i]));
+      report(ok, std::string("multi-device search_batch ") + (tol.kind == Tolerance::Kind::ppm ? "20 ppm" : "500 Da"));
+    }
+    const Tolerance narrow{Tolerance::Kind::ppm, 20.0}, wide{Tolerance::Kind::dalton, 500.0};
+    const auto want = homs::cascade_search(ref_q.encoded, ref_ix, narrow, wide, 0.01, homs::SearchOptions{8, 64});
+    const auto got = gpu::cascade_search<HomsApi>(gpu_q.encoded, ix2, narrow, wide, 0.01);
+    bool ok = want.size() == got.size();
+    for (std::size_t i = 0; ok && i < want.size(); ++i) ok = same_ssm(want[i], got[i]);
+    report(ok, "multi-device cascade_search: identical accepted list = " + std::to_string(got.size()));
+    std::size_t dropped = 0;
+    const auto fused2 = gpu::encode_and_index<HomsApi>(synth.library, cb, pre, &dropped);
+    const auto want_w = homs::search_batch(ref_q.encoded, ref_ix, wide, homs::SearchOptions{8, 64});
+    const auto got_w = gpu::search_batch<HomsApi>(gpu_q.encoded, fused2, wide);
+    ok = dropped == ref_lib.unprocessable && want_w.size() == got_w.size();
+    for (std::size_t i = 0; ok && i < want_w.size(); ++i)
+      ok = want_w[i].has_value() == got_w[i].has_value() && (!want_w[i] || same_ssm(*want_w[i], *got_w[i]));
+    report(ok, "multi-device encode_and_index: identical search results");
+    gpu::set_devices({0});
+  }
   // error behaviour
   {
     bool threw = false;

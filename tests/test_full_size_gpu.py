@@ -19,7 +19,7 @@ def _take(spec, rows, peaks):
 
 
 def test_iprg2012_full_size_properties(hb):
-    from paper_2211_16422_b200 import workload as wl
+    import workload as wl
     n_targets, _, dim, peaks, seed = wl.WORKLOADS["iprg2012"]
     lib = wl.synth_library(n_targets, peaks, 1.0, seed)
     n = len(lib["precursor_mz"])

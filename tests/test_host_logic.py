@@ -15,7 +15,7 @@ def test_library_exports_every_declared_symbol(hb):
     assert len(names) >= 30
     missing = [n for n in names if not hasattr(capi.lib, n)]
     assert not missing, missing
-    assert capi.abi_version() == 1
+    assert capi.abi_version() == 2
     assert ctypes.sizeof(capi.PreprocessConfigPod) == 48
     assert ctypes.sizeof(capi.EncoderConfigPod) == 24
     assert ctypes.sizeof(capi.TolerancePod) == 16

@@ -9,10 +9,10 @@ from tests import _util as U
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["tensor_fp4", "tensor", "popc", "direct", "auto"])
+@pytest.fixture(params=["tensor_fp4", "popc", "direct", "auto"])
 def ctx(hb, request):
-    """Every search test runs on all engines: tcgen05 mxf4 (e2m1), tcgen05 int8, XOR+POPC, the
-    warp-per-query direct engine, and AUTO (which picks direct or tensor_fp4 per call)."""
+    """Every search test runs on all engines: tcgen05 mxf4 (e2m1), XOR+POPC, the warp-per-query
+    direct engine, and AUTO (which picks direct or tensor_fp4 per call)."""
     c = hb.Context(0)
     c.set_engine(request.param)
     c.engine_name = request.param
@@ -358,7 +358,7 @@ def test_many_queries_span_planning_batches(hb, best_oracle):
     qmz = np.round(rng.uniform(380.0, 1220.0, nq), 2)
     qch = rng.integers(1, 4, nq).astype(np.uint8)
     got = {}
-    for eng in ("tensor", "tensor_fp4", "popc", "direct"):
+    for eng in ("tensor_fp4", "popc", "direct"):
         with hb.Context(0) as c:
             c.set_engine(eng)
             c.build_index(dim, words, mz, charge, ids=ids)
@@ -366,7 +366,7 @@ def test_many_queries_span_planning_batches(hb, best_oracle):
             got[eng + "/k3"] = c.search_batch(qw, qmz, qch, hb.Tolerance("dalton", 3.0), k=3)
             none = c.search_batch(qw[:300], qmz[:300], np.zeros(300, np.uint8), hb.Tolerance("dalton", 3.0))
             assert not none.has_hit.any()
-    for eng in ("tensor", "tensor_fp4", "direct"):
+    for eng in ("tensor_fp4", "direct"):
         assert np.array_equal(got[eng].ordinal, got["popc"].ordinal), eng
         assert np.array_equal(got[eng].raw_score, got["popc"].raw_score), eng
         # top-3 across planning batches: per-item lists, class-slot floors and the list merge
@@ -376,8 +376,8 @@ def test_many_queries_span_planning_batches(hb, best_oracle):
     oix = best_oracle.build_index(dim, words, mz, charge, None, ids)
     sample = rng.integers(0, nq, 2000)
     has, score, ordinal, _ = oix.search_batch(qw[sample], qmz[sample], qch[sample], ("da", 3.0), threads=8)
-    assert np.array_equal(got["tensor"].ordinal[sample, 0], ordinal)
-    assert np.array_equal(got["tensor"].raw_score[sample, 0], score)
+    assert np.array_equal(got["tensor_fp4"].ordinal[sample, 0], ordinal)
+    assert np.array_equal(got["tensor_fp4"].raw_score[sample, 0], score)
     oix.close()
 
 
@@ -401,13 +401,16 @@ def test_planner_under_a_tight_item_capacity(hb, monkeypatch):
         c.set_engine("tensor_fp4")
         c.build_index(dim, words, mz, charge)
         want = {k: c.search_batch(qw, qmz, qch, tol, k=k) for k in (1, 3)}
-        for cap in ("400", "120", "10"):
-            monkeypatch.setenv("HOMS_B200_TC_ITEM_CAP", cap)
+    for cap in ("400", "120", "10"):
+        monkeypatch.setenv("HOMS_B200_TC_ITEM_CAP", cap)  # read once, when the context is created
+        with hb.Context(0) as c:
+            c.set_engine("tensor_fp4")
+            c.build_index(dim, words, mz, charge)
             for k in (1, 3):
                 got = c.search_batch(qw, qmz, qch, tol, k=k)
                 assert np.array_equal(got.ordinal, want[k].ordinal), (cap, k)
                 assert np.array_equal(got.raw_score, want[k].raw_score), (cap, k)
-        monkeypatch.delenv("HOMS_B200_TC_ITEM_CAP")
+    monkeypatch.delenv("HOMS_B200_TC_ITEM_CAP")
 
 
 def test_concurrent_callers(hb):
@@ -462,9 +465,10 @@ def test_engine_selection_errors(hb):
         rng = np.random.default_rng(3)
         c.build_index(256, U.random_hvs(rng, 10, 256), np.linspace(500, 600, 10), [2] * 10)
         with pytest.raises(hb.HomsError):  # no tensor image was built for this library
-            c.set_engine("tensor")
+            c.set_engine("tensor_fp4")
         c.set_engine("auto")
         c.build_index(256, U.random_hvs(rng, 10, 256), np.linspace(500, 600, 10), [2] * 10)
         c.set_engine("tensor_fp4")  # auto builds the e2m1 image
-        with pytest.raises(hb.HomsError):
-            c.set_engine("tensor")
+        c.set_engine("tensor")      # ABI 1's int8 code: now an alias of tensor_fp4
+        got = c.search_batch(U.random_hvs(rng, 4, 256), [550.0] * 4, [2] * 4, hb.Tolerance("dalton", 500.0))
+        assert c.last_engine() == "tensor_fp4" and got.has_hit.all()

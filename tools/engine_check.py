@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 import paper_2211_16422_b200 as hb  # noqa: E402
 
 
-ENGINES = ("popc", "tensor", "tensor_fp4")
+ENGINES = ("popc", "direct", "tensor_fp4")
 
 
 def random_hvs(rng, n, dim):

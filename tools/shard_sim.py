@@ -37,7 +37,7 @@ def main():
 
     import paper_2211_16422_b200 as hb
     from paper_2211_16422_b200 import capi
-    from paper_2211_16422_b200 import workload as wl
+    import workload as wl
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)

@@ -3,9 +3,19 @@
 Shapes follow the reference's benchmark generator (src/synth.cpp:114-197: fragment m/z on a
 0.01 Th grid in [150, 1300), intensities U[0.05, 1], precursors U[380, 1070], charge in {2, 3},
 one decoy per target with the target's precursor/charge/intensities on fresh positions, queries
-derived from targets with a planted +79.97 Da shift and 5 % intensity noise), but this is an
-independent vectorised generator: the streams are NOT the reference's, only the distribution is.
-Bit-exact parity tests use the reference's own generator instead; this module feeds bench.py.
+derived from targets with a planted +79.97 Da shift and 5 % intensity noise).
+
+Two generators feed bench.py and the tests (`make(name, generator)`):
+
+* "reference": the reference's OWN generator, `generate_benchmark(SynthConfig{...})`
+  (src/synth.cpp:114-197) as compiled into oracle/_ref -- SURVEY.md section 8(d)'s exact inputs
+  (configs 1-3 = seeds 1-3).  A data source, not a checker: nothing of the search/encode path runs
+  in it.  Needs the built oracle/_ref (it travels to the GPU box as a built .so).
+* "numpy": an independent vectorised generator of the same distribution (NOT the reference's
+  streams); the fallback when oracle/_ref is absent, and the source of the encode / MGF workloads.
+
+This module lives outside the product package on purpose: the reference arm of bench.py imports
+it without mapping libhoms_b200.so.
 """
 from __future__ import annotations
 
@@ -107,3 +117,32 @@ WORKLOADS = {
     "hek293_full": (2_150_000, 1_000_000, 8192, 50, 3),  # BASELINE config 3 at full size (seconds per step)
     "tiny": (2_000, 256, 2048, 50, 9),            # CI-sized
 }
+
+
+def reference_generator_available() -> bool:
+    from oracle import binding as ob
+    return ob.available("ref")
+
+
+def make(name: str, generator: str = "auto"):
+    """-> (library dict, query dict, dim, generator used).  Dicts carry CSR spectra (offsets, mz,
+    intensity), precursor_mz, charge, is_decoy, ids; queries also `source` and `modified`."""
+    n_targets, n_query, dim, peaks, seed = WORKLOADS[name]
+    if generator == "auto":
+        generator = "reference" if reference_generator_available() else "numpy"
+    if generator == "reference":
+        from oracle import binding as ob
+        o = ob.Oracle("ref")
+        s = o.synth(ob.SynthCfg(n_library=n_targets, n_query=n_query, peaks_per_spectrum=peaks,
+                                fraction_modified=0.6, precursor_shift_da=79.97, fraction_peaks_shifted=0.3,
+                                intensity_noise=0.05, decoy_ratio=1.0, seed=seed))
+        lib, qry = s["library"], s["queries"]
+        lib["n_targets"], lib["peaks"] = n_targets, peaks
+        qry["source"] = s["truth"]["source_index"].astype(np.int64)
+        qry["modified"] = s["truth"]["modified"].astype(bool)
+        return lib, qry, dim, "reference"
+    if generator != "numpy":
+        raise ValueError(f"unknown generator {generator!r}")
+    lib = synth_library(n_targets, peaks, 1.0, seed)
+    qry = synth_queries(lib, n_query, seed=seed)
+    return lib, qry, dim, "numpy"
