@@ -138,10 +138,10 @@ enum {
                                       twice the image, 2.3x slower, identical results) */
   HOMS_B200_ENGINE_TENSOR_FP4 = 3, /* e2m1 operands with unit block scales, fp32 accumulate (kind::mxf4) */
   HOMS_B200_ENGINE_DIRECT = 4      /* one warp per query over exactly its window rows (XOR + POPC, warp-level
-                                      top-k, k <= 16): the engine for windows of a few dozen rows (ppm
-                                      tolerances).  AUTO picks it per call when the rows it would read are
-                                      far fewer bytes than one pass over the tensor image; forcing it keeps
-                                      only the packed rows, k > 16 then runs on the POPC engine */
+                                      top-k): the engine for windows of a few dozen rows (ppm tolerances).
+                                      AUTO picks it per call when the rows it would read are far fewer bytes
+                                      than one pass over the tensor image; forcing it keeps only the packed
+                                      rows */
 };
 int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine);
 /* The engine the last search call of this context ran on (one of the non-AUTO codes; reporting aid). */
@@ -304,7 +304,9 @@ int homs_b200_window_bounds(homs_b200_ctx* ctx, uint64_t nq, const double* q_mz,
                             uint64_t* out_first, uint64_t* out_last, uint8_t* out_has_bucket);
 
 /* search_batch, src/search.cpp:171-183, generalised to the k best per query (k = 1 is the
- * reference's search_one).  Entry j of query i: out_raw_score[i*k+j] (Hamming similarity) and
+ * reference's search_one; 1 <= k <= HOMS_B200_MAX_TOPK).  The tensor and direct engines keep up to 32
+ * candidates per query in one pass and take a second pass, bounded below by the first pass's last key,
+ * for 33 <= k <= 64; the POPC engine runs k passes.  Entry j of query i: out_raw_score[i*k+j] (Hamming similarity) and
  * out_ordinal[i*k+j] (input position of the library entry; HOMS_B200_NO_HIT and score 0 when
  * fewer than j+1 candidates exist).  out_first / out_last (nullable) as in window_bounds.
  * The library must be whole behind this handle (one device, or a multi-device context); a context
@@ -399,6 +401,17 @@ int homs_b200_mgf_fetch(homs_b200_ctx* ctx, uint64_t* offsets, double* mz, doubl
 int homs_b200_mgf_device_csr(homs_b200_ctx* ctx, uint64_t* out_n_spectra, uint64_t* out_n_peaks,
                              const uint64_t** d_offsets, const double** d_mz, const double** d_intensity,
                              const double** d_precursor_mz, const uint8_t** d_charge);
+
+/* The query side of run_search (src/pipeline.cpp:119-150) with nothing but the text crossing PCIe:
+ *   homs_b200_mgf_parse(image)          parse_mgf_file            (:121)
+ *   homs_b200_queries_from_mgf(cfg)     known-charge filter + encode_spectra  (:127-141)
+ *   homs_b200_cascade_resident(...)     cascade_search            (:146-147)
+ * queries_from_mgf encodes the CSR the last mgf_parse* left resident, where it lies, and makes the
+ * result the resident query set: query e is the e-th spectrum with out_state == 0.
+ * out_state[i] (n_spectra entries, may be NULL): 0 = resident query, 1 = skipped, charge unknown
+ * (the reference never encodes it), 2 = unprocessable (dropped by encode_spectra, :75-83). */
+int homs_b200_queries_from_mgf(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint8_t* out_state,
+                               uint64_t* out_n_queries);
 
 /* cascade_search, src/search.cpp:219-248 (run_stage :188-215): narrow stage on all queries,
  * target-decoy FDR, wide stage on the not-accepted rest, FDR again.  lib_is_decoy is indexed by

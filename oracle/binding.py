@@ -536,6 +536,27 @@ class Index:
                                    _p(score, C.c_uint32), _p(ordinal, C.c_uint32)))
         return score, ordinal
 
+    def query_flow(self, cb: "Codebook", cfg: "PreCfg", text: bytes, narrow, wide, fdr_q, threads=1, batch=64,
+                   decoy_prefix: str = "DECOY_") -> dict:
+        """The query side of the reference's run_search (pipeline.cpp:119-150) on an MGF image: parse_mgf ->
+        known charges -> encode_spectra -> cascade_search -> write_ssm_tsv.  ref only.  Library peptides in
+        the TSV are the decimal ordinals the shim tags entries with."""
+        fn = self.o._fn("query_flow", C.c_longlong,
+                        [C.c_void_p, C.c_void_p, C.POINTER(PreCfg), C.c_char_p, C.c_uint64, C.c_char_p, C.c_int,
+                         C.c_double, C.c_int, C.c_double, C.c_double, C.c_uint, C.c_uint64, C.POINTER(C.c_double),
+                         C.POINTER(C.c_uint64), C.c_char_p, C.c_uint64])
+        sec = (C.c_double * 3)()
+        stats = (C.c_uint64 * 6)()
+        args = (self.h, cb.handle, C.byref(cfg), text, len(text), decoy_prefix.encode(), tol_kind(narrow[0]),
+                float(narrow[1]), tol_kind(wide[0]), float(wide[1]), float(fdr_q), threads, batch)
+        size = self.o._check(fn(*args, sec, stats, None, 0))
+        buf = C.create_string_buffer(max(1, size))
+        self.o._check(fn(*args, sec, stats, buf, size))
+        names = ("total_queries", "skipped_unknown_charge", "unprocessable", "accepted_narrow", "accepted_wide",
+                 "unidentified")
+        return dict(tsv=buf.raw[:size], seconds=dict(parse=sec[0], encode=sec[1], cascade=sec[2]),
+                    stats={k: int(v) for k, v in zip(names, stats)})
+
     def cascade_search(self, q_words, q_mz, q_charge, narrow, wide, fdr_q, threads=1, batch=64):
         q_words, q_mz, q_charge = _u64(q_words), _f64(q_mz), _u8(q_charge)
         nq = len(q_mz)

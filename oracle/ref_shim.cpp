@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <charconv>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <iterator>
@@ -655,6 +656,62 @@ long long hr_mgf_write(std::uint64_t n, const std::uint64_t* offsets, const doub
     const std::string text = os.str();
     if (out && text.size() <= cap) std::memcpy(out, text.data(), text.size());
     return static_cast<long long>(text.size());
+  });
+}
+
+// The query side of run_search (pipeline.cpp:119-150) on an MGF text image, against an index built by
+// hr_index_build, with the codebook made elsewhere (make_codebook is not part of the timed stages):
+// parse_mgf -> drop unknown charges (:127-134) -> encode_spectra (:140-141) -> cascade_search (:146-147)
+// -> write_ssm_tsv (:179-195).  stage_seconds: parse, encode, cascade.  stats: total queries, skipped
+// (unknown charge), unprocessable, accepted narrow, accepted wide, unidentified.  Returns the TSV size
+// (copied when it fits in cap).
+long long hr_query_flow(const void* index, const void* codebook, const PreCfgPod* cfg, const char* text,
+                        std::uint64_t n_bytes, const char* decoy_prefix, int narrow_kind, double narrow_value,
+                        int wide_kind, double wide_value, double fdr_q, unsigned threads, std::uint64_t batch,
+                        double* stage_seconds, std::uint64_t* stats, char* tsv, std::uint64_t cap) {
+  return guarded([&]() -> long long {
+    using Clock = std::chrono::steady_clock;
+    const auto* box = static_cast<const IndexBox*>(index);
+    const auto* cb = static_cast<const homs::Codebook*>(codebook);
+    auto t0 = Clock::now();
+    std::istringstream in(std::string(text, n_bytes));
+    const auto raw = homs::parse_mgf(in, decoy_prefix ? decoy_prefix : "");
+    auto t1 = Clock::now();
+    std::vector<homs::RawSpectrum> with_charge;
+    with_charge.reserve(raw.size());
+    std::size_t skipped = 0;
+    for (const auto& q : raw) {
+      if (q.meta.has_known_charge()) with_charge.push_back(q);
+      else ++skipped;
+    }
+    auto encoded = homs::encode_spectra(with_charge, *cb, to_cfg(cfg), threads, batch);
+    auto t2 = Clock::now();
+    homs::SearchOptions opt;
+    opt.threads = threads;
+    opt.batch_size = batch;
+    const auto accepted = homs::cascade_search(encoded.encoded, box->index, make_tol(narrow_kind, narrow_value),
+                                               make_tol(wide_kind, wide_value), fdr_q, opt);
+    auto t3 = Clock::now();
+    if (stage_seconds) {
+      stage_seconds[0] = std::chrono::duration<double>(t1 - t0).count();
+      stage_seconds[1] = std::chrono::duration<double>(t2 - t1).count();
+      stage_seconds[2] = std::chrono::duration<double>(t3 - t2).count();
+    }
+    if (stats) {
+      std::uint64_t narrow = 0;
+      for (const auto& s : accepted) narrow += s.stage == homs::SearchStage::narrow;
+      stats[0] = raw.size();
+      stats[1] = skipped;
+      stats[2] = encoded.unprocessable;
+      stats[3] = narrow;
+      stats[4] = accepted.size() - narrow;
+      stats[5] = encoded.encoded.size() - accepted.size();
+    }
+    std::ostringstream os;
+    homs::write_ssm_tsv(os, accepted);
+    const std::string out = os.str();
+    if (tsv && out.size() <= cap) std::memcpy(tsv, out.data(), out.size());
+    return static_cast<long long>(out.size());
   });
 }
 

@@ -138,6 +138,7 @@ library_build_from_spectra = _decl("homs_b200_library_build_from_spectra", _I,
                                     _VP, _P(_U64)])
 queries_from_spectra = _decl("homs_b200_queries_from_spectra", _I,
                              [_VP, _P(PreprocessConfigPod), _U64, _VP, _VP, _VP, _VP, _VP, _VP, _P(_U64)])
+queries_from_mgf = _decl("homs_b200_queries_from_mgf", _I, [_VP, _P(PreprocessConfigPod), _VP, _P(_U64)])
 search_resident = _decl("homs_b200_search_resident", _I, [_VP, _P(TolerancePod), _U32, _VP, _VP, _VP, _VP])
 cascade_resident = _decl("homs_b200_cascade_resident", _I,
                          [_VP, _P(TolerancePod), _P(TolerancePod), _F64, _VP, _VP, _VP, _VP, _VP, _VP, _P(_U64)])

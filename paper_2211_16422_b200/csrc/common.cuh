@@ -229,6 +229,10 @@ int repack_rows_dev(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src, 
 int encode_pipeline(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint64_t n,
                     const uint64_t* offsets, const double* mz, const double* intensity, uint64_t* d_keep,
                     uint8_t* d_keep_ok, uint64_t* h_words, uint8_t* h_ok);
+// refine_peaks -> vectorize -> encode of n spectra whose CSR is on the device; dense rows + ok flags out
+int encode_dev_locked(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint64_t n,
+                      const uint64_t* d_off, const double* d_mz, const double* d_int, uint64_t* d_out,
+                      uint8_t* d_ok);
 // build_index over rows already on the device; row_of_entry (host, may be null) maps entry i of the
 // metadata arrays to its row in d_words
 int library_build_from_device(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* d_words,

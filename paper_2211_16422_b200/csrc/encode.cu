@@ -500,9 +500,9 @@ static int launch_encode(homs_b200_ctx* ctx, uint64_t n, const uint64_t* d_sv_of
   return HOMS_B200_OK;
 }
 
-static int encode_dev_locked(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint64_t n,
-                             const uint64_t* d_off, const double* d_mz, const double* d_int,
-                             uint64_t* d_out, uint8_t* d_ok) {
+int encode_dev_locked(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint64_t n,
+                      const uint64_t* d_off, const double* d_mz, const double* d_int,
+                      uint64_t* d_out, uint8_t* d_ok) {
   HB_REQUIRE(ctx, ctx->cb.ready, HOMS_B200_ERR_STATE, "encode: no codebook uploaded");
   PreParams p;
   HB_TRY(fill_pre_params(ctx, cfg, ctx->cb.levels, &p));

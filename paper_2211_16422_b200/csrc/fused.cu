@@ -42,6 +42,16 @@ static int encode_keep(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cf
   return HOMS_B200_OK;
 }
 
+// precursor m/z and charge of the kept spectra, gathered on the device
+__global__ void gather_meta_kernel(uint64_t m, const uint32_t* __restrict__ idx, const double* __restrict__ src_mz,
+                                   const uint8_t* __restrict__ src_charge, double* __restrict__ dst_mz,
+                                   uint8_t* __restrict__ dst_charge) {
+  const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  dst_mz[e] = src_mz[idx[e]];
+  dst_charge[e] = src_charge[idx[e]];
+}
+
 }  // namespace hb
 
 using namespace hb;
@@ -132,6 +142,72 @@ int homs_b200_queries_from_spectra(homs_b200_ctx* ctx, const homs_b200_preproces
   }
   q.ready = true;
   if (is_group(ctx)) HB_TRY(queries_replicate_locked(ctx));  // encoded on the leading device, searched on all
+  return HOMS_B200_OK;
+}
+
+int homs_b200_queries_from_mgf(homs_b200_ctx* ctx, const homs_b200_preprocess_config* cfg, uint8_t* out_state,
+                               uint64_t* out_n_queries) {
+  if (!ctx) return HOMS_B200_ERR_ARGUMENT;
+  Lock lock(ctx);
+  HB_REQUIRE(ctx, ctx->cb.ready, HOMS_B200_ERR_STATE, "encode: no codebook uploaded");
+  HB_REQUIRE(ctx, ctx->mgf.ready, HOMS_B200_ERR_STATE, "queries_from_mgf: no parsed MGF resident (call mgf_parse first)");
+  const MgfState& mg = ctx->mgf;
+  const uint64_t n = mg.n_spectra;
+  HB_REQUIRE(ctx, n < 0xFFFFFFFFull, HOMS_B200_ERR_ARGUMENT, "more than 2^32-2 spectra");
+  const uint32_t W = ctx->cb.W;
+  HB_TRY(ensure(ctx, ctx->scratch[kScrFusedRows], std::max<size_t>(1, n) * W * 8));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrEncOk], std::max<size_t>(1, n)));
+  auto* d_rows = ctx->scratch[kScrFusedRows].as<uint64_t>();
+  auto* d_ok = ctx->scratch[kScrEncOk].as<uint8_t>();
+  cudaStream_t st = ctx->stream;
+  // encode every parsed spectrum where it lies (the CSR never left the device) ...
+  HB_TRY(encode_dev_locked(ctx, cfg, n, mg.d_offsets, mg.d_mz, mg.d_int, d_rows, d_ok));
+  // ... and let the host decide the order-preserving compaction from two bytes per spectrum
+  std::vector<uint8_t> ok(n), charge(n);
+  if (n) {
+    HB_CUDA(ctx, cudaMemcpyAsync(ok.data(), d_ok, n, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(ctx, cudaMemcpyAsync(charge.data(), mg.d_charge, n, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(ctx, cudaStreamSynchronize(st));
+  }
+  std::vector<uint32_t> rows;
+  rows.reserve(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint8_t state = 0;
+    if (charge[i] == 0) {
+      state = 1;  // pipeline.cpp:127-134: no known charge, never encoded by the reference
+    } else {
+      // quantize_intensity's exception escapes the reference's encode_spectra (pipeline.cpp:67-72)
+      HB_REQUIRE(ctx, ok[i] != HOMS_B200_OK_FLAG_INVARIANT, HOMS_B200_ERR_INVARIANT,
+                 "quantize_intensity: intensity outside [0, 1]");
+      if (!ok[i]) state = 2;
+      else rows.push_back(static_cast<uint32_t>(i));
+    }
+    if (out_state) out_state[i] = state;
+  }
+  const uint64_t m = rows.size();
+  if (out_n_queries) *out_n_queries = m;
+  Queries& q = ctx->q;
+  q.ready = false;
+  q.dim = ctx->cb.dim;
+  q.nq = m;
+  const uint32_t S = stride_for(q.dim);
+  HB_TRY(ensure(ctx, q.d_words, m * S * 8));
+  HB_TRY(ensure(ctx, q.d_mz, m * 8));
+  HB_TRY(ensure(ctx, q.d_charge, m));
+  if (m) {
+    HB_TRY(ensure(ctx, ctx->scratch[kScrFusedOk], m * 4));
+    auto* d_idx = ctx->scratch[kScrFusedOk].as<uint32_t>();
+    HB_CUDA(ctx, cudaMemcpyAsync(d_idx, rows.data(), m * 4, cudaMemcpyHostToDevice, st));
+    gather_rows_kernel<<<static_cast<unsigned>((m * 32 + 255) / 256), 256, 0, st>>>(m, d_idx, d_rows,
+                                                                                   q.d_words.as<uint64_t>(), W, S);
+    HB_LAUNCHED(ctx);
+    gather_meta_kernel<<<static_cast<unsigned>((m + 255) / 256), 256, 0, st>>>(
+        m, d_idx, mg.d_pepmass, mg.d_charge, q.d_mz.as<double>(), q.d_charge.as<uint8_t>());
+    HB_LAUNCHED(ctx);
+    HB_CUDA(ctx, cudaStreamSynchronize(st));  // `rows` goes out of scope
+  }
+  q.ready = true;
+  if (is_group(ctx)) HB_TRY(queries_replicate_locked(ctx));
   return HOMS_B200_OK;
 }
 

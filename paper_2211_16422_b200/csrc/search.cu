@@ -508,13 +508,14 @@ __global__ void decode_kernel(uint64_t total, const Cand* __restrict__ rec, uint
 
 // KM = 1: running best; KM > 1: the k <= KM best in a register list every lane holds identically
 // (the comparisons are warp-uniform) -- the warp-level top-k with the reference's tie-break.
+constexpr uint32_t kDirectMaxK = 32;  // list depth of one pass; deeper top-k takes ceil(k / 32) passes
 template <int KM>
 __global__ void __launch_bounds__(256)
 direct_search_kernel(uint64_t n, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                      const uint32_t* __restrict__ subset, const uint4* __restrict__ q_words,
                      const double* __restrict__ q_mz, const uint4* __restrict__ lib_words,
                      const double* __restrict__ lib_mz, const uint32_t* __restrict__ lib_rank, uint32_t row_u4,
-                     Cand* __restrict__ out, uint32_t k, uint32_t k_stride) {
+                     Cand* __restrict__ out, uint32_t k, uint32_t k_stride, uint32_t col0, uint32_t prev_col) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t pos = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (pos >= n) return;
@@ -528,6 +529,21 @@ direct_search_kernel(uint64_t n, const uint64_t* __restrict__ keys, const uint32
   }
   const double qmz = q_mz[qi];
   const uint4* q = q_words + size_t(qi) * row_u4;
+  // pass > 0 of a deep top-k (KM > 1 only): keys up to and including out[slot][prev_col] are taken
+  bool has_prev = false;
+  uint32_t prev_d = 0, prev_rk = 0;
+  uint64_t prev_ad = 0;
+  if (prev_col != kNone) {
+    const Cand pv = out[uint64_t(slot) * k_stride + prev_col];
+    if (pv.d == kNone) {
+      lf = ll = 0;  // the previous pass already ran out of candidates
+    } else {
+      has_prev = true;
+      prev_d = pv.d;
+      prev_rk = pv.rk;
+      prev_ad = pv.ad;
+    }
+  }
   uint32_t best_d = kNone, best_rk = kNone, best_row = kNone;
   uint64_t best_ad = ~0ull;
   bool have_key = false;
@@ -543,6 +559,10 @@ direct_search_kernel(uint64_t n, const uint64_t* __restrict__ keys, const uint32
     if constexpr (KM > 1) {
       const int dot = -static_cast<int>(d);
       if (dot < kth) return;  // below the k-th best so far (ties with it are looked at)
+      if (has_prev) {
+        if (d < prev_d) return;  // ranked before the previous pass's last key: already reported
+        if (d == prev_d && !key_less(prev_ad, prev_rk, abs_diff_bits(qmz, lib_mz[row]), lib_rank[row])) return;
+      }
       tc_topk_insert<KM>(topk, lib_mz, lib_rank, qmz, dot, row);
       kth = tc_topk_kth<KM>(topk, k);
       return;
@@ -596,7 +616,7 @@ direct_search_kernel(uint64_t n, const uint64_t* __restrict__ keys, const uint32
     consider(r, __reduce_add_sync(0xffffffffu, c0));
   }
   if (lane != 0) return;
-  Cand* dst = out + uint64_t(slot) * k_stride;
+  Cand* dst = out + uint64_t(slot) * k_stride + col0;
   if constexpr (KM > 1) {
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
@@ -721,9 +741,8 @@ int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n,
                     d_last, d_has));
 
   const bool tensor_ok = ctx->engine != HOMS_B200_ENGINE_POPC && ctx->engine != HOMS_B200_ENGINE_DIRECT && tc_available(ctx);
-  const bool use_direct =
-      k <= tc_max_topk() && (ctx->engine == HOMS_B200_ENGINE_DIRECT ||
-                             (ctx->engine == HOMS_B200_ENGINE_AUTO && tensor_ok && direct_is_cheaper(ctx, n, tol)));
+  const bool use_direct = ctx->engine == HOMS_B200_ENGINE_DIRECT ||
+                          (ctx->engine == HOMS_B200_ENGINE_AUTO && tensor_ok && direct_is_cheaper(ctx, n, tol));
   // Sort the slots by window start (upper 32 key bits): neighbours then share library rows on chip.
   // The direct engine skips it when the windows are so sparse that neighbours would share nothing
   // anyway (expected rows read < rows resident: every row comes from HBM once either way).
@@ -751,20 +770,26 @@ int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n,
 #define HB_DIRECT_LAUNCH(KM)                                                                                  \
   direct_search_kernel<KM><<<blocks, 256, 0, ctx->stream>>>(                                                  \
       n, keys, vals, d_subset, q.d_words.as<uint4>(), q.d_mz.as<double>(), lib.d_words.as<uint4>(),           \
-      lib.d_mz_local.as<double>(), lib.d_id_rank_local.as<uint32_t>(), lib.S / 2, d_out, k, k)
-    {
-      KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
-      if (k == 1) HB_DIRECT_LAUNCH(1);
-      else if (k <= 4) HB_DIRECT_LAUNCH(4);
-      else if (k <= 8) HB_DIRECT_LAUNCH(8);
-      else HB_DIRECT_LAUNCH(16);
+      lib.d_mz_local.as<double>(), lib.d_id_rank_local.as<uint32_t>(), lib.S / 2, d_out, kr, k, col0, prev_col)
+    // k > 32: passes of up to 32, each bounded below by the previous pass's last key (as on the tensor engine)
+    for (uint32_t col0 = 0; col0 < k; col0 += kDirectMaxK) {
+      const uint32_t kr = std::min<uint32_t>(kDirectMaxK, k - col0);
+      const uint32_t prev_col = col0 ? col0 - 1 : kNone;
+      {
+        KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
+        if (kr == 1 && col0 == 0) HB_DIRECT_LAUNCH(1);
+        else if (kr <= 4) HB_DIRECT_LAUNCH(4);
+        else if (kr <= 8) HB_DIRECT_LAUNCH(8);
+        else if (kr <= 16) HB_DIRECT_LAUNCH(16);
+        else HB_DIRECT_LAUNCH(32);
+      }
+      HB_LAUNCHED(ctx);
     }
 #undef HB_DIRECT_LAUNCH
-    HB_LAUNCHED(ctx);
     ctx->last_engine = HOMS_B200_ENGINE_DIRECT;
     return HOMS_B200_OK;
   }
-  if (k <= tc_max_topk() && tensor_ok) {
+  if (tensor_ok) {
     ctx->last_engine = HOMS_B200_ENGINE_TENSOR_FP4;
     return tc_search_sorted(ctx, d_subset, n, keys, vals, d_out, k, k);
   }

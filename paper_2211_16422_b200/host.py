@@ -411,6 +411,7 @@ class Context:
         _check(capi.library_upload(self._h, dim, n, _ptr(words), _ptr(precursor_mz), _ptr(charge),
                                    _ptr(rank), shard_index, shard_count), self._h)
         self._set_lib(dim, n, is_decoy)
+        self.lib_precursor_mz = precursor_mz
 
     def build_index_dev(self, dim: int, d_words: int, n: int, precursor_mz, charge, ids=None,
                         is_decoy=None, shard_index: int = 0, shard_count: int = 1,
@@ -424,6 +425,7 @@ class Context:
         _check(capi.library_upload_dev(self._h, dim, n, d_words, _ptr(precursor_mz), _ptr(charge),
                                        _ptr(rank), shard_index, shard_count), self._h)
         self._set_lib(dim, n, is_decoy)
+        self.lib_precursor_mz = precursor_mz
 
     def _set_lib(self, dim, n, is_decoy):
         self.lib_dim, self.lib_n = dim, n
@@ -637,6 +639,48 @@ class Context:
                                          C.byref(cnt)), self._h)
         self.resident_queries = int(cnt.value)
         return ok
+
+    def queries_from_mgf(self, preprocess: PreprocessConfig, n_spectra: int) -> np.ndarray:
+        """Known-charge filter + encode_spectra (pipeline.cpp:127-141) of the CSR the last parse_mgf left on the
+        device; the result becomes the resident query set.  Returns state u8[n_spectra]: 0 = query, 1 = skipped
+        (unknown charge), 2 = unprocessable."""
+        state = np.zeros(n_spectra, np.uint8)
+        cnt = C.c_uint64()
+        _check(capi.queries_from_mgf(self._h, C.byref(preprocess.pod()), _ptr(state), C.byref(cnt)), self._h)
+        self.resident_queries = int(cnt.value)
+        return state
+
+    def search_file(self, text: bytes, preprocess: PreprocessConfig, narrow: Tolerance, wide: Tolerance, fdr_q: float,
+                    lib_ids, lib_peptides=None, decoy_prefix: str = "DECOY_") -> dict:
+        """The query side of run_search (pipeline.cpp:119-150): MGF text in, accepted SSMs + statistics + the
+        reference's TSV (write_ssm_tsv, :179-195) out.  The peaks never come back to the host; only titles,
+        precursors and charges do (for the Ssm records)."""
+        buf = np.frombuffer(text, np.uint8)
+        info = capi.MgfInfoPod()
+        _check(capi.mgf_parse(self._h, _ptr(buf) if len(buf) else 0, len(buf), C.byref(info)), self._h)
+        n = int(info.n_spectra)
+        state = self.queries_from_mgf(preprocess, n)
+        acc = self.cascade_resident(narrow, wide, fdr_q)
+        prec, charge = np.zeros(n, np.float64), np.zeros(n, np.uint8)
+        toff, tlen = np.zeros(n, np.uint32), np.zeros(n, np.uint32)
+        _check(capi.mgf_fetch(self._h, 0, 0, 0, _ptr(prec), _ptr(charge), _ptr(toff), _ptr(tlen), 0, 0), self._h)
+        kept = np.flatnonzero(state == 0)
+        lib_mz = self.lib_precursor_mz
+        lines = ["query_id\tlibrary_id\tpeptide\tcharge\tquery_precursor_mz\tlibrary_precursor_mz\tmass_diff\tscore\t"
+                 "stage\tq_value\n"]
+        dim_d = float(self.lib_dim)
+        for qi, o, st, sc, qv in zip(acc["query"], acc["ordinal"], acc["stage"], acc["raw_score"], acc["q_value"]):
+            i = int(kept[int(qi)])
+            qid = bytes(text[int(toff[i]):int(toff[i]) + int(tlen[i])]).decode() if tlen[i] else f"spectrum_{i + 1}"
+            lid = lib_ids[int(o)]
+            pep = lib_peptides[int(o)] if lib_peptides is not None else ""
+            lines.append("%s\t%s\t%s\t%u\t%.5f\t%.5f\t%.5f\t%.6f\t%s\t%.6g\n" % (
+                qid, lid, pep, charge[i], prec[i], lib_mz[int(o)], prec[i] - lib_mz[int(o)], float(sc) / dim_d,
+                "narrow" if st == 0 else "wide", qv))
+        stats = dict(total_queries=n, skipped_unknown_charge=int((state == 1).sum()), unprocessable=int((state == 2).sum()),
+                     accepted_narrow=int((acc["stage"] == 0).sum()), accepted_wide=int((acc["stage"] == 1).sum()),
+                     unidentified=int(len(kept) - len(acc["query"])))
+        return dict(accepted=acc, stats=stats, tsv="".join(lines).encode(), kept=kept)
 
     def search_resident(self, tol: Tolerance, k: int = 1, nq: int | None = None) -> Match:
         """search_batch over the resident queries."""

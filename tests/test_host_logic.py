@@ -113,3 +113,22 @@ def test_id_ranks(hb):
     want = np.empty(len(ids), np.uint32)
     want[order] = np.arange(len(ids))
     assert np.array_equal(rank, want)
+
+
+def test_config4_counter_stream_replays_on_the_host():
+    """the counter-based spectra bench.py generates with torch (on the device there,
+    on the CPU here) are bit-identical to the numpy replay, distinct and ascending on the 0.01 Th grid,
+    intensities in [0.05, 1); any window of the stream can be regenerated in isolation."""
+    import torch
+    import workload as wl
+    o, mz, it = wl.config4_numpy(7_654_321, 4096, 150)
+    o2, mz2, it2 = wl.config4_torch(7_654_321, 4096, "cpu", 150)
+    assert np.array_equal(mz, mz2.numpy()) and np.array_equal(it, it2.numpy())
+    assert np.array_equal(o.astype(np.int64), o2.numpy())
+    rows = mz.reshape(-1, 150)
+    assert (np.diff(rows, axis=1) > 0).all() and rows.min() >= 150.0 and rows.max() < 1300.0
+    assert it.min() >= 0.05 and it.max() < 1.0
+    # a window cut out of the middle is the same numbers
+    _, mz3, it3 = wl.config4_numpy(7_654_321 + 1000, 10, 150)
+    assert np.array_equal(mz3, mz[1000 * 150:1010 * 150]) and np.array_equal(it3, it[1000 * 150:1010 * 150])
+    assert torch.equal(wl.config4_torch(5, 3, "cpu", 150)[1], torch.from_numpy(wl.config4_numpy(5, 3, 150)[1]))

@@ -227,7 +227,10 @@ def test_topk_many_work_items_vs_port(hb, ctx, port):
     """Top-k where every query tile is cut into many work items (20k rows: ~12 strips of at most 8
     row tiles per query tile), so that the tensor engines' per-item k-lists, the published k-th-best
     floor and the list merge are all exercised; heavy score ties (rows duplicated four times, few
-    distinct m/z values and ids).  k = 16 is the tensor engines' depth, k = 17 falls to XOR+POPC."""
+    distinct m/z values and ids).  One pass of the tensor / direct engines keeps 32 candidates per query
+    (register lists of depth 4 / 8 / 16 / 32); k = 33 ... 64 take a second pass bounded below by the first
+    pass's last key -- with rows duplicated four times that key sits inside a run of equal scores, so
+    the (|mass diff|, id, ordinal) part of the bound decides."""
     rng = np.random.default_rng(29)
     dim, n, nq = 256, 20000, 300
     base = U.random_hvs(rng, n // 4, dim)
@@ -241,11 +244,17 @@ def test_topk_many_work_items_vs_port(hb, ctx, port):
     qch = np.full(nq, 2, np.uint8)
     ctx.build_index(dim, words, mz, charge, ids=ids)
     oix = port.build_index(dim, words, mz, charge, None, ids)
-    for tol, k in ((("da", 500.0), 2), (("da", 500.0), 16), (("da", 3.0), 7), (("da", 500.0), 17)):
+    ks = ((("da", 500.0), 2), (("da", 500.0), 16), (("da", 3.0), 7), (("da", 500.0), 17), (("da", 500.0), 32),
+          (("da", 500.0), 33), (("da", 500.0), 64), (("da", 0.3), 64), (("ppm", 200.0), 40))
+    if ctx.engine_name == "popc":  # k full passes on the XOR+POPC engine: keep it short
+        ks = ks[:4] + ((("da", 0.3), 64),)
+    for tol, k in ks:
         m = ctx.search_batch(qw, qmz, qch, U.product_tol(tol), k=k)
         score, ordinal = oix.search_topk(qw, qmz, qch, tol, k)
         assert np.array_equal(m.ordinal, ordinal), (tol, k)
         assert np.array_equal(m.raw_score, score), (tol, k)
+        if ctx.engine_name in ("tensor_fp4", "direct"):  # no fall-back to another engine at any depth
+            assert ctx.last_engine() == ctx.engine_name, (tol, k)
     oix.close()
 
 
@@ -259,7 +268,7 @@ def test_search_fuzz_vs_port(hb, ctx, port):
         dim = int(rng.choice([64, 100, 256, 500, 1024, 2048]))
         n = int(rng.integers(1, 2500))
         nq = int(rng.integers(1, 300))
-        k = int(rng.choice([1, 1, 2, 3, 5, 16, 17, 20]))
+        k = int(rng.choice([1, 1, 2, 3, 5, 16, 17, 20, 33, 48, 64]))
         distinct = max(1, int(n * rng.choice([0.02, 0.3, 1.0])))
         pool = U.random_hvs(rng, distinct, dim)
         words = pool[rng.integers(0, distinct, n)]

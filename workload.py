@@ -146,3 +146,83 @@ def make(name: str, generator: str = "auto"):
     lib = synth_library(n_targets, peaks, 1.0, seed)
     qry = synth_queries(lib, n_query, seed=seed)
     return lib, qry, dim, "numpy"
+
+
+# ---- BASELINE config 4: counter-based spectra -------------------------------------
+# "10 M spectra x 150 distinct-grid peaks ... generated on device with a counter-based splitmix64 stream
+# keyed by (seed = 4, spectrum, peak) so the CPU oracle can regenerate any sample."  Peak p of spectrum s
+# is a pure function of (seed, s, p): bench.py generates the whole set ON THE GPU with the torch form
+# (integer ops only, then exact int -> double conversions) and replays any sample on the host with the
+# numpy form -- the two are bit-identical, which tests/test_host_logic.py checks.
+#   stream(tag)[i] = finalise(base(tag) + (i + 1) * GOLDEN), base(tag) = finalise'(seed ^ finalise'(tag))
+#   m/z:       the 0.01 Th grid of synth.cpp:25 on [150, 1300) cut into `peaks` equal strata; peak p sits at
+#              cell 15000 + p * width + (top 32 bits of stream("mz")[s * peaks + p]) % width  (distinct, ascending)
+#   intensity: 0.05 + 0.95 * (stream("in")[s * peaks + p] >> 11) * 2^-53   (U[0.05, 1), synth.cpp:69)
+_GOLDEN = 0x9E3779B97F4A7C15
+_C1, _C2 = 0xBF58476D1CE4E5B9, 0x94D049BB133111EB
+_M64 = (1 << 64) - 1
+_GRID_LO, _GRID_CELLS = 15000, 115000
+
+
+def _mix_int(x: int) -> int:
+    x = (x + _GOLDEN) & _M64
+    x = ((x ^ (x >> 30)) * _C1) & _M64
+    x = ((x ^ (x >> 27)) * _C2) & _M64
+    return x ^ (x >> 31)
+
+
+def _stream_base(seed: int, tag: int) -> int:
+    return _mix_int(seed ^ _mix_int(tag))
+
+
+def _signed(x: int) -> int:
+    return x - (1 << 64) if x >= (1 << 63) else x
+
+
+def config4_numpy(first: int, n: int, peaks: int = 150, seed: int = 4):
+    """Spectra [first, first + n) of the config-4 set as host CSR arrays (offsets u64, mz f64, intensity f64)."""
+    with np.errstate(over="ignore"):
+        idx = np.arange(first * peaks, (first + n) * peaks, dtype=np.uint64) + np.uint64(1)
+
+        def stream(tag):
+            x = np.uint64(_stream_base(seed, tag)) + idx * np.uint64(_GOLDEN)
+            x = (x ^ (x >> np.uint64(30))) * np.uint64(_C1)
+            x = (x ^ (x >> np.uint64(27))) * np.uint64(_C2)
+            return x ^ (x >> np.uint64(31))
+
+        width = _GRID_CELLS // peaks
+        p = (np.arange(n * peaks, dtype=np.uint64) % np.uint64(peaks))
+        cell = np.uint64(_GRID_LO) + p * np.uint64(width) + (stream(0x6D7A) >> np.uint64(32)) % np.uint64(width)
+        mz = cell.astype(np.float64) * 0.01
+        u = (stream(0x696E) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+        inten = 0.95 * u
+        inten = inten + 0.05
+    offsets = np.arange(n + 1, dtype=np.uint64) * np.uint64(peaks)
+    return offsets, mz, inten
+
+
+def config4_torch(first: int, n: int, device, peaks: int = 150, seed: int = 4):
+    """The same spectra generated on `device` with torch integer ops (int64 wraps like uint64; logical
+    shifts are arithmetic shifts with the sign extension masked off)."""
+    import torch
+
+    def lsr(x, s):
+        return (x >> s) & ((1 << (64 - s)) - 1)
+
+    idx = torch.arange(first * peaks, (first + n) * peaks, dtype=torch.int64, device=device) + 1
+
+    def stream(tag):
+        x = idx * _signed(_GOLDEN) + _signed(_stream_base(seed, tag))
+        x = (x ^ lsr(x, 30)) * _signed(_C1)
+        x = (x ^ lsr(x, 27)) * _signed(_C2)
+        return x ^ lsr(x, 31)
+
+    width = _GRID_CELLS // peaks
+    p = torch.arange(n * peaks, dtype=torch.int64, device=device) % peaks
+    cell = _GRID_LO + p * width + lsr(stream(0x6D7A), 32) % width
+    mz = cell.to(torch.float64) * 0.01
+    u = lsr(stream(0x696E), 11).to(torch.float64) * (2.0 ** -53)
+    inten = 0.95 * u
+    inten = inten + 0.05
+    offsets = torch.arange(n + 1, dtype=torch.int64, device=device) * peaks
+    return offsets, mz, inten
