@@ -99,7 +99,8 @@ struct GroupWorkers;  // group.cu: one issuing thread per non-leading member of 
 // development knobs of the tensor-engine planner, read from the environment ONCE per context
 // (homs_b200_ctx_create), never on the search path; 0 = the built-in choice
 struct TcKnobs {
-  uint32_t group_tiles = 0, items_per_sm = 0, max_strip = 0, item_cap = 0;
+  uint32_t group_tiles = 0, items_per_sm = 0, max_strip = 0, item_cap = 0, group_mb = 0;
+  uint32_t l2_hints = 2;  // see TcParams::l2_hints (default: library tiles evict_first)
 };
 
 }  // namespace hb

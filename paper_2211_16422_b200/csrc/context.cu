@@ -134,6 +134,8 @@ int ctx_create_single(int device, homs_b200_ctx** out) {
   ctx->knobs.items_per_sm = env_u32("HOMS_B200_TC_ITEMS_PER_SM");
   ctx->knobs.max_strip = env_u32("HOMS_B200_TC_MAX_STRIP");
   ctx->knobs.item_cap = env_u32("HOMS_B200_TC_ITEM_CAP");
+  ctx->knobs.group_mb = env_u32("HOMS_B200_TC_GROUP_MB");
+  if (const char* e = getenv("HOMS_B200_TC_L2_HINTS")) ctx->knobs.l2_hints = static_cast<uint32_t>(atoi(e)) & 3u;
   *out = ctx;
   return HOMS_B200_OK;
 }

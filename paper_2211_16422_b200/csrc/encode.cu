@@ -211,6 +211,9 @@ __device__ __forceinline__ U4 ld_global_u4(const uint4* p) {
 #define HB_ENC_MINB 2   // resident CTAs per SM the register budget is sized for (A/B: profiles/)
 #define HB_ENC_WARPS 8  // warps (= spectra in flight) per CTA
 #endif
+#ifndef HB_ENC_PIPELINED
+#define HB_ENC_PIPELINED 1  // gathers of the next group issued while the current one is reduced (A/B: profiles/)
+#endif
 template <int NP, bool kLvlSmem>
 __global__ void __launch_bounds__(HB_ENC_WARPS * 32, HB_ENC_MINB)
 encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stride,
@@ -274,6 +277,123 @@ encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stri
       const unsigned char* lvl_b = reinterpret_cast<const unsigned char*>((kLvlSmem ? s_lvl : lvl_global) + uu);
       const uint32_t row_bytes = row_u4 * 16;
       const uint32_t null_lev = n_level_rows * row_bytes;  // the extra row
+#if HB_ENC_PIPELINED
+      // Software-pipelined gathers.  A group's 8 position-row gathers land ~1000 cycles after issue
+      // (L2 under load) and the XNOR + carry-save work on them is ~180 issue slots per warp; run back
+      // to back (load 8, wait, compute) the two add up and the kernel sits at 0.58 of the measured
+      // random-row gather ceiling (tools/l2_gather_bench).  Here the gathers of group t+1 are issued
+      // pairwise into the registers of group t as soon as the carry-save tree has consumed them, so
+      // every warp keeps ~8 gathers in flight WHILE it computes, at no extra registers.
+      uint32_t my_bin = 0, my_lev = null_lev, nxt_bin = 0, nxt_lev = null_lev;
+      if (lane < nb) {
+        my_bin = sv_bins[start + lane];
+        my_lev = sv_levels[start + lane] * row_bytes;
+      }
+      U4 x[8];
+      uint32_t lev[8];
+#define HB_ENC_ISSUE(j, src_bin, src_lev, kk)                                                         \
+  do {                                                                                                \
+    const uint32_t bin_ = __shfl_sync(0xffffffffu, (src_bin), (kk));                                  \
+    lev[j] = __shfl_sync(0xffffffffu, (src_lev), (kk));                                               \
+    x[j] = ld_global_u4(reinterpret_cast<const uint4*>(pos_b + uint64_t(bin_) * row_bytes));          \
+  } while (0)
+#define HB_ENC_XNOR(j)                                                                                \
+  do {                                                                                                \
+    const uint4* lp_ = reinterpret_cast<const uint4*>(lvl_b + lev[j]);                                \
+    const uint4 lw4_ = kLvlSmem ? *lp_ : __ldg(lp_);                                                  \
+    x[j].v[0] = ~(x[j].v[0] ^ lw4_.x); /* encoder.cpp:41 agree = ~(pos ^ lvl) */                      \
+    x[j].v[1] = ~(x[j].v[1] ^ lw4_.y);                                                                \
+    x[j].v[2] = ~(x[j].v[2] ^ lw4_.z);                                                                \
+    x[j].v[3] = ~(x[j].v[3] ^ lw4_.w);                                                                \
+  } while (0)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) HB_ENC_ISSUE(j, my_bin, my_lev, j);  // prologue: group 0 (nb >= 1)
+      for (uint32_t c0 = 0; c0 < nb; c0 += 32) {
+        if (c0 + 32 + lane < nb) {  // stage the next block of 32 entries (lane j holds entry c0 + 32 + j)
+          nxt_bin = sv_bins[start + c0 + 32 + lane];
+          nxt_lev = sv_levels[start + c0 + 32 + lane] * row_bytes;
+        } else {
+          nxt_bin = 0;
+          nxt_lev = null_lev;
+        }
+        const uint32_t cn = min(32u, nb - c0);
+        const uint32_t cn_next = c0 + 32 < nb ? min(32u, nb - c0 - 32) : 0u;
+        const uint32_t n_groups = 2 * ((cn + 15) / 16);  // groups of 8, an even number of them
+        U4 pend8{{0, 0, 0, 0}}, pend16{{0, 0, 0, 0}};
+#pragma unroll 1
+        for (uint32_t g = 0; g < n_groups; ++g) {
+          // the group after this one: in this block, or group 0 of the next block
+          const bool in_block = g + 1 < n_groups;
+          const bool has_next = in_block ? 8 * (g + 1) < cn : cn_next > 0;
+          const uint32_t nb_src = in_block ? my_bin : nxt_bin, nl_src = in_block ? my_lev : nxt_lev;
+          const uint32_t kb = in_block ? 8 * (g + 1) : 0;
+          U4 e{{0, 0, 0, 0}};
+          if (8 * g < cn) {  // a group wholly past the end of the list only completes the carry pairing
+            // 8 inputs -> c[0..2] updated, one carry e of weight 8; consumed registers refill at once
+            U4 ta, tb, fa, fb;
+            HB_ENC_XNOR(0);
+            HB_ENC_XNOR(1);
+            HB_CSA(c[0], ta, c[0], x[0], x[1]);
+            if (has_next) {
+              HB_ENC_ISSUE(0, nb_src, nl_src, kb + 0);
+              HB_ENC_ISSUE(1, nb_src, nl_src, kb + 1);
+            }
+            HB_ENC_XNOR(2);
+            HB_ENC_XNOR(3);
+            HB_CSA(c[0], tb, c[0], x[2], x[3]);
+            if (has_next) {
+              HB_ENC_ISSUE(2, nb_src, nl_src, kb + 2);
+              HB_ENC_ISSUE(3, nb_src, nl_src, kb + 3);
+            }
+            HB_CSA(c[1], fa, c[1], ta, tb);
+            HB_ENC_XNOR(4);
+            HB_ENC_XNOR(5);
+            HB_CSA(c[0], ta, c[0], x[4], x[5]);
+            if (has_next) {
+              HB_ENC_ISSUE(4, nb_src, nl_src, kb + 4);
+              HB_ENC_ISSUE(5, nb_src, nl_src, kb + 5);
+            }
+            HB_ENC_XNOR(6);
+            HB_ENC_XNOR(7);
+            HB_CSA(c[0], tb, c[0], x[6], x[7]);
+            if (has_next) {
+              HB_ENC_ISSUE(6, nb_src, nl_src, kb + 6);
+              HB_ENC_ISSUE(7, nb_src, nl_src, kb + 7);
+            }
+            HB_CSA(c[1], fb, c[1], ta, tb);
+            HB_CSA(c[2], e, c[2], fa, fb);
+          } else if (has_next) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) HB_ENC_ISSUE(j, nb_src, nl_src, kb + j);
+          }
+          if ((g & 1u) == 0) {
+            pend8 = e;
+          } else {  // the weight-8 carries of an even/odd pair meet in c[3] ...
+            U4 carry;
+            HB_CSA(c[3], carry, c[3], pend8, e);
+            if ((g & 2u) == 0 && g + 1 < n_groups) {
+              pend16 = carry;
+            } else {  // ... the weight-16 carries of two pairs in c[4], and the rest ripples up
+              if ((g & 2u) == 0) pend16 = U4{{0, 0, 0, 0}};  // a lone pair (at most 16 entries left)
+              HB_CSA(c[4], carry, c[4], pend16, carry);
+#pragma unroll
+              for (int b = 5; b < NP; ++b) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const uint32_t a = c[b].v[i];
+                  c[b].v[i] = a ^ carry.v[i];
+                  carry.v[i] = a & carry.v[i];
+                }
+              }
+            }
+          }
+        }
+        my_bin = nxt_bin;
+        my_lev = nxt_lev;
+      }
+#undef HB_ENC_ISSUE
+#undef HB_ENC_XNOR
+#else
       uint32_t nxt_bin = 0, nxt_lev = null_lev;
       if (lane < nb) {
         nxt_bin = sv_bins[start + lane];
@@ -346,6 +466,8 @@ encode_kernel(uint64_t n, const uint64_t* __restrict__ sv_offsets, uint32_t stri
           }
         }
       }
+
+#endif
 
       // votes >= thresh, plane by plane from the top
       U4 res;

@@ -102,7 +102,7 @@ struct TcParams {
   uint32_t prev_col;      // pass > 0: column of `prev` holding the last key of the previous pass
   const Cand* prev;       // pass > 0: the output so far, [slot][prev_stride]; only keys strictly after
   uint32_t prev_stride;   //           prev[slot][prev_col] are candidates of this pass (nullptr: pass 0)
-  uint32_t pad2;
+  uint32_t l2_hints;      // bit 0: query tiles (A) evict_last, bit 1: library tiles (B) evict_first
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
@@ -144,6 +144,23 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
+}
+// the same copy with an L2 eviction-priority hint (createpolicy descriptor)
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -546,6 +563,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     // ===== producer: two bulk copies per stage =====
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, qslot = 0, qphase = 0;
+      // L2 residency: a library strip (B) is read by the group's query tiles within one short window and is
+      // then dead, while the group's query tiles (A) are re-read for every strip of the sweep.  Fetching B
+      // with evict_first keeps the streaming strips from pushing A out (default; -1.7 ... -3.7 % kernel time
+      // on configs 2, 3 and D = 16384); evict_last on A on top of that measured no gain (bit 0, off).
+      const bool hint_a = p.l2_hints & 1u, hint_b = p.l2_hints & 2u;
+      const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
       uint32_t next = atomicAdd(p.counter, 1u);
       for (;;) {
         const uint32_t item = next;
@@ -567,8 +590,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
             mbar_wait(empty_bar(stage), phase ^ 1u);
             const uint32_t sa = base + stage * Mode::StageBytes;
             mbar_expect_tx(full_bar(stage), Mode::StageBytes);
-            bulk_g2s(sa, a_src + uint64_t(kc) * p.q_rows * kTcKB, kTcABytes, full_bar(stage));
-            bulk_g2s(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, Mode::BBytes, full_bar(stage));
+            if (hint_a) bulk_g2s_hint(sa, a_src + uint64_t(kc) * p.q_rows * kTcKB, kTcABytes, full_bar(stage), pol_a);
+            else bulk_g2s(sa, a_src + uint64_t(kc) * p.q_rows * kTcKB, kTcABytes, full_bar(stage));
+            if (hint_b)
+              bulk_g2s_hint(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, Mode::BBytes, full_bar(stage), pol_b);
+            else bulk_g2s(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, Mode::BBytes, full_bar(stage));
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1u;
@@ -961,11 +987,17 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   //    host knows: every tile's window is at most the whole local library.
   TcPlanCfg pc;
   pc.n_tiles = n_tiles;
-  // query tiles per group: as many as keep the group's A operand (tiles x n_kc x 16 KB) resident in
-  // about a quarter of the L2 while the group sweeps the strips -- every B strip is then fetched from DRAM
-  // once per group (measured with the dynamic queue, config 2: 12 -> 125 tiles per group, 23.6 -> 22.4 ms)
-  pc.group_tiles = static_cast<uint32_t>(
-      std::max<uint64_t>(kTcGroupTiles, (32ull << 20) / (uint64_t(kTcM) * lib.n_kc * kTcKB)));
+  // Query tiles per group.  A group's A operand (tiles x n_kc x 16 KB) is re-read for every strip of the
+  // sweep, so it has to stay in L2 while the library strips stream through (fetched with an evict_first
+  // hint, see the producer): 32 MB groups in general; when ALL query tiles of the batch fit in 64 MB they
+  // form one group and every library strip is fetched from DRAM exactly once (config 2: 125 tiles = 62.5 MB,
+  // DRAM 8.4 -> 5.9 GB per launch = 1.19x the compulsory bytes, 22.4 -> 21.6 ms; 64 MB groups on longer
+  // query sets -- several groups, each sweeping the whole library -- measured 8 % slower than 32 MB:
+  // profiles/r02_sweep_l2_hints_group.log)
+  const uint64_t a_tile = uint64_t(kTcM) * lib.n_kc * kTcKB;
+  uint64_t a_budget = uint64_t(n_tiles) * a_tile <= (64ull << 20) ? 64ull << 20 : 32ull << 20;
+  if (knobs.group_mb) a_budget = uint64_t(knobs.group_mb) << 20;
+  pc.group_tiles = static_cast<uint32_t>(std::max<uint64_t>(kTcGroupTiles, a_budget / a_tile));
   pc.max_strip = 8;
   uint32_t items_per_sm = 400;
   if (knobs.group_tiles) pc.group_tiles = knobs.group_tiles;
@@ -1045,7 +1077,7 @@ static int tc_run_pass(homs_b200_ctx* ctx, const TcBatch& tb, const uint32_t* d_
   tp.prev = prev_col != kNone ? d_out_full : nullptr;
   tp.prev_stride = k_stride;
   tp.prev_col = prev_col;
-  tp.pad2 = 0;
+  tp.l2_hints = ctx->knobs.l2_hints;
   {
     KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
     tc_search_kernel<KM><<<ctx->sm_count, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
