@@ -212,7 +212,12 @@ __device__ __forceinline__ U4 ld_global_u4(const uint4* p) {
 #define HB_ENC_WARPS 8  // warps (= spectra in flight) per CTA
 #endif
 #ifndef HB_ENC_PIPELINED
-#define HB_ENC_PIPELINED 1  // gathers of the next group issued while the current one is reduced (A/B: profiles/)
+// 1: the gathers of group t+1 are issued pairwise into the registers of group t as the carry-save tree
+// consumes them (software pipelining at no extra registers).  MEASURED AND LEFT OFF: 3.31 -> 5.86 ms per
+// 250 k spectra (profiles/r02_ab_encode_pipelined.log) -- with four refill points per iteration the
+// refilled pairs share scoreboards with pairs still awaited, so every wait also covers loads issued a few
+// instructions earlier and the L2 latency is exposed four times per group instead of once.
+#define HB_ENC_PIPELINED 0
 #endif
 template <int NP, bool kLvlSmem>
 __global__ void __launch_bounds__(HB_ENC_WARPS * 32, HB_ENC_MINB)
