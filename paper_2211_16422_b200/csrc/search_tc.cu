@@ -998,14 +998,14 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   uint64_t a_budget = uint64_t(n_tiles) * a_tile <= (64ull << 20) ? 64ull << 20 : 32ull << 20;
   if (knobs.group_mb) a_budget = uint64_t(knobs.group_mb) << 20;
   pc.group_tiles = static_cast<uint32_t>(std::max<uint64_t>(kTcGroupTiles, a_budget / a_tile));
-  // Work-item length.  An item costs its drain warps a few dependent global loads (window, precursor, floor)
-  // before the first accumulator can be released: ~2-3 us, hidden behind two row tiles of MMAs at D = 8192
-  // (8.6 us each) but not at D = 1024 (1.1 us each), where items of 8 row tiles lost 23 % to it.  Items
-  // are therefore sized in BYTES of library tile streamed (strip x n_kc x 28 KB, the D = 8192 shape:
-  // 8 row tiles x 32 k-chunks), which also keeps the L2 footprint of co-running strips constant.
-  const uint32_t kc_ratio = std::max(1u, 32u / std::max(1u, lib.n_kc));  // 1 at D >= 8192, 8 at D = 1024
-  pc.max_strip = std::min(64u, 8u * kc_ratio);
-  uint32_t items_per_sm = std::max(64u, 400u / kc_ratio);
+  // Work-item length: about 400 items per SM of at most 8 row tiles keep co-running CTAs on neighbouring
+  // tiles (L2 sharing) and the tail short.  An item also costs its drain warps 2-3 us of dependent global
+  // loads (window, precursor, floor) before the first accumulator can be released; two 8.6 us row tiles hide
+  // that at D = 8192, 1.1 us row tiles at D <= 1024 do not, so there items are 4x longer (interleaved A/B on
+  // one box, profiles/r02_ab_item_sizing.log: D = 1024 3.18 -> 3.03 ms; D = 2048 and 4096 no gain, left alone).
+  const bool short_k = lib.n_kc <= 4;
+  pc.max_strip = short_k ? 32 : 8;
+  uint32_t items_per_sm = short_k ? 100 : 400;
   if (knobs.group_tiles) pc.group_tiles = knobs.group_tiles;
   if (knobs.items_per_sm) items_per_sm = knobs.items_per_sm;
   if (knobs.max_strip) pc.max_strip = knobs.max_strip;
