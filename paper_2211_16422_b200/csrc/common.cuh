@@ -101,6 +101,8 @@ struct GroupWorkers;  // group.cu: one issuing thread per non-leading member of 
 struct TcKnobs {
   uint32_t group_tiles = 0, items_per_sm = 0, max_strip = 0, item_cap = 0, group_mb = 0;
   uint32_t l2_hints = 2;  // see TcParams::l2_hints (default: library tiles evict_first)
+  uint32_t topk_lists = 0;  // 1: top-k through the register-list passes instead of collect + select
+  uint32_t ccap = 0;        // collect mode: candidate buffer entries per query (0: built-in)
 };
 
 }  // namespace hb
@@ -118,7 +120,7 @@ struct homs_b200_ctx {
   hb::Queries q;
   hb::MgfState mgf;
   // grow-only scratch, keyed by purpose
-  enum { kScratchSlots = 48 };
+  enum { kScratchSlots = 56 };
   hb::DevBuf scratch[kScratchSlots];
   int engine = HOMS_B200_ENGINE_AUTO;  // homs_b200_ctx_set_engine
   int last_engine = HOMS_B200_ENGINE_AUTO;  // engine the last search call ran on (never AUTO after a search)
@@ -203,7 +205,8 @@ enum Scratch {
   kScrPartial, kScrRecords, kScrSubset, kScrDecode, kScrMisc, kScrMisc2, kScrRecords2, kScrHas,
   kScrTcQx, kScrTcPlan, kScrTcPartial, kScrTcTiles, kScrTcBest, kScrFnv, kScrCacheBlock,
   kScrPipeIn0, kScrPipeIn1, kScrPipeOut0, kScrPipeOut1, kScrFusedRows, kScrFusedOk,
-  kScrMgfText, kScrMgfTiles, kScrMgfLines, kScrMgfBlocks, kScrMgfPeaks, kScrMgfHard, kScrIndexSort
+  kScrMgfText, kScrMgfTiles, kScrMgfLines, kScrMgfBlocks, kScrMgfPeaks, kScrMgfHard, kScrIndexSort,
+  kScrTcCount, kScrTcBuf, kScrTcOverflow, kScrTcKeysFix
 };
 
 // Tensor-core engine (search_tc.cu).  expand: packed rows -> +-1 e2m1 swizzled image.

@@ -135,6 +135,8 @@ int ctx_create_single(int device, homs_b200_ctx** out) {
   ctx->knobs.max_strip = env_u32("HOMS_B200_TC_MAX_STRIP");
   ctx->knobs.item_cap = env_u32("HOMS_B200_TC_ITEM_CAP");
   ctx->knobs.group_mb = env_u32("HOMS_B200_TC_GROUP_MB");
+  ctx->knobs.ccap = env_u32("HOMS_B200_TC_CCAP");
+  if (const char* e = getenv("HOMS_B200_TC_TOPK")) ctx->knobs.topk_lists = std::string(e) == "lists" ? 1u : 0u;
   if (const char* e = getenv("HOMS_B200_TC_L2_HINTS")) ctx->knobs.l2_hints = static_cast<uint32_t>(atoi(e)) & 3u;
   *out = ctx;
   return HOMS_B200_OK;

@@ -103,6 +103,11 @@ struct TcParams {
   const Cand* prev;       // pass > 0: the output so far, [slot][prev_stride]; only keys strictly after
   uint32_t prev_stride;   //           prev[slot][prev_col] are candidates of this pass (nullptr: pass 0)
   uint32_t l2_hints;      // bit 0: query tiles (A) evict_last, bit 1: library tiles (B) evict_first
+  // collect mode (KM == 0): candidates at or above the query's floor are appended to its buffer
+  uint32_t* ccount;       // [q_rows] entries appended so far (may run past ccap: overflow, see tc_select_kernel)
+  uint2* cbuf;            // [q_rows][ccap] (dot, local row)
+  uint32_t ccap;
+  uint32_t pad3;
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
@@ -489,7 +494,9 @@ struct TcAcc {
 // KM = 1: plain top-1 drain; KM > 1: the drain keeps the best KM >= p.k candidates per query
 template <int KM>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams p) {
-  constexpr bool kTopK = KM > 1;
+  constexpr bool kTopK = KM > 1;      // register lists of depth KM
+  constexpr bool kCollect = KM == 0;  // append candidates above the floor, select exactly afterwards
+  constexpr int kList = KM > 0 ? KM : 1;
   using Mode = TcMode;
   using Acc = TcAcc;
   using AccT = typename Acc::T;
@@ -682,7 +689,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         }
         const uint32_t slot = p.vals[pos];
         qmz = p.q_mz[p.subset ? p.subset[slot] : slot];
-        if constexpr (kTopK) {  // k dots of distinct candidates: the smallest bounds the final k-th best
+        if constexpr (kTopK || kCollect) {  // k dots of distinct candidates: the smallest bounds the final k-th best
           floor_i = INT_MAX;
           for (uint32_t j = 0; j < p.k; ++j) floor_i = min(floor_i, __ldcg(p.gbest + pos * p.k + j));
         } else {
@@ -712,12 +719,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
       uint32_t best_row = kNone, best_rk = 0;
       uint64_t best_ad = 0;
       bool have_key = false;
-      TcTopK<KM> topk;  // kTopK only
+      TcTopK<kList> topk;  // kTopK only
 #pragma unroll
-      for (int i = 0; i < KM; ++i) {
+      for (int i = 0; i < kList; ++i) {
         topk.dot[i] = kTcNoDot;
         topk.row[i] = kNone;
       }
+      uint32_t fresh = 0;  // kCollect: candidates appended since the floor was last read
 
       for (uint32_t nt = 0; nt < n_nt; ++nt) {
         const uint32_t row0 = it.row_begin + nt * kN;
@@ -726,6 +734,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         int c1 = ll > row0 ? static_cast<int>(min(ll - row0, uint32_t(kN))) : 0;
         if (c1 <= c0) c0 = c1 = 0;
 
+        if constexpr (kCollect) {
+          // While the floor is still weak a thread appends most of what it sees; its own appends (and
+          // those of items running elsewhere) have raised the class slots meanwhile: read them again.
+          if (fresh >= 4) {
+            int f = INT_MAX;
+            for (uint32_t j = 0; j < p.k; ++j) f = min(f, __ldcg(p.gbest + pos * p.k + j));
+            bar = max(bar, Acc::from_int(f));
+            fresh = 0;
+          }
+        }
         mbar_wait(tfull_bar(acc), (tphase >> acc) & 1u);
         tphase ^= 1u << acc;
         tc_fence_after();
@@ -744,6 +762,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
             return;
           }
           if (cm < bar) return;
+          if constexpr (kCollect) {
+            // Every valid column at or above the floor goes to the query's buffer; nothing else happens
+            // here: no list, no tie-break loads, a few instructions per candidate.  The floor is the
+            // smallest of k class maxima (class = row mod k), i.e. a dot that k DISTINCT rows of this
+            // query's window reach, so the final k-th best dot can never be below it and every row
+            // that ties with or beats the final k-th best is appended.  tc_select_kernel picks the exact
+            // k best (full reference key) out of the buffer.
+            uint32_t hits = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) hits |= (Acc::get(v[j]) >= bar ? 1u : 0u) << j;
+            const int lo = max(c0 - cb, 0), hi = min(c1 - cb, 32);  // 0 <= lo < hi <= 32 here
+            hits &= (hi >= 32 ? 0xffffffffu : (1u << hi) - 1u) & ~((1u << lo) - 1u);
+            while (hits) {
+              const int jj = __ffs(hits) - 1;
+              hits &= hits - 1;
+              AccT vj = Acc::lowest();
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j == jj) vj = Acc::get(v[j]);
+              const int dot = Acc::to_int(vj);
+              const uint32_t r = row0 + cb + jj;
+              const uint32_t idx = atomicAdd(p.ccount + pos, 1u);
+              if (idx < p.ccap) p.cbuf[pos * p.ccap + idx] = make_uint2(static_cast<uint32_t>(dot), r);
+              atomicMax(p.gbest + pos * p.k + r % p.k, dot);
+              ++fresh;
+            }
+            return;
+          }
           if constexpr (kTopK) {
             // every valid column at or above the bar is a candidate for the k best; the bar rises
             // to the list's k-th dot as soon as the list is full (ties with it must still be looked at)
@@ -769,8 +815,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
                   if (!key_less(prev_ad, prev_rk, ad, p.lib_rank[r])) continue;
                 }
               }
-              tc_topk_insert<KM>(topk, p.lib_mz, p.lib_rank, qmz, Acc::to_int(vj), row0 + cb + jj);
-              bar = max(bar, Acc::from_int(tc_topk_kth<KM>(topk, p.k)));
+              tc_topk_insert<kList>(topk, p.lib_mz, p.lib_rank, qmz, Acc::to_int(vj), row0 + cb + jj);
+              bar = max(bar, Acc::from_int(tc_topk_kth<kList>(topk, p.k)));
             }
             return;
           }
@@ -824,6 +870,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         acc ^= 1u;
       }
 
+      if constexpr (kCollect) continue;  // everything this item found is already in the query's buffer
       if constexpr (kTopK) {
         const uint32_t k = p.k;
         Cand* dst = p.partial + (uint64_t(item) * kTcM + qrow) * k;
@@ -903,9 +950,11 @@ tc_reduce_kernel(uint64_t n, const uint32_t* __restrict__ vals, const uint32_t* 
 __global__ void tc_reduce_topk_kernel(uint64_t n, const uint32_t* __restrict__ vals,
                                       const uint32_t* __restrict__ tile_item_start,
                                       const uint32_t* __restrict__ tile_items, const Cand* __restrict__ partial,
-                                      Cand* __restrict__ out, uint32_t k, uint32_t k_stride) {
+                                      Cand* __restrict__ out, uint32_t k, uint32_t k_stride,
+                                      const uint8_t* __restrict__ only) {
   const uint64_t pos = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (pos >= n) return;
+  if (only != nullptr && !only[pos]) return;  // fix-up pass: this query already has its exact answer
   const uint32_t t = static_cast<uint32_t>(pos / kTcM), r = static_cast<uint32_t>(pos % kTcM);
   Cand best[kTcMaxK];  // k <= kTcMaxK per pass
   uint32_t count = 0;
@@ -933,6 +982,123 @@ __global__ void tc_reduce_topk_kernel(uint64_t n, const uint32_t* __restrict__ v
   }
   Cand* dst = out + uint64_t(vals[pos]) * k_stride;
   for (uint32_t j = 0; j < k; ++j) dst[j] = j < count ? best[j] : Cand{kNone, kNone, ~0ull};
+}
+
+// ---- collect mode: exact selection ------------------------------------------------------------
+// One warp per sorted position: the k best, by the full reference key, of the candidates the drain appended.
+//   1. T = the k-th largest dot in the buffer (binary search on the value, counting with the whole warp);
+//      everything below T is out, everything above it is in, rows with dot == T compete on (|dm|, id_rank).
+//   2. the survivors (dot >= T; k plus the ties at T) are expanded to full 16-byte keys once, in shared
+//      memory, and the k smallest are extracted in order.  A buffer with more survivors than the staging
+//      area (degenerate libraries: thousands of equal scores) is extracted straight from global memory.
+// A query whose buffer overflowed (ccount > ccap) is flagged and left to the fix-up pass of the caller.
+constexpr int kSelWarps = 4;
+constexpr uint32_t kSelStage = 256;  // survivors staged per warp (16 B each)
+__global__ void __launch_bounds__(kSelWarps * 32)
+tc_select_kernel(uint64_t n, const uint32_t* __restrict__ vals, const uint32_t* __restrict__ subset,
+                 const uint32_t* __restrict__ ccount, const uint2* __restrict__ cbuf, uint32_t ccap, uint32_t k,
+                 uint32_t k_stride, uint32_t dim, const double* __restrict__ q_mz,
+                 const double* __restrict__ lib_mz, const uint32_t* __restrict__ lib_rank, Cand* __restrict__ out,
+                 uint8_t* __restrict__ overflow) {
+  __shared__ Cand s_stage[kSelWarps][kSelStage];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t pos = uint64_t(blockIdx.x) * kSelWarps + warp;
+  if (pos >= n) return;
+  const uint32_t cnt = ccount[pos];
+  if (cnt > ccap) {
+    if (lane == 0) overflow[pos] = 1;
+    return;
+  }
+  if (lane == 0) overflow[pos] = 0;
+  const uint32_t slot = vals[pos];
+  const double qmz = q_mz[subset ? subset[slot] : slot];
+  const uint2* e = cbuf + pos * ccap;
+  Cand* dst = out + uint64_t(slot) * k_stride;
+
+  // 1. T
+  int T = INT_MIN;
+  if (cnt > k) {
+    int lo = INT_MAX, hi = INT_MIN;
+    for (uint32_t i = lane; i < cnt; i += 32) {
+      const int d = static_cast<int>(e[i].x);
+      lo = min(lo, d);
+      hi = max(hi, d);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    while (lo < hi) {  // largest v with count(dot >= v) >= k
+      const int mid = lo + (hi - lo + 1) / 2;
+      uint32_t c = 0;
+      for (uint32_t i = lane; i < cnt; i += 32) c += static_cast<int>(e[i].x) >= mid ? 1u : 0u;
+      c = __reduce_add_sync(0xffffffffu, c);
+      if (c >= k) lo = mid;
+      else hi = mid - 1;
+    }
+    T = lo;
+  }
+  // 2. survivors
+  uint32_t m = 0;
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const bool keep = i < cnt && static_cast<int>(e[i].x) >= T;
+    const uint32_t mask = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const uint32_t at = m + __popc(mask & ((1u << lane) - 1u));
+      if (at < kSelStage) {
+        const uint32_t row = e[i].y;
+        s_stage[warp][at] = Cand{static_cast<uint32_t>(static_cast<int>(dim) - static_cast<int>(e[i].x)) >> 1,
+                                 lib_rank[row], static_cast<uint64_t>(__double_as_longlong(fabs(qmz - lib_mz[row])))};
+      }
+    }
+    m += __popc(mask);
+  }
+  __syncwarp();
+  Cand last{0, 0, 0};
+  bool have_last = false;
+  for (uint32_t j = 0; j < k; ++j) {
+    Cand best{kNone, kNone, ~0ull};
+    if (m <= kSelStage) {
+      for (uint32_t i = lane; i < m; i += 32) {
+        const Cand c = s_stage[warp][i];
+        if (have_last && !(last.d != c.d ? last.d < c.d : key_less(last.ad, last.rk, c.ad, c.rk))) continue;
+        if (c.d != best.d ? c.d < best.d : key_less(c.ad, c.rk, best.ad, best.rk)) best = c;
+      }
+    } else {  // too many survivors to stage: straight from the buffer, keys rebuilt on demand
+      for (uint32_t i = lane; i < cnt; i += 32) {
+        const int dot = static_cast<int>(e[i].x);
+        if (dot < T) continue;
+        const uint32_t d = static_cast<uint32_t>(static_cast<int>(dim) - dot) >> 1;
+        if ((have_last && d < last.d) || d > best.d) continue;
+        const uint32_t row = e[i].y;
+        const Cand c{d, lib_rank[row], static_cast<uint64_t>(__double_as_longlong(fabs(qmz - lib_mz[row])))};
+        if (have_last && !(last.d != c.d ? last.d < c.d : key_less(last.ad, last.rk, c.ad, c.rk))) continue;
+        if (c.d != best.d ? c.d < best.d : key_less(c.ad, c.rk, best.ad, best.rk)) best = c;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      Cand c;
+      c.d = __shfl_xor_sync(0xffffffffu, best.d, o);
+      c.rk = __shfl_xor_sync(0xffffffffu, best.rk, o);
+      c.ad = __shfl_xor_sync(0xffffffffu, best.ad, o);
+      if (c.d != best.d ? c.d < best.d : key_less(c.ad, c.rk, best.ad, best.rk)) best = c;
+    }
+    if (lane == 0) dst[j] = best;
+    if (best.d == kNone) {  // fewer than k candidates: the rest is empty
+      for (uint32_t jj = j + 1 + lane; jj < k; jj += 32) dst[jj] = Cand{kNone, kNone, ~0ull};
+      break;
+    }
+    last = best;
+    have_last = true;
+  }
+}
+
+// fix-up pass of collect mode: only the flagged queries keep their window
+__global__ void tc_mask_keys_kernel(uint64_t n, const uint64_t* __restrict__ keys, const uint8_t* __restrict__ flag,
+                                    uint64_t* __restrict__ out) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = flag[i] ? keys[i] : ~0ull;
 }
 
 // ---- host side --------------------------------------------------------------------------------
@@ -968,8 +1134,11 @@ struct TcBatch {
   TcPlanPtrs pp{};
 };
 
+// k_partial: list depth the per-item partial block is sized for (0: none, collect mode); reuse_qx: the
+// expanded queries of this very batch are already in place (fix-up pass)
 static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const uint64_t* d_keys,
-                            const uint32_t* d_vals, uint64_t b0, uint64_t nb, uint32_t k_pass, TcBatch* out) {
+                            const uint32_t* d_vals, uint64_t b0, uint64_t nb, uint32_t k_pass, uint32_t k_partial,
+                            bool reuse_qx, TcBatch* out) {
   constexpr uint32_t kN = TcMode::N;
   const Library& lib = ctx->lib;
   const Queries& q = ctx->q;
@@ -1014,8 +1183,8 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   const uint64_t slack = 2ull * n_tiles + 16;
   const uint64_t by_shape =
       std::max<uint64_t>(pc.target_items, (uint64_t(n_tiles) * pc.tiles_total + pc.max_strip - 1) / pc.max_strip) + slack;
-  const uint64_t by_memory =
-      std::max<uint64_t>((4ull << 30) / (size_t(kTcM) * k_pass * sizeof(Cand)), slack + 4ull * ctx->sm_count);
+  const uint64_t by_memory = std::max<uint64_t>(
+      (4ull << 30) / (size_t(kTcM) * std::max(1u, k_partial) * sizeof(Cand)), slack + 4ull * ctx->sm_count);
   pc.item_cap = static_cast<uint32_t>(std::min<uint64_t>(std::min(by_shape, by_memory), 0x7fffffffull));
   if (knobs.item_cap)  // development / test knob: force the capacity-bound plan
     pc.item_cap = static_cast<uint32_t>(std::min<uint64_t>(pc.item_cap, std::max<uint64_t>(slack + 1, knobs.item_cap)));
@@ -1029,10 +1198,12 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   HB_LAUNCHED(ctx);
 
   // 3. expand the batch's queries in sorted order
-  HB_TRY(ensure(ctx, ctx->scratch[kScrTcQx], size_t(lib.n_kc) * q_rows * kTcKB));
-  HB_TRY(expand_launch(ctx, q_rows, nb, d_vals, d_subset, b0, q.d_words.as<uint64_t>(), stride_for(q.dim), q.dim,
-                       lib.n_kc, ctx->scratch[kScrTcQx].as<uint8_t>()));
-  HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], size_t(pc.item_cap) * kTcM * k_pass * sizeof(Cand)));
+  if (!reuse_qx) {
+    HB_TRY(ensure(ctx, ctx->scratch[kScrTcQx], size_t(lib.n_kc) * q_rows * kTcKB));
+    HB_TRY(expand_launch(ctx, q_rows, nb, d_vals, d_subset, b0, q.d_words.as<uint64_t>(), stride_for(q.dim), q.dim,
+                         lib.n_kc, ctx->scratch[kScrTcQx].as<uint8_t>()));
+  }
+  if (k_partial) HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], size_t(pc.item_cap) * kTcM * k_partial * sizeof(Cand)));
   HB_TRY(ensure(ctx, ctx->scratch[kScrTcBest], q_rows * k_pass * sizeof(int)));
   out->b0 = b0;
   out->nb = nb;
@@ -1047,7 +1218,7 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
 template <int KM>
 static int tc_run_pass(homs_b200_ctx* ctx, const TcBatch& tb, const uint32_t* d_subset, const uint64_t* d_keys,
                        const uint32_t* d_vals, Cand* d_out_full, uint32_t k_stride, uint32_t col0, uint32_t k,
-                       uint32_t prev_col) {
+                       uint32_t prev_col, const uint8_t* d_only = nullptr) {
   using Mode = TcMode;
   const Library& lib = ctx->lib;
   const Queries& q = ctx->q;
@@ -1084,6 +1255,10 @@ static int tc_run_pass(homs_b200_ctx* ctx, const TcBatch& tb, const uint32_t* d_
   tp.prev_stride = k_stride;
   tp.prev_col = prev_col;
   tp.l2_hints = ctx->knobs.l2_hints;
+  tp.ccount = nullptr;
+  tp.cbuf = nullptr;
+  tp.ccap = 0;
+  tp.pad3 = 0;
   {
     KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
     tc_search_kernel<KM><<<ctx->sm_count, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
@@ -1092,7 +1267,7 @@ static int tc_run_pass(homs_b200_ctx* ctx, const TcBatch& tb, const uint32_t* d_
   if constexpr (KM > 1)
     tc_reduce_topk_kernel<<<static_cast<unsigned>((tb.nb + 127) / 128), 128, 0, ctx->stream>>>(
         tb.nb, d_vals + tb.b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out_full + col0,
-        k, k_stride);
+        k, k_stride, d_only);
   else
     tc_reduce_kernel<<<tb.n_tiles, dim3(kTcM, kTcReduceSlices), 0, ctx->stream>>>(
         tb.nb, d_vals + tb.b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out_full + col0,
@@ -1101,25 +1276,111 @@ static int tc_run_pass(homs_b200_ctx* ctx, const TcBatch& tb, const uint32_t* d_
   return HOMS_B200_OK;
 }
 
-uint32_t tc_max_topk() { return HOMS_B200_MAX_TOPK; }  // any k the ABI allows: ceil(k / 32) passes
+uint32_t tc_max_topk() { return HOMS_B200_MAX_TOPK; }  // any k the ABI allows
+
+// The register-list passes: ceil(k / 32) passes of up to 32 candidates per query over a prepared batch.
+static int tc_list_passes(homs_b200_ctx* ctx, const TcBatch& tb, const uint32_t* d_subset, const uint64_t* d_keys,
+                          const uint32_t* d_vals, Cand* d_out, uint32_t k, uint32_t k_stride, const uint8_t* d_only) {
+  for (uint32_t col0 = 0; col0 < k; col0 += kTcMaxK) {
+    const uint32_t kr = std::min<uint32_t>(kTcMaxK, k - col0);
+    const uint32_t prev_col = col0 ? col0 - 1 : kNone;
+    // a later pass needs the top-k drain (it is the one that knows about the lower bound), even for kr = 1
+    if (kr == 1 && col0 == 0) HB_TRY(tc_run_pass<1>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col));
+    else if (kr <= 4) HB_TRY(tc_run_pass<4>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col, d_only));
+    else if (kr <= 8) HB_TRY(tc_run_pass<8>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col, d_only));
+    else if (kr <= 16) HB_TRY(tc_run_pass<16>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col, d_only));
+    else HB_TRY(tc_run_pass<kTcMaxK>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col, d_only));
+  }
+  return HOMS_B200_OK;
+}
+
+// Collect mode (k >= 2): ONE pass whose drain only appends the candidates at or above each query's floor to
+// a per-query buffer, tc_select_kernel for the exact k best, then a fix-up run of the list passes restricted
+// to the queries whose buffer overflowed (none, unless thousands of rows tie at the top of a window: the
+// fix-up plan is then empty and its kernels return at once).  Everything stays stream-ordered.
+static int tc_collect_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const uint64_t* d_keys,
+                            const uint32_t* d_vals, uint64_t* d_keys_fix, uint64_t b0, uint64_t nb, Cand* d_out,
+                            uint32_t k, uint32_t k_stride, uint32_t ccap) {
+  using Mode = TcMode;
+  const Library& lib = ctx->lib;
+  const Queries& q = ctx->q;
+  TcBatch tb;
+  HB_TRY(tc_prepare_batch(ctx, d_subset, d_keys, d_vals, b0, nb, k, 0, false, &tb));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrTcCount], tb.q_rows * sizeof(uint32_t)));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrTcBuf], tb.q_rows * size_t(ccap) * sizeof(uint2)));
+  HB_TRY(ensure(ctx, ctx->scratch[kScrTcOverflow], tb.q_rows));
+  HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(Mode::SmemBytes)));
+  HB_CUDA(ctx, cudaMemsetAsync(ctx->scratch[kScrTcCount].p, 0, tb.q_rows * sizeof(uint32_t), ctx->stream));
+  HB_CUDA(ctx, cudaMemsetAsync(ctx->scratch[kScrTcBest].p, 0x80, tb.q_rows * k * sizeof(int), ctx->stream));
+  TcParams tp{};
+  tp.lib_x = lib.d_x.as<uint8_t>();
+  tp.q_x = ctx->scratch[kScrTcQx].as<uint8_t>();
+  tp.lib_rows = lib.x_rows;
+  tp.q_rows = tb.q_rows;
+  tp.n_kc = lib.n_kc;
+  tp.dim = lib.dim;
+  tp.items = tb.pp.items;
+  tp.n_items = &tb.pp.head->n_items;
+  tp.counter = &tb.pp.head->counter;
+  tp.keys = d_keys + b0;
+  tp.vals = d_vals + b0;
+  tp.subset = d_subset;
+  tp.q_mz = q.d_mz.as<double>();
+  tp.lib_mz = lib.d_mz_local.as<double>();
+  tp.lib_rank = lib.d_id_rank_local.as<uint32_t>();
+  tp.n = nb;
+  tp.partial = nullptr;
+  tp.gbest = ctx->scratch[kScrTcBest].as<int>();
+  tp.k = k;
+  tp.prev = nullptr;
+  tp.prev_stride = k_stride;
+  tp.prev_col = kNone;
+  tp.l2_hints = ctx->knobs.l2_hints;
+  tp.ccount = ctx->scratch[kScrTcCount].as<uint32_t>();
+  tp.cbuf = ctx->scratch[kScrTcBuf].as<uint2>();
+  tp.ccap = ccap;
+  {
+    KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
+    tc_search_kernel<0><<<ctx->sm_count, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
+  }
+  HB_LAUNCHED(ctx);
+  auto* d_over = ctx->scratch[kScrTcOverflow].as<uint8_t>();
+  tc_select_kernel<<<static_cast<unsigned>((nb + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, ctx->stream>>>(
+      nb, d_vals + b0, d_subset, tp.ccount, tp.cbuf, ccap, k, k_stride, lib.dim, q.d_mz.as<double>(),
+      lib.d_mz_local.as<double>(), lib.d_id_rank_local.as<uint32_t>(), d_out, d_over);
+  HB_LAUNCHED(ctx);
+  // fix-up: the exact list passes over the flagged queries only (their windows survive in d_keys_fix)
+  tc_mask_keys_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, ctx->stream>>>(nb, d_keys + b0, d_over,
+                                                                                      d_keys_fix + b0);
+  HB_LAUNCHED(ctx);
+  TcBatch fix;
+  HB_TRY(tc_prepare_batch(ctx, d_subset, d_keys_fix, d_vals, b0, nb, std::min<uint32_t>(k, kTcMaxK),
+                          std::min<uint32_t>(k, kTcMaxK), true, &fix));
+  return tc_list_passes(ctx, fix, d_subset, d_keys_fix, d_vals, d_out, k, k_stride, d_over);
+}
 
 int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
                      const uint32_t* d_vals, Cand* d_out, uint32_t k, uint32_t k_stride) {
   HB_REQUIRE(ctx, k >= 1 && k <= HOMS_B200_MAX_TOPK, HOMS_B200_ERR_ARGUMENT, "tensor engine: k out of range");
+  if (k >= 2 && ctx->knobs.topk_lists == 0) {
+    // buffer capacity per query: the floor admits about k x H(k) x ln(window / strip) candidates plus what the
+    // first, floor-less items append (measured counts: DESIGN.md K4a); batches sized for <= 1 GB of buffers
+    const uint32_t ccap = ctx->knobs.ccap ? ctx->knobs.ccap : std::min(8192u, std::max(1024u, 128u * k));
+    uint64_t batch = std::max<uint64_t>(kTcM, ((1ull << 30) / (uint64_t(ccap) * sizeof(uint2))) / kTcM * kTcM);
+    batch = std::min<uint64_t>(batch, kTcBatch);
+    HB_TRY(ensure(ctx, ctx->scratch[kScrTcKeysFix], n * sizeof(uint64_t)));
+    for (uint64_t b0 = 0; b0 < n; b0 += batch)
+      HB_TRY(tc_collect_batch(ctx, d_subset, d_keys, d_vals, ctx->scratch[kScrTcKeysFix].as<uint64_t>(), b0,
+                              std::min<uint64_t>(batch, n - b0), d_out, k, k_stride, ccap));
+    return HOMS_B200_OK;
+  }
   const uint32_t k_pass = std::min<uint32_t>(k, kTcMaxK);
   for (uint64_t b0 = 0; b0 < n; b0 += kTcBatch) {
     TcBatch tb;
-    HB_TRY(tc_prepare_batch(ctx, d_subset, d_keys, d_vals, b0, std::min<uint64_t>(kTcBatch, n - b0), k_pass, &tb));
-    for (uint32_t col0 = 0; col0 < k; col0 += kTcMaxK) {
-      const uint32_t kr = std::min<uint32_t>(kTcMaxK, k - col0);
-      const uint32_t prev_col = col0 ? col0 - 1 : kNone;
-      // a later pass needs the top-k drain (it is the one that knows about the lower bound), even for kr = 1
-      if (kr == 1 && col0 == 0) HB_TRY(tc_run_pass<1>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col));
-      else if (kr <= 4) HB_TRY(tc_run_pass<4>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col));
-      else if (kr <= 8) HB_TRY(tc_run_pass<8>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col));
-      else if (kr <= 16) HB_TRY(tc_run_pass<16>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col));
-      else HB_TRY(tc_run_pass<kTcMaxK>(ctx, tb, d_subset, d_keys, d_vals, d_out, k_stride, col0, kr, prev_col));
-    }
+    HB_TRY(tc_prepare_batch(ctx, d_subset, d_keys, d_vals, b0, std::min<uint64_t>(kTcBatch, n - b0), k_pass, k_pass,
+                            false, &tb));
+    HB_TRY(tc_list_passes(ctx, tb, d_subset, d_keys, d_vals, d_out, k, k_stride, nullptr));
     // the next batch reuses the plan / operand / partial blocks: stream order keeps that safe
   }
   return HOMS_B200_OK;

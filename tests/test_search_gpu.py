@@ -481,3 +481,48 @@ def test_engine_selection_errors(hb):
         c.set_engine("tensor")      # ABI 1's int8 code: now an alias of tensor_fp4
         got = c.search_batch(U.random_hvs(rng, 4, 256), [550.0] * 4, [2] * 4, hb.Tolerance("dalton", 500.0))
         assert c.last_engine() == "tensor_fp4" and got.has_hit.all()
+
+
+@pytest.mark.parametrize("mode", ["collect", "collect_overflow", "collect_tiny_stage", "lists"])
+def test_tensor_topk_modes_vs_port(hb, port, monkeypatch, mode):
+    """The tensor engine's top-k paths against the full-sort oracle on tie-heavy data: collect + select (default),
+    the same with a candidate buffer so small that (nearly) every query overflows and the fix-up list passes
+    produce the answer, a buffer that holds everything but far more survivors than the selection stages
+    (rows duplicated: hundreds of equal scores), and the register-list passes alone."""
+    if mode == "collect_overflow":
+        monkeypatch.setenv("HOMS_B200_TC_CCAP", "24")
+    elif mode == "collect_tiny_stage":
+        monkeypatch.setenv("HOMS_B200_TC_CCAP", "8192")
+    elif mode == "lists":
+        monkeypatch.setenv("HOMS_B200_TC_TOPK", "lists")
+    rng = np.random.default_rng(37)
+    dim, n, nq = 256, 24000, 400
+    n_base = n // 600 if mode == "collect_tiny_stage" else n // 4  # 600 copies of every row: > 256 ties at the top
+    base = U.random_hvs(rng, n_base, dim)
+    words = base[np.arange(n) % n_base]
+    mz = np.round(rng.uniform(500.0, 520.0, n), 1)
+    charge = rng.integers(2, 4, n).astype(np.uint8)
+    ids = [f"id{rng.integers(0, 50)}" for _ in range(n)]
+    qw = base[rng.integers(0, n_base, nq)] ^ (U.random_hvs(rng, nq, dim) & U.random_hvs(rng, nq, dim)
+                                               & U.random_hvs(rng, nq, dim))
+    qmz = np.round(rng.uniform(495.0, 525.0, nq), 1)
+    qch = rng.integers(1, 4, nq).astype(np.uint8)
+    oix = port.build_index(dim, words, mz, charge, None, ids)
+    with hb.Context(0) as c:
+        c.set_engine("tensor_fp4")
+        c.build_index(dim, words, mz, charge, ids=ids)
+        for tol, k in ((("da", 500.0), 2), (("da", 500.0), 16), (("da", 500.0), 33), (("da", 500.0), 64), (("da", 2.0), 5),
+                       (("ppm", 300.0), 64)):
+            m = c.search_batch(qw, qmz, qch, U.product_tol(tol), k=k)
+            score, ordinal = oix.search_topk(qw, qmz, qch, tol, k)
+            assert np.array_equal(m.ordinal, ordinal), (mode, tol, k)
+            assert np.array_equal(m.raw_score, score), (mode, tol, k)
+            assert c.last_engine() == "tensor_fp4"
+        # the cascade and top-1 do not go through this path; a sharded library (two members on one device) does
+        with hb.Context(devices=[0, 0]) as grp:
+            grp.set_engine("tensor_fp4")
+            grp.build_index(dim, words, mz, charge, ids=ids)
+            got = grp.search_batch(qw, qmz, qch, hb.Tolerance("dalton", 500.0), k=40)
+            score, ordinal = oix.search_topk(qw, qmz, qch, ("da", 500.0), 40)
+            assert np.array_equal(got.ordinal, ordinal) and np.array_equal(got.raw_score, score), mode
+    oix.close()
