@@ -101,8 +101,9 @@ struct GroupWorkers;  // group.cu: one issuing thread per non-leading member of 
 struct TcKnobs {
   uint32_t group_tiles = 0, items_per_sm = 0, max_strip = 0, item_cap = 0, group_mb = 0;
   uint32_t l2_hints = 2;  // see TcParams::l2_hints (default: library tiles evict_first)
-  uint32_t topk_lists = 0;  // 1: top-k through the register-list passes instead of collect + select
+  uint32_t topk_lists = 0;  // top-k path: 0 = by k (lists up to 8, collect + select above), 1 = lists, 2 = collect
   uint32_t ccap = 0;        // collect mode: candidate buffer entries per query (0: built-in)
+  uint32_t pair = 0;        // 1: the tensor search runs on CTA pairs (cta_group::2, search_tc.cu TcShape<true>)
 };
 
 }  // namespace hb
@@ -135,6 +136,7 @@ struct homs_b200_ctx {
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[3];
   hb::TcKnobs knobs;
+  int tc_pair_ctas = 0;  // grid of the CTA-pair search kernel: 2 x co-resident 2-CTA clusters (0: unavailable)
   // ---- multi-GPU group (homs_b200_ctx_create_multi, group.cu) --------------------------------
   // members[0] == this (the leader, on devices[0]); members[g >= 1] are owned single-device contexts
   // that are only ever driven through the leader (under the leader's mutex).  Empty: a plain context.
@@ -217,6 +219,7 @@ int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, c
 uint32_t tc_max_topk();
 bool tc_available(const homs_b200_ctx* ctx);
 int tc_peak_probe(homs_b200_ctx* ctx, double seconds, double* out_ops_per_s, double* out_ms);
+int tc_query_pair_ctas(homs_b200_ctx* ctx);
 
 // dense host rows (W words) -> padded device rows (S words), zero padded.  Async on ctx->stream.
 int upload_rows(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* h_src, uint64_t n, uint32_t W,

@@ -136,8 +136,11 @@ int ctx_create_single(int device, homs_b200_ctx** out) {
   ctx->knobs.item_cap = env_u32("HOMS_B200_TC_ITEM_CAP");
   ctx->knobs.group_mb = env_u32("HOMS_B200_TC_GROUP_MB");
   ctx->knobs.ccap = env_u32("HOMS_B200_TC_CCAP");
-  if (const char* e = getenv("HOMS_B200_TC_TOPK")) ctx->knobs.topk_lists = std::string(e) == "lists" ? 1u : 0u;
+  if (const char* e = getenv("HOMS_B200_TC_TOPK"))
+    ctx->knobs.topk_lists = std::string(e) == "lists" ? 1u : (std::string(e) == "collect" ? 2u : 0u);
   if (const char* e = getenv("HOMS_B200_TC_L2_HINTS")) ctx->knobs.l2_hints = static_cast<uint32_t>(atoi(e)) & 3u;
+  ctx->knobs.pair = env_u32("HOMS_B200_TC_PAIR");
+  ctx->tc_pair_ctas = ctx->knobs.pair ? tc_query_pair_ctas(ctx) : 0;
   *out = ctx;
   return HOMS_B200_OK;
 }

@@ -9,13 +9,12 @@
 // Sharding: shard g of G keeps rows [size*g/G, size*(g+1)/G) of EVERY bucket
 // (contiguous m/z slices); precursor m/z, id_rank and the rank->ordinal table are replicated so
 // that window bounds are computed in full-bucket coordinates on every rank.
-#include <cub/device/device_radix_sort.cuh>
-
 #include <algorithm>
 #include <cstring>
 #include <numeric>
 
 #include "common.cuh"
+#include "radix.cuh"
 
 namespace hb {
 
@@ -32,7 +31,7 @@ __global__ void gather_rows_kernel(uint64_t n_rows, const uint32_t* __restrict__
 }
 
 // ---- (charge, precursor m/z, id, ordinal) order on the device (search.cpp:37-46) ---------------
-// Three stable LSD radix sorts of the entry indices, least significant key first: id_rank (when ids
+// Three stable LSD radix sorts (radix.cu) of the entry indices, least significant key first: id_rank (when ids
 // are given; otherwise the initial order already is the ordinal order), the m/z bits mapped to an
 // order-preserving u64, the charge.  1.2 M entries sort in well under a millisecond; the host's
 // comparison sort took 0.2-0.3 s.
@@ -59,20 +58,9 @@ __global__ void index_iota_kernel(uint64_t n, uint32_t* __restrict__ idx) {
 
 static int device_sort_order(homs_b200_ctx* ctx, uint64_t n, const double* mz, const uint8_t* charge,
                              const uint32_t* id_rank, uint32_t* h_order) {
-  const int ni = static_cast<int>(n);
-  size_t t1 = 0, t2 = 0, t3 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, t1, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
-                                  static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), ni, 0, 32,
-                                  ctx->stream);
-  cub::DeviceRadixSort::SortPairs(nullptr, t2, static_cast<const uint64_t*>(nullptr), static_cast<uint64_t*>(nullptr),
-                                  static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), ni, 0, 64,
-                                  ctx->stream);
-  cub::DeviceRadixSort::SortPairs(nullptr, t3, static_cast<const uint8_t*>(nullptr), static_cast<uint8_t*>(nullptr),
-                                  static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), ni, 0, 8,
-                                  ctx->stream);
-  const size_t temp = (std::max({t1, t2, t3}) + 255) / 256 * 256;
+  const size_t temp = (radix_temp_bytes(n) + 255) / 256 * 256;
   const size_t a8 = (n * 8 + 255) / 256 * 256, a4 = (n * 4 + 255) / 256 * 256, a1 = (n + 255) / 256 * 256;
-  // layout: mz | key64 a | key64 b | idx a | idx b | rank a | rank b | charge | key8 a | key8 b | cub temp
+  // layout: mz | key64 a | key64 b | idx a | idx b | rank a | rank b | charge | key8 a | key8 b | sort scratch
   HB_TRY(ensure(ctx, ctx->scratch[kScrIndexSort], 3 * a8 + 4 * a4 + 3 * a1 + temp));
   auto* base = ctx->scratch[kScrIndexSort].as<unsigned char>();
   auto* d_mz = reinterpret_cast<double*>(base);
@@ -90,30 +78,27 @@ static int device_sort_order(homs_b200_ctx* ctx, uint64_t n, const double* mz, c
   const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
   HB_CUDA(ctx, cudaMemcpyAsync(d_mz, mz, n * 8, cudaMemcpyHostToDevice, st));
   HB_CUDA(ctx, cudaMemcpyAsync(d_charge, charge, n, cudaMemcpyHostToDevice, st));
-  index_iota_kernel<<<blocks, 256, 0, st>>>(n, idx_a);
-  HB_LAUNCHED(ctx);
   uint32_t* cur = idx_a;
   uint32_t* alt = idx_b;
-  if (id_rank) {
+  bool in_b = false;
+  if (id_rank) {  // ranks are positions in a sort of n entries: only the low bit_width(n - 1) bits differ
+    int bits = 1;
+    while (bits < 32 && (uint64_t(1) << bits) < n) ++bits;
     HB_CUDA(ctx, cudaMemcpyAsync(rank_a, id_rank, n * 4, cudaMemcpyHostToDevice, st));
-    size_t t = temp;
-    HB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(d_temp, t, rank_a, rank_b, cur, alt, ni, 0, 32, st));
-    std::swap(cur, alt);
+    HB_TRY(radix_sort_pairs<uint32_t>(ctx, rank_a, rank_b, cur, alt, n, 0, bits, d_temp, true, &in_b));
+    if (in_b) std::swap(cur, alt);
+  } else {
+    index_iota_kernel<<<blocks, 256, 0, st>>>(n, cur);
+    HB_LAUNCHED(ctx);
   }
   index_mz_keys_kernel<<<blocks, 256, 0, st>>>(n, d_mz, cur, k64a);
   HB_LAUNCHED(ctx);
-  {
-    size_t t = temp;
-    HB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(d_temp, t, k64a, k64b, cur, alt, ni, 0, 64, st));
-    std::swap(cur, alt);
-  }
+  HB_TRY(radix_sort_pairs<uint64_t>(ctx, k64a, k64b, cur, alt, n, 0, 64, d_temp, false, &in_b));
+  if (in_b) std::swap(cur, alt);
   index_charge_keys_kernel<<<blocks, 256, 0, st>>>(n, d_charge, cur, k8a);
   HB_LAUNCHED(ctx);
-  {
-    size_t t = temp;
-    HB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(d_temp, t, k8a, k8b, cur, alt, ni, 0, 8, st));
-    std::swap(cur, alt);
-  }
+  HB_TRY(radix_sort_pairs<uint8_t>(ctx, k8a, k8b, cur, alt, n, 0, 8, d_temp, false, &in_b));
+  if (in_b) std::swap(cur, alt);
   HB_CUDA(ctx, cudaMemcpyAsync(h_order, cur, n * 4, cudaMemcpyDeviceToHost, st));
   HB_CUDA(ctx, cudaStreamSynchronize(st));
   return HOMS_B200_OK;
@@ -125,7 +110,6 @@ int library_build(homs_b200_ctx* ctx, uint32_t dim, uint64_t n, const uint64_t* 
                   const uint32_t* row_of_entry) {
   HB_REQUIRE(ctx, n >= 1, HOMS_B200_ERR_INVARIANT, "build_index: library is empty");  // search.cpp:18
   HB_REQUIRE(ctx, dim >= 1, HOMS_B200_ERR_ARGUMENT, "build_index: dim must be positive");
-  // the device radix sorts of the entry order count their items in an int
   HB_REQUIRE(ctx, n <= 0x7FFFFFFFull, HOMS_B200_ERR_ARGUMENT, "build_index: more than 2^31-1 entries");
   HB_REQUIRE(ctx, mz && charge && (h_words || d_words_in), HOMS_B200_ERR_ARGUMENT,
              "build_index: null argument");

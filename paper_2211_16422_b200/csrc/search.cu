@@ -23,7 +23,6 @@
 //   5. reduce_kernel      per query lexicographic minimum over the work items of its block.
 // Top-k (k > 1) repeats 4-5 with the previous round's key as an exclusive lower bound, which
 // yields exactly the k smallest keys in order.
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -31,6 +30,7 @@
 #include <numeric>
 
 #include "common.cuh"
+#include "radix.cuh"
 #include "topk.cuh"
 
 namespace hb {
@@ -731,7 +731,6 @@ int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n,
   HB_REQUIRE(ctx, q.dim == lib.dim, HOMS_B200_ERR_INVARIANT,
              "search_one: query dimensionality does not match index");
   if (n == 0) return HOMS_B200_OK;
-  // the device radix sort of the query order counts its items in an int
   HB_REQUIRE(ctx, n <= 0x7FFFFFFFull, HOMS_B200_ERR_ARGUMENT, "search: more than 2^31-1 queries in one call");
   const uint32_t row_bytes = lib.S * 8;
   const int qb = pick_qb(row_bytes);
@@ -752,17 +751,20 @@ int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n,
   if (!sparse) {
     HB_TRY(ensure(ctx, ctx->scratch[kScrKeysAlt], n * 8));
     HB_TRY(ensure(ctx, ctx->scratch[kScrValsAlt], n * 4));
-    size_t cub_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, static_cast<const uint64_t*>(nullptr),
-                                    static_cast<uint64_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
-                                    static_cast<uint32_t*>(nullptr), static_cast<int>(n), 32, 64, ctx->stream);
-    HB_TRY(ensure(ctx, ctx->scratch[kScrCub], cub_bytes));
-    HB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(
-                     ctx->scratch[kScrCub].p, cub_bytes, ctx->scratch[kScrKeys].as<uint64_t>(),
-                     ctx->scratch[kScrKeysAlt].as<uint64_t>(), ctx->scratch[kScrVals].as<uint32_t>(),
-                     ctx->scratch[kScrValsAlt].as<uint32_t>(), static_cast<int>(n), 32, 64, ctx->stream));
-    keys = ctx->scratch[kScrKeysAlt].as<uint64_t>();
-    vals = ctx->scratch[kScrValsAlt].as<uint32_t>();
+    // key = window start << 32 | window end; a slot without a window carries ~0.  Starts are local rows
+    // (<= n_local), so only the low bits of the upper half can differ -- and an all-ones start still
+    // sorts last when truncated to them, as long as it is above every real start.
+    int bits = 8;
+    while (bits < 32 && ((uint64_t(1) << bits) - 1) <= lib.n_local) bits += 8;
+    HB_TRY(ensure(ctx, ctx->scratch[kScrCub], radix_temp_bytes(n)));
+    bool in_b = false;
+    HB_TRY(radix_sort_pairs<uint64_t>(ctx, ctx->scratch[kScrKeys].as<uint64_t>(), ctx->scratch[kScrKeysAlt].as<uint64_t>(),
+                                      ctx->scratch[kScrVals].as<uint32_t>(), ctx->scratch[kScrValsAlt].as<uint32_t>(), n,
+                                      32, 32 + bits, ctx->scratch[kScrCub].p, false, &in_b));
+    if (in_b) {
+      keys = ctx->scratch[kScrKeysAlt].as<uint64_t>();
+      vals = ctx->scratch[kScrValsAlt].as<uint32_t>();
+    }
   }
 
   if (use_direct) {

@@ -47,7 +47,7 @@ constexpr int kTcM = 128;      // queries per tile == TMEM lanes
 constexpr int kTcKB = 128;     // K bytes per pipeline stage == one swizzle atom
 constexpr uint32_t kTcABytes = kTcM * kTcKB;  // 16 KB
 constexpr int kTcThreads = 192;
-constexpr uint32_t kTcBarBytes = 256;
+constexpr uint32_t kTcBarBytes = 512;
 constexpr uint32_t kTcTmemCols = 512;  // two accumulators (+ the scale-factor columns in fp4 mode)
 
 // Operand encoding of the +-1 contraction: e2m1 nibbles (+1.0 = 0x2, -1.0 = 0xA), 256 dimensions per
@@ -67,6 +67,22 @@ struct TcMode {
   static constexpr uint32_t SmemBytes = Stages * StageBytes + 1024 + kTcBarBytes;
   static constexpr uint32_t SfCol = 480;           // scale-factor columns [480, 512)
 };
+// Shape of one CTA's share of a pipeline stage.  Single: the CTA holds the whole 128 x N tile pair (A 16 KB +
+// B 28 KB, 5 stages).  Pair (cta_group::2): two CTAs of one cluster (one TPC) work on a 256-query x N-row tile
+// with M = 256; each holds its own 128 query rows and HALF of the library tile (A 16 KB + B 14 KB, 7 stages):
+// a third fewer bytes from L2 per MMA and a third fewer shared-memory operand reads, which under the board's
+// power cap is clock.
+template <bool kPair>
+struct TcShape {
+  static constexpr int BRows = kPair ? TcMode::N / 2 : TcMode::N;
+  static constexpr uint32_t BBytes = BRows * kTcKB;
+  static constexpr uint32_t StageBytes = kTcABytes + BBytes;  // multiple of 1024
+  static constexpr int Stages = kPair ? 7 : TcMode::Stages;
+  static constexpr uint32_t SmemBytes = Stages * StageBytes + 1024 + kTcBarBytes;
+  static constexpr uint32_t TileQ = kPair ? 2 * kTcM : kTcM;  // sorted positions per planning tile
+};
+static_assert(TcShape<true>::StageBytes % 1024 == 0 && TcShape<false>::StageBytes % 1024 == 0, "stage alignment");
+static_assert(TcShape<true>::SmemBytes <= 227 * 1024 && TcShape<false>::SmemBytes <= 227 * 1024, "shared memory");
 constexpr uint32_t kTcGroupTiles = 12;  // query tiles per L2 group, at least
 constexpr int kTcMaxK = 32;             // top-k depth the drain keeps per query in ONE pass; larger k runs
                                         // ceil(k / 32) passes, each bounded below by the previous pass's last key
@@ -167,6 +183,64 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// ---- cluster (CTA pair) helpers ----
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cta address -> shared::cluster address of the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void st_remote_v4(uint32_t cluster_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+// wait that also acquires what a thread of the OTHER CTA of the cluster published before its arrive
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  if (mbar_try_wait_cluster(bar, parity)) return;
+  const long long t0 = clock64();
+  uint32_t spins = 0;
+  while (!mbar_try_wait_cluster(bar, parity)) {
+    if ((++spins & 0xFFFu) == 0 && clock64() - t0 > 8000000000ll) __trap();
+  }
+}
+// completion of every MMA issued so far by this thread, signalled to the barrier at this offset in BOTH CTAs
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+               "h"(static_cast<uint16_t>(3))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_fp4_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(
+          tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
@@ -232,6 +306,8 @@ __device__ __forceinline__ uint64_t tc_smem_desc(uint32_t smem_addr) {
 // N >> 3 in [17,23), scale format UE8M0 (bit 23), M >> 4 in [24,29), scale-factor ids 0, K = 64.
 constexpr uint32_t kTcIdescFp4 = (1u << 7) | (1u << 10) | (uint32_t(TcMode::N >> 3) << 17) | (1u << 23) |
                                  (uint32_t(kTcM >> 4) << 24);
+constexpr uint32_t kTcIdescFp4Pair = (1u << 7) | (1u << 10) | (uint32_t(TcMode::N >> 3) << 17) | (1u << 23) |
+                                     (uint32_t((2 * kTcM) >> 4) << 24);  // M = 256 over the CTA pair
 
 // ---- expansion: packed bits -> swizzled +-1 operand image -----------------------------------
 
@@ -281,15 +357,15 @@ __global__ void tc_expand_kernel(uint64_t out_rows, uint64_t n_rows, const uint3
   *reinterpret_cast<uint4*>(dst) = o;
 }
 
-// per query tile of the batch: union [lo, hi) of the windows of its 128 sorted positions
-__global__ void tc_tile_ranges_kernel(uint64_t n, const uint64_t* __restrict__ keys, uint32_t n_tiles,
+// per planning tile of the batch: union [lo, hi) of the windows of its tile_q (128, CTA pair: 256) sorted positions
+__global__ void tc_tile_ranges_kernel(uint64_t n, const uint64_t* __restrict__ keys, uint32_t n_tiles, uint32_t tile_q,
                                       uint2* __restrict__ ranges) {
   const uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   if (tile >= n_tiles) return;
   uint32_t lo = kNone, hi = 0;
-  for (uint32_t j = lane; j < kTcM; j += 32) {
-    const uint64_t p = uint64_t(tile) * kTcM + j;
+  for (uint32_t j = lane; j < tile_q; j += 32) {
+    const uint64_t p = uint64_t(tile) * tile_q + j;
     if (p >= n) break;
     const uint64_t key = keys[p];
     if (key == ~0ull) continue;
@@ -491,69 +567,93 @@ struct TcAcc {
   static __device__ __forceinline__ T from_int(int v) { return static_cast<float>(v); }
 };
 
-// KM = 1: plain top-1 drain; KM > 1: the drain keeps the best KM >= p.k candidates per query
-template <int KM>
+// KM = 1: plain top-1 drain; KM > 1: the drain keeps the best KM >= p.k candidates per query; KM = 0: collect.
+// kPair: two CTAs of a cluster share every work item (see TcShape): the leader (cluster rank 0) draws the
+// items and issues the M = 256 MMAs for both, each CTA streams its own operand share and drains its own
+// 128 queries.  What crosses the pair: the item FIFO (leader -> peer, DSMEM store + remote arrive), "my stage is
+// full" (peer -> leader, relayed by the peer's otherwise idle warp 1), "accumulator drained" and "item slot
+// free" (peer -> leader, remote arrives); "stage free" and "accumulator complete" reach both CTAs through the
+// multicast form of tcgen05.commit.
+template <int KM, bool kPair>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams p) {
   constexpr bool kTopK = KM > 1;      // register lists of depth KM
   constexpr bool kCollect = KM == 0;  // append candidates above the floor, select exactly afterwards
   constexpr int kList = KM > 0 ? KM : 1;
   using Mode = TcMode;
+  using Shape = TcShape<kPair>;
   using Acc = TcAcc;
   using AccT = typename Acc::T;
   constexpr int kN = Mode::N;
-  constexpr int kStages = Mode::Stages;
+  constexpr int kStages = Shape::Stages;
   extern __shared__ unsigned char tc_smem_raw[];
   const uint32_t raw = smem_u32(tc_smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-byte alignment
   unsigned char* gen_base = tc_smem_raw + (base - raw);
-  const uint32_t bar0 = base + kStages * Mode::StageBytes;
-  // barriers: full[4], empty[4], tfull[2], tempty[2]; then the TMEM base address
+  const uint32_t bar0 = base + kStages * Shape::StageBytes;
+  // barrier block: full[S], empty[S], tfull[2], tempty[2], TMEM base address, ifull[Q], iempty[Q], pfull[S], items[Q]
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
   auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kStages + a); };
   auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kStages + 2 + a); };
   volatile uint32_t* tmem_slot =
-      reinterpret_cast<volatile uint32_t*>(gen_base + kStages * Mode::StageBytes + 8 * (2 * kStages + 4));
+      reinterpret_cast<volatile uint32_t*>(gen_base + kStages * Shape::StageBytes + 8 * (2 * kStages + 4));
   // Work items are handed out dynamically, in plan order, through one device-wide counter: however
   // long a CTA's drain takes, the CTAs running at any moment work on ~gridDim consecutive items, which
   // is what keeps their operand tiles shared in L2 (with a static round-robin a delayed CTA stays
   // behind for good and drifts out of its neighbours' tiles: top-5 read 108 GB from DRAM per launch
-  // instead of 29).  The producer draws the ids and passes them to the MMA thread and the drain warps
+  // instead of 29).  The producer draws the ids and passes the items to the MMA thread and the drain warps
   // through a small FIFO in shared memory (ifull / iempty barriers per slot).
   constexpr int kItemQ = 4;
-  const uint32_t ibar_off = 8u * (2 * kStages + 4) + 8u;
+  constexpr uint32_t ibar_off = 8u * (2 * kStages + 4) + 8u;
   auto ifull_bar = [&](int s) { return bar0 + ibar_off + 8u * s; };
   auto iempty_bar = [&](int s) { return bar0 + ibar_off + 8u * (kItemQ + s); };
-  volatile uint32_t* s_item = reinterpret_cast<volatile uint32_t*>(gen_base + kStages * Mode::StageBytes + ibar_off +
-                                                                   8 * 2 * kItemQ);
-  static_assert(8 * (2 * Mode::Stages + 4) + 8 + 8 * 2 * kItemQ + 4 * kItemQ <= kTcBarBytes, "barrier block too small");
+  auto pfull_bar = [&](int s) { return bar0 + ibar_off + 8u * (2 * kItemQ + s); };  // pair: the peer's stage s is full
+  constexpr uint32_t item_off = (ibar_off + 8u * (2 * kItemQ + kStages) + 15u) & ~15u;
+  static_assert(item_off + 16 * kItemQ <= kTcBarBytes, "barrier block too small");
+  // one FIFO entry: {item id or kNone, tile, row_begin, row_end}
+  volatile uint32_t* s_item = reinterpret_cast<volatile uint32_t*>(gen_base + kStages * Shape::StageBytes + item_off);
+  const uint32_t s_item_addr = bar0 + item_off;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;  // 0: leader (draws items, issues the MMAs)
+  // consumers of an item slot: the MMA thread + 4 drain warps here; in a pair also the peer's producer, relay
+  // and 4 drain warps (they arrive on the LEADER's barrier)
+  constexpr uint32_t kItemConsumers = kPair ? 11 : 5;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
+      mbar_init(pfull_bar(s), 1);
     }
     for (int s = 0; s < kItemQ; ++s) {
       mbar_init(ifull_bar(s), 1);
-      mbar_init(iempty_bar(s), 5);  // the MMA thread and one lane per drain warp
+      mbar_init(iempty_bar(s), kItemConsumers);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 4);  // one arrival per drain warp
+      mbar_init(tempty_bar(a), kPair ? 8 : 4);  // one arrival per drain warp (of both CTAs)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(const_cast<uint32_t*>(tmem_slot))),
-                 "r"(kTcTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(const_cast<uint32_t*>(tmem_slot))),
+                   "r"(kTcTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(const_cast<uint32_t*>(tmem_slot))),
+                   "r"(kTcTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // the peer's barriers are initialised before anything arrives on them
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // every block scale is 1.0 = UE8M0 0x7F: fill all 32 scale-factor columns of all 128 lanes once,
@@ -561,10 +661,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   if (warp >= 2) tc_st32_fill(tmem_base + (uint32_t((warp & 3) * 32) << 16) + Mode::SfCol, 0x7F7F7F7Fu);
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // both CTAs' scale factors are in place before the first MMA
   tc_fence_after();
 
   const uint32_t n_kc = p.n_kc;
   const uint32_t n_items = __ldg(p.n_items);
+  // an item slot is released to the leader's producer
+  auto release_item_slot = [&](int s) {
+    if (kPair && rank != 0) mbar_arrive_remote(mapa_u32(iempty_bar(s), 0));
+    else mbar_arrive(iempty_bar(s));
+  };
+  auto wait_item_slot = [&](int s, uint32_t parity) {
+    if constexpr (kPair) mbar_wait_cluster(ifull_bar(s), parity);
+    else mbar_wait(ifull_bar(s), parity);
+  };
 
   if (warp == 0) {
     // ===== producer: two bulk copies per stage =====
@@ -576,32 +686,57 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
       // on configs 2, 3 and D = 16384); evict_last on A on top of that measured no gain (bit 0, off).
       const bool hint_a = p.l2_hints & 1u, hint_b = p.l2_hints & 2u;
       const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
-      uint32_t next = atomicAdd(p.counter, 1u);
+      uint32_t next = rank == 0 ? atomicAdd(p.counter, 1u) : 0u;
       for (;;) {
-        const uint32_t item = next;
-        mbar_wait(iempty_bar(qslot), qphase ^ 1u);
-        s_item[qslot] = item < n_items ? item : kNone;
-        mbar_arrive(ifull_bar(qslot));
+        TcItem it{0, 0, 0, 0};
+        uint32_t item;
+        if (rank == 0) {
+          item = next;
+          mbar_wait(iempty_bar(qslot), qphase ^ 1u);
+          if (item < n_items) it = p.items[item];
+          const uint32_t id = item < n_items ? item : kNone;
+          volatile uint32_t* e = s_item + 4 * qslot;
+          e[0] = id;
+          e[1] = it.tile;
+          e[2] = it.row_begin;
+          e[3] = it.row_end;
+          mbar_arrive(ifull_bar(qslot));
+          if constexpr (kPair) {
+            st_remote_v4(mapa_u32(s_item_addr + 16u * qslot, 1), id, it.tile, it.row_begin, it.row_end);
+            mbar_arrive_remote(mapa_u32(ifull_bar(qslot), 1));
+          }
+        } else {  // the pair's second CTA follows the leader's FIFO
+          wait_item_slot(qslot, qphase);
+          volatile uint32_t* e = s_item + 4 * qslot;
+          item = e[0];
+          it.tile = e[1];
+          it.row_begin = e[2];
+          it.row_end = e[3];
+          release_item_slot(qslot);
+          if (item == kNone) item = n_items;
+        }
         if (++qslot == kItemQ) {
           qslot = 0;
           qphase ^= 1u;
         }
         if (item >= n_items) break;
-        const TcItem it = p.items[item];
-        next = atomicAdd(p.counter, 1u);  // the next id arrives while this item streams
+        if (rank == 0) next = atomicAdd(p.counter, 1u);  // the next id arrives while this item streams
         const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
-        const uint8_t* a_src = p.q_x + uint64_t(it.tile) * kTcM * kTcKB;
+        // own query rows: tile it.tile (single) or half `rank` of the 256-query tile it.tile (pair)
+        const uint8_t* a_src = p.q_x + (uint64_t(it.tile) * Shape::TileQ + uint64_t(rank) * kTcM) * kTcKB;
         for (uint32_t nt = 0; nt < n_nt; ++nt) {
-          const uint8_t* b_src = p.lib_x + (uint64_t(it.row_begin) + uint64_t(nt) * kN) * kTcKB;
+          // own library rows: the whole N-row tile (single) or half `rank` of it (pair)
+          const uint8_t* b_src =
+              p.lib_x + (uint64_t(it.row_begin) + uint64_t(nt) * kN + uint64_t(rank) * Shape::BRows) * kTcKB;
           for (uint32_t kc = 0; kc < n_kc; ++kc) {
             mbar_wait(empty_bar(stage), phase ^ 1u);
-            const uint32_t sa = base + stage * Mode::StageBytes;
-            mbar_expect_tx(full_bar(stage), Mode::StageBytes);
+            const uint32_t sa = base + stage * Shape::StageBytes;
+            mbar_expect_tx(full_bar(stage), Shape::StageBytes);
             if (hint_a) bulk_g2s_hint(sa, a_src + uint64_t(kc) * p.q_rows * kTcKB, kTcABytes, full_bar(stage), pol_a);
             else bulk_g2s(sa, a_src + uint64_t(kc) * p.q_rows * kTcKB, kTcABytes, full_bar(stage));
             if (hint_b)
-              bulk_g2s_hint(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, Mode::BBytes, full_bar(stage), pol_b);
-            else bulk_g2s(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, Mode::BBytes, full_bar(stage));
+              bulk_g2s_hint(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, Shape::BBytes, full_bar(stage), pol_b);
+            else bulk_g2s(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, Shape::BBytes, full_bar(stage));
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1u;
@@ -611,21 +746,32 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer: one thread =====
+    // ===== MMA issuer: one thread (of the leader); in the peer the same thread relays "stage full" =====
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;  // aphase: one parity bit per accumulator
       uint32_t qslot = 0, qphase = 0;
       for (;;) {
-        mbar_wait(ifull_bar(qslot), qphase);
-        const uint32_t item = s_item[qslot];
-        mbar_arrive(iempty_bar(qslot));
+        wait_item_slot(qslot, qphase);
+        volatile uint32_t* e = s_item + 4 * qslot;
+        const uint32_t item = e[0], row_begin = e[2], row_end = e[3];
+        release_item_slot(qslot);
         if (++qslot == kItemQ) {
           qslot = 0;
           qphase ^= 1u;
         }
         if (item == kNone) break;
-        const TcItem it = p.items[item];
-        const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
+        const uint32_t n_nt = (row_end - row_begin + kN - 1) / kN;
+        if (kPair && rank != 0) {  // relay: my share of stage s has landed -> the leader's pfull[s]
+          for (uint32_t i = 0; i < n_nt * n_kc; ++i) {
+            mbar_wait(full_bar(stage), phase);
+            mbar_arrive_remote(mapa_u32(pfull_bar(stage), 0));
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          continue;
+        }
         for (uint32_t nt = 0; nt < n_nt; ++nt) {
           mbar_wait(tempty_bar(acc), ((aphase >> acc) & 1u) ^ 1u);  // drain warps released this accumulator
           aphase ^= 1u << acc;
@@ -633,22 +779,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           const uint32_t tmem_d = tmem_base + acc * kN;
           for (uint32_t kc = 0; kc < n_kc; ++kc) {
             mbar_wait(full_bar(stage), phase);
+            if constexpr (kPair) mbar_wait_cluster(pfull_bar(stage), phase);
             tc_fence_after();
-            const uint32_t sa = base + stage * Mode::StageBytes;
+            const uint32_t sa = base + stage * Shape::StageBytes;
             const uint64_t adesc = tc_smem_desc(sa);
             const uint64_t bdesc = tc_smem_desc(sa + kTcABytes);
 #pragma unroll
             for (uint32_t k = 0; k < kTcKB / 32; ++k) {  // +32 bytes along K inside the swizzle atom
-              tc_mma_fp4(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescFp4, tmem_base + Mode::SfCol,
-                         tmem_base + Mode::SfCol + 16, (kc | k) != 0u);
+              if constexpr (kPair)
+                tc_mma_fp4_pair(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescFp4Pair, tmem_base + Mode::SfCol,
+                                tmem_base + Mode::SfCol + 16, (kc | k) != 0u);
+              else
+                tc_mma_fp4(tmem_d, adesc + 2 * k, bdesc + 2 * k, kTcIdescFp4, tmem_base + Mode::SfCol,
+                           tmem_base + Mode::SfCol + 16, (kc | k) != 0u);
             }
-            tc_commit(empty_bar(stage));  // stage reusable once these MMAs have read it
+            // stage reusable (in both CTAs) once these MMAs have read it
+            if constexpr (kPair) tc_commit_pair(empty_bar(stage));
+            else tc_commit(empty_bar(stage));
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1u;
             }
           }
-          tc_commit(tfull_bar(acc));  // accumulator complete
+          // accumulator complete (in both CTAs)
+          if constexpr (kPair) tc_commit_pair(tfull_bar(acc));
+          else tc_commit(tfull_bar(acc));
           acc ^= 1u;
         }
       }
@@ -666,18 +821,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     constexpr int kChunks = (kN + 31) / 32;
     uint32_t acc = 0, tphase = 0, qslot = 0, qphase = 0;
     for (;;) {
-      mbar_wait(ifull_bar(qslot), qphase);
-      const uint32_t item = s_item[qslot];
+      wait_item_slot(qslot, qphase);
+      TcItem it;
+      const uint32_t item = s_item[4 * qslot];
+      it.tile = s_item[4 * qslot + 1];
+      it.row_begin = s_item[4 * qslot + 2];
+      it.row_end = s_item[4 * qslot + 3];
       __syncwarp();
-      if (lane == 0) mbar_arrive(iempty_bar(qslot));
+      if (lane == 0) release_item_slot(qslot);
       if (++qslot == kItemQ) {
         qslot = 0;
         qphase ^= 1u;
       }
       if (item == kNone) break;
-      const TcItem it = p.items[item];
       const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
-      const uint64_t pos = uint64_t(it.tile) * kTcM + qrow;
+      const uint64_t pos = uint64_t(it.tile) * Shape::TileQ + uint64_t(rank) * kTcM + qrow;
       uint32_t lf = 0, ll = 0;
       double qmz = 0.0;
       int floor_i = INT_MIN;
@@ -866,14 +1024,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty_bar(acc));
+        if (lane == 0) {  // the accumulator is released to the (leader's) MMA thread
+          if (kPair && rank != 0) mbar_arrive_remote(mapa_u32(tempty_bar(acc), 0));
+          else mbar_arrive(tempty_bar(acc));
+        }
         acc ^= 1u;
       }
 
       if constexpr (kCollect) continue;  // everything this item found is already in the query's buffer
       if constexpr (kTopK) {
         const uint32_t k = p.k;
-        Cand* dst = p.partial + (uint64_t(item) * kTcM + qrow) * k;
+        Cand* dst = p.partial + (uint64_t(item) * Shape::TileQ + rank * kTcM + qrow) * k;
 #pragma unroll
         for (int j = 0; j < KM; ++j) {
           if (uint32_t(j) < k) {
@@ -908,16 +1069,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         out.rk = best_rk;
         out.ad = best_ad;
       }
-      p.partial[uint64_t(item) * kTcM + qrow] = out;
+      p.partial[uint64_t(item) * Shape::TileQ + rank * kTcM + qrow] = out;
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // no remote arrive or MMA of the pair is still under way
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcTmemCols)
-                 : "memory");
+    if constexpr (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcTmemCols) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcTmemCols) : "memory");
   }
 }
 
@@ -927,12 +1091,14 @@ constexpr int kTcReduceSlices = 8;
 __global__ void __launch_bounds__(kTcM * kTcReduceSlices)
 tc_reduce_kernel(uint64_t n, const uint32_t* __restrict__ vals, const uint32_t* __restrict__ tile_item_start,
                  const uint32_t* __restrict__ tile_items, const Cand* __restrict__ partial,
-                 Cand* __restrict__ out, uint32_t k_stride) {
+                 Cand* __restrict__ out, uint32_t k_stride, uint32_t tile_shift) {
   __shared__ Cand s_best[kTcReduceSlices][kTcM];
   const uint32_t t = blockIdx.x, r = threadIdx.x, slice = threadIdx.y;
+  // planning tile (128 << tile_shift positions) and this block's 128-position part of it
+  const uint32_t pt = t >> tile_shift, part = (t & ((1u << tile_shift) - 1u)) * kTcM;
   Cand best{kNone, kNone, ~0ull};
-  for (uint32_t i = tile_item_start[t] + slice; i < tile_item_start[t + 1]; i += kTcReduceSlices) {
-    const Cand c = partial[uint64_t(tile_items[i]) * kTcM + r];
+  for (uint32_t i = tile_item_start[pt] + slice; i < tile_item_start[pt + 1]; i += kTcReduceSlices) {
+    const Cand c = partial[(uint64_t(tile_items[i]) << tile_shift) * kTcM + part + r];
     if (c.d != best.d ? c.d < best.d : key_less(c.ad, c.rk, best.ad, best.rk)) best = c;
   }
   s_best[slice][r] = best;
@@ -951,15 +1117,15 @@ __global__ void tc_reduce_topk_kernel(uint64_t n, const uint32_t* __restrict__ v
                                       const uint32_t* __restrict__ tile_item_start,
                                       const uint32_t* __restrict__ tile_items, const Cand* __restrict__ partial,
                                       Cand* __restrict__ out, uint32_t k, uint32_t k_stride,
-                                      const uint8_t* __restrict__ only) {
+                                      const uint8_t* __restrict__ only, uint32_t tile_q) {
   const uint64_t pos = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (pos >= n) return;
   if (only != nullptr && !only[pos]) return;  // fix-up pass: this query already has its exact answer
-  const uint32_t t = static_cast<uint32_t>(pos / kTcM), r = static_cast<uint32_t>(pos % kTcM);
+  const uint32_t t = static_cast<uint32_t>(pos / tile_q), r = static_cast<uint32_t>(pos % tile_q);
   Cand best[kTcMaxK];  // k <= kTcMaxK per pass
   uint32_t count = 0;
   for (uint32_t i = tile_item_start[t]; i < tile_item_start[t + 1]; ++i) {
-    const Cand* src = partial + (uint64_t(tile_items[i]) * kTcM + r) * k;
+    const Cand* src = partial + (uint64_t(tile_items[i]) * tile_q + r) * k;
     for (uint32_t j = 0; j < k; ++j) {
       const Cand c = src[j];
       if (c.d == kNone) break;  // lists are sorted, empty entries last
@@ -1130,9 +1296,13 @@ int tc_expand_library(homs_b200_ctx* ctx) {
 // every pass of a deep top-k over the batch.
 struct TcBatch {
   uint64_t b0 = 0, nb = 0, q_rows = 0;
-  uint32_t n_tiles = 0;
+  uint32_t n_tiles = 0;  // planning tiles: 128 sorted positions each, 256 when CTA pairs run the search
+  bool pair = false;
   TcPlanPtrs pp{};
 };
+
+// CTA pairs (TcShape<true>) when the device can co-schedule one 2-CTA cluster on (nearly) every SM pair
+static bool tc_use_pair(const homs_b200_ctx* ctx) { return ctx->knobs.pair != 0 && ctx->tc_pair_ctas >= 2; }
 
 // k_partial: list depth the per-item partial block is sized for (0: none, collect mode); reuse_qx: the
 // expanded queries of this very batch are already in place (fix-up pass)
@@ -1143,13 +1313,15 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   const Library& lib = ctx->lib;
   const Queries& q = ctx->q;
   const TcKnobs& knobs = ctx->knobs;  // development knobs, read from the environment at ctx_create
-  const uint32_t n_tiles = static_cast<uint32_t>((nb + kTcM - 1) / kTcM);
-  const uint64_t q_rows = uint64_t(n_tiles) * kTcM;
+  const bool pair = tc_use_pair(ctx);
+  const uint32_t tile_q = pair ? TcShape<true>::TileQ : TcShape<false>::TileQ;
+  const uint32_t n_tiles = static_cast<uint32_t>((nb + tile_q - 1) / tile_q);
+  const uint64_t q_rows = uint64_t(n_tiles) * tile_q;
 
   // 1. union window of every query tile
   HB_TRY(ensure(ctx, ctx->scratch[kScrTcTiles], size_t(n_tiles) * sizeof(uint2)));
   auto* d_ranges = ctx->scratch[kScrTcTiles].as<uint2>();
-  tc_tile_ranges_kernel<<<(n_tiles * 32 + 255) / 256, 256, 0, ctx->stream>>>(nb, d_keys + b0, n_tiles, d_ranges);
+  tc_tile_ranges_kernel<<<(n_tiles * 32 + 255) / 256, 256, 0, ctx->stream>>>(nb, d_keys + b0, n_tiles, tile_q, d_ranges);
   HB_LAUNCHED(ctx);
 
   // 2. plan on the device (see the planner above).  Capacity of the item arrays from what the
@@ -1163,7 +1335,7 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   // DRAM 8.4 -> 5.9 GB per launch = 1.19x the compulsory bytes, 22.4 -> 21.6 ms; 64 MB groups on longer
   // query sets -- several groups, each sweeping the whole library -- measured 8 % slower than 32 MB:
   // profiles/r02_sweep_l2_hints_group.log)
-  const uint64_t a_tile = uint64_t(kTcM) * lib.n_kc * kTcKB;
+  const uint64_t a_tile = uint64_t(tile_q) * lib.n_kc * kTcKB;
   uint64_t a_budget = uint64_t(n_tiles) * a_tile <= (64ull << 20) ? 64ull << 20 : 32ull << 20;
   if (knobs.group_mb) a_budget = uint64_t(knobs.group_mb) << 20;
   pc.group_tiles = static_cast<uint32_t>(std::max<uint64_t>(kTcGroupTiles, a_budget / a_tile));
@@ -1179,12 +1351,12 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   if (knobs.items_per_sm) items_per_sm = knobs.items_per_sm;
   if (knobs.max_strip) pc.max_strip = knobs.max_strip;
   pc.tiles_total = static_cast<uint32_t>((lib.n_local + kN - 1) / kN + 1);
-  pc.target_items = uint64_t(ctx->sm_count) * items_per_sm;
+  pc.target_items = uint64_t(pair ? ctx->tc_pair_ctas / 2 : ctx->sm_count) * items_per_sm;  // per CTA (pair)
   const uint64_t slack = 2ull * n_tiles + 16;
   const uint64_t by_shape =
       std::max<uint64_t>(pc.target_items, (uint64_t(n_tiles) * pc.tiles_total + pc.max_strip - 1) / pc.max_strip) + slack;
   const uint64_t by_memory = std::max<uint64_t>(
-      (4ull << 30) / (size_t(kTcM) * std::max(1u, k_partial) * sizeof(Cand)), slack + 4ull * ctx->sm_count);
+      (4ull << 30) / (size_t(tile_q) * std::max(1u, k_partial) * sizeof(Cand)), slack + 4ull * ctx->sm_count);
   pc.item_cap = static_cast<uint32_t>(std::min<uint64_t>(std::min(by_shape, by_memory), 0x7fffffffull));
   if (knobs.item_cap)  // development / test knob: force the capacity-bound plan
     pc.item_cap = static_cast<uint32_t>(std::min<uint64_t>(pc.item_cap, std::max<uint64_t>(slack + 1, knobs.item_cap)));
@@ -1203,14 +1375,72 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
     HB_TRY(expand_launch(ctx, q_rows, nb, d_vals, d_subset, b0, q.d_words.as<uint64_t>(), stride_for(q.dim), q.dim,
                          lib.n_kc, ctx->scratch[kScrTcQx].as<uint8_t>()));
   }
-  if (k_partial) HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], size_t(pc.item_cap) * kTcM * k_partial * sizeof(Cand)));
+  if (k_partial) HB_TRY(ensure(ctx, ctx->scratch[kScrTcPartial], size_t(pc.item_cap) * tile_q * k_partial * sizeof(Cand)));
   HB_TRY(ensure(ctx, ctx->scratch[kScrTcBest], q_rows * k_pass * sizeof(int)));
   out->b0 = b0;
   out->nb = nb;
   out->q_rows = q_rows;
   out->n_tiles = n_tiles;
+  out->pair = pair;
   out->pp = tc_plan_layout(d_plan, n_tiles, pc.item_cap);
   return HOMS_B200_OK;
+}
+
+// the search kernel over a prepared batch: one CTA per SM, or one 2-CTA cluster per SM pair
+template <int KM>
+static int tc_launch_search(homs_b200_ctx* ctx, const TcBatch& tb, const TcParams& tp) {
+  KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
+  if (tb.pair) {
+    using Shape = TcShape<true>;
+    HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<KM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Shape::SmemBytes)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctx->tc_pair_ctas);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = Shape::SmemBytes;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    HB_CUDA(ctx, cudaLaunchKernelEx(&cfg, tc_search_kernel<KM, true>, tp));
+  } else {
+    using Shape = TcShape<false>;
+    HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<KM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Shape::SmemBytes)));
+    tc_search_kernel<KM, false><<<ctx->sm_count, kTcThreads, Shape::SmemBytes, ctx->stream>>>(tp);
+  }
+  return HOMS_B200_OK;
+}
+
+// co-resident 2-CTA clusters of the search kernel x 2 (0: pairs cannot be scheduled); asked once per context
+int tc_query_pair_ctas(homs_b200_ctx* ctx) {
+  using Shape = TcShape<true>;
+  if (cudaFuncSetAttribute(tc_search_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(Shape::SmemBytes)) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctx->sm_count / 2 * 2);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = Shape::SmemBytes;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, tc_search_kernel<1, true>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return std::min(clusters, ctx->sm_count / 2) * 2;
 }
 
 // One pass over a prepared batch: the k best per query (k <= KM) -- after the key in column prev_col of
@@ -1223,8 +1453,6 @@ static int tc_run_pass(homs_b200_ctx* ctx, const TcBatch& tb, const uint32_t* d_
   const Library& lib = ctx->lib;
   const Queries& q = ctx->q;
   const TcPlanPtrs& pp = tb.pp;
-  HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(Mode::SmemBytes)));
   if (prev_col != kNone)  // a later pass over the same plan: hand the work items out again
     HB_CUDA(ctx, cudaMemsetAsync(&pp.head->counter, 0, sizeof(uint32_t), ctx->stream));
   // every byte 0x80: a dot no candidate can be below
@@ -1259,19 +1487,16 @@ static int tc_run_pass(homs_b200_ctx* ctx, const TcBatch& tb, const uint32_t* d_
   tp.cbuf = nullptr;
   tp.ccap = 0;
   tp.pad3 = 0;
-  {
-    KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
-    tc_search_kernel<KM><<<ctx->sm_count, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
-  }
+  HB_TRY(tc_launch_search<KM>(ctx, tb, tp));
   HB_LAUNCHED(ctx);
   if constexpr (KM > 1)
     tc_reduce_topk_kernel<<<static_cast<unsigned>((tb.nb + 127) / 128), 128, 0, ctx->stream>>>(
         tb.nb, d_vals + tb.b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out_full + col0,
-        k, k_stride, d_only);
+        k, k_stride, d_only, tb.pair ? TcShape<true>::TileQ : TcShape<false>::TileQ);
   else
-    tc_reduce_kernel<<<tb.n_tiles, dim3(kTcM, kTcReduceSlices), 0, ctx->stream>>>(
+    tc_reduce_kernel<<<static_cast<unsigned>((tb.nb + kTcM - 1) / kTcM), dim3(kTcM, kTcReduceSlices), 0, ctx->stream>>>(
         tb.nb, d_vals + tb.b0, pp.tile_start, pp.tile_items, ctx->scratch[kScrTcPartial].as<Cand>(), d_out_full + col0,
-        k_stride);
+        k_stride, tb.pair ? 1u : 0u);
   HB_LAUNCHED(ctx);
   return HOMS_B200_OK;
 }
@@ -1309,8 +1534,6 @@ static int tc_collect_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   HB_TRY(ensure(ctx, ctx->scratch[kScrTcCount], tb.q_rows * sizeof(uint32_t)));
   HB_TRY(ensure(ctx, ctx->scratch[kScrTcBuf], tb.q_rows * size_t(ccap) * sizeof(uint2)));
   HB_TRY(ensure(ctx, ctx->scratch[kScrTcOverflow], tb.q_rows));
-  HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(Mode::SmemBytes)));
   HB_CUDA(ctx, cudaMemsetAsync(ctx->scratch[kScrTcCount].p, 0, tb.q_rows * sizeof(uint32_t), ctx->stream));
   HB_CUDA(ctx, cudaMemsetAsync(ctx->scratch[kScrTcBest].p, 0x80, tb.q_rows * k * sizeof(int), ctx->stream));
   TcParams tp{};
@@ -1340,10 +1563,7 @@ static int tc_collect_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   tp.ccount = ctx->scratch[kScrTcCount].as<uint32_t>();
   tp.cbuf = ctx->scratch[kScrTcBuf].as<uint2>();
   tp.ccap = ccap;
-  {
-    KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
-    tc_search_kernel<0><<<ctx->sm_count, kTcThreads, Mode::SmemBytes, ctx->stream>>>(tp);
-  }
+  HB_TRY(tc_launch_search<0>(ctx, tb, tp));
   HB_LAUNCHED(ctx);
   auto* d_over = ctx->scratch[kScrTcOverflow].as<uint8_t>();
   tc_select_kernel<<<static_cast<unsigned>((nb + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, ctx->stream>>>(
@@ -1363,7 +1583,11 @@ static int tc_collect_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
 int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
                      const uint32_t* d_vals, Cand* d_out, uint32_t k, uint32_t k_stride) {
   HB_REQUIRE(ctx, k >= 1 && k <= HOMS_B200_MAX_TOPK, HOMS_B200_ERR_ARGUMENT, "tensor engine: k out of range");
-  if (k >= 2 && ctx->knobs.topk_lists == 0) {
+  // Shallow lists are cheapest in registers (k = 5: 24.6 ms against 28.5 ms collected, config 2); from k = 9 on
+  // the register insert path costs more than appending and selecting afterwards (k = 16: 28.7 -> 24.1 ms,
+  // k = 32: 56.5 -> 25.7 ms, k = 64: 113 -> 29.1 ms; profiles/r02_ab_topk_collect_vs_lists.log).
+  const bool collect = k >= 2 && (ctx->knobs.topk_lists == 2 || (ctx->knobs.topk_lists == 0 && k > 8));
+  if (collect) {
     // buffer capacity per query: the floor admits about k x H(k) x ln(window / strip) candidates plus what the
     // first, floor-less items append (measured counts: DESIGN.md K4a); batches sized for <= 1 GB of buffers
     const uint32_t ccap = ctx->knobs.ccap ? ctx->knobs.ccap : std::min(8192u, std::max(1024u, 128u * k));

@@ -483,12 +483,14 @@ def test_engine_selection_errors(hb):
         assert c.last_engine() == "tensor_fp4" and got.has_hit.all()
 
 
-@pytest.mark.parametrize("mode", ["collect", "collect_overflow", "collect_tiny_stage", "lists"])
+@pytest.mark.parametrize("mode", ["default", "collect", "collect_overflow", "collect_tiny_stage", "lists"])
 def test_tensor_topk_modes_vs_port(hb, port, monkeypatch, mode):
     """The tensor engine's top-k paths against the full-sort oracle on tie-heavy data: collect + select (default),
     the same with a candidate buffer so small that (nearly) every query overflows and the fix-up list passes
     produce the answer, a buffer that holds everything but far more survivors than the selection stages
     (rows duplicated: hundreds of equal scores), and the register-list passes alone."""
+    if mode.startswith("collect"):
+        monkeypatch.setenv("HOMS_B200_TC_TOPK", "collect")  # also for the shallow k the default serves from lists
     if mode == "collect_overflow":
         monkeypatch.setenv("HOMS_B200_TC_CCAP", "24")
     elif mode == "collect_tiny_stage":
