@@ -26,13 +26,13 @@
 // rational value with 54 quotient bits by shift-and-subtract on multi-word integers in shared
 // memory and rounds to nearest even; overflow and underflow-to-zero are from_chars' out-of-range
 // errors.  No value is ever approximated.
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <string>
 #include <vector>
 
 #include "common.cuh"
+#include "radix.cuh"
 
 namespace hb {
 
@@ -76,9 +76,7 @@ __global__ void mgf_count_newlines_kernel(const uint8_t* __restrict__ text, uint
   } else {
     for (uint64_t i = base; i < n; ++i) c += text[i] == '\n';
   }
-  using Reduce = cub::BlockReduce<uint32_t, kM1Threads>;
-  __shared__ typename Reduce::TempStorage tmp;
-  const uint32_t total = Reduce(tmp).Sum(c);
+  const uint32_t total = block_sum_u32<kM1Threads>(c);
   if (threadIdx.x == 0) tile_count[blockIdx.x] = total;
 }
 
@@ -88,10 +86,7 @@ __global__ void mgf_line_starts_kernel(const uint8_t* __restrict__ text, uint64_
   uint32_t mask = 0;
   for (int i = 0; i < kM1Bytes; ++i)
     if (base + i < n && text[base + i] == '\n') mask |= 1u << i;
-  using Scan = cub::BlockScan<uint32_t, kM1Threads>;
-  __shared__ typename Scan::TempStorage tmp;
-  uint32_t before;
-  Scan(tmp).ExclusiveSum(__popc(mask), before);
+  const uint32_t before = block_exclusive_sum_u32<kM1Threads>(__popc(mask));
   uint32_t k = tile_base[blockIdx.x] + before;  // newlines before this thread's bytes
   while (mask) {
     const int i = __ffs(mask) - 1;
@@ -709,13 +704,8 @@ __global__ void mgf_compact_kernel(uint32_t n_blocks, const uint64_t* __restrict
 
 template <typename T>
 static int scan_u32(homs_b200_ctx* ctx, const T* d_in, T* d_out, uint64_t n) {
-  size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, d_in, d_out, static_cast<int>(n), ctx->stream);
-  HB_TRY(ensure(ctx, ctx->scratch[kScrCub], bytes));
-  HB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->scratch[kScrCub].p, bytes, d_in, d_out, static_cast<int>(n),
-                                             ctx->stream));
-  HB_LAUNCHED(ctx);
-  return HOMS_B200_OK;
+  HB_TRY(ensure(ctx, ctx->scratch[kScrCub], exclusive_sum_temp_bytes(n)));
+  return exclusive_sum<T>(ctx, d_in, d_out, n, ctx->scratch[kScrCub].p);
 }
 
 }  // namespace hb

@@ -55,50 +55,109 @@ radix_hist_kernel(const K* __restrict__ keys, uint64_t n, int shift, uint32_t n_
   hist[uint64_t(threadIdx.x) * n_tiles + blockIdx.x] = s_cnt[threadIdx.x];
 }
 
-// in-place exclusive prefix sum of `count` entries by one CTA of 1024 threads
-__global__ void __launch_bounds__(1024) radix_scan_kernel(uint32_t* __restrict__ data, uint64_t count) {
-  __shared__ uint32_t s_warp[32];
-  __shared__ uint32_t s_carry;
+// exclusive prefix sum of `count` entries by one CTA of 1024 threads (in == out allowed); `add` is added to every
+// result (multi-tile scans pass the tile's offset)
+template <typename T>
+__device__ __forceinline__ void scan_cta_1024(const T* in, T* out, uint64_t count, T add,
+                                              T* total_out) {
+  __shared__ T s_warp[32];
+  __shared__ T s_carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
+  if (threadIdx.x == 0) s_carry = add;
   __syncthreads();
   for (uint64_t base = 0; base < count; base += 4096) {  // 4 consecutive entries per thread
     const uint64_t i0 = base + uint64_t(threadIdx.x) * 4;
-    uint32_t v[4];
+    T v[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) v[j] = i0 + j < count ? data[i0 + j] : 0u;
-    const uint32_t mine = v[0] + v[1] + v[2] + v[3];
-    uint32_t incl = mine;
+    for (int j = 0; j < 4; ++j) v[j] = i0 + j < count ? in[i0 + j] : T(0);
+    const T mine = v[0] + v[1] + v[2] + v[3];
+    T incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      const T t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-      const uint32_t w = s_warp[lane];
-      uint32_t wi = w;
+      const T w = s_warp[lane];
+      T wi = w;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+        const T t = __shfl_up_sync(0xffffffffu, wi, o);
         if (lane >= o) wi += t;
       }
       s_warp[lane] = wi - w;  // exclusive over the warps
     }
     __syncthreads();
-    const uint32_t carry = s_carry;
-    uint32_t run = carry + s_warp[warp] + incl - mine;
+    T run = s_carry + s_warp[warp] + incl - mine;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      if (i0 + j < count) data[i0 + j] = run;
+      if (i0 + j < count) out[i0 + j] = run;
       run += v[j];
     }
     __syncthreads();
     if (threadIdx.x == 1023) s_carry = run;
     __syncthreads();
   }
+  if (total_out != nullptr && threadIdx.x == 0) *total_out = s_carry - add;
 }
+
+template <typename T>
+__global__ void __launch_bounds__(1024) scan_single_kernel(const T* in, T* out, uint64_t count) {
+  scan_cta_1024<T>(in, out, count, T(0), nullptr);
+}
+__global__ void __launch_bounds__(1024) radix_scan_kernel(uint32_t* __restrict__ data, uint64_t count) {
+  scan_cta_1024<uint32_t>(data, data, count, 0u, nullptr);
+}
+
+// ---- device-wide exclusive sum (three kernels: tile totals, scan of the totals, per-tile scan) ----------------
+constexpr uint64_t kScanTile = 16384;  // entries per CTA
+
+template <typename T>
+__global__ void __launch_bounds__(1024) scan_tile_totals_kernel(const T* __restrict__ in, uint64_t n, T* __restrict__ totals) {
+  __shared__ T s_warp[32];
+  const uint64_t t0 = uint64_t(blockIdx.x) * kScanTile;
+  T acc = 0;
+  for (uint64_t i = t0 + threadIdx.x; i < min(n, t0 + kScanTile); i += 1024) acc += in[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    T v = s_warp[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) totals[blockIdx.x] = v;
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(1024)
+scan_tiles_kernel(const T* __restrict__ in, T* __restrict__ out, uint64_t n, const T* __restrict__ tile_offs) {
+  const uint64_t t0 = uint64_t(blockIdx.x) * kScanTile;
+  scan_cta_1024<T>(in + t0, out + t0, min(kScanTile, n - t0), tile_offs[blockIdx.x], nullptr);
+}
+
+size_t exclusive_sum_temp_bytes(uint64_t n) { return static_cast<size_t>((n + kScanTile - 1) / kScanTile + 1) * 8; }
+
+template <typename T>
+int exclusive_sum(homs_b200_ctx* ctx, const T* d_in, T* d_out, uint64_t n, void* d_temp) {
+  if (n == 0) return HOMS_B200_OK;
+  if (n <= kScanTile) {
+    scan_single_kernel<T><<<1, 1024, 0, ctx->stream>>>(d_in, d_out, n);
+    HB_LAUNCHED(ctx);
+    return HOMS_B200_OK;
+  }
+  const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
+  T* totals = static_cast<T*>(d_temp);
+  scan_tile_totals_kernel<T><<<static_cast<unsigned>(tiles), 1024, 0, ctx->stream>>>(d_in, n, totals);
+  HB_LAUNCHED(ctx);
+  scan_single_kernel<T><<<1, 1024, 0, ctx->stream>>>(totals, totals, tiles);
+  HB_LAUNCHED(ctx);
+  scan_tiles_kernel<T><<<static_cast<unsigned>(tiles), 1024, 0, ctx->stream>>>(d_in, d_out, n, totals);
+  HB_LAUNCHED(ctx);
+  return HOMS_B200_OK;
+}
+template int exclusive_sum<uint32_t>(homs_b200_ctx*, const uint32_t*, uint32_t*, uint64_t, void*);
+template int exclusive_sum<uint64_t>(homs_b200_ctx*, const uint64_t*, uint64_t*, uint64_t, void*);
 
 template <typename K>
 __global__ void __launch_bounds__(kRadixThreads)

@@ -123,7 +123,7 @@ struct TcParams {
   uint32_t* ccount;       // [q_rows] entries appended so far (may run past ccap: overflow, see tc_select_kernel)
   uint2* cbuf;            // [q_rows][ccap] (dot, local row)
   uint32_t ccap;
-  uint32_t pad3;
+  uint32_t l2_prefetch;   // 0: off; m: the CTAs working on query tiles = 0 (mod m) prefetch the next row tile into L2
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
@@ -173,6 +173,10 @@ __device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uin
       "l"(src), "r"(bytes), "r"(bar), "l"(policy)
       : "memory");
 }
+// pull `bytes` (a multiple of 16) at src into L2 only, with an eviction-priority hint
+__device__ __forceinline__ void bulk_prefetch_l2_hint(const void* src, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes), "l"(policy) : "memory");
+}
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -198,12 +202,24 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+// Remote arrives.  The release form orders this thread's earlier stores (the FIFO entry written into the peer's
+// shared memory) before the arrive; it costs a MEMBAR.ALL.GPU and is used once per work item.  The relaxed form is
+// a bare arrive for the signals that publish no data of this thread: "my stage has landed" (the bytes sit in the
+// signalling SM's own shared memory and are read by that SM's tensor core), "accumulator drained", "slot free".
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
 __device__ __forceinline__ void st_remote_v4(uint32_t cluster_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_volatile_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+  return v;
 }
 // wait that also acquires what a thread of the OTHER CTA of the cluster published before its arrive
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
@@ -620,6 +636,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   // and 4 drain warps (they arrive on the LEADER's barrier)
   constexpr uint32_t kItemConsumers = kPair ? 11 : 5;
 
+  // no FIFO entry left over from an earlier launch may pass for a hand-out of this one (see read_item)
+  if (threadIdx.x >= 32 && threadIdx.x < 32 + 4 * kItemQ) s_item[threadIdx.x - 32] = 0xFFFFFFFFu;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full_bar(s), 1);
@@ -668,13 +686,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   const uint32_t n_items = __ldg(p.n_items);
   // an item slot is released to the leader's producer
   auto release_item_slot = [&](int s) {
-    if (kPair && rank != 0) mbar_arrive_remote(mapa_u32(iempty_bar(s), 0));
+    if (kPair && rank != 0) mbar_arrive_remote_relaxed(mapa_u32(iempty_bar(s), 0));
     else mbar_arrive(iempty_bar(s));
   };
-  auto wait_item_slot = [&](int s, uint32_t parity) {
-    if constexpr (kPair) mbar_wait_cluster(ifull_bar(s), parity);
-    else mbar_wait(ifull_bar(s), parity);
+  // One FIFO entry = 16 bytes {item id or kNone, tile | seq << 16, row_begin, row_end}, seq = number of the hand-out
+  // (mod 2^16).  In the leader's own CTA the entry is ordinary shared memory behind an mbarrier.  The peer's copy is
+  // written through DSMEM with ONE 16-byte store followed by a relaxed remote arrive -- no cluster-scope fence on
+  // either side (a release / acquire pair at cluster scope is a MEMBAR.ALL.GPU plus an L1 invalidate per item and
+  // waiting thread, on the producers' critical path).  Should the arrive ever overtake the store, the reader sees
+  // the previous occupant of the slot, whose seq differs, and re-reads until the entry of this hand-out is there.
+  auto read_item = [&](int s, uint32_t parity, uint32_t seq, uint32_t& item, TcItem& it) {
+    mbar_wait(ifull_bar(s), parity);
+    uint4 e = ld_shared_volatile_v4(s_item_addr + 16u * s);
+    if constexpr (kPair) {
+      while ((e.y >> 16) != (seq & 0xFFFFu)) e = ld_shared_volatile_v4(s_item_addr + 16u * s);
+    }
+    item = e.x;
+    it.tile = e.y & 0xFFFFu;
+    it.row_begin = e.z;
+    it.row_end = e.w;
+    it.pad = 0;
   };
+  static_assert(kTcBatch / kTcM <= 0xFFFF, "tile ids share a word with the hand-out number");
 
   if (warp == 0) {
     // ===== producer: two bulk copies per stage =====
@@ -687,6 +720,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
       const bool hint_a = p.l2_hints & 1u, hint_b = p.l2_hints & 2u;
       const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
       uint32_t next = rank == 0 ? atomicAdd(p.counter, 1u) : 0u;
+      uint32_t iseq = 0;
       for (;;) {
         TcItem it{0, 0, 0, 0};
         uint32_t item;
@@ -695,26 +729,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           mbar_wait(iempty_bar(qslot), qphase ^ 1u);
           if (item < n_items) it = p.items[item];
           const uint32_t id = item < n_items ? item : kNone;
+          const uint32_t w1 = it.tile | (iseq << 16);
           volatile uint32_t* e = s_item + 4 * qslot;
           e[0] = id;
-          e[1] = it.tile;
+          e[1] = w1;
           e[2] = it.row_begin;
           e[3] = it.row_end;
           mbar_arrive(ifull_bar(qslot));
           if constexpr (kPair) {
-            st_remote_v4(mapa_u32(s_item_addr + 16u * qslot, 1), id, it.tile, it.row_begin, it.row_end);
-            mbar_arrive_remote(mapa_u32(ifull_bar(qslot), 1));
+            st_remote_v4(mapa_u32(s_item_addr + 16u * qslot, 1), id, w1, it.row_begin, it.row_end);
+            mbar_arrive_remote_relaxed(mapa_u32(ifull_bar(qslot), 1));
           }
         } else {  // the pair's second CTA follows the leader's FIFO
-          wait_item_slot(qslot, qphase);
-          volatile uint32_t* e = s_item + 4 * qslot;
-          item = e[0];
-          it.tile = e[1];
-          it.row_begin = e[2];
-          it.row_end = e[3];
+          read_item(qslot, qphase, iseq, item, it);
           release_item_slot(qslot);
           if (item == kNone) item = n_items;
         }
+        ++iseq;
         if (++qslot == kItemQ) {
           qslot = 0;
           qphase ^= 1u;
@@ -728,7 +759,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           // own library rows: the whole N-row tile (single) or half `rank` of it (pair)
           const uint8_t* b_src =
               p.lib_x + (uint64_t(it.row_begin) + uint64_t(nt) * kN + uint64_t(rank) * Shape::BRows) * kTcKB;
+          // L2 prefetch of the NEXT row tile's library block (the next tile of this item, or the first tile of the
+          // next strip, which other CTAs start on a few tens of microseconds later), one k-chunk per stage: the
+          // first CTA to touch a library block pays the DRAM latency, which is longer than the shared-memory ring
+          // can cover; one query tile in `l2_prefetch` does this for its neighbours.  The tile after the last real
+          // one is the all-zero slack tile, so the address is always inside the image.
+          const bool pf = p.l2_prefetch != 0 && (it.tile % p.l2_prefetch) == 0;
           for (uint32_t kc = 0; kc < n_kc; ++kc) {
+            if (pf)
+              bulk_prefetch_l2_hint(b_src + uint64_t(kN) * kTcKB + uint64_t(kc) * p.lib_rows * kTcKB, Shape::BBytes, pol_b);
             mbar_wait(empty_bar(stage), phase ^ 1u);
             const uint32_t sa = base + stage * Shape::StageBytes;
             mbar_expect_tx(full_bar(stage), Shape::StageBytes);
@@ -749,11 +788,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     // ===== MMA issuer: one thread (of the leader); in the peer the same thread relays "stage full" =====
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;  // aphase: one parity bit per accumulator
-      uint32_t qslot = 0, qphase = 0;
+      uint32_t qslot = 0, qphase = 0, iseq = 0;
       for (;;) {
-        wait_item_slot(qslot, qphase);
-        volatile uint32_t* e = s_item + 4 * qslot;
-        const uint32_t item = e[0], row_begin = e[2], row_end = e[3];
+        uint32_t item;
+        TcItem mit;
+        read_item(qslot, qphase, iseq, item, mit);
+        ++iseq;
+        const uint32_t row_begin = mit.row_begin, row_end = mit.row_end;
         release_item_slot(qslot);
         if (++qslot == kItemQ) {
           qslot = 0;
@@ -764,7 +805,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         if (kPair && rank != 0) {  // relay: my share of stage s has landed -> the leader's pfull[s]
           for (uint32_t i = 0; i < n_nt * n_kc; ++i) {
             mbar_wait(full_bar(stage), phase);
-            mbar_arrive_remote(mapa_u32(pfull_bar(stage), 0));
+            mbar_arrive_remote_relaxed(mapa_u32(pfull_bar(stage), 0));
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1u;
@@ -779,7 +820,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           const uint32_t tmem_d = tmem_base + acc * kN;
           for (uint32_t kc = 0; kc < n_kc; ++kc) {
             mbar_wait(full_bar(stage), phase);
-            if constexpr (kPair) mbar_wait_cluster(pfull_bar(stage), phase);
+            if constexpr (kPair) mbar_wait(pfull_bar(stage), phase);  // the peer's share has landed in ITS shared memory
             tc_fence_after();
             const uint32_t sa = base + stage * Shape::StageBytes;
             const uint64_t adesc = tc_smem_desc(sa);
@@ -819,14 +860,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     const int quarter = warp & 3;  // a warp may only touch TMEM lanes [32 * (warp % 4), +32)
     const int qrow = quarter * 32 + lane;
     constexpr int kChunks = (kN + 31) / 32;
-    uint32_t acc = 0, tphase = 0, qslot = 0, qphase = 0;
+    uint32_t acc = 0, tphase = 0, qslot = 0, qphase = 0, iseq = 0;
     for (;;) {
-      wait_item_slot(qslot, qphase);
+      uint32_t item;
       TcItem it;
-      const uint32_t item = s_item[4 * qslot];
-      it.tile = s_item[4 * qslot + 1];
-      it.row_begin = s_item[4 * qslot + 2];
-      it.row_end = s_item[4 * qslot + 3];
+      read_item(qslot, qphase, iseq, item, it);
+      ++iseq;
       __syncwarp();
       if (lane == 0) release_item_slot(qslot);
       if (++qslot == kItemQ) {
@@ -892,22 +931,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         int c1 = ll > row0 ? static_cast<int>(min(ll - row0, uint32_t(kN))) : 0;
         if (c1 <= c0) c0 = c1 = 0;
 
-        if constexpr (kCollect) {
-          // While the floor is still weak a thread appends most of what it sees; its own appends (and
-          // those of items running elsewhere) have raised the class slots meanwhile: read them again.
-          if (fresh >= 4) {
-            int f = INT_MAX;
-            for (uint32_t j = 0; j < p.k; ++j) f = min(f, __ldcg(p.gbest + pos * p.k + j));
-            bar = max(bar, Acc::from_int(f));
-            fresh = 0;
-          }
-        }
         mbar_wait(tfull_bar(acc), (tphase >> acc) & 1u);
         tphase ^= 1u << acc;
         tc_fence_after();
         const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + acc * kN;
 
         auto reduce_chunk = [&](const int (&v)[32], int cb) {
+          if constexpr (kCollect) {
+            // While the floor is still weak a thread appends most of what it sees (the first tile of a query's
+            // first item would append all 224 rows, and two or three of its items start at once: measured mean
+            // 620 entries per query at k = 5, of which ~90 are needed).  Its own appends (and those of items
+            // running elsewhere) have raised the class slots meanwhile: read them again, per chunk.
+            if (fresh >= 4) {
+              int f = INT_MAX;
+              for (uint32_t j = 0; j < p.k; ++j) f = min(f, __ldcg(p.gbest + pos * p.k + j));
+              bar = max(bar, Acc::from_int(f));
+              fresh = 0;
+            }
+          }
           AccT cm = Acc::lowest();
           if (c0 <= cb && cb + 32 <= c1) {
 #pragma unroll
@@ -1025,7 +1066,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {  // the accumulator is released to the (leader's) MMA thread
-          if (kPair && rank != 0) mbar_arrive_remote(mapa_u32(tempty_bar(acc), 0));
+          if (kPair && rank != 0) mbar_arrive_remote_relaxed(mapa_u32(tempty_bar(acc), 0));
           else mbar_arrive(tempty_bar(acc));
         }
         acc ^= 1u;
@@ -1486,7 +1527,7 @@ static int tc_run_pass(homs_b200_ctx* ctx, const TcBatch& tb, const uint32_t* d_
   tp.ccount = nullptr;
   tp.cbuf = nullptr;
   tp.ccap = 0;
-  tp.pad3 = 0;
+  tp.l2_prefetch = ctx->knobs.l2_prefetch;
   HB_TRY(tc_launch_search<KM>(ctx, tb, tp));
   HB_LAUNCHED(ctx);
   if constexpr (KM > 1)
@@ -1563,8 +1604,24 @@ static int tc_collect_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   tp.ccount = ctx->scratch[kScrTcCount].as<uint32_t>();
   tp.cbuf = ctx->scratch[kScrTcBuf].as<uint2>();
   tp.ccap = ccap;
+  tp.l2_prefetch = ctx->knobs.l2_prefetch;
   HB_TRY(tc_launch_search<0>(ctx, tb, tp));
   HB_LAUNCHED(ctx);
+  if (ctx->knobs.debug) {  // development: how full did the candidate buffers get?
+    std::vector<uint32_t> h(nb);
+    cudaMemcpyAsync(h.data(), tp.ccount, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    uint64_t sum = 0, over = 0;
+    uint32_t mx = 0;
+    for (uint32_t c : h) {
+      sum += c;
+      mx = std::max(mx, c);
+      over += c > ccap;
+    }
+    std::sort(h.begin(), h.end());
+    fprintf(stderr, "[tc collect] k=%u ccap=%u queries=%llu mean=%.1f p50=%u p99=%u max=%u overflowed=%llu\n", k, ccap,
+            (unsigned long long)nb, double(sum) / double(nb), h[nb / 2], h[nb - 1 - nb / 100], mx, (unsigned long long)over);
+  }
   auto* d_over = ctx->scratch[kScrTcOverflow].as<uint8_t>();
   tc_select_kernel<<<static_cast<unsigned>((nb + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, ctx->stream>>>(
       nb, d_vals + b0, d_subset, tp.ccount, tp.cbuf, ccap, k, k_stride, lib.dim, q.d_mz.as<double>(),
@@ -1583,14 +1640,15 @@ static int tc_collect_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
 int tc_search_sorted(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n, const uint64_t* d_keys,
                      const uint32_t* d_vals, Cand* d_out, uint32_t k, uint32_t k_stride) {
   HB_REQUIRE(ctx, k >= 1 && k <= HOMS_B200_MAX_TOPK, HOMS_B200_ERR_ARGUMENT, "tensor engine: k out of range");
-  // Shallow lists are cheapest in registers (k = 5: 24.6 ms against 28.5 ms collected, config 2); from k = 9 on
-  // the register insert path costs more than appending and selecting afterwards (k = 16: 28.7 -> 24.1 ms,
-  // k = 32: 56.5 -> 25.7 ms, k = 64: 113 -> 29.1 ms; profiles/r02_ab_topk_collect_vs_lists.log).
-  const bool collect = k >= 2 && (ctx->knobs.topk_lists == 2 || (ctx->knobs.topk_lists == 0 && k > 8));
+  // Collect + select serves every k >= 2 (one pass; interleaved A/B against the register-list passes on config 2,
+  // ms per 16 000-query step, lists -> collect: k = 2: 22.8 -> 22.5, k = 5: 24.4 -> 23.3, k = 8: 25.4 -> 23.2,
+  // k = 16: 28.3 -> 24.1, k = 64: 113.8 -> 31.6; profiles/r02_ab_topk_collect_vs_lists_v2.log).  The register
+  // lists remain as the fix-up for overflowed buffers and behind HOMS_B200_TC_TOPK=lists.
+  const bool collect = k >= 2 && ctx->knobs.topk_lists != 1;
   if (collect) {
     // buffer capacity per query: the floor admits about k x H(k) x ln(window / strip) candidates plus what the
     // first, floor-less items append (measured counts: DESIGN.md K4a); batches sized for <= 1 GB of buffers
-    const uint32_t ccap = ctx->knobs.ccap ? ctx->knobs.ccap : std::min(8192u, std::max(1024u, 128u * k));
+    const uint32_t ccap = ctx->knobs.ccap ? ctx->knobs.ccap : std::min(8192u, std::max(2048u, 128u * k));
     uint64_t batch = std::max<uint64_t>(kTcM, ((1ull << 30) / (uint64_t(ccap) * sizeof(uint2))) / kTcM * kTcM);
     batch = std::min<uint64_t>(batch, kTcBatch);
     HB_TRY(ensure(ctx, ctx->scratch[kScrTcKeysFix], n * sizeof(uint64_t)));
