@@ -509,7 +509,11 @@ __global__ void decode_kernel(uint64_t total, const Cand* __restrict__ rec, uint
 // KM = 1: running best; KM > 1: the k <= KM best in a register list every lane holds identically
 // (the comparisons are warp-uniform) -- the warp-level top-k with the reference's tie-break.
 constexpr uint32_t kDirectMaxK = 32;  // list depth of one pass; deeper top-k takes ceil(k / 32) passes
-template <int KM>
+// LPR = 0: a row spans the warp (row_u4 lanes of every 32 at a time).  LPR = 8 / 16: rows of exactly LPR 16-byte
+// slabs (D <= 1024 / D <= 2048): 32 / LPR rows side by side in the warp, so that every lane loads and four
+// passes keep 16 / 8 rows in flight instead of 4 (at D = 1024 three quarters of the lanes used to idle and the
+// kernel was bound by the latency of 23 dependent rounds per 90-row window).
+template <int KM, int LPR>
 __global__ void __launch_bounds__(256)
 direct_search_kernel(uint64_t n, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                      const uint32_t* __restrict__ subset, const uint4* __restrict__ q_words,
@@ -588,6 +592,34 @@ direct_search_kernel(uint64_t n, const uint64_t* __restrict__ keys, const uint32
   };
 
   uint32_t r = lf;
+  if constexpr (LPR != 0) {
+    constexpr uint32_t kRpp = 32 / LPR;  // rows per pass
+    const uint32_t sub = lane / LPR, sl = lane % LPR;
+    const uint4 a = q[sl];
+    for (; r < ll; r += 4 * kRpp) {  // four passes in flight per lane
+      uint32_t c[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t row = r + j * kRpp + sub;
+        uint4 x = a;  // a row past the window: distance 0, never looked at
+        if (row < ll) x = __ldg(lib_words + size_t(row) * LPR + sl);
+        c[j] = __popc(a.x ^ x.x) + __popc(a.y ^ x.y) + __popc(a.z ^ x.z) + __popc(a.w ^ x.w);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) c[j] += __shfl_xor_sync(0xffffffffu, c[j], o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (uint32_t sb = 0; sb < kRpp; ++sb) {
+          const uint32_t d = __shfl_sync(0xffffffffu, c[j], sb * LPR);
+          const uint32_t row = r + j * kRpp + sb;
+          if (row < ll) consider(row, d);
+        }
+    }
+    r = ll;
+  }
   for (; r + 4 <= ll; r += 4) {  // four rows in flight per lane
     uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
     const uint4* b = lib_words + size_t(r) * row_u4;
@@ -769,10 +801,15 @@ int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n,
 
   if (use_direct) {
     const unsigned blocks = static_cast<unsigned>((n * 32 + 255) / 256);
+#define HB_DIRECT_ARGS                                                                                        \
+  n, keys, vals, d_subset, q.d_words.as<uint4>(), q.d_mz.as<double>(), lib.d_words.as<uint4>(),               \
+      lib.d_mz_local.as<double>(), lib.d_id_rank_local.as<uint32_t>(), lib.S / 2, d_out, kr, k, col0, prev_col
 #define HB_DIRECT_LAUNCH(KM)                                                                                  \
-  direct_search_kernel<KM><<<blocks, 256, 0, ctx->stream>>>(                                                  \
-      n, keys, vals, d_subset, q.d_words.as<uint4>(), q.d_mz.as<double>(), lib.d_words.as<uint4>(),           \
-      lib.d_mz_local.as<double>(), lib.d_id_rank_local.as<uint32_t>(), lib.S / 2, d_out, kr, k, col0, prev_col)
+  do {                                                                                                        \
+    if (lib.S / 2 == 8) direct_search_kernel<KM, 8><<<blocks, 256, 0, ctx->stream>>>(HB_DIRECT_ARGS);         \
+    else if (lib.S / 2 == 16) direct_search_kernel<KM, 16><<<blocks, 256, 0, ctx->stream>>>(HB_DIRECT_ARGS);  \
+    else direct_search_kernel<KM, 0><<<blocks, 256, 0, ctx->stream>>>(HB_DIRECT_ARGS);                        \
+  } while (0)
     // k > 32: passes of up to 32, each bounded below by the previous pass's last key (as on the tensor engine)
     for (uint32_t col0 = 0; col0 < k; col0 += kDirectMaxK) {
       const uint32_t kr = std::min<uint32_t>(kDirectMaxK, k - col0);
@@ -788,6 +825,7 @@ int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n,
       HB_LAUNCHED(ctx);
     }
 #undef HB_DIRECT_LAUNCH
+#undef HB_DIRECT_ARGS
     ctx->last_engine = HOMS_B200_ENGINE_DIRECT;
     return HOMS_B200_OK;
   }

@@ -123,7 +123,7 @@ struct TcParams {
   uint32_t* ccount;       // [q_rows] entries appended so far (may run past ccap: overflow, see tc_select_kernel)
   uint2* cbuf;            // [q_rows][ccap] (dot, local row)
   uint32_t ccap;
-  uint32_t l2_prefetch;   // 0: off; m: the CTAs working on query tiles = 0 (mod m) prefetch the next row tile into L2
+  uint32_t pad3;
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
@@ -172,10 +172,6 @@ __device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uin
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
       "l"(src), "r"(bytes), "r"(bar), "l"(policy)
       : "memory");
-}
-// pull `bytes` (a multiple of 16) at src into L2 only, with an eviction-priority hint
-__device__ __forceinline__ void bulk_prefetch_l2_hint(const void* src, uint32_t bytes, uint64_t policy) {
-  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes), "l"(policy) : "memory");
 }
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;
@@ -759,15 +755,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           // own library rows: the whole N-row tile (single) or half `rank` of it (pair)
           const uint8_t* b_src =
               p.lib_x + (uint64_t(it.row_begin) + uint64_t(nt) * kN + uint64_t(rank) * Shape::BRows) * kTcKB;
-          // L2 prefetch of the NEXT row tile's library block (the next tile of this item, or the first tile of the
-          // next strip, which other CTAs start on a few tens of microseconds later), one k-chunk per stage: the
-          // first CTA to touch a library block pays the DRAM latency, which is longer than the shared-memory ring
-          // can cover; one query tile in `l2_prefetch` does this for its neighbours.  The tile after the last real
-          // one is the all-zero slack tile, so the address is always inside the image.
-          const bool pf = p.l2_prefetch != 0 && (it.tile % p.l2_prefetch) == 0;
+          // (An L2 prefetch of the next row tile's library block, cp.async.bulk.prefetch.L2 one k-chunk per stage by
+          // every query tile or by one in eight, was measured 11-16 % SLOWER: profiles/r02_ab_l2_prefetch.log.)
           for (uint32_t kc = 0; kc < n_kc; ++kc) {
-            if (pf)
-              bulk_prefetch_l2_hint(b_src + uint64_t(kN) * kTcKB + uint64_t(kc) * p.lib_rows * kTcKB, Shape::BBytes, pol_b);
             mbar_wait(empty_bar(stage), phase ^ 1u);
             const uint32_t sa = base + stage * Shape::StageBytes;
             mbar_expect_tx(full_bar(stage), Shape::StageBytes);
@@ -1428,9 +1418,18 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
 }
 
 // the search kernel over a prepared batch: one CTA per SM, or one 2-CTA cluster per SM pair
+// HB_TC_PAIR: the CTA-pair form of the search kernel (TcShape<true>, HOMS_B200_TC_PAIR=1 at run time) is compiled
+// only on request.  MEASURED AND LEFT OFF: bit-exact on the whole search suite, SM clock 5 % higher under the power
+// cap (a third fewer operand bytes per MMA), but 1 % slower at D = 8192, equal at 16384, 7 % slower at 1024 --
+// what the pair saves in operand traffic it loses to the cross-CTA hand-offs (profiles/r02_ab_cta_pair.log).
+#ifndef HB_TC_PAIR
+#define HB_TC_PAIR 0
+#endif
+
 template <int KM>
 static int tc_launch_search(homs_b200_ctx* ctx, const TcBatch& tb, const TcParams& tp) {
   KernelTimer timer(ctx, HOMS_B200_KERNEL_SEARCH);
+#if HB_TC_PAIR
   if (tb.pair) {
     using Shape = TcShape<true>;
     HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<KM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1448,7 +1447,10 @@ static int tc_launch_search(homs_b200_ctx* ctx, const TcBatch& tb, const TcParam
     cfg.attrs = at;
     cfg.numAttrs = 1;
     HB_CUDA(ctx, cudaLaunchKernelEx(&cfg, tc_search_kernel<KM, true>, tp));
-  } else {
+    return HOMS_B200_OK;
+  }
+#endif
+  {
     using Shape = TcShape<false>;
     HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<KM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Shape::SmemBytes)));
@@ -1459,6 +1461,10 @@ static int tc_launch_search(homs_b200_ctx* ctx, const TcBatch& tb, const TcParam
 
 // co-resident 2-CTA clusters of the search kernel x 2 (0: pairs cannot be scheduled); asked once per context
 int tc_query_pair_ctas(homs_b200_ctx* ctx) {
+#if !HB_TC_PAIR
+  (void)ctx;
+  return 0;
+#else
   using Shape = TcShape<true>;
   if (cudaFuncSetAttribute(tc_search_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(Shape::SmemBytes)) != cudaSuccess) {
@@ -1482,6 +1488,7 @@ int tc_query_pair_ctas(homs_b200_ctx* ctx) {
     return 0;
   }
   return std::min(clusters, ctx->sm_count / 2) * 2;
+#endif
 }
 
 // One pass over a prepared batch: the k best per query (k <= KM) -- after the key in column prev_col of
@@ -1527,7 +1534,7 @@ static int tc_run_pass(homs_b200_ctx* ctx, const TcBatch& tb, const uint32_t* d_
   tp.ccount = nullptr;
   tp.cbuf = nullptr;
   tp.ccap = 0;
-  tp.l2_prefetch = ctx->knobs.l2_prefetch;
+  tp.pad3 = 0;
   HB_TRY(tc_launch_search<KM>(ctx, tb, tp));
   HB_LAUNCHED(ctx);
   if constexpr (KM > 1)
@@ -1604,7 +1611,7 @@ static int tc_collect_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   tp.ccount = ctx->scratch[kScrTcCount].as<uint32_t>();
   tp.cbuf = ctx->scratch[kScrTcBuf].as<uint2>();
   tp.ccap = ccap;
-  tp.l2_prefetch = ctx->knobs.l2_prefetch;
+  tp.pad3 = 0;
   HB_TRY(tc_launch_search<0>(ctx, tb, tp));
   HB_LAUNCHED(ctx);
   if (ctx->knobs.debug) {  // development: how full did the candidate buffers get?

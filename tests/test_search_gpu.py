@@ -528,3 +528,29 @@ def test_tensor_topk_modes_vs_port(hb, port, monkeypatch, mode):
             score, ordinal = oix.search_topk(qw, qmz, qch, ("da", 500.0), 40)
             assert np.array_equal(got.ordinal, ordinal) and np.array_equal(got.raw_score, score), mode
     oix.close()
+
+
+@pytest.mark.parametrize("n", [1, 2, 511, 512, 513, 4095, 4096, 4097, 12289])
+def test_index_order_at_sort_tile_boundaries(hb, port, n):
+    """build_index's (charge, precursor m/z, id, ordinal) order comes from the library's own stable LSD radix sort
+    (csrc/radix.cu: 512-element warp chunks, 4096-element tiles): sizes around those boundaries, heavy ties on
+    every key level (few distinct m/z values incl. -0.0 / +0.0 and negative ones, duplicate ids, one or many
+    charges), against the oracle's comparison sort (search.cpp:37-46)."""
+    rng = np.random.default_rng(1000 + n)
+    dim = 128
+    words = U.random_hvs(rng, n, dim)
+    mz = rng.choice(np.array([-3.5, -0.0, 0.0, 1e-300, 380.25, 380.25000000000006, 1070.5, 1e9]), n)
+    charge = rng.integers(1, 6 if n > 100 else 2, n).astype(np.uint8)
+    ids = [f"s{rng.integers(0, max(2, n // 3))}" for _ in range(n)]
+    oix = port.build_index(dim, words, mz, charge, None, ids)
+    with hb.Context(0) as c:
+        c.build_index(dim, words, mz, charge, ids=ids)
+        got = c.buckets()
+        want = oix.buckets()
+        assert len(got) == len(want)
+        for g, w in zip(got, want):
+            assert g["charge"] == w["charge"]
+            assert np.array_equal(g["ordinal"], w["ordinal"]), (n, g["charge"])
+            assert np.array_equal(g["precursor_mz"], w["precursor_mz"]), (n, g["charge"])
+            assert np.array_equal(g["words"], w["words"]), (n, g["charge"])
+    oix.close()
