@@ -88,6 +88,51 @@ preprocess_kernel(PreParams p, uint64_t n, const uint64_t* __restrict__ offsets,
     for (int o = 16; o > 0; o >>= 1) m_surv += __shfl_xor_sync(0xffffffffu, m_surv, o);
     const bool truncate = m_surv > MP;  // :58
 
+    // :60-64 keep the max_peaks first in (intensity desc, m/z asc) order.  Selection instead of ranking: T = the
+    // MP-th largest surviving intensity (positive doubles order like their bit patterns, so T is built bit by bit
+    // from the top: 63 counting passes over the peaks, O(63 P / 32) per lane where the all-pairs rank took
+    // O(P^2 / 32)); everything above T is kept, and of the peaks AT T the first `need_ties` by (m/z asc, position).
+    // Spectra of up to 256 raw peaks hold their intensity bits in registers (8 per lane) for the counting passes.
+    uint64_t thr = 0;
+    uint32_t need_ties = 0;
+    bool ties_all = true;
+    if (truncate) {
+      constexpr int kRegPeaks = 8;
+      const bool in_regs = b - a <= 32ull * kRegPeaks;
+      uint64_t vb[kRegPeaks];
+#pragma unroll
+      for (int r = 0; r < kRegPeaks; ++r) {
+        vb[r] = 0;  // not a survivor: below every candidate threshold (candidates are > 0)
+        const uint64_t j = a + uint64_t(r) * 32 + lane;
+        if (in_regs && j < b) {
+          const double m = mz[j], v = inten[j];
+          if (m >= p.min_mz && m < p.max_mz && v > 0.0 && !(v < floor_intensity))
+            vb[r] = static_cast<uint64_t>(__double_as_longlong(v));
+        }
+      }
+      auto count_ge = [&](uint64_t cand) {  // survivors whose intensity bits are >= cand (cand > 0)
+        uint32_t c = 0;
+        if (in_regs) {
+#pragma unroll
+          for (int r = 0; r < kRegPeaks; ++r) c += vb[r] >= cand;
+        } else {
+          for (uint64_t j = a + lane; j < b; j += 32) {
+            const double m = mz[j], v = inten[j];
+            c += m >= p.min_mz && m < p.max_mz && v > 0.0 && !(v < floor_intensity) &&
+                 static_cast<uint64_t>(__double_as_longlong(v)) >= cand;
+          }
+        }
+        return __reduce_add_sync(0xffffffffu, c);
+      };
+      for (int bit = 62; bit >= 0; --bit) {
+        const uint64_t cand = thr | (1ull << bit);
+        if (count_ge(cand) >= MP) thr = cand;
+      }
+      const uint32_t n_gt = count_ge(thr + 1), n_ge = count_ge(thr);
+      need_ties = MP - n_gt;               // >= 1 by the choice of thr
+      ties_all = n_ge - n_gt == need_ties;  // every peak at the threshold is kept: no order among them needed
+    }
+
     // ordered compaction of the kept peaks into shared memory
     uint32_t kept = 0;
     for (uint64_t c = a; c < b; c += 32) {
@@ -99,17 +144,20 @@ preprocess_kernel(PreParams p, uint64_t n, const uint64_t* __restrict__ offsets,
         v = inten[j];
         keep = m >= p.min_mz && m < p.max_mz && v > 0.0 && !(v < floor_intensity);
       }
-      if (truncate && __any_sync(0xffffffffu, keep)) {
-        // :60-64 keep the max_peaks first in (intensity desc, m/z asc) order.  rank = number of
-        // survivors that precede this peak in that order (position breaks exact duplicates).
-        uint32_t rank = 0;
-        for (uint64_t jj = a; jj < b; ++jj) {
-          const double m2 = mz[jj], v2 = inten[jj];  // warp-uniform address: broadcast load
-          const bool surv2 = m2 >= p.min_mz && m2 < p.max_mz && v2 > 0.0 && !(v2 < floor_intensity);
-          const bool before = v2 > v || (v2 == v && (m2 < m || (m2 == m && jj < j)));
-          rank += (surv2 && before);
+      if (truncate) {
+        const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v));
+        const bool at_thr = keep && bits == thr;
+        keep = keep && bits >= thr;
+        if (!ties_all && __any_sync(0xffffffffu, at_thr)) {
+          // rank among the peaks at the threshold: (m/z asc, position breaks exact duplicates)
+          uint32_t rank = 0;
+          for (uint64_t jj = a; jj < b; ++jj) {
+            const double m2 = mz[jj], v2 = inten[jj];  // warp-uniform address: broadcast load
+            const bool tie2 = m2 >= p.min_mz && m2 < p.max_mz && static_cast<uint64_t>(__double_as_longlong(v2)) == thr;
+            rank += tie2 && (m2 < m || (m2 == m && jj < j));
+          }
+          if (at_thr) keep = rank < need_ties;
         }
-        keep = keep && rank < MP;
       }
       const uint32_t mask = __ballot_sync(0xffffffffu, keep);
       if (keep) {

@@ -253,6 +253,17 @@ __device__ __forceinline__ void tc_mma_fp4_pair(uint32_t tmem_d, uint64_t adesc,
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate)
       : "memory");
 }
+// true in exactly one lane of the (converged) warp; unlike `lane == 0` the compiler KNOWS the guarded code runs in
+// a single thread and issues the uniform-datapath instructions (UBLKCP, UTCOMMA, UTCBAR) without wrapping each one
+// in a loop over the distinct operand values of the active threads
+__device__ __forceinline__ bool elect_one() {
+#ifdef HB_TC_NO_ELECT  // A/B build: the round-1 form (profiles/r02_ab_elect.log)
+  return (threadIdx.x & 31) == 0;
+#endif
+  uint32_t pred;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
@@ -707,7 +718,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
 
   if (warp == 0) {
     // ===== producer: two bulk copies per stage =====
-    if (lane == 0) {
+    if (elect_one()) {
       uint32_t stage = 0, phase = 0, qslot = 0, qphase = 0;
       // L2 residency: a library strip (B) is read by the group's query tiles within one short window and is
       // then dead, while the group's query tiles (A) are re-read for every strip of the sweep.  Fetching B
@@ -776,7 +787,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     }
   } else if (warp == 1) {
     // ===== MMA issuer: one thread (of the leader); in the peer the same thread relays "stage full" =====
-    if (lane == 0) {
+    if (elect_one()) {
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;  // aphase: one parity bit per accumulator
       uint32_t qslot = 0, qphase = 0, iseq = 0;
       for (;;) {
@@ -1716,7 +1727,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_peak_kernel(uint32_t groups)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1 && lane == 0) {
+  if (warp == 1 && elect_one()) {
     const uint64_t adesc = tc_smem_desc(base);
     const uint64_t bdesc = tc_smem_desc(base + kTcABytes);
     for (uint32_t g = 0; g < groups; ++g) {
