@@ -178,6 +178,11 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -724,8 +729,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
       // then dead, while the group's query tiles (A) are re-read for every strip of the sweep.  Fetching B
       // with evict_first keeps the streaming strips from pushing A out (default; -1.7 ... -3.7 % kernel time
       // on configs 2, 3 and D = 16384); evict_last on A on top of that measured no gain (bit 0, off).
-      const bool hint_a = p.l2_hints & 1u, hint_b = p.l2_hints & 2u;
-      const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
+      const uint64_t pol_a = (p.l2_hints & 1u) ? l2_policy_evict_last() : l2_policy_evict_normal();
+      const uint64_t pol_b = (p.l2_hints & 2u) ? l2_policy_evict_first() : l2_policy_evict_normal();
+      // everything the inner loop needs lives in registers: no parameter reloads, no 64-bit multiplies per stage
+      const uint64_t a_step = p.q_rows * kTcKB, b_step = p.lib_rows * kTcKB;  // bytes between k-chunk planes
+      const uint8_t* const q_x = p.q_x;
+      const uint8_t* const lib_x = p.lib_x;
       uint32_t next = rank == 0 ? atomicAdd(p.counter, 1u) : 0u;
       uint32_t iseq = 0;
       for (;;) {
@@ -761,22 +770,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         if (rank == 0) next = atomicAdd(p.counter, 1u);  // the next id arrives while this item streams
         const uint32_t n_nt = (it.row_end - it.row_begin + kN - 1) / kN;
         // own query rows: tile it.tile (single) or half `rank` of the 256-query tile it.tile (pair)
-        const uint8_t* a_src = p.q_x + (uint64_t(it.tile) * Shape::TileQ + uint64_t(rank) * kTcM) * kTcKB;
-        for (uint32_t nt = 0; nt < n_nt; ++nt) {
-          // own library rows: the whole N-row tile (single) or half `rank` of it (pair)
-          const uint8_t* b_src =
-              p.lib_x + (uint64_t(it.row_begin) + uint64_t(nt) * kN + uint64_t(rank) * Shape::BRows) * kTcKB;
-          // (An L2 prefetch of the next row tile's library block, cp.async.bulk.prefetch.L2 one k-chunk per stage by
-          // every query tile or by one in eight, was measured 11-16 % SLOWER: profiles/r02_ab_l2_prefetch.log.)
-          for (uint32_t kc = 0; kc < n_kc; ++kc) {
+        const uint8_t* a_src = q_x + (uint64_t(it.tile) * Shape::TileQ + uint64_t(rank) * kTcM) * kTcKB;
+        // own library rows: the whole N-row tile (single) or half `rank` of it (pair)
+        const uint8_t* b_src = lib_x + (uint64_t(it.row_begin) + uint64_t(rank) * Shape::BRows) * kTcKB;
+        // (An L2 prefetch of the next row tile's library block, cp.async.bulk.prefetch.L2 one k-chunk per stage by
+        // every query tile or by one in eight, was measured 11-16 % SLOWER: profiles/r02_ab_l2_prefetch.log.)
+        for (uint32_t nt = 0; nt < n_nt; ++nt, b_src += uint64_t(kN) * kTcKB) {
+          const uint8_t* ap = a_src;
+          const uint8_t* bp = b_src;
+          for (uint32_t kc = 0; kc < n_kc; ++kc, ap += a_step, bp += b_step) {
             mbar_wait(empty_bar(stage), phase ^ 1u);
             const uint32_t sa = base + stage * Shape::StageBytes;
-            mbar_expect_tx(full_bar(stage), Shape::StageBytes);
-            if (hint_a) bulk_g2s_hint(sa, a_src + uint64_t(kc) * p.q_rows * kTcKB, kTcABytes, full_bar(stage), pol_a);
-            else bulk_g2s(sa, a_src + uint64_t(kc) * p.q_rows * kTcKB, kTcABytes, full_bar(stage));
-            if (hint_b)
-              bulk_g2s_hint(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, Shape::BBytes, full_bar(stage), pol_b);
-            else bulk_g2s(sa + kTcABytes, b_src + uint64_t(kc) * p.lib_rows * kTcKB, Shape::BBytes, full_bar(stage));
+            const uint32_t fb = full_bar(stage);
+            mbar_expect_tx(fb, Shape::StageBytes);
+            bulk_g2s_hint(sa, ap, kTcABytes, fb, pol_a);
+            bulk_g2s_hint(sa + kTcABytes, bp, Shape::BBytes, fb, pol_b);
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1u;
@@ -1343,8 +1351,18 @@ struct TcBatch {
   TcPlanPtrs pp{};
 };
 
-// CTA pairs (TcShape<true>) when the device can co-schedule one 2-CTA cluster on (nearly) every SM pair
-static bool tc_use_pair(const homs_b200_ctx* ctx) { return ctx->knobs.pair != 0 && ctx->tc_pair_ctas >= 2; }
+// CTA pairs (TcShape<true>, cta_group::2) or one CTA per SM?  A pair moves a third fewer operand bytes per MMA
+// (L2 -> shared memory and shared memory -> tensor core), which under the board's power cap is SM clock (+5 %), and
+// its ring is 7 stages deep instead of 5; it pays with cross-CTA hand-offs per work item and row tile.  Interleaved
+// A/B on one box (profiles/r02_ab_cta_pair_v2.log): D = 16384 -4.7 %, config-3 prefix -3.4 %, config 2 (D = 8192)
+// -2.3 %, D = 1024 +4.8 % -- so pairs serve D >= kTcPairMinDim when the device co-schedules a 2-CTA cluster on
+// every SM pair (HOMS_B200_TC_PAIR=0 / 1 forces either form).
+constexpr uint32_t kTcPairMinKc = 32;  // k-chunks of 256 dimensions: D >= 8192
+static bool tc_use_pair(const homs_b200_ctx* ctx) {
+  if (ctx->knobs.pair == 0 || ctx->tc_pair_ctas < 2) return false;
+  if (ctx->knobs.pair == 1) return true;
+  return ctx->lib.n_kc >= kTcPairMinKc && ctx->tc_pair_ctas + 1 >= ctx->sm_count;
+}
 
 // k_partial: list depth the per-item partial block is sized for (0: none, collect mode); reuse_qx: the
 // expanded queries of this very batch are already in place (fix-up pass)
@@ -1429,12 +1447,9 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
 }
 
 // the search kernel over a prepared batch: one CTA per SM, or one 2-CTA cluster per SM pair
-// HB_TC_PAIR: the CTA-pair form of the search kernel (TcShape<true>, HOMS_B200_TC_PAIR=1 at run time) is compiled
-// only on request.  MEASURED AND LEFT OFF: bit-exact on the whole search suite, SM clock 5 % higher under the power
-// cap (a third fewer operand bytes per MMA), but 1 % slower at D = 8192, equal at 16384, 7 % slower at 1024 --
-// what the pair saves in operand traffic it loses to the cross-CTA hand-offs (profiles/r02_ab_cta_pair.log).
+// HB_TC_PAIR = 0 compiles the CTA-pair form of the search kernel (TcShape<true>) out.
 #ifndef HB_TC_PAIR
-#define HB_TC_PAIR 0
+#define HB_TC_PAIR 1
 #endif
 
 template <int KM>

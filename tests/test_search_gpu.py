@@ -554,3 +554,40 @@ def test_index_order_at_sort_tile_boundaries(hb, port, n):
             assert np.array_equal(g["precursor_mz"], w["precursor_mz"]), (n, g["charge"])
             assert np.array_equal(g["words"], w["words"]), (n, g["charge"])
     oix.close()
+
+
+@pytest.mark.parametrize("form,dim", [("pair", 256), ("pair", 2048), ("single", 8192)])
+def test_tensor_kernel_forms_vs_port(hb, port, monkeypatch, form, dim):
+    """Both forms of the tensor search kernel whatever the dimension: one CTA per SM (M = 128 tiles) and CTA pairs
+    (cta_group::2, M = 256 tiles over a 2-CTA cluster, default from D = 8192 up).  An odd number of 128-query
+    tiles (the pair's second half is empty), several planning tiles, top-1, collected top-k, the register-list
+    passes and a sharded group -- against the full-sort oracle."""
+    monkeypatch.setenv("HOMS_B200_TC_PAIR", "1" if form == "pair" else "0")
+    rng = np.random.default_rng(91 + dim)
+    n, nq = (24000, 700) if dim < 8192 else (6000, 300)
+    base = U.random_hvs(rng, n // 4, dim)
+    words = base[np.arange(n) % (n // 4)]  # every row four times: ties on the score
+    mz = np.round(rng.uniform(500.0, 530.0, n), 2)
+    charge = rng.integers(2, 4, n).astype(np.uint8)
+    ids = [f"id{rng.integers(0, 80)}" for _ in range(n)]
+    qw = base[rng.integers(0, n // 4, nq)] ^ (U.random_hvs(rng, nq, dim) & U.random_hvs(rng, nq, dim))
+    qmz = np.round(rng.uniform(495.0, 535.0, nq), 2)
+    qch = rng.integers(1, 4, nq).astype(np.uint8)
+    oix = port.build_index(dim, words, mz, charge, None, ids)
+    with hb.Context(0) as c:
+        c.set_engine("tensor_fp4")
+        c.build_index(dim, words, mz, charge, ids=ids)
+        for tol, k in ((("da", 500.0), 1), (("da", 3.0), 1), (("da", 500.0), 5), (("ppm", 4000.0), 40)):
+            m = c.search_batch(qw, qmz, qch, U.product_tol(tol), k=k)
+            score, ordinal = oix.search_topk(qw, qmz, qch, tol, k)
+            assert np.array_equal(m.ordinal, ordinal), (form, dim, tol, k)
+            assert np.array_equal(m.raw_score, score), (form, dim, tol, k)
+            assert c.last_engine() == "tensor_fp4"
+    monkeypatch.setenv("HOMS_B200_TC_TOPK", "lists")
+    with hb.Context(devices=[0, 0, 0]) as grp:
+        grp.set_engine("tensor_fp4")
+        grp.build_index(dim, words, mz, charge, ids=ids)
+        got = grp.search_batch(qw, qmz, qch, hb.Tolerance("dalton", 500.0), k=7)
+        score, ordinal = oix.search_topk(qw, qmz, qch, ("da", 500.0), 7)
+        assert np.array_equal(got.ordinal, ordinal) and np.array_equal(got.raw_score, score), (form, dim)
+    oix.close()
