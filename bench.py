@@ -538,7 +538,8 @@ def run_ours(args) -> None:
                     "traffic_over_compulsory": traffic / compulsory if traffic else None,
                     "traffic_source": cap and {"file": cap.get("source"), "command": cap.get("command")},
                     "tensor_pipe_active_pct_ncu": cap and cap.get("tensor_pipe_active_pct"),
-                    "kernel": "tc_search_kernel", "kernel_ms_per_launch": kernel_ms,
+                    "kernel": "tc_search_kernel<KM, pair=%s>" % ("true: CTA pairs, tcgen05 cta_group::2, M256 N224 K64 per MMA" if ctx.tensor_cta_pairs() else "false: one CTA per SM, M128 N224 K64 per MMA"),
+                    "kernel_ms_per_launch": kernel_ms,
                     "kernel_share_of_step": search_ms / ms_total if ms_total > 0 else None,
                     "algorithmic_ops_per_launch": ops, "pairs_per_launch": n_pairs / world / launches_per_step,
                     "launches_per_step": launches_per_step,

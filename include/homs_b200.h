@@ -146,6 +146,9 @@ enum {
 int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine);
 /* The engine the last search call of this context ran on (one of the non-AUTO codes; reporting aid). */
 int homs_b200_ctx_last_engine(const homs_b200_ctx* ctx);
+/* 1 when the tensor engine runs the resident library on CTA pairs (tcgen05 cta_group::2: two SMs per 256-query
+ * tile, from D = 2048 up), 0 for one CTA per SM, -1 without a context (reporting aid). */
+int homs_b200_ctx_tensor_cta_pairs(const homs_b200_ctx* ctx);
 int homs_b200_ctx_profile(homs_b200_ctx* ctx, int enable);
 int homs_b200_ctx_kernel_time(homs_b200_ctx* ctx, int which, double* out_total_ms,
                               uint64_t* out_launches);
@@ -304,9 +307,10 @@ int homs_b200_window_bounds(homs_b200_ctx* ctx, uint64_t nq, const double* q_mz,
                             uint64_t* out_first, uint64_t* out_last, uint8_t* out_has_bucket);
 
 /* search_batch, src/search.cpp:171-183, generalised to the k best per query (k = 1 is the
- * reference's search_one; 1 <= k <= HOMS_B200_MAX_TOPK).  The tensor and direct engines keep up to 32
- * candidates per query in one pass and take a second pass, bounded below by the first pass's last key,
- * for 33 <= k <= 64; the POPC engine runs k passes.  Entry j of query i: out_raw_score[i*k+j] (Hamming similarity) and
+ * reference's search_one; 1 <= k <= HOMS_B200_MAX_TOPK).  The tensor engine serves any k in ONE pass over the
+ * library (candidates at or above a per-query floor are buffered, the k best selected exactly afterwards); the
+ * direct engine keeps up to 32 candidates per query in registers and takes a second pass, bounded below by the
+ * first pass's last key, for 33 <= k <= 64; the POPC engine runs k passes.  Entry j of query i: out_raw_score[i*k+j] (Hamming similarity) and
  * out_ordinal[i*k+j] (input position of the library entry; HOMS_B200_NO_HIT and score 0 when
  * fewer than j+1 candidates exist).  out_first / out_last (nullable) as in window_bounds.
  * The library must be whole behind this handle (one device, or a multi-device context); a context

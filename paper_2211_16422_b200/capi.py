@@ -87,6 +87,7 @@ ctx_synchronize = _decl("homs_b200_ctx_synchronize", _I, [_VP])
 ctx_launch_count = _decl("homs_b200_ctx_launch_count", _U64, [_VP])
 ctx_set_engine = _decl("homs_b200_ctx_set_engine", _I, [_VP, _I])
 ctx_last_engine = _decl("homs_b200_ctx_last_engine", _I, [_VP])
+ctx_tensor_cta_pairs = _decl("homs_b200_ctx_tensor_cta_pairs", _I, [_VP])
 ENGINE_AUTO, ENGINE_POPC, ENGINE_TENSOR, ENGINE_TENSOR_FP4, ENGINE_DIRECT = 0, 1, 2, 3, 4
 ctx_profile = _decl("homs_b200_ctx_profile", _I, [_VP, _I])
 ctx_kernel_time = _decl("homs_b200_ctx_kernel_time", _I, [_VP, _I, _P(_F64), _P(_U64)])

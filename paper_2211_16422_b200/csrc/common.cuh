@@ -221,6 +221,7 @@ uint32_t tc_max_topk();
 bool tc_available(const homs_b200_ctx* ctx);
 int tc_peak_probe(homs_b200_ctx* ctx, double seconds, double* out_ops_per_s, double* out_ms);
 int tc_query_pair_ctas(homs_b200_ctx* ctx);
+bool tc_uses_pairs(const homs_b200_ctx* ctx);  // CTA pairs (cta_group::2) for the resident library?
 
 // dense host rows (W words) -> padded device rows (S words), zero padded.  Async on ctx->stream.
 int upload_rows(homs_b200_ctx* ctx, uint64_t* d_dst, const uint64_t* h_src, uint64_t n, uint32_t W,

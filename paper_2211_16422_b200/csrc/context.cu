@@ -222,6 +222,7 @@ int homs_b200_ctx_set_engine(homs_b200_ctx* ctx, int engine) {
 }
 
 int homs_b200_ctx_last_engine(const homs_b200_ctx* ctx) { return ctx ? ctx->last_engine : -1; }
+int homs_b200_ctx_tensor_cta_pairs(const homs_b200_ctx* ctx) { return ctx ? (hb::tc_uses_pairs(ctx) ? 1 : 0) : -1; }
 
 int homs_b200_ctx_synchronize(homs_b200_ctx* ctx) {
   if (!ctx) return HOMS_B200_ERR_ARGUMENT;

@@ -1,4 +1,5 @@
-// Tensor-core engine of the windowed Hamming top-k search (k <= 16) (sm_100a: tcgen05 + TMEM + bulk copies).
+// Tensor-core engine of the windowed Hamming top-k search (k <= 64) (sm_100a: tcgen05 + TMEM + bulk copies,
+// CTA pairs / cta_group::2 from D = 2048 up).
 //
 // Reference semantics are those of search.cu (search.cpp:93-169): per query the candidate row with
 // the largest Hamming similarity inside its precursor window, ties broken by (|q - r|, id, ordinal).
@@ -23,11 +24,13 @@
 // * queries are sorted by window start (search.cu) and cut into tiles of 128 = the 128 TMEM lanes;
 //   the library rows a tile needs (union of its windows) are cut into N-row MMA tiles aligned to
 //   absolute multiples of N, so that different query tiles fetch identical blocks (L2 hits).
-// * one CTA per SM, 6 warps: warp 0 draws work items and issues the bulk copies, one thread of
-//   warp 1 issues the MMAs (4 per stage) into one of two 128 x N accumulators in TMEM, warps 2-5
-//   drain the other accumulator: lane = query, column = library row; every thread keeps the
-//   running best (or the k <= 16 best, in registers) of its query with the exact 3-level key and
-//   masks columns outside the query's own window.  The drain overlaps with the next tile's MMAs.
+// * one CTA per SM, 6 warps: one (elected) thread of warp 0 draws work items and issues the bulk copies, one
+//   thread of warp 1 issues the MMAs (4 per stage) into one of two 128 x N accumulators in TMEM, warps 2-5
+//   drain the other accumulator: lane = query, column = library row; every thread keeps the running best of
+//   its query with the exact 3-level key (top-k: appends the candidates above the query's floor to a buffer,
+//   tc_select_kernel picks the k best exactly) and masks columns outside the query's own window.  The drain
+//   overlaps with the next tile's MMAs.  From D = 2048 up two CTAs of a cluster pair up on 256-query tiles
+//   (cta_group::2, TcShape<true>): each streams its own queries and half of every library tile.
 // * work items (query tile x strip of row tiles) are planned on the device (tc_plan_*_kernel),
 //   ordered (group of query tiles, strip, tile) and handed out dynamically in that order, so that
 //   the CTAs running at any moment share both query and row tiles in L2; the whole search is
@@ -213,9 +216,13 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
 __device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
-__device__ __forceinline__ void st_remote_v4(uint32_t cluster_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "r"(a), "r"(b), "r"(c), "r"(d)
-               : "memory");
+__device__ __forceinline__ void st_remote_b64(uint32_t cluster_addr, uint64_t v) {
+  asm volatile("st.shared::cluster.b64 [%0], %1;" ::"r"(cluster_addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_shared_volatile_b64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+  return v;
 }
 __device__ __forceinline__ uint4 ld_shared_volatile_v4(uint32_t addr) {
   uint4 v;
@@ -638,7 +645,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   auto pfull_bar = [&](int s) { return bar0 + ibar_off + 8u * (2 * kItemQ + s); };  // pair: the peer's stage s is full
   constexpr uint32_t item_off = (ibar_off + 8u * (2 * kItemQ + kStages) + 15u) & ~15u;
   static_assert(item_off + 16 * kItemQ <= kTcBarBytes, "barrier block too small");
-  // one FIFO entry: {item id or kNone, tile, row_begin, row_end}
   volatile uint32_t* s_item = reinterpret_cast<volatile uint32_t*>(gen_base + kStages * Shape::StageBytes + item_off);
   const uint32_t s_item_addr = bar0 + item_off;
 
@@ -701,25 +707,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     if (kPair && rank != 0) mbar_arrive_remote_relaxed(mapa_u32(iempty_bar(s), 0));
     else mbar_arrive(iempty_bar(s));
   };
-  // One FIFO entry = 16 bytes {item id or kNone, tile | seq << 16, row_begin, row_end}, seq = number of the hand-out
-  // (mod 2^16).  In the leader's own CTA the entry is ordinary shared memory behind an mbarrier.  The peer's copy is
-  // written through DSMEM with ONE 16-byte store followed by a relaxed remote arrive -- no cluster-scope fence on
-  // either side (a release / acquire pair at cluster scope is a MEMBAR.ALL.GPU plus an L1 invalidate per item and
-  // waiting thread, on the producers' critical path).  Should the arrive ever overtake the store, the reader sees
-  // the previous occupant of the slot, whose seq differs, and re-reads until the entry of this hand-out is there.
+  // One FIFO entry = 16 bytes {item id or kNone, tile, row_begin, row_end}: ordinary shared memory behind an
+  // mbarrier in the CTA that draws the items.  The PEER's copy of the FIFO carries 8 bytes per slot, {item id,
+  // hand-out number}, written through DSMEM with ONE 64-bit store (single-copy atomic) followed by a relaxed remote
+  // arrive -- no cluster-scope fence on either side (a release / acquire pair at cluster scope is a
+  // MEMBAR.ALL.GPU plus an L1 invalidate per item and waiting thread, on the producers' critical path).  Should the
+  // arrive overtake the store (it does), the reader sees the slot's previous occupant, whose hand-out number
+  // differs, and re-reads until the entry of this hand-out is there; the item itself it then loads from the plan.
   auto read_item = [&](int s, uint32_t parity, uint32_t seq, uint32_t& item, TcItem& it) {
     mbar_wait(ifull_bar(s), parity);
-    uint4 e = ld_shared_volatile_v4(s_item_addr + 16u * s);
-    if constexpr (kPair) {
-      while ((e.y >> 16) != (seq & 0xFFFFu)) e = ld_shared_volatile_v4(s_item_addr + 16u * s);
+    if (kPair && rank != 0) {
+      uint64_t e = ld_shared_volatile_b64(s_item_addr + 16u * s);
+      while (static_cast<uint32_t>(e >> 32) != seq) e = ld_shared_volatile_b64(s_item_addr + 16u * s);
+      item = static_cast<uint32_t>(e);
+      it = item != kNone ? p.items[item] : TcItem{0, 0, 0, 0};
+    } else {
+      const uint4 e = ld_shared_volatile_v4(s_item_addr + 16u * s);
+      item = e.x;
+      it.tile = e.y;
+      it.row_begin = e.z;
+      it.row_end = e.w;
+      it.pad = 0;
     }
-    item = e.x;
-    it.tile = e.y & 0xFFFFu;
-    it.row_begin = e.z;
-    it.row_end = e.w;
-    it.pad = 0;
   };
-  static_assert(kTcBatch / kTcM <= 0xFFFF, "tile ids share a word with the hand-out number");
 
   if (warp == 0) {
     // ===== producer: two bulk copies per stage =====
@@ -745,15 +755,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           mbar_wait(iempty_bar(qslot), qphase ^ 1u);
           if (item < n_items) it = p.items[item];
           const uint32_t id = item < n_items ? item : kNone;
-          const uint32_t w1 = it.tile | (iseq << 16);
           volatile uint32_t* e = s_item + 4 * qslot;
           e[0] = id;
-          e[1] = w1;
+          e[1] = it.tile;
           e[2] = it.row_begin;
           e[3] = it.row_end;
           mbar_arrive(ifull_bar(qslot));
           if constexpr (kPair) {
-            st_remote_v4(mapa_u32(s_item_addr + 16u * qslot, 1), id, w1, it.row_begin, it.row_end);
+            st_remote_b64(mapa_u32(s_item_addr + 16u * qslot, 1), (uint64_t(iseq) << 32) | id);
             mbar_arrive_remote_relaxed(mapa_u32(ifull_bar(qslot), 1));
           }
         } else {  // the pair's second CTA follows the leader's FIFO
@@ -1353,11 +1362,14 @@ struct TcBatch {
 
 // CTA pairs (TcShape<true>, cta_group::2) or one CTA per SM?  A pair moves a third fewer operand bytes per MMA
 // (L2 -> shared memory and shared memory -> tensor core), which under the board's power cap is SM clock (+5 %), and
-// its ring is 7 stages deep instead of 5; it pays with cross-CTA hand-offs per work item and row tile.  Interleaved
-// A/B on one box (profiles/r02_ab_cta_pair_v2.log): D = 16384 -4.7 %, config-3 prefix -3.4 %, config 2 (D = 8192)
-// -2.3 %, D = 1024 +4.8 % -- so pairs serve D >= kTcPairMinDim when the device co-schedules a 2-CTA cluster on
-// every SM pair (HOMS_B200_TC_PAIR=0 / 1 forces either form).
-constexpr uint32_t kTcPairMinKc = 32;  // k-chunks of 256 dimensions: D >= 8192
+// its ring is 7 stages deep instead of 5 (ncu: tensor pipe 99.6 % active against 95.7 %); it pays with cross-CTA
+// hand-offs per work item and row tile.  Interleaved A/B on one box (profiles/r02_ab_cta_pair_v2.log,
+// r02_ab_cta_pair_threshold.log): D = 16384 -4.7 %, config-3 prefix -3.4 % (-7 % at D = 2048), config 2 -1.5 ... -2.3 %,
+// D = 4096 -2 ... -6 %, D = 2048 -4 %, D = 1024 +4.8 % -- so pairs serve D >= 2048 when the device co-schedules a
+// 2-CTA cluster on every SM pair (HOMS_B200_TC_PAIR=0 / 1 forces either form).
+static bool tc_use_pair(const homs_b200_ctx* ctx);
+constexpr uint32_t kTcPairMinKc = 8;  // k-chunks of 256 dimensions: D >= 2048
+bool tc_uses_pairs(const homs_b200_ctx* ctx) { return tc_use_pair(ctx); }
 static bool tc_use_pair(const homs_b200_ctx* ctx) {
   if (ctx->knobs.pair == 0 || ctx->tc_pair_ctas < 2) return false;
   if (ctx->knobs.pair == 1) return true;

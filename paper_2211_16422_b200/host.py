@@ -297,6 +297,10 @@ class Context:
                 "tensor_fp4": capi.ENGINE_TENSOR_FP4, "direct": capi.ENGINE_DIRECT}.get(engine, engine)
         _check(capi.ctx_set_engine(self._h, int(code)), self._h)
 
+    def tensor_cta_pairs(self) -> bool:
+        """True when the tensor engine searches the resident library on CTA pairs (cta_group::2)."""
+        return int(capi.ctx_tensor_cta_pairs(self._h)) == 1
+
     def last_engine(self) -> str:
         """Engine the last search call ran on: "popc", "tensor", "tensor_fp4" or "direct"."""
         return {capi.ENGINE_POPC: "popc", capi.ENGINE_TENSOR: "tensor", capi.ENGINE_TENSOR_FP4: "tensor_fp4",

@@ -556,10 +556,10 @@ def test_index_order_at_sort_tile_boundaries(hb, port, n):
     oix.close()
 
 
-@pytest.mark.parametrize("form,dim", [("pair", 256), ("pair", 2048), ("single", 8192)])
+@pytest.mark.parametrize("form,dim", [("pair", 256), ("pair", 1024), ("single", 2048), ("single", 8192)])
 def test_tensor_kernel_forms_vs_port(hb, port, monkeypatch, form, dim):
     """Both forms of the tensor search kernel whatever the dimension: one CTA per SM (M = 128 tiles) and CTA pairs
-    (cta_group::2, M = 256 tiles over a 2-CTA cluster, default from D = 8192 up).  An odd number of 128-query
+    (cta_group::2, M = 256 tiles over a 2-CTA cluster, default from D = 2048 up).  An odd number of 128-query
     tiles (the pair's second half is empty), several planning tiles, top-1, collected top-k, the register-list
     passes and a sharded group -- against the full-sort oracle."""
     monkeypatch.setenv("HOMS_B200_TC_PAIR", "1" if form == "pair" else "0")
