@@ -26,31 +26,37 @@ constexpr int kRadixPerLane = 16;
 constexpr uint32_t kRadixChunk = 32 * kRadixPerLane;       // elements per warp
 constexpr uint32_t kRadixTile = kRadixChunk * kRadixWarps;  // elements per CTA
 
-// shift_mask = shift | (digit mask << 8): the last pass of a bit range may be narrower than 8 bits
-template <typename K>
+// shift_mask = shift | (digit mask << 8): the last pass of a bit range may be narrower than 8 bits.
+// kSum (64-bit keys only): the pairs are ordered by (high half + low half) of the key instead of the key itself --
+// the search orders its queries by window start + window end (search.cu).
+template <typename K, bool kSum>
 __device__ __forceinline__ uint32_t radix_digit(K key, int shift_mask) {
+  if constexpr (kSum) {
+    const uint64_t v = (static_cast<uint64_t>(key) >> 32) + (static_cast<uint64_t>(key) & 0xFFFFFFFFull);
+    return static_cast<uint32_t>(v >> (shift_mask & 0xFF)) & static_cast<uint32_t>(shift_mask >> 8);
+  }
   return static_cast<uint32_t>(key >> (shift_mask & 0xFF)) & static_cast<uint32_t>(shift_mask >> 8);
 }
 
 // counts of this warp's chunk into its private row of s_cnt (zeroed by the caller)
-template <typename K>
+template <typename K, bool kSum>
 __device__ __forceinline__ void radix_count_chunk(const K* __restrict__ keys, uint64_t n, uint64_t chunk0, int shift,
                                                   uint32_t* s_row, int lane) {
 #pragma unroll 4
   for (int j = 0; j < kRadixPerLane; ++j) {
     const uint64_t i = chunk0 + uint64_t(j) * 32 + lane;
-    if (i < n) atomicAdd(&s_row[radix_digit(keys[i], shift)], 1u);
+    if (i < n) atomicAdd(&s_row[radix_digit<K, kSum>(keys[i], shift)], 1u);
   }
 }
 
-template <typename K>
+template <typename K, bool kSum>
 __global__ void __launch_bounds__(kRadixThreads)
 radix_hist_kernel(const K* __restrict__ keys, uint64_t n, int shift, uint32_t n_tiles, uint32_t* __restrict__ hist) {
   __shared__ uint32_t s_cnt[256];
   s_cnt[threadIdx.x] = 0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  radix_count_chunk(keys, n, uint64_t(blockIdx.x) * kRadixTile + uint64_t(warp) * kRadixChunk, shift, s_cnt, lane);
+  radix_count_chunk<K, kSum>(keys, n, uint64_t(blockIdx.x) * kRadixTile + uint64_t(warp) * kRadixChunk, shift, s_cnt, lane);
   __syncthreads();
   hist[uint64_t(threadIdx.x) * n_tiles + blockIdx.x] = s_cnt[threadIdx.x];
 }
@@ -159,7 +165,7 @@ int exclusive_sum(homs_b200_ctx* ctx, const T* d_in, T* d_out, uint64_t n, void*
 template int exclusive_sum<uint32_t>(homs_b200_ctx*, const uint32_t*, uint32_t*, uint64_t, void*);
 template int exclusive_sum<uint64_t>(homs_b200_ctx*, const uint64_t*, uint64_t*, uint64_t, void*);
 
-template <typename K>
+template <typename K, bool kSum>
 __global__ void __launch_bounds__(kRadixThreads)
 radix_scatter_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, K* __restrict__ keys_out,
                      uint32_t* __restrict__ vals_out, uint64_t n, int shift, uint32_t n_tiles,
@@ -170,7 +176,7 @@ radix_scatter_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__
   for (int w = 0; w < kRadixWarps; ++w) s_cnt[w][threadIdx.x] = 0;
   __syncthreads();
   const uint64_t chunk0 = uint64_t(blockIdx.x) * kRadixTile + uint64_t(warp) * kRadixChunk;
-  radix_count_chunk(keys_in, n, chunk0, shift, s_cnt[warp], lane);
+  radix_count_chunk<K, kSum>(keys_in, n, chunk0, shift, s_cnt[warp], lane);
   __syncthreads();
   {
     uint32_t run = offs[uint64_t(threadIdx.x) * n_tiles + blockIdx.x];  // thread = digit
@@ -192,7 +198,7 @@ radix_scatter_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__
       key = keys_in[i];
       val = vals_in ? vals_in[i] : static_cast<uint32_t>(i);
     }
-    const uint32_t d = live ? radix_digit(key, shift) : 256u;  // dead lanes form their own group
+    const uint32_t d = live ? radix_digit<K, kSum>(key, shift) : 256u;  // dead lanes form their own group
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
     const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
     if (live) {
@@ -211,9 +217,9 @@ size_t radix_temp_bytes(uint64_t n) {
   return static_cast<size_t>(std::max<uint64_t>(1, tiles)) * 256 * sizeof(uint32_t);
 }
 
-template <typename K>
-int radix_sort_pairs(homs_b200_ctx* ctx, K* keys_a, K* keys_b, uint32_t* vals_a, uint32_t* vals_b, uint64_t n,
-                     int begin_bit, int end_bit, void* d_temp, bool first_vals_iota, bool* result_in_b) {
+template <typename K, bool kSum>
+static int radix_sort_impl(homs_b200_ctx* ctx, K* keys_a, K* keys_b, uint32_t* vals_a, uint32_t* vals_b, uint64_t n,
+                           int begin_bit, int end_bit, void* d_temp, bool first_vals_iota, bool* result_in_b) {
   *result_in_b = false;
   if (n == 0 || end_bit <= begin_bit) return HOMS_B200_OK;
   HB_REQUIRE(ctx, n <= 0xFFFFFFFFull, HOMS_B200_ERR_ARGUMENT, "radix sort: more than 2^32-1 items");
@@ -224,11 +230,11 @@ int radix_sort_pairs(homs_b200_ctx* ctx, K* keys_a, K* keys_b, uint32_t* vals_a,
   bool iota = first_vals_iota;
   for (int bit = begin_bit; bit < end_bit; bit += 8) {
     const int shift = bit | (((1 << std::min(8, end_bit - bit)) - 1) << 8);
-    radix_hist_kernel<K><<<tiles, kRadixThreads, 0, ctx->stream>>>(kin, n, shift, tiles, hist);
+    radix_hist_kernel<K, kSum><<<tiles, kRadixThreads, 0, ctx->stream>>>(kin, n, shift, tiles, hist);
     HB_LAUNCHED(ctx);
     radix_scan_kernel<<<1, 1024, 0, ctx->stream>>>(hist, uint64_t(tiles) * 256);
     HB_LAUNCHED(ctx);
-    radix_scatter_kernel<K><<<tiles, kRadixThreads, 0, ctx->stream>>>(kin, iota ? nullptr : vin, kout, vout, n, shift,
+    radix_scatter_kernel<K, kSum><<<tiles, kRadixThreads, 0, ctx->stream>>>(kin, iota ? nullptr : vin, kout, vout, n, shift,
                                                                        tiles, hist);
     HB_LAUNCHED(ctx);
     iota = false;
@@ -239,6 +245,16 @@ int radix_sort_pairs(homs_b200_ctx* ctx, K* keys_a, K* keys_b, uint32_t* vals_a,
   return HOMS_B200_OK;
 }
 
+template <typename K>
+int radix_sort_pairs(homs_b200_ctx* ctx, K* keys_a, K* keys_b, uint32_t* vals_a, uint32_t* vals_b, uint64_t n,
+                     int begin_bit, int end_bit, void* d_temp, bool first_vals_iota, bool* result_in_b) {
+  return radix_sort_impl<K, false>(ctx, keys_a, keys_b, vals_a, vals_b, n, begin_bit, end_bit, d_temp, first_vals_iota,
+                                   result_in_b);
+}
+int radix_sort_pairs_by_half_sum(homs_b200_ctx* ctx, uint64_t* keys_a, uint64_t* keys_b, uint32_t* vals_a,
+                                 uint32_t* vals_b, uint64_t n, int end_bit, void* d_temp, bool* result_in_b) {
+  return radix_sort_impl<uint64_t, true>(ctx, keys_a, keys_b, vals_a, vals_b, n, 0, end_bit, d_temp, false, result_in_b);
+}
 template int radix_sort_pairs<uint8_t>(homs_b200_ctx*, uint8_t*, uint8_t*, uint32_t*, uint32_t*, uint64_t, int, int,
                                        void*, bool, bool*);
 template int radix_sort_pairs<uint32_t>(homs_b200_ctx*, uint32_t*, uint32_t*, uint32_t*, uint32_t*, uint64_t, int, int,

@@ -20,6 +20,10 @@ template <typename K>
 int radix_sort_pairs(homs_b200_ctx* ctx, K* keys_a, K* keys_b, uint32_t* vals_a, uint32_t* vals_b, uint64_t n,
                      int begin_bit, int end_bit, void* d_temp, bool first_vals_iota, bool* result_in_b);
 
+// The same for 64-bit keys ordered by (high 32 bits + low 32 bits), bits [0, end_bit) of that sum.
+int radix_sort_pairs_by_half_sum(homs_b200_ctx* ctx, uint64_t* keys_a, uint64_t* keys_b, uint32_t* vals_a,
+                                 uint32_t* vals_b, uint64_t n, int end_bit, void* d_temp, bool* result_in_b);
+
 // Device-wide exclusive prefix sum of n entries (T = uint32_t or uint64_t; in != out), stream-ordered.
 size_t exclusive_sum_temp_bytes(uint64_t n);
 template <typename T>

@@ -10,7 +10,8 @@
 // Pipeline of one search call (all on the context's stream, no host round trip):
 //   1. bounds_kernel      K3: per query, two binary searches of the exact fp64 predicates
 //                         (q - r > w) and (r - q > w) over the bucket's sorted precursor m/z.
-//   2. radix sort         queries ordered by window start, so neighbours share reference rows.
+//   2. radix sort         queries ordered by window start + end (= by precursor m/z inside a bucket), so
+//                         neighbours share reference rows and a tile of queries has a tight union window.
 //   3. plan_*_kernel      groups QB consecutive queries into a block, takes the union of their
 //                         windows, cuts it into row chunks -> work items (device-side, no sync).
 //   4. search_kernel      K4: persistent CTAs pull work items from an atomic counter.  A CTA
@@ -774,7 +775,7 @@ int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n,
   const bool tensor_ok = ctx->engine != HOMS_B200_ENGINE_POPC && ctx->engine != HOMS_B200_ENGINE_DIRECT && tc_available(ctx);
   const bool use_direct = ctx->engine == HOMS_B200_ENGINE_DIRECT ||
                           (ctx->engine == HOMS_B200_ENGINE_AUTO && tensor_ok && direct_is_cheaper(ctx, n, tol));
-  // Sort the slots by window start (upper 32 key bits): neighbours then share library rows on chip.
+  // Sort the slots by window position: neighbours then share library rows on chip.
   // The direct engine skips it when the windows are so sparse that neighbours would share nothing
   // anyway (expected rows read < rows resident: every row comes from HBM once either way).
   const bool sparse = use_direct && expected_window_rows(lib, tol) * static_cast<double>(n) < static_cast<double>(lib.n);
@@ -783,16 +784,20 @@ int search_dev_locked(homs_b200_ctx* ctx, const uint32_t* d_subset, uint64_t n,
   if (!sparse) {
     HB_TRY(ensure(ctx, ctx->scratch[kScrKeysAlt], n * 8));
     HB_TRY(ensure(ctx, ctx->scratch[kScrValsAlt], n * 4));
-    // key = window start << 32 | window end; a slot without a window carries ~0.  Starts are local rows
-    // (<= n_local), so only the low bits of the upper half can differ -- and an all-ones start still
-    // sorts last when truncated to them, as long as it is above every real start.
+    // key = window start << 32 | window end; a slot without a window carries ~0.  The slots are ordered by
+    // start + end: inside a charge bucket that is the order of the precursor m/z, so BOTH ends of the windows of
+    // neighbouring slots are close and the union window of a query tile stays tight (ordering by the start alone
+    // left the ends of all the queries whose window begins at the bucket's first row in input order: 4.2 % of the
+    // tensor engine's MMA work was masked columns on config 2, 1.1 % now; 5.5 % -> 2.8 % with 256-query tiles).
+    // Sums are below 2 x n_local; the all-ones key of a slot without a window sums to 2^33 - 2 and still sorts last
+    // when truncated to `bits` bits, as long as 2^bits - 2 is above every real sum.
     int bits = 8;
-    while (bits < 32 && ((uint64_t(1) << bits) - 1) <= lib.n_local) bits += 8;
+    while (bits < 40 && ((uint64_t(1) << bits) - 2) <= 2 * lib.n_local) bits += 8;
     HB_TRY(ensure(ctx, ctx->scratch[kScrCub], radix_temp_bytes(n)));
     bool in_b = false;
-    HB_TRY(radix_sort_pairs<uint64_t>(ctx, ctx->scratch[kScrKeys].as<uint64_t>(), ctx->scratch[kScrKeysAlt].as<uint64_t>(),
-                                      ctx->scratch[kScrVals].as<uint32_t>(), ctx->scratch[kScrValsAlt].as<uint32_t>(), n,
-                                      32, 32 + bits, ctx->scratch[kScrCub].p, false, &in_b));
+    HB_TRY(radix_sort_pairs_by_half_sum(ctx, ctx->scratch[kScrKeys].as<uint64_t>(), ctx->scratch[kScrKeysAlt].as<uint64_t>(),
+                                        ctx->scratch[kScrVals].as<uint32_t>(), ctx->scratch[kScrValsAlt].as<uint32_t>(), n,
+                                        bits, ctx->scratch[kScrCub].p, &in_b));
     if (in_b) {
       keys = ctx->scratch[kScrKeysAlt].as<uint64_t>();
       vals = ctx->scratch[kScrValsAlt].as<uint32_t>();

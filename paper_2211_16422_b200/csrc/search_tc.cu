@@ -21,7 +21,7 @@
 //   two cp.async.bulk copies (no tensor map needed) completing on an mbarrier.  Operands are e2m1
 //   nibbles (kind::mxf4 with unit block scales, 256 dimensions per row, N = 224, 5 stages); the
 //   int8 encoding of round 1 (kind::i8: twice the bytes, half the rate, same results) was removed.
-// * queries are sorted by window start (search.cu) and cut into tiles of 128 = the 128 TMEM lanes;
+// * queries are sorted by window start + end (search.cu) and cut into tiles of 128 = the 128 TMEM lanes;
 //   the library rows a tile needs (union of its windows) are cut into N-row MMA tiles aligned to
 //   absolute multiples of N, so that different query tiles fetch identical blocks (L2 hits).
 // * one CTA per SM, 6 warps: one (elected) thread of warp 0 draws work items and issues the bulk copies, one
