@@ -103,6 +103,7 @@ struct TcKnobs {
   uint32_t l2_hints = 2;  // see TcParams::l2_hints (default: library tiles evict_first)
   uint32_t topk_lists = 0;  // top-k path: 0 / 2 = collect + select (default), 1 = register-list passes
   uint32_t ccap = 0;        // collect mode: candidate buffer entries per query (0: built-in)
+  uint32_t ares = 1;        // 0: never keep the query tile's k-chunks resident in shared memory (HOMS_B200_TC_ARES)
   uint32_t debug = 0;       // 1: development statistics on stderr (HOMS_B200_TC_DEBUG)
   uint32_t pair = 2;        // tensor search on CTA pairs (cta_group::2, search_tc.cu TcShape<true>): 0 never, 1 always, 2 by dimension
 };

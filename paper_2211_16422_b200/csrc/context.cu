@@ -140,6 +140,7 @@ int ctx_create_single(int device, homs_b200_ctx** out) {
     ctx->knobs.topk_lists = std::string(e) == "lists" ? 1u : (std::string(e) == "collect" ? 2u : 0u);
   if (const char* e = getenv("HOMS_B200_TC_L2_HINTS")) ctx->knobs.l2_hints = static_cast<uint32_t>(atoi(e)) & 3u;
   ctx->knobs.debug = env_u32("HOMS_B200_TC_DEBUG");
+  if (const char* e = getenv("HOMS_B200_TC_ARES")) ctx->knobs.ares = atoi(e) != 0 ? 1u : 0u;
   if (const char* e = getenv("HOMS_B200_TC_PAIR")) ctx->knobs.pair = atoi(e) != 0 ? 1u : 0u;
   ctx->tc_pair_ctas = ctx->knobs.pair ? tc_query_pair_ctas(ctx) : 0;
   *out = ctx;

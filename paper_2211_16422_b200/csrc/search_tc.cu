@@ -75,17 +75,30 @@ struct TcMode {
 // with M = 256; each holds its own 128 query rows and HALF of the library tile (A 16 KB + B 14 KB, 7 stages):
 // a third fewer bytes from L2 per MMA and a third fewer shared-memory operand reads, which under the board's
 // power cap is clock.
-template <bool kPair>
+// kARes (single CTA, D <= 1024): the query tile's k-chunks (<= 4 x 16 KB) are loaded ONCE per work item into a
+// resident area and only the library tiles stream through the ring -- at D = 1024 every row tile re-fetched the same
+// four A chunks, 36 % of the operand bytes, and the kernel was bound by the L2 -> SM fills (ncu: lts throughput 82 %,
+// 20 TB/s of fills, tensor pipe 75 % active).
+constexpr uint32_t kTcAResChunks = 4;
+template <bool kPair, bool kARes = false>
 struct TcShape {
+  static_assert(!(kPair && kARes), "the resident-A form is a single-CTA form");
   static constexpr int BRows = kPair ? TcMode::N / 2 : TcMode::N;
   static constexpr uint32_t BBytes = BRows * kTcKB;
-  static constexpr uint32_t StageBytes = kTcABytes + BBytes;  // multiple of 1024
+  static constexpr uint32_t StageBytes = (kARes ? 0u : kTcABytes) + BBytes;  // multiple of 1024
+  static constexpr uint32_t AOff = kARes ? 0u : 0u;                            // A inside a stage (streamed forms)
+  static constexpr uint32_t BOff = kARes ? 0u : kTcABytes;                     // B inside a stage
+  static constexpr uint32_t ResBytes = kARes ? kTcAResChunks * kTcABytes : 0u;  // resident A area in front of the ring
   static constexpr int Stages = kPair ? 7 : TcMode::Stages;
-  static constexpr uint32_t SmemBytes = Stages * StageBytes + 1024 + kTcBarBytes;
+  static constexpr uint32_t SmemBytes = ResBytes + Stages * StageBytes + 1024 + kTcBarBytes;
   static constexpr uint32_t TileQ = kPair ? 2 * kTcM : kTcM;  // sorted positions per planning tile
 };
-static_assert(TcShape<true>::StageBytes % 1024 == 0 && TcShape<false>::StageBytes % 1024 == 0, "stage alignment");
-static_assert(TcShape<true>::SmemBytes <= 227 * 1024 && TcShape<false>::SmemBytes <= 227 * 1024, "shared memory");
+static_assert(TcShape<true>::StageBytes % 1024 == 0 && TcShape<false>::StageBytes % 1024 == 0 &&
+                  TcShape<false, true>::StageBytes % 1024 == 0,
+              "stage alignment");
+static_assert(TcShape<true>::SmemBytes <= 227 * 1024 && TcShape<false>::SmemBytes <= 227 * 1024 &&
+                  TcShape<false, true>::SmemBytes <= 227 * 1024,
+              "shared memory");
 constexpr uint32_t kTcGroupTiles = 12;  // query tiles per L2 group, at least
 constexpr int kTcMaxK = 32;             // top-k depth the drain keeps per query in ONE pass; larger k runs
                                         // ceil(k / 32) passes, each bounded below by the previous pass's last key
@@ -609,23 +622,25 @@ struct TcAcc {
 // full" (peer -> leader, relayed by the peer's otherwise idle warp 1), "accumulator drained" and "item slot
 // free" (peer -> leader, remote arrives); "stage free" and "accumulator complete" reach both CTAs through the
 // multicast form of tcgen05.commit.
-template <int KM, bool kPair>
+template <int KM, bool kPair, bool kARes>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams p) {
   constexpr bool kTopK = KM > 1;      // register lists of depth KM
   constexpr bool kCollect = KM == 0;  // append candidates above the floor, select exactly afterwards
   constexpr int kList = KM > 0 ? KM : 1;
   using Mode = TcMode;
-  using Shape = TcShape<kPair>;
+  using Shape = TcShape<kPair, kARes>;
   using Acc = TcAcc;
   using AccT = typename Acc::T;
   constexpr int kN = Mode::N;
   constexpr int kStages = Shape::Stages;
   extern __shared__ unsigned char tc_smem_raw[];
   const uint32_t raw = smem_u32(tc_smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-byte alignment
+  const uint32_t res_base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-byte alignment
+  const uint32_t base = res_base + Shape::ResBytes;  // the ring; the resident A area (kARes) sits in front of it
   unsigned char* gen_base = tc_smem_raw + (base - raw);
   const uint32_t bar0 = base + kStages * Shape::StageBytes;
-  // barrier block: full[S], empty[S], tfull[2], tempty[2], TMEM base address, ifull[Q], iempty[Q], pfull[S], items[Q]
+  // barrier block: full[S], empty[S], tfull[2], tempty[2], TMEM base address, ifull[Q], iempty[Q], pfull[S], items[Q],
+  // afull, aempty (kARes: the resident A area is loaded / may be overwritten)
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
   auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kStages + a); };
@@ -644,7 +659,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
   auto iempty_bar = [&](int s) { return bar0 + ibar_off + 8u * (kItemQ + s); };
   auto pfull_bar = [&](int s) { return bar0 + ibar_off + 8u * (2 * kItemQ + s); };  // pair: the peer's stage s is full
   constexpr uint32_t item_off = (ibar_off + 8u * (2 * kItemQ + kStages) + 15u) & ~15u;
-  static_assert(item_off + 16 * kItemQ <= kTcBarBytes, "barrier block too small");
+  static_assert(item_off + 16 * kItemQ + 16 <= kTcBarBytes, "barrier block too small");
+  const uint32_t afull_bar = bar0 + item_off + 16u * kItemQ, aempty_bar = afull_bar + 8u;
   volatile uint32_t* s_item = reinterpret_cast<volatile uint32_t*>(gen_base + kStages * Shape::StageBytes + item_off);
   const uint32_t s_item_addr = bar0 + item_off;
 
@@ -670,6 +686,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), kPair ? 8 : 4);  // one arrival per drain warp (of both CTAs)
     }
+    mbar_init(afull_bar, 1);
+    mbar_init(aempty_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -784,6 +802,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
         const uint8_t* b_src = lib_x + (uint64_t(it.row_begin) + uint64_t(rank) * Shape::BRows) * kTcKB;
         // (An L2 prefetch of the next row tile's library block, cp.async.bulk.prefetch.L2 one k-chunk per stage by
         // every query tile or by one in eight, was measured 11-16 % SLOWER: profiles/r02_ab_l2_prefetch.log.)
+        if constexpr (kARes) {  // the item's query chunks, once: when the previous item's MMAs have read theirs
+          mbar_wait(aempty_bar, iseq & 1u);  // iseq = item number + 1: passes at once for the first item
+          mbar_expect_tx(afull_bar, n_kc * kTcABytes);
+          const uint8_t* ap = a_src;
+          for (uint32_t kc = 0; kc < n_kc; ++kc, ap += a_step)
+            bulk_g2s_hint(res_base + kc * kTcABytes, ap, kTcABytes, afull_bar, pol_a);
+        }
         for (uint32_t nt = 0; nt < n_nt; ++nt, b_src += uint64_t(kN) * kTcKB) {
           const uint8_t* ap = a_src;
           const uint8_t* bp = b_src;
@@ -792,8 +817,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
             const uint32_t sa = base + stage * Shape::StageBytes;
             const uint32_t fb = full_bar(stage);
             mbar_expect_tx(fb, Shape::StageBytes);
-            bulk_g2s_hint(sa, ap, kTcABytes, fb, pol_a);
-            bulk_g2s_hint(sa + kTcABytes, bp, Shape::BBytes, fb, pol_b);
+            if constexpr (!kARes) bulk_g2s_hint(sa, ap, kTcABytes, fb, pol_a);
+            bulk_g2s_hint(sa + Shape::BOff, bp, Shape::BBytes, fb, pol_b);
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1u;
@@ -831,6 +856,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           }
           continue;
         }
+        if constexpr (kARes) mbar_wait(afull_bar, (iseq & 1u) ^ 1u);  // this item's query chunks have landed
         for (uint32_t nt = 0; nt < n_nt; ++nt) {
           mbar_wait(tempty_bar(acc), ((aphase >> acc) & 1u) ^ 1u);  // drain warps released this accumulator
           aphase ^= 1u << acc;
@@ -841,8 +867,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
             if constexpr (kPair) mbar_wait(pfull_bar(stage), phase);  // the peer's share has landed in ITS shared memory
             tc_fence_after();
             const uint32_t sa = base + stage * Shape::StageBytes;
-            const uint64_t adesc = tc_smem_desc(sa);
-            const uint64_t bdesc = tc_smem_desc(sa + kTcABytes);
+            const uint64_t adesc = tc_smem_desc(kARes ? res_base + kc * kTcABytes : sa);
+            const uint64_t bdesc = tc_smem_desc(sa + Shape::BOff);
 #pragma unroll
             for (uint32_t k = 0; k < kTcKB / 32; ++k) {  // +32 bytes along K inside the swizzle atom
               if constexpr (kPair)
@@ -865,6 +891,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
           else tc_commit(tfull_bar(acc));
           acc ^= 1u;
         }
+        if constexpr (kARes) tc_commit(aempty_bar);  // the resident query chunks may be replaced
       }
     }
   } else {
@@ -1357,6 +1384,7 @@ struct TcBatch {
   uint64_t b0 = 0, nb = 0, q_rows = 0;
   uint32_t n_tiles = 0;  // planning tiles: 128 sorted positions each, 256 when CTA pairs run the search
   bool pair = false;
+  bool ares = false;  // single CTAs with the query tile's k-chunks resident in shared memory (D <= 1024)
   TcPlanPtrs pp{};
 };
 
@@ -1454,6 +1482,7 @@ static int tc_prepare_batch(homs_b200_ctx* ctx, const uint32_t* d_subset, const 
   out->q_rows = q_rows;
   out->n_tiles = n_tiles;
   out->pair = pair;
+  out->ares = !pair && lib.n_kc <= kTcAResChunks && ctx->knobs.ares != 0;
   out->pp = tc_plan_layout(d_plan, n_tiles, pc.item_cap);
   return HOMS_B200_OK;
 }
@@ -1470,7 +1499,7 @@ static int tc_launch_search(homs_b200_ctx* ctx, const TcBatch& tb, const TcParam
 #if HB_TC_PAIR
   if (tb.pair) {
     using Shape = TcShape<true>;
-    HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<KM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<KM, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Shape::SmemBytes)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ctx->tc_pair_ctas);
@@ -1484,15 +1513,20 @@ static int tc_launch_search(homs_b200_ctx* ctx, const TcBatch& tb, const TcParam
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    HB_CUDA(ctx, cudaLaunchKernelEx(&cfg, tc_search_kernel<KM, true>, tp));
+    HB_CUDA(ctx, cudaLaunchKernelEx(&cfg, tc_search_kernel<KM, true, false>, tp));
     return HOMS_B200_OK;
   }
 #endif
-  {
-    using Shape = TcShape<false>;
-    HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<KM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (tb.ares) {
+    using Shape = TcShape<false, true>;
+    HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<KM, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Shape::SmemBytes)));
-    tc_search_kernel<KM, false><<<ctx->sm_count, kTcThreads, Shape::SmemBytes, ctx->stream>>>(tp);
+    tc_search_kernel<KM, false, true><<<ctx->sm_count, kTcThreads, Shape::SmemBytes, ctx->stream>>>(tp);
+  } else {
+    using Shape = TcShape<false>;
+    HB_CUDA(ctx, cudaFuncSetAttribute(tc_search_kernel<KM, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Shape::SmemBytes)));
+    tc_search_kernel<KM, false, false><<<ctx->sm_count, kTcThreads, Shape::SmemBytes, ctx->stream>>>(tp);
   }
   return HOMS_B200_OK;
 }
@@ -1504,7 +1538,7 @@ int tc_query_pair_ctas(homs_b200_ctx* ctx) {
   return 0;
 #else
   using Shape = TcShape<true>;
-  if (cudaFuncSetAttribute(tc_search_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(tc_search_kernel<1, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(Shape::SmemBytes)) != cudaSuccess) {
     cudaGetLastError();
     return 0;
@@ -1521,7 +1555,7 @@ int tc_query_pair_ctas(homs_b200_ctx* ctx) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int clusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&clusters, tc_search_kernel<1, true>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&clusters, tc_search_kernel<1, true, false>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
