@@ -22,9 +22,7 @@ namespace hb {
 
 constexpr int kRadixThreads = 256;
 constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kRadixPerLane = 16;
-constexpr uint32_t kRadixChunk = 32 * kRadixPerLane;       // elements per warp
-constexpr uint32_t kRadixTile = kRadixChunk * kRadixWarps;  // elements per CTA
+constexpr int kRadixMaxPerLane = 16;  // a warp's chunk is 32 x per_lane consecutive elements, a CTA's tile 8 chunks
 
 // shift_mask = shift | (digit mask << 8): the last pass of a bit range may be narrower than 8 bits.
 // kSum (64-bit keys only): the pairs are ordered by (high half + low half) of the key instead of the key itself --
@@ -41,9 +39,9 @@ __device__ __forceinline__ uint32_t radix_digit(K key, int shift_mask) {
 // counts of this warp's chunk into its private row of s_cnt (zeroed by the caller)
 template <typename K, bool kSum>
 __device__ __forceinline__ void radix_count_chunk(const K* __restrict__ keys, uint64_t n, uint64_t chunk0, int shift,
-                                                  uint32_t* s_row, int lane) {
+                                                  uint32_t* s_row, int lane, int per_lane) {
 #pragma unroll 4
-  for (int j = 0; j < kRadixPerLane; ++j) {
+  for (int j = 0; j < per_lane; ++j) {
     const uint64_t i = chunk0 + uint64_t(j) * 32 + lane;
     if (i < n) atomicAdd(&s_row[radix_digit<K, kSum>(keys[i], shift)], 1u);
   }
@@ -51,12 +49,14 @@ __device__ __forceinline__ void radix_count_chunk(const K* __restrict__ keys, ui
 
 template <typename K, bool kSum>
 __global__ void __launch_bounds__(kRadixThreads)
-radix_hist_kernel(const K* __restrict__ keys, uint64_t n, int shift, uint32_t n_tiles, uint32_t* __restrict__ hist) {
+radix_hist_kernel(const K* __restrict__ keys, uint64_t n, int shift, uint32_t n_tiles, uint32_t* __restrict__ hist,
+                  int per_lane) {
   __shared__ uint32_t s_cnt[256];
   s_cnt[threadIdx.x] = 0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  radix_count_chunk<K, kSum>(keys, n, uint64_t(blockIdx.x) * kRadixTile + uint64_t(warp) * kRadixChunk, shift, s_cnt, lane);
+  const uint64_t chunk = 32ull * per_lane;
+  radix_count_chunk<K, kSum>(keys, n, (uint64_t(blockIdx.x) * kRadixWarps + warp) * chunk, shift, s_cnt, lane, per_lane);
   __syncthreads();
   hist[uint64_t(threadIdx.x) * n_tiles + blockIdx.x] = s_cnt[threadIdx.x];
 }
@@ -169,14 +169,14 @@ template <typename K, bool kSum>
 __global__ void __launch_bounds__(kRadixThreads)
 radix_scatter_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, K* __restrict__ keys_out,
                      uint32_t* __restrict__ vals_out, uint64_t n, int shift, uint32_t n_tiles,
-                     const uint32_t* __restrict__ offs) {
+                     const uint32_t* __restrict__ offs, int per_lane) {
   __shared__ uint32_t s_cnt[kRadixWarps][256];  // counts, then the first output slot of (warp, digit)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int w = 0; w < kRadixWarps; ++w) s_cnt[w][threadIdx.x] = 0;
   __syncthreads();
-  const uint64_t chunk0 = uint64_t(blockIdx.x) * kRadixTile + uint64_t(warp) * kRadixChunk;
-  radix_count_chunk<K, kSum>(keys_in, n, chunk0, shift, s_cnt[warp], lane);
+  const uint64_t chunk0 = (uint64_t(blockIdx.x) * kRadixWarps + warp) * (32ull * per_lane);
+  radix_count_chunk<K, kSum>(keys_in, n, chunk0, shift, s_cnt[warp], lane, per_lane);
   __syncthreads();
   {
     uint32_t run = offs[uint64_t(threadIdx.x) * n_tiles + blockIdx.x];  // thread = digit
@@ -189,7 +189,7 @@ radix_scatter_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__
   }
   __syncthreads();
   uint32_t* slot = s_cnt[warp];
-  for (int j = 0; j < kRadixPerLane; ++j) {
+  for (int j = 0; j < per_lane; ++j) {
     const uint64_t i = chunk0 + uint64_t(j) * 32 + lane;
     const bool live = i < n;
     K key = 0;
@@ -212,8 +212,15 @@ radix_scatter_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__
   }
 }
 
-size_t radix_temp_bytes(uint64_t n) {
-  const uint64_t tiles = (n + kRadixTile - 1) / kRadixTile;
+// Elements per lane: long chunks (16 per lane) amortise the per-tile counters at library sizes; at query counts
+// (16 K ... 64 K) they would leave a few dozen warps on the whole GPU walking their chunks serially (measured 35 us
+// per pass at n = 16 000), so the chunk shrinks until every SM has a couple of CTAs.
+static int radix_per_lane(const homs_b200_ctx* ctx, uint64_t n) {
+  const uint64_t want = n / (uint64_t(kRadixThreads) * 2 * static_cast<uint64_t>(std::max(1, ctx->sm_count)));
+  return static_cast<int>(std::min<uint64_t>(kRadixMaxPerLane, std::max<uint64_t>(1, want)));
+}
+size_t radix_temp_bytes(uint64_t n) {  // sized for the shortest chunks
+  const uint64_t tiles = (n + kRadixThreads - 1) / kRadixThreads;
   return static_cast<size_t>(std::max<uint64_t>(1, tiles)) * 256 * sizeof(uint32_t);
 }
 
@@ -223,19 +230,21 @@ static int radix_sort_impl(homs_b200_ctx* ctx, K* keys_a, K* keys_b, uint32_t* v
   *result_in_b = false;
   if (n == 0 || end_bit <= begin_bit) return HOMS_B200_OK;
   HB_REQUIRE(ctx, n <= 0xFFFFFFFFull, HOMS_B200_ERR_ARGUMENT, "radix sort: more than 2^32-1 items");
-  const uint32_t tiles = static_cast<uint32_t>((n + kRadixTile - 1) / kRadixTile);
+  const int per_lane = radix_per_lane(ctx, n);
+  const uint64_t tile = uint64_t(kRadixThreads) * per_lane;
+  const uint32_t tiles = static_cast<uint32_t>((n + tile - 1) / tile);
   auto* hist = static_cast<uint32_t*>(d_temp);
   K *kin = keys_a, *kout = keys_b;
   uint32_t *vin = vals_a, *vout = vals_b;
   bool iota = first_vals_iota;
   for (int bit = begin_bit; bit < end_bit; bit += 8) {
     const int shift = bit | (((1 << std::min(8, end_bit - bit)) - 1) << 8);
-    radix_hist_kernel<K, kSum><<<tiles, kRadixThreads, 0, ctx->stream>>>(kin, n, shift, tiles, hist);
+    radix_hist_kernel<K, kSum><<<tiles, kRadixThreads, 0, ctx->stream>>>(kin, n, shift, tiles, hist, per_lane);
     HB_LAUNCHED(ctx);
     radix_scan_kernel<<<1, 1024, 0, ctx->stream>>>(hist, uint64_t(tiles) * 256);
     HB_LAUNCHED(ctx);
     radix_scatter_kernel<K, kSum><<<tiles, kRadixThreads, 0, ctx->stream>>>(kin, iota ? nullptr : vin, kout, vout, n, shift,
-                                                                       tiles, hist);
+                                                                             tiles, hist, per_lane);
     HB_LAUNCHED(ctx);
     iota = false;
     std::swap(kin, kout);
