@@ -352,12 +352,13 @@ def test_large_open_search_properties(hb, ctx):
         prev = s
 
 
-def test_many_queries_span_planning_batches(hb, best_oracle):
-    """More than 65536 queries: the tensor engine plans in batches of 64k sorted slots; results
-    must equal the POPC engine's and (on a sample) the oracle's.  Also: a query set that reaches
-    no bucket at all (no work items)."""
+@pytest.mark.parametrize("dim", [128, 2048])
+def test_many_queries_span_planning_batches(hb, best_oracle, dim):
+    """More than 65536 queries: the tensor engine plans in batches of 64k sorted slots (single CTAs with resident
+    query chunks at D = 128, CTA pairs at D = 2048); results must equal the POPC engine's and (on a sample) the
+    oracle's.  Also: a query set that reaches no bucket at all (no work items)."""
     rng = np.random.default_rng(41)
-    dim, n, nq = 128, 3000, 70000
+    n, nq = 3000, 70000
     words = U.random_hvs(rng, n, dim)
     words[2500:] = words[:500]
     mz = np.round(rng.uniform(400.0, 1200.0, n), 2)
