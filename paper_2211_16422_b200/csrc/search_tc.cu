@@ -42,6 +42,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "radix.cuh"
 #include "topk.cuh"
 
 namespace hb {
@@ -475,9 +476,9 @@ template <uint32_t kN>
 __global__ void __launch_bounds__(kTcPlanThreads) tc_plan_head_kernel(TcPlanCfg c, const uint2* __restrict__ ranges,
                                                                       void* plan) {
   const TcPlanPtrs q = tc_plan_layout(plan, c.n_tiles, c.item_cap);
-  __shared__ uint32_t s_scan[kTcPlanThreads];
+  __shared__ uint32_t s_lo[kTcPlanThreads], s_hi[kTcPlanThreads];  // row-tile range of every query tile
   __shared__ unsigned long long s_work;
-  __shared__ uint32_t s_strip;
+  __shared__ uint32_t s_strip, s_total[3];
   const uint32_t t = threadIdx.x;
   uint32_t lo = 0, hi = 0;
   if (t < c.n_tiles) {
@@ -487,6 +488,8 @@ __global__ void __launch_bounds__(kTcPlanThreads) tc_plan_head_kernel(TcPlanCfg 
     q.tlo[t] = lo;
     q.thi[t] = hi;
   }
+  s_lo[t] = lo;
+  s_hi[t] = hi;
   if (t == 0) s_work = 0;
   __syncthreads();
   if (hi > lo) atomicAdd(&s_work, static_cast<unsigned long long>(hi - lo));
@@ -505,26 +508,18 @@ __global__ void __launch_bounds__(kTcPlanThreads) tc_plan_head_kernel(TcPlanCfg 
   __syncthreads();
   const uint32_t strip = s_strip;
   const uint32_t ns = hi > lo ? (hi + strip - 1) / strip - lo / strip : 0;  // strips this tile overlaps
-  // exclusive scan of ns over the tiles (Hillis-Steele in shared memory; 512 entries)
-  s_scan[t] = ns;
-  __syncthreads();
-  for (uint32_t o = 1; o < kTcPlanThreads; o <<= 1) {
-    const uint32_t v = t >= o ? s_scan[t - o] : 0;
-    __syncthreads();
-    s_scan[t] += v;
-    __syncthreads();
-  }
-  if (t < c.n_tiles) q.tile_start[t] = s_scan[t] - ns;
-  if (t == c.n_tiles - 1) q.tile_start[c.n_tiles] = s_scan[t];
+  // exclusive scan of ns over the tiles (warp shuffles + one shared-memory step, radix.cuh)
+  const uint32_t ns_before = block_exclusive_sum_u32<kTcPlanThreads>(ns);
+  if (t < c.n_tiles) q.tile_start[t] = ns_before;
+  if (t == c.n_tiles - 1) q.tile_start[c.n_tiles] = ns_before + ns;
   // groups of consecutive query tiles
   const uint32_t n_groups = (c.n_tiles + c.group_tiles - 1) / c.group_tiles;
-  __syncthreads();
   uint32_t g_items = 0, g_pairs = 0, g_lo_strip = 0;
   if (t < n_groups) {
     const uint32_t t0 = t * c.group_tiles, t1 = min(c.n_tiles, t0 + c.group_tiles);
     uint32_t glo = 0xffffffffu, ghi = 0;
     for (uint32_t j = t0; j < t1; ++j) {
-      const uint32_t a = q.tlo[j], b = q.thi[j];
+      const uint32_t a = s_lo[j], b = s_hi[j];
       if (b > a) {
         glo = min(glo, a);
         ghi = max(ghi, b);
@@ -537,44 +532,38 @@ __global__ void __launch_bounds__(kTcPlanThreads) tc_plan_head_kernel(TcPlanCfg 
     }
     q.grp_lo_strip[t] = g_lo_strip;
   }
-  // exclusive scans over the groups (reuse the scan buffer twice)
-  s_scan[t] = g_items;
-  __syncthreads();
-  for (uint32_t o = 1; o < kTcPlanThreads; o <<= 1) {
-    const uint32_t v = t >= o ? s_scan[t - o] : 0;
-    __syncthreads();
-    s_scan[t] += v;
-    __syncthreads();
+  // exclusive scans over the groups
+  const uint32_t items_before = block_exclusive_sum_u32<kTcPlanThreads>(g_items);
+  const uint32_t pairs_before = block_exclusive_sum_u32<kTcPlanThreads>(g_pairs);
+  if (t < n_groups) {
+    q.grp_item_base[t] = items_before;
+    q.grp_pair_base[t] = pairs_before;
   }
-  if (t < n_groups) q.grp_item_base[t] = s_scan[t] - g_items;
-  const uint32_t total_items = s_scan[kTcPlanThreads - 1];
-  __syncthreads();
-  s_scan[t] = g_pairs;
-  __syncthreads();
-  for (uint32_t o = 1; o < kTcPlanThreads; o <<= 1) {
-    const uint32_t v = t >= o ? s_scan[t - o] : 0;
-    __syncthreads();
-    s_scan[t] += v;
-    __syncthreads();
+  if (t == kTcPlanThreads - 1) {  // the last thread's exclusive sums + its own values are the totals
+    s_total[0] = items_before + g_items;
+    s_total[1] = pairs_before + g_pairs;
   }
-  if (t < n_groups) q.grp_pair_base[t] = s_scan[t] - g_pairs;
+  __syncthreads();
   if (t == 0) {
-    q.grp_item_base[n_groups] = total_items;
-    q.grp_pair_base[n_groups] = s_scan[kTcPlanThreads - 1];
-    q.head->n_items = total_items;
+    q.grp_item_base[n_groups] = s_total[0];
+    q.grp_pair_base[n_groups] = s_total[1];
+    q.head->n_items = s_total[0];
     q.head->counter = 0;
     q.head->strip = strip;
-    q.head->n_pairs = s_scan[kTcPlanThreads - 1];
+    q.head->n_pairs = s_total[1];
     q.head->n_groups = n_groups;
   }
 }
 
-// one thread per (group, strip) pair: its items, in tile order, and the per-tile item lists
+// one WARP per (group, strip) pair: its items, in tile order, and the per-tile item lists.  (One thread per pair
+// walked the group's tiles twice in a chain of dependent loads: 34 us for config 2's 307 strips.)
 template <uint32_t kN>
 __global__ void tc_plan_items_kernel(TcPlanCfg c, void* plan) {
   const TcPlanPtrs q = tc_plan_layout(plan, c.n_tiles, c.item_cap);
   const uint32_t n_pairs = q.head->n_pairs, n_groups = q.head->n_groups, strip = q.head->strip;
-  for (uint32_t pr = blockIdx.x * blockDim.x + threadIdx.x; pr < n_pairs; pr += gridDim.x * blockDim.x) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, n_warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t pr = warp; pr < n_pairs; pr += n_warps) {
     uint32_t g = 0, gh = n_groups;  // last group whose pair base is <= pr
     while (gh - g > 1) {
       const uint32_t mid = (g + gh) >> 1;
@@ -584,21 +573,31 @@ __global__ void tc_plan_items_kernel(TcPlanCfg c, void* plan) {
     const uint32_t sidx = q.grp_lo_strip[g] + (pr - q.grp_pair_base[g]);
     const uint32_t t0 = g * c.group_tiles, t1 = min(c.n_tiles, t0 + c.group_tiles);
     // items of this group that come before strip sidx: per tile, its strips below sidx
-    uint32_t idx = q.grp_item_base[g];
-    for (uint32_t j = t0; j < t1; ++j) {
+    uint32_t before = 0;
+    for (uint32_t j = t0 + lane; j < t1; j += 32) {
       const uint32_t a = q.tlo[j], b = q.thi[j];
       if (b <= a) continue;
       const uint32_t first = a / strip, cnt = (b + strip - 1) / strip - first;
-      idx += sidx > first ? min(sidx - first, cnt) : 0;
+      before += sidx > first ? min(sidx - first, cnt) : 0;
     }
+    uint32_t idx = q.grp_item_base[g] + __reduce_add_sync(0xffffffffu, before);
     const uint64_t s_lo = uint64_t(sidx) * strip, s_hi = s_lo + strip;
-    for (uint32_t j = t0; j < t1; ++j) {
-      const uint32_t tl = q.tlo[j], th = q.thi[j];
+    for (uint32_t j0 = t0; j0 < t1; j0 += 32) {  // 32 tiles per round, items numbered in tile order
+      const uint32_t j = j0 + lane;
+      uint32_t tl = 0, th = 0;
+      if (j < t1) {
+        tl = q.tlo[j];
+        th = q.thi[j];
+      }
       const uint64_t a = max(uint64_t(tl), s_lo), b = min(uint64_t(th), s_hi);
-      if (b <= a) continue;
-      q.items[idx] = TcItem{j, static_cast<uint32_t>(a) * kN, static_cast<uint32_t>(b) * kN, 0};
-      q.tile_items[q.tile_start[j] + (sidx - tl / strip)] = idx;
-      ++idx;
+      const bool has = j < t1 && b > a;
+      const uint32_t mask = __ballot_sync(0xffffffffu, has);
+      if (has) {
+        const uint32_t my = idx + __popc(mask & ((1u << lane) - 1u));
+        q.items[my] = TcItem{j, static_cast<uint32_t>(a) * kN, static_cast<uint32_t>(b) * kN, 0};
+        q.tile_items[q.tile_start[j] + (sidx - tl / strip)] = my;
+      }
+      idx += __popc(mask);
     }
   }
 }
