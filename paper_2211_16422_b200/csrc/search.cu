@@ -505,7 +505,7 @@ __global__ void decode_kernel(uint64_t total, const Cand* __restrict__ rec, uint
 // The tensor engine's cost has a floor of one pass over the library image per call (every query
 // tile's union window, summed over the tiles, covers the library once: 0.7 ms on config 2 however
 // narrow the tolerance).  A 20 ppm window holds ~25 rows: reading exactly those rows (neighbouring
-// sorted queries share them in L2) is an order of magnitude less traffic.  k <= 16.
+// sorted queries share them in L2) is an order of magnitude less traffic.  k <= 64 (32 per pass).
 
 // KM = 1: running best; KM > 1: the k <= KM best in a register list every lane holds identically
 // (the comparisons are warp-uniform) -- the warp-level top-k with the reference's tie-break.

@@ -30,7 +30,8 @@
 //   its query with the exact 3-level key (top-k: appends the candidates above the query's floor to a buffer,
 //   tc_select_kernel picks the k best exactly) and masks columns outside the query's own window.  The drain
 //   overlaps with the next tile's MMAs.  From D = 2048 up two CTAs of a cluster pair up on 256-query tiles
-//   (cta_group::2, TcShape<true>): each streams its own queries and half of every library tile.
+//   (cta_group::2, TcShape<true>): each streams its own queries and half of every library tile.  At D <= 1024
+//   the query tile's k-chunks stay resident in shared memory for a whole work item (TcShape<false, true>).
 // * work items (query tile x strip of row tiles) are planned on the device (tc_plan_*_kernel),
 //   ordered (group of query tiles, strip, tile) and handed out dynamically in that order, so that
 //   the CTAs running at any moment share both query and row tiles in L2; the whole search is
