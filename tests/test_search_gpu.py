@@ -592,3 +592,21 @@ def test_tensor_kernel_forms_vs_port(hb, port, monkeypatch, form, dim):
         score, ordinal = oix.search_topk(qw, qmz, qch, ("da", 500.0), 7)
         assert np.array_equal(got.ordinal, ordinal) and np.array_equal(got.raw_score, score), (form, dim)
     oix.close()
+
+
+def test_tensor_cta_pairs_by_dimension(hb, monkeypatch):
+    """homs_b200_ctx_tensor_cta_pairs: CTA pairs (cta_group::2) serve the resident library from D = 2048 up on a
+    device that co-schedules a 2-CTA cluster on every SM pair (a B200 does); HOMS_B200_TC_PAIR forces either form."""
+    rng = np.random.default_rng(3)
+    for dim, want in ((256, False), (1024, False), (2048, True), (8192, True)):
+        with hb.Context(0) as c:
+            c.build_index(dim, U.random_hvs(rng, 64, dim), np.linspace(500.0, 600.0, 64), np.full(64, 2, np.uint8))
+            assert c.tensor_cta_pairs() == want, dim
+    monkeypatch.setenv("HOMS_B200_TC_PAIR", "0")
+    with hb.Context(0) as c:
+        c.build_index(4096, U.random_hvs(rng, 64, 4096), np.linspace(500.0, 600.0, 64), np.full(64, 2, np.uint8))
+        assert not c.tensor_cta_pairs()
+    monkeypatch.setenv("HOMS_B200_TC_PAIR", "1")
+    with hb.Context(0) as c:
+        c.build_index(256, U.random_hvs(rng, 64, 256), np.linspace(500.0, 600.0, 64), np.full(64, 2, np.uint8))
+        assert c.tensor_cta_pairs()
