@@ -100,7 +100,7 @@ struct GroupWorkers;  // group.cu: one issuing thread per non-leading member of 
 // (homs_b200_ctx_create), never on the search path; 0 = the built-in choice
 struct TcKnobs {
   uint32_t group_tiles = 0, items_per_sm = 0, max_strip = 0, item_cap = 0, group_mb = 0;
-  uint32_t l2_hints = 2;  // see TcParams::l2_hints (default: library tiles evict_first)
+  uint32_t l2_hints = 0;  // see TcParams::l2_hints (default: none; round 2's evict_first on library tiles stopped paying)
   uint32_t topk_lists = 0;  // top-k path: 0 / 2 = collect + select (default), 1 = register-list passes
   uint32_t ccap = 0;        // collect mode: candidate buffer entries per query (0: built-in)
   uint32_t ares = 1;        // 0: never keep the query tile's k-chunks resident in shared memory (HOMS_B200_TC_ARES)

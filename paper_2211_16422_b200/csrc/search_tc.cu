@@ -754,9 +754,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_search_kernel(const TcParams
     if (elect_one()) {
       uint32_t stage = 0, phase = 0, qslot = 0, qphase = 0;
       // L2 residency: a library strip (B) is read by the group's query tiles within one short window and is
-      // then dead, while the group's query tiles (A) are re-read for every strip of the sweep.  Fetching B
-      // with evict_first keeps the streaming strips from pushing A out (default; -1.7 ... -3.7 % kernel time
-      // on configs 2, 3 and D = 16384); evict_last on A on top of that measured no gain (bit 0, off).
+      // then dead, while the group's query tiles (A) are re-read for every strip of the sweep.  Fetching B with
+      // evict_first kept the streaming strips from pushing A out and paid 1.7 ... 3.7 % with the single-CTA kernel
+      // of early round 2; with CTA pairs and lean issue threads it no longer changes the time (+-0.3 % on configs
+      // 2, 3 and D = 1024 ... 16384) but costs DRAM traffic (strips evicted before the slowest pair has read them:
+      // 9.0 vs 6.0 GB per launch on config 2, 240 vs 183 GB on the config-3 prefix), so both hints are off by
+      // default (profiles/r02_ab_l2_hints_pair.log; HOMS_B200_TC_L2_HINTS bit 0 = A evict_last, bit 1 = B evict_first).
       const uint64_t pol_a = (p.l2_hints & 1u) ? l2_policy_evict_last() : l2_policy_evict_normal();
       const uint64_t pol_b = (p.l2_hints & 2u) ? l2_policy_evict_first() : l2_policy_evict_normal();
       // everything the inner loop needs lives in registers: no parameter reloads, no 64-bit multiplies per stage
